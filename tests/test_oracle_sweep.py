@@ -1,0 +1,284 @@
+"""Pins for the oracle's whole-sweep algorithms (no GPU).
+
+Pinned to: closed-form spectra of pencils built with known generalized
+singular values (BASELINE north_star; SURVEY C-20, C-21), the S = I special
+case reducing to a Hermitian eigenproblem (numpy eigvalsh), a Cholesky-free
+brute force in mpmath at 40 digits on tiny general pencils, the GHSVD
+definition (V^*V = I, F columns J-orthogonal,
+Sigma_F^2 + Sigma_G^2 = 1), the congruence F_c = F Z', and residuals.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1907_08560_b200 import inputs
+
+EPS = oracle.EPS
+
+
+def relerr(a, b):
+    a = np.sort(np.asarray(a))
+    b = np.sort(np.asarray(b))
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+def residual(F, J, G, lam, Z):
+    """BASELINE residual ||Hx - lam Sx|| / ((||F||_F^2 + ||G||_F^2) ||x||), per column (C-15)."""
+    nf2 = np.linalg.norm(F) ** 2 + np.linalg.norm(G) ** 2
+    Hx = F.conj().T @ (J[:, None] * (F @ Z))
+    Sx = G.conj().T @ (G @ Z)
+    r = np.linalg.norm(Hx - Sx * lam[None, :], axis=0) / (nf2 * np.linalg.norm(Z, axis=0))
+    return float(r.max())
+
+
+def run(P, **kw):
+    F, G, Zp, st = oracle.hz_pointwise(P.F, P.J, P.G, **kw)
+    lam, sf, sg, Z = oracle.extract(F, P.J, G, Zp)
+    return F, G, Zp, st, lam, sf, sg, Z
+
+
+@pytest.mark.parametrize("m,n,seed", [(64, 32, 1), (128, 64, 2), (96, 96, 3), (200, 40, 4)])
+def test_known_gsvd_J_identity(m, n, seed):
+    """J = I: lambda = alpha^2/beta^2 exactly (config-1 recipe, BASELINE configs[1])."""
+    P = inputs.known_gsvd(seed, m, n)
+    F, G, Zp, st, lam, sf, sg, Z = run(P)
+    assert st["converged"] and st["big_per_sweep"][-1] == 0
+    assert relerr(lam, P.lam_true) < 1e-10
+    assert residual(P.F, P.J, P.G, lam, Z) < 1e-12 * n
+    # GHSVD definition: Sigma_F^2 + Sigma_G^2 = 1 ; V = G' Sigma_G'^-1 unitary
+    assert np.allclose(sf ** 2 + sg ** 2, 1.0, atol=4 * EPS)
+    V = G / np.linalg.norm(G, axis=0)
+    assert np.abs(V.conj().T @ V - np.eye(n)).max() < 1e-12
+    # congruence: converged factors equal the inputs times the accumulated Z'
+    assert np.linalg.norm(F - P.F @ Zp) / np.linalg.norm(F) < 1e-11
+    assert np.linalg.norm(G - P.G @ Zp) / np.linalg.norm(G) < 1e-11
+    # at convergence no pair passes the relative criterion (C-1/C-3, J = I)
+    tol = EPS * np.sqrt(n)
+    Hm = F.conj().T @ F
+    Sm = G.conj().T @ G
+    d = 1 / np.sqrt(np.diag(Sm).real)
+    Hs = Hm * np.outer(d, d)
+    Ss = Sm * np.outer(d, d)
+    off = np.abs(Hs) / np.sqrt(np.outer(np.abs(np.diag(Hs)), np.abs(np.diag(Hs))))
+    np.fill_diagonal(off, 0)
+    so = np.abs(Ss - np.diag(np.diag(Ss)))
+    assert off.max() < 1e3 * tol and so.max() < 1e3 * tol
+
+
+@pytest.mark.parametrize("m,n,seed,neg", [(64, 32, 5, 0.4), (128, 64, 6, 0.5), (80, 80, 7, 0.3), (160, 48, 8, 0.6)])
+def test_known_hyperbolic(m, n, seed, neg):
+    """J != I: lambda_i = j'_i alpha_i^2 / beta_i^2 with Q_J J-unitary (C-21)."""
+    P = inputs.known_hyperbolic(seed, m, n, neg)
+    F, G, Zp, st, lam, sf, sg, Z = run(P)
+    assert st["converged"]
+    assert relerr(lam, P.lam_true) < 1e-10
+    assert residual(P.F, P.J, P.G, lam, Z) < 1e-12 * n
+    # converged F columns mutually J-orthogonal
+    Hc = F.conj().T @ (P.J[:, None] * F)
+    nrm = np.sqrt(np.abs(np.diag(Hc)))
+    off = np.abs(Hc) / np.outer(nrm, nrm)
+    np.fill_diagonal(off, 0)
+    assert off.max() < 1e-10
+    assert np.all(np.sign(lam) == np.sign(np.diag(Hc).real))
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_orthonormal_G_reduces_to_hermitian_eig(seed):
+    """S = I special case: lambda = eig(F^* J F) by an independent library routine."""
+    P = inputs.orthonormal_G(seed, 90, 40)
+    _, _, _, st, lam, *_ = run(P)
+    H = P.F.conj().T @ (P.J[:, None] * P.F)
+    ref = np.linalg.eigvalsh(0.5 * (H + H.conj().T))
+    assert relerr(lam, ref) < 1e-10
+
+
+def _mp_brute(F, J, G, dps=40):
+    """Cholesky-free brute force at dps digits: S = Q L Q^*, S^{-1/2} H S^{-1/2} eigenvalues."""
+    import mpmath as mp
+    mp.mp.dps = dps
+    n = F.shape[1]
+    Fm = mp.matrix(F.tolist())
+    Gm = mp.matrix(G.tolist())
+    Jm = mp.diag([int(j) for j in J])
+    H = Fm.H * Jm * Fm
+    S = Gm.H * Gm
+    ev, Q = mp.eighe(S)
+    Sih = Q * mp.diag([1 / mp.sqrt(e) for e in ev]) * Q.H
+    A = Sih * H * Sih
+    A = (A + A.H) / 2
+    w, _ = mp.eighe(A)
+    return np.array([float(w[i]) for i in range(n)])
+
+
+@pytest.mark.parametrize("m,n,seed", [(10, 6, 21), (16, 12, 22), (20, 9, 23)])
+def test_mpmath_bruteforce_tiny(m, n, seed):
+    """Tiny general pencils (odd n exercises bordering, Sec 6.3.2) vs 40-digit brute force."""
+    P = inputs.random_pencil(seed, m, n, 0.5)
+    _, _, _, st, lam, *_ = run(P)
+    ref = _mp_brute(P.F, P.J, P.G)
+    assert relerr(lam, ref) < 1e-11
+
+
+def test_illconditioned_small_analog_vs_mpmath():
+    """Config-3 analog (coupled, S singular values 1 ... 1e-12, C-14) vs 60-digit brute force:
+    the GHSVD keeps eigenvalue accuracy where Cholesky-based solvers lose ~1e-6."""
+    at = inputs.illcond_atoms(31, 2, 5, 12, smin=1e-6)
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    Fo, Go, Zp, st = oracle.hz_pointwise(F, J, G)
+    lam, *_ = oracle.extract(Fo, J, Go, Zp)
+    ref = _mp_brute(F, J, G, dps=60)
+    assert relerr(lam, ref) < 1e-8
+
+
+def test_determinism_across_threads():
+    """PAPER.md:529-535 reproducibility: same inputs -> bitwise same outputs for any thread count."""
+    P = inputs.known_hyperbolic(9, 96, 64, 0.5)
+    a = oracle.hz_pointwise(P.F, P.J, P.G, nthreads=1)
+    b = oracle.hz_pointwise(P.F, P.J, P.G, nthreads=4)
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x, y)
+    assert a[3] == b[3]
+
+
+def test_steps_equal_first_sweep():
+    """or_hz_steps over all n-1 steps == the first sweep of Algorithm 2 (bitwise)."""
+    P = inputs.random_pencil(10, 40, 20, 0.5)
+    n = 20
+    F1, G1, Z1, st = oracle.hz_pointwise(P.F, P.J, P.G, cmax=1)
+    Z0 = np.eye(n, dtype=complex)
+    F2, G2, Z2, a, b = oracle.hz_steps(P.F, P.J, P.G, Z0, 0, n - 1)
+    F3, G3, Z3, a1, b1 = oracle.hz_steps(P.F, P.J, P.G, Z0, 0, 7)
+    F3, G3, Z3, a2, b2 = oracle.hz_steps(F3, P.J, G3, Z3, 7, n - 8)
+    assert np.array_equal(F1, F2) and np.array_equal(G1, G2) and np.array_equal(Z1, Z2)
+    assert np.array_equal(F2, F3) and np.array_equal(Z2, Z3)
+    assert st["transforms_all"] == a == a1 + a2 and st["transforms_big"] == b == b1 + b2
+
+
+def test_stop_rule_and_cmax():
+    """C-3: stop when a sweep has no big transform; C_max caps the sweeps (not converged)."""
+    P = inputs.known_gsvd(3, 64, 32)
+    *_, st, lam, sf, sg, Z = run(P, cmax=3)
+    assert st["sweeps"] == 3 and not st["converged"]
+    *_, st, lam, sf, sg, Z = run(P, cmax=30)
+    assert st["converged"] and st["big_per_sweep"][-1] == 0 and all(b > 0 for b in st["big_per_sweep"][:-1])
+
+
+def test_literal_criterion_same_eigenvalues():
+    """C-1: the literal (6.12) reading gives the same lambda when stopping on big == 0."""
+    P = inputs.known_hyperbolic(13, 64, 32, 0.5)
+    *_, st1, l1, _, _, _ = run(P, criterion=oracle.CRIT_RELATIVE)
+    *_, st2, l2, _, _, _ = run(P, criterion=oracle.CRIT_LITERAL)
+    assert relerr(l1, P.lam_true) < 1e-10 and relerr(l2, P.lam_true) < 1e-10
+
+
+@pytest.mark.parametrize("nblk,inner", [(4, 1), (8, 1), (6, 1), (10, 1), (8, 30)])
+def test_blocked_matches_known_spectrum(nblk, inner):
+    """Level-2 BO (inner 1 sweep) and FB (inner to convergence), Sec 6.4: same lambda;
+    nblk = 6, 10 with n = 64 give widths w, w-1 and odd block pivots (bordered)."""
+    P = inputs.known_hyperbolic(14, 96, 64, 0.4)
+    F, G, Zp, st = oracle.hz_blocked(P.F, P.J, P.G, nblk, inner_sweeps=inner)
+    lam, sf, sg, Z = oracle.extract(F, P.J, G, Zp)
+    assert st["converged"]
+    assert relerr(lam, P.lam_true) < 1e-10
+    assert residual(P.F, P.J, P.G, lam, Z) < 1e-12 * 64
+
+
+# -------------------------------------------------------------- HEBPJ / pchol
+@pytest.mark.parametrize("r,seed", [(1, 0), (2, 1), (7, 2), (8, 3), (40, 4), (98, 5), (162, 6)])
+def test_hebpj_reconstruction_and_inertia(r, seed):
+    """Sec 4.2-4.3: T = M^* J M, J sorted (+ first); #(+) equals the number of positive
+    eigenvalues (Sylvester's law of inertia, numpy eigvalsh)."""
+    rng = np.random.default_rng(seed)
+    X = inputs.cgauss(rng, (r, r))
+    T = X + X.conj().T
+    M, J, npos = oracle.hebpj(T)
+    assert np.linalg.norm(M.conj().T @ (J[:, None] * M) - T) / np.linalg.norm(T) < 100 * r * r * EPS
+    assert npos == int((np.linalg.eigvalsh(T) > 0).sum())
+    assert np.all(J[:npos] == 1) and np.all(J[npos:] == -1)
+
+
+def test_hebpj_golden():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))["hebpj"]
+    for ex in g:
+        T = np.array([[complex(*v) for v in row] for row in ex["T"]])
+        M, J, npos = oracle.hebpj(T)
+        assert list(J) == ex["J"], ex["cite"]
+        if "absM" in ex:
+            assert np.allclose(np.abs(M), ex["absM"], atol=4 * EPS), ex["cite"]
+        assert np.allclose(M.conj().T @ (J[:, None] * M), T, atol=8 * EPS)
+
+
+def test_hebpj_rank_deficient_raises():
+    T = np.zeros((3, 3), complex)
+    with pytest.raises(oracle.OracleError):
+        oracle.hebpj(T)
+
+
+def test_pchol():
+    rng = np.random.default_rng(7)
+    for r in (1, 5, 33):
+        X = inputs.cgauss(rng, (r + 3, r))
+        S = X.conj().T @ X
+        Gh = oracle.pchol(S)
+        assert np.linalg.norm(Gh.conj().T @ Gh - S) / np.linalg.norm(S) < 50 * r * EPS
+    with pytest.raises(oracle.OracleError):
+        oracle.pchol(-np.eye(2, dtype=complex))
+
+
+# ------------------------------------------------------------- phases 1, 2
+def _HS_from_atoms(at):
+    NA = at.A.shape[0]
+    H = 0
+    S = 0
+    for a in range(NA):
+        T = np.block([[at.TAA[a], at.TAB[a]], [at.TAB[a].conj().T, at.TBB[a]]])
+        Ha = np.vstack([at.A[a], at.B[a]])
+        Sa = np.vstack([at.A[a], at.U[a][:, None] * at.B[a]])
+        H = H + Ha.conj().T @ T @ Ha                    # eq (4.1)
+        S = S + Sa.conj().T @ Sa
+    return H, S
+
+
+@pytest.mark.parametrize("NA,NL,NG,neg", [(2, 4, 12, 0.5), (3, 5, 20, 0.4), (4, 9, 40, 0.5)])
+def test_factor_grammians(NA, NL, NG, neg):
+    """Phase 1 (Alg. 1, eqs 4.1-4.2): F^* J F = sum_a H_a^* T_a H_a, G^* G = sum_a S_a^* S_a;
+    per-atom #(-) = number of negative eigenvalues of T_a (inertia)."""
+    at = inputs.lapw_atoms(40 + NA, NA, NL, NG, neg)
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    H, S = _HS_from_atoms(at)
+    assert np.linalg.norm(F.conj().T @ (J[:, None] * F) - H) / np.linalg.norm(H) < 1e-13
+    assert np.linalg.norm(G.conj().T @ G - S) / np.linalg.norm(S) < 1e-14
+    for a in range(NA):
+        blk = J[2 * NL * a: 2 * NL * (a + 1)]
+        assert (blk < 0).sum() == (at.d[a] < 0).sum()
+        assert np.all(np.diff(blk.astype(int)) <= 0)   # + before -
+
+
+@pytest.mark.parametrize("m,n,neg", [(60, 12, 0.5), (200, 40, 0.4), (150, 150, 0.5), (300, 64, 0.1)])
+def test_reduce_grammian_preservation(m, n, neg):
+    """Phase 2 (eq 5.1): P2^T Ft^* Jt Ft P2 = F^* J F, likewise for G; F block upper
+    triangular (1x1/2x2 diagonal blocks), G upper triangular with real diagonal >= 0."""
+    P = inputs.random_pencil(50 + m, m, n, neg)
+    Fs, Js, Gs, p2, n2 = oracle.reduce(P.F, P.J, P.G)
+    H = P.F.conj().T @ (P.J[:, None] * P.F)
+    S = P.G.conj().T @ P.G
+    assert sorted(p2) == list(range(n))
+    Hp = H[np.ix_(p2, p2)]
+    Sp = S[np.ix_(p2, p2)]
+    assert np.linalg.norm(Fs.conj().T @ (Js[:, None] * Fs) - Hp) / np.linalg.norm(H) < 1e-11
+    assert np.linalg.norm(Gs.conj().T @ Gs - Sp) / np.linalg.norm(S) < 1e-12
+    assert np.abs(np.tril(Fs, -2)).max() == 0 and np.abs(np.tril(Gs, -1)).max() == 0
+    assert np.all(np.diag(Gs).real >= 0) and np.all(np.diag(Gs).imag == 0)
+
+
+def test_reduce_then_sweep_same_eigenvalues():
+    """the GHSVD is invariant under Phase 2 (Lambda unchanged)."""
+    at = inputs.lapw_atoms(60, 4, 6, 30, 0.4)
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    Fo, Go, Zp, _ = oracle.hz_pointwise(F, J, G)
+    l1, *_ = oracle.extract(Fo, J, Go, Zp)
+    Fs, Js, Gs, p2, n2 = oracle.reduce(F, J, G)
+    Fo, Go, Zp, _ = oracle.hz_pointwise(Fs, Js, Gs)
+    l2, *_ = oracle.extract(Fo, Js, Go, Zp)
+    assert relerr(l2, l1) < 1e-9

@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""Benchmark of the GHSVD sweep engine (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3] [--variant pointwise|bo] [--cluster C] [--threads T]
+
+One "step" = one complete Phase-3 solve (ghsvd_sweep to convergence: all sweeps of
+the round-robin HZ iteration) on BASELINE configs[3]
+(N_A=64, N_L=81, N_G=4096: F, G 10368 x 4096 complex128, ill-conditioned S, J 50 %
+negative), from the factors Phase 1 (ghsvd_factor, timed separately) produced.
+
+* value  = time-to-converge in seconds, device time (CUDA events on the context
+           stream) of ghsvd_sweep with the factors already resident in HBM; mean of
+           the K timed steps, max over ranks.  Inputs (1.6 GB) exceed L2 (126 MB).
+* e2e    = the same solve through the C ABI from pinned HOST buffers: H2D of F, G, J
+           (ghsvd_set_factors) + sweep + D2H of lambda, Sigma_F, Sigma_G (ghsvd_extract).
+* roofline: the dominant kernel k_pair_step; algorithmic bytes (128m+64n per
+           transformed pair, 64m per skipped pair, counted from the device counters)
+           / its summed CUDA-event time; peak = MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline: the oracle (oracle/, plain C + OpenMP) timed on a bounded sample
+           (a few steps of sweep 1 on the same factors), extrapolated to the GPU's
+           sweep count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GHSVD time-to-converge (s) c128 N_G=4096"
+UNIT = "s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_factors(cfg: int, backend: str):
+    from paper_1907_08560_b200 import inputs
+    return inputs.make_config(cfg, backend=backend)
+
+
+def cpu_baseline_sample(F0, J0, G0, sweeps: int, budget_s: float = 15.0):
+    """Oracle on a bounded sample: steps of sweep 1 on the same factors, extrapolated
+    to (n-1) * sweeps steps.  Returns the cpu_baseline object."""
+    import oracle
+    m, n = F0.shape
+    Z = np.eye(n, dtype=np.complex128, order="F")
+    t = time.perf_counter()
+    F1, G1, Z1, a, b = oracle.hz_steps(F0, J0, G0, Z, 0, 1)
+    t1 = time.perf_counter() - t
+    ns = int(max(1, min(n - 2, budget_s / max(t1, 1e-6))))
+    t = time.perf_counter()
+    oracle.hz_steps(F1, J0, G1, Z1, 1, ns)
+    tn = time.perf_counter() - t
+    per_step = tn / ns
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"value": per_step * (n - 1) * sweeps, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{ns} round-robin steps (of {n - 1}) of sweep 2-prefix on the full {m}x{n} factors, "
+                      f"{per_step:.3f} s/step, extrapolated x{n - 1} steps x {sweeps} sweeps (GPU sweep count)",
+            "seconds_measured": t1 + tn}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on host cores, same config/metric."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_1907_08560_b200 import inputs
+    kind, payload = make_factors(args.config, "numpy")
+    if kind == "atoms":
+        at = payload
+        F0, J0, G0 = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    else:
+        F0, J0, G0 = payload.F, payload.J, payload.G
+    sweeps = args.ref_sweeps
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline_sample(F0, J0, G0, sweeps, budget_s=args.ref_budget)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = float(np.mean(vals))
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": inputs.CONFIGS[args.config]["name"], "variant": "oracle-pointwise"},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    from paper_1907_08560_b200 import build, ghsvd, inputs
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    build.build()
+    stream = torch.cuda.Stream(dev)
+    cfg = inputs.CONFIGS[args.config]
+    # ---- inputs (seeded, synthetic) and Phase 1 on the device
+    kind, payload = make_factors(args.config, "torch")
+    if kind == "atoms":
+        at = payload
+        NA, NL, NG = at.A.shape
+        m, n, nl = 2 * NA * NL, NG, NL
+    else:
+        m, n = payload.F.shape
+        nl = 0
+    ctx = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=args.max_sweeps,
+                        cluster=args.cluster, threads=args.threads, nblocks=args.nblocks)
+    t0 = time.perf_counter()
+    phase1_s = None
+    with torch.cuda.stream(stream):
+        if kind == "atoms":
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(stream)
+            ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+            ev[1].record(stream)
+            stream.synchronize()
+            phase1_s = ev[0].elapsed_time(ev[1]) * 1e-3
+        else:
+            ctx.set_factors(payload.F, payload.J, payload.G)
+        mb, nb = ctx.factor_shape()
+        # pinned host copies of the starting factors (e2e inputs) and device copies
+        Fh = torch.empty((nb, mb), dtype=torch.complex128, pin_memory=True).t()
+        Gh = torch.empty((nb, mb), dtype=torch.complex128, pin_memory=True).t()
+        Jh = torch.empty(mb, dtype=torch.int8, pin_memory=True)
+        ctx.export_factors(Fh, Jh, Gh)
+        stream.synchronize()
+    lam_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    sf_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    sg_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+
+    def one_step():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        with torch.cuda.stream(stream):
+            e[0].record(stream)
+            ctx.set_factors(Fh, Jh, Gh)                 # H2D from pinned host
+            e[1].record(stream)
+            st = ctx.sweep()                            # Phase 3 to convergence
+            e[2].record(stream)
+            ctx.extract(want_z=False, out=(lam_h, sf_h, sg_h, None))   # D2H of the result
+            e[3].record(stream)
+        stream.synchronize()
+        return st, e[1].elapsed_time(e[2]) * 1e-3, e[0].elapsed_time(e[3]) * 1e-3
+
+    for _ in range(args.warmup):
+        one_step()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    dev_t, e2e_t, stats = [], [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            st, td, te = one_step()
+            dev_t.append(td)
+            e2e_t.append(te)
+            stats.append(st)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    value = float(np.mean(dev_t))
+    e2e = float(np.mean(e2e_t))
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([value, e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        value, e2e = float(t[0]), float(t[1])
+    kern_s = sum(s["kernel_seconds"] for s in stats)
+    alg = sum(s["alg_bytes"] for s in stats)
+    launches = sum(s["launches"] for s in stats)
+    sweeps = stats[-1]["sweeps"]
+    pairs = stats[-1]["pairs_visited"]
+    peaks = _peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg / kern_s / 1e9 if kern_s > 0 else 0.0
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak" if ws > 1 else "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant,
+                   "cluster": ctx.opts.cluster, "l2": "inputs (1.6 GB) larger than L2", "phase2": "skipped"},
+        "sweeps": sweeps, "converged": stats[-1]["converged"],
+        "pair_updates_per_s": pairs / value, "transforms_per_s": stats[-1]["transforms_all"] / value,
+        "phase1_seconds": phase1_s,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "k_pair_step", "alg_bytes_per_launch": alg / max(launches, 1),
+                     "avg_launch_us": kern_s / max(launches, 1) * 1e6,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(2 * mb * nb * 16 + mb),
+                "d2h_bytes_per_step": int(3 * n * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        F0 = np.asfortranarray(Fh.numpy())
+        G0 = np.asfortranarray(Gh.numpy())
+        J0 = Jh.numpy().copy()
+        line["cpu_baseline"] = cpu_baseline_sample(F0, J0, G0, sweeps, budget_s=args.ref_budget)
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--variant", default="pointwise", choices=["pointwise", "bo", "fb"])
+    ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--nblocks", type=int, default=0)
+    ap.add_argument("--max-sweeps", type=int, default=30)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--ref-sweeps", type=int, default=20,
+                    help="sweep count used to extrapolate the oracle sample in --impl reference")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

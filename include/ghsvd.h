@@ -1,0 +1,176 @@
+/*
+ * ghsvd.h -- C ABI of the B200-native implicit Hari-Zimmermann J-GHSVD engine.
+ *
+ * Computes the generalized hyperbolic SVD (GSVD when J = I) of a complex128
+ * factor pair (F, G) under a diagonal sign matrix J, i.e. the eigenpairs of the
+ * Hermitian-definite pencil (H, S) = (F^* J F, G^* G) without forming H or S
+ * (Novakovic, Singer, Singer, Hari, arXiv:1907.08560; cited as PAPER.md:<line>).
+ *
+ * Conventions (all entry points):
+ *  - Matrices are column-major complex128 = two IEEE doubles (re, im), column
+ *    stride `ld*` in complex elements.  Unless stated otherwise a pointer may be
+ *    HOST or DEVICE memory (the library copies with cudaMemcpyDefault, so host
+ *    pointers cost a PCIe transfer on the context stream).
+ *  - The library never allocates device memory: the caller passes one device
+ *    workspace of ghsvd_workspace_bytes() bytes to ghsvd_create() and keeps it
+ *    alive until ghsvd_destroy().  The library owns no caller buffer after a
+ *    call returns (inputs are copied into the workspace).
+ *  - Every call is enqueued on opts.stream and returns after the stream has
+ *    drained (the calls are synchronous w.r.t. the host).
+ *  - Status: 0 = OK, > 0 = warning (results valid), < 0 = error; after an
+ *    error ghsvd_last_error() describes it and the context stays usable for
+ *    ghsvd_destroy() (and for a new set_factors/factor).
+ *  - Call order: create -> (factor | set_factors) -> [reduce] -> [get_factors]
+ *    -> sweep -> extract -> destroy.  Out-of-order calls return GHSVD_E_STATE.
+ */
+#ifndef GHSVD_H
+#define GHSVD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ghsvd_ctx_s* ghsvd_ctx;
+
+typedef enum {
+  GHSVD_OK = 0,
+  GHSVD_NOT_CONVERGED = 1,     /* warning: C_max sweeps reached; results still extractable */
+  GHSVD_E_INVALID_ARG = -1,    /* null pointer, m < n, ld < rows, J entry not +-1, bad option */
+  GHSVD_E_STATE = -2,          /* call order violated */
+  GHSVD_E_CUDA = -3,           /* a CUDA runtime call failed (message in ghsvd_last_error) */
+  GHSVD_E_NCCL = -4,           /* NCCL unavailable or a collective failed */
+  GHSVD_E_WORKSPACE = -5,      /* workspace smaller than ghsvd_workspace_bytes() */
+  GHSVD_E_INDEFINITE_S = -6,   /* s_pp <= 0 or |s_pq| >= 1 after prescaling (G rank-deficient) */
+  GHSVD_E_RANK_DEFICIENT = -7, /* singular T_a / block pivot / degenerate JQR pivot */
+  GHSVD_E_NONFINITE = -8       /* NaN/Inf met in a Gram or a transformation */
+} ghsvd_status;
+
+enum { GHSVD_POINTWISE = 0, GHSVD_BLOCKED_BO = 1, GHSVD_BLOCKED_FB = 2 };
+enum { GHSVD_ORDER_ROUND_ROBIN = 0 };
+/* Transformation criterion, eq (6.12) PAPER.md:1552-1562.  RELATIVE (default):
+ * |H_pq| >= eps sqrt(n) |H_pp|^(1/2) |H_qq|^(1/2) or |S_pq| >= eps sqrt(n) on the
+ * prescaled pivot; LITERAL: |H_pq| >= (max|H_ii| eps sqrt(n)) min|H_ii| as printed. */
+enum { GHSVD_CRIT_RELATIVE = 0, GHSVD_CRIT_LITERAL = 1 };
+
+typedef struct {
+  int device;          /* CUDA ordinal of this rank's GPU */
+  void* stream;        /* cudaStream_t owned by the caller (e.g. a torch stream); NULL = legacy default */
+  int world_size;      /* 1 for a single GPU */
+  int rank;            /* 0 .. world_size-1 */
+  const void* nccl_id; /* 128-byte ncclUniqueId shared by all ranks; NULL if world_size == 1 */
+  int variant;         /* GHSVD_POINTWISE | GHSVD_BLOCKED_BO | GHSVD_BLOCKED_FB */
+  int ordering;        /* GHSVD_ORDER_ROUND_ROBIN */
+  int nblocks;         /* blocked: number of block columns (even; 0 = auto); Sec 6.4.1 */
+  int max_sweeps;      /* C_max, default 30 (Algorithm 2) */
+  int criterion;       /* GHSVD_CRIT_RELATIVE | GHSVD_CRIT_LITERAL */
+  double eps;          /* machine precision in (6.12); 0 => 2^-53 */
+  int cluster;         /* pointwise: CTAs per column pair (0 = auto; 1,2,4,8,16) */
+  int threads;         /* pointwise: threads per CTA (0 = auto) */
+  int use_graph;       /* capture each sweep's steps in a CUDA graph (default 1) */
+} ghsvd_options;
+
+typedef struct {
+  int sweeps;                 /* sweeps performed */
+  int converged;              /* 1: stopped because a sweep had no "big" transformation */
+  uint64_t pairs_visited;     /* sweeps * n(n-1)/2 */
+  uint64_t transforms_all;    /* transformations applied (small + big) */
+  uint64_t transforms_big;    /* "big" transformations (cos phi or cos psi != 1) */
+  double seconds;             /* device time of the sweep loop (CUDA events) */
+  double kernel_seconds;      /* device time of the sweep kernels alone (per-sweep events) */
+  uint64_t launches;          /* sweep-kernel launches issued (pointwise: sweeps * (n-1)) */
+  uint64_t alg_bytes;         /* algorithmic HBM bytes of the sweeps: per transformed pair
+                                 128m+64n, per skipped pair 64m */
+  double max_offdiag_last;    /* max scaled off-diagonal measure seen in the last sweep */
+  uint64_t all_per_sweep[64]; /* per-sweep counters (first 64 sweeps) */
+  uint64_t big_per_sweep[64];
+} ghsvd_stats;
+
+/* Fill *opts with the defaults described above (device 0, world_size 1). */
+void ghsvd_default_options(ghsvd_options* opts);
+
+/* Device workspace needed for factors with at most m rows and n columns
+ * (nl > 0: also room for ghsvd_factor with N_L = nl).  Returns 0 on bad args. */
+size_t ghsvd_workspace_bytes(const ghsvd_options* opts, int64_t m, int64_t n, int64_t nl);
+
+/* Create a context bound to opts->device/stream over a device workspace sized
+ * by ghsvd_workspace_bytes(opts, m, n, nl).  *out is set on success. */
+ghsvd_status ghsvd_create(const ghsvd_options* opts, int64_t m, int64_t n, int64_t nl,
+                          void* workspace, size_t bytes, ghsvd_ctx* out);
+
+/* Phase 1 (Algorithm 1; eqs 4.1-4.3):  per atom a,
+ * T_a = [[TAA_a, TAB_a], [TAB_a^*, TBB_a]] (lower triangle read) is factored by
+ * HEBPJ (Bunch-Parlett complete pivoting, Sec 4.2-4.3) into Mt_a^* Jt_a Mt_a,
+ * F_a = Mt_a [A_a; B_a] and G_a = [A_a; U_a B_a].  A, B: NA blocks of NL x NG
+ * (block a at offset a*NL*NG, ld NL); U: NA*NL reals; TAA, TAB, TBB: NA blocks
+ * of NL x NL (ld NL).  m = 2*NA*NL and n = NG must fit the context.  The rows of
+ * F are then stably sorted so that J = diag(I_{n+}, -I_{m-n+}) (Sec 4.5.1).
+ * Errors: GHSVD_E_RANK_DEFICIENT if some T_a is numerically singular. */
+ghsvd_status ghsvd_factor(ghsvd_ctx ctx, int64_t NA, int64_t NL, int64_t NG,
+                          const void* A, const void* B, const double* U,
+                          const void* TAA, const void* TAB, const void* TBB);
+
+/* Direct entry: F, G are m x n (ld >= m), J has m entries of +-1 (int8).
+ * F's rows are stably sorted by J (+ first); G is copied as is.  Odd n is
+ * bordered by one row and column (Sec 6.3.2).  Errors: INVALID_ARG. */
+ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* F, int64_t ldf,
+                               const int8_t* J, const void* G, int64_t ldg);
+
+/* Optional Phase 2 (Sec 5, eq 5.1): JQR of F with diagonal + partial pivoting,
+ * hyperbolic Householder reflectors and (J,I) URV 2x2 pivots; G prepermuted by
+ * P2 and reduced by Householder QR (R kept, diag real >= 0).  Afterwards
+ * m = n.  flags: reserved, pass 0. */
+ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
+
+/* Export the factors the sweep will start from (after factor/set_factors,
+ * the J row sort, [reduce] and bordering): *m, *n (bordered sizes); F, G
+ * (m x n, ld >= m) and J (m int8) if non-NULL; p2 (n int64, column j of the
+ * current factors is column p2[j] of the Phase-1/set_factors factors) if
+ * non-NULL.  Used so the CPU oracle runs on exactly the same bytes. */
+ghsvd_status ghsvd_get_factors(ghsvd_ctx ctx, int64_t* m, int64_t* n, void* F, int64_t ldf,
+                               int8_t* J, void* G, int64_t ldg, int64_t* p2);
+
+/* Phase 3: sweeps (Algorithm 2; Alg. 3 per step) until a
+ * sweep has no "big" transformation (Sec 6.1.7) or C_max sweeps.  Z' starts at
+ * I.  Returns GHSVD_OK or GHSVD_NOT_CONVERGED (warning) or an error; *out
+ * (may be NULL) receives counters and device time. */
+ghsvd_status ghsvd_sweep(ghsvd_ctx ctx, ghsvd_stats* out);
+
+/* Diagnostic: run only steps [s0, s0+ns) of the pointwise round-robin sweep
+ * on the current factors (Z' initialised to I on the first call after
+ * factor/set_factors).  *all / *big receive the transformations applied. */
+ghsvd_status ghsvd_run_steps(ghsvd_ctx ctx, int64_t s0, int64_t ns, uint64_t* all, uint64_t* big);
+
+/* Outputs of Sec 6.1.7 and eq (3.2): for each column i,
+ * lambda_i = (f_i^* J f_i) / (g_i^* g_i), sigma_f = Sigma'_F/Sigma,
+ * sigma_g = Sigma'_G/Sigma, Z = Z' Sigma^-1 with rows un-permuted by P2
+ * (Z~ = P2 Z); bordered column stripped.  Any output
+ * pointer may be NULL.  Z is n x n (ldz >= n).  col_ids (n int64) receives the
+ * global column index of each output column (identity on one GPU). */
+ghsvd_status ghsvd_extract(ghsvd_ctx ctx, double* lambda, double* sigma_f, double* sigma_g,
+                           void* Z, int64_t ldz, int64_t* col_ids);
+
+/* Copy the current transformed factors F', G' (m x n) to F, G (NULL = skip). */
+ghsvd_status ghsvd_get_transformed(ghsvd_ctx ctx, void* F, int64_t ldf, void* G, int64_t ldg,
+                                   void* Zp, int64_t ldz);
+
+/* Test hook: evaluate the device 2x2 transformation (Sec 6.1, eqs 6.1-6.12)
+ * on `count` pivots.  in: 8 doubles per pivot {hpp, hqq, hpq.re, hpq.im, spp,
+ * sqq, spq.re, spq.im}; out: 8 doubles per pivot (z11, z21, z12, z22 complex,
+ * Z' column-major); kind: int per pivot (0 skip, 1 identity, 2 small, 3 big,
+ * < 0 error).  All three are DEVICE pointers.  tol = eps*sqrt(n). */
+ghsvd_status ghsvd_hz2x2_batch(ghsvd_ctx ctx, int64_t count, const double* in, double tol,
+                               int criterion, double* out, int* kind);
+
+const char* ghsvd_last_error(ghsvd_ctx ctx);
+void ghsvd_destroy(ghsvd_ctx ctx);
+
+/* Library version string. */
+const char* ghsvd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GHSVD_H */

@@ -1,0 +1,468 @@
+// phase1.cu -- ghsvd_factor: Phase 1 (Algorithm 1; eqs 4.1-4.3).
+//
+// Per atom a (one CTA each, all atoms concurrently):
+//   T_a = [[T_AA, T_AB], [T_AB^*, T_BB]]  (eq 3.3; lower triangle read)
+//   HEBPJ (Sec 4.2-4.3): Bunch-Parlett complete pivoting LDL^*, alpha =
+//   (1+sqrt 17)/8; 2x2 pivots diagonalised by a Jacobi rotation; rows scaled
+//   by |d|^1/2; Mhat = M P; rows sorted + before -.
+// Then F_a = Mtilde_a [A_a; B_a] (the paper's ZGEMM, here an smem-tiled
+// in-place complex product per atom and column tile), G_a = [A_a; U_a B_a]
+// (ZDSCAL), and the rows of F are stably sorted by sign across atoms so the
+// sweep sees J = diag(I_{n+}, -I) (Sec 4.5.1 n+ representation).
+// Runs once per problem (boundary, not hot path).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace ghsvd {
+
+namespace {
+
+__device__ __forceinline__ double2 c_mk(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return c_mk(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return c_mk(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+  return c_mk(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 c_conj(double2 a) { return c_mk(a.x, -a.y); }
+__device__ __forceinline__ double2 c_scale(double2 a, double s) { return c_mk(__dmul_rn(a.x, s), __dmul_rn(a.y, s)); }
+__device__ __forceinline__ double c_abs(double2 a) { return __dsqrt_rn(__dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y))); }
+__device__ __forceinline__ double c_abs2(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+
+struct P1Scr {
+  double2* Taa;   // NA * NL*NL staging
+  double2* Tab;
+  double2* Tbb;
+  double* U;      // NA * NL
+  double2* W;     // NA * r*r working matrix (L stored below the diagonal)
+  double2* M;     // NA * r*r output Mtilde_a
+  double2* R;     // NA * r * 4 Jacobi rotations of 2x2 pivots
+  double* d;      // NA * r   pivot values / eigenvalues
+  int* bsz;       // NA * r   1, 2 (first of a pair), 0 (second of a pair)
+  int* perm;      // NA * r
+  int* npos;      // NA
+  int* info;      // NA  (0 ok, -7 rank deficient)
+};
+
+size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+P1Scr carve(char* base, int64_t NA, int64_t NL) {
+  const int64_t r = 2 * NL;
+  P1Scr s;
+  char* p = base;
+  s.Taa = (double2*)p; p += al256((size_t)NA * NL * NL * 16);
+  s.Tab = (double2*)p; p += al256((size_t)NA * NL * NL * 16);
+  s.Tbb = (double2*)p; p += al256((size_t)NA * NL * NL * 16);
+  s.U = (double*)p; p += al256((size_t)NA * NL * 8);
+  s.W = (double2*)p; p += al256((size_t)NA * r * r * 16);
+  s.M = (double2*)p; p += al256((size_t)NA * r * r * 16);
+  s.R = (double2*)p; p += al256((size_t)NA * r * 4 * 16);
+  s.d = (double*)p; p += al256((size_t)NA * r * 8);
+  s.bsz = (int*)p; p += al256((size_t)NA * r * 4);
+  s.perm = (int*)p; p += al256((size_t)NA * r * 4);
+  s.npos = (int*)p; p += al256((size_t)NA * 4);
+  s.info = (int*)p; p += al256((size_t)NA * 4);
+  return s;
+}
+
+size_t carve_bytes(int64_t NA, int64_t NL) {
+  const int64_t r = 2 * NL;
+  return 3 * al256((size_t)NA * NL * NL * 16) + al256((size_t)NA * NL * 8) + 2 * al256((size_t)NA * r * r * 16) +
+         al256((size_t)NA * r * 64) + al256((size_t)NA * r * 8) + 2 * al256((size_t)NA * r * 4) +
+         2 * al256((size_t)NA * 4) + 256;
+}
+
+constexpr int P1T = 256;
+
+// (value, index) argmax keeping the smallest index among equal maxima.
+__device__ __forceinline__ void amax_merge(double& v, long long& i, double v2, long long i2) {
+  if (v2 > v || (v2 == v && i2 < i)) {
+    v = v2;
+    i = i2;
+  }
+}
+
+__device__ void block_amax(double& v, long long& i, double* sv, long long* si) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    amax_merge(v, i, v2, i2);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[w] = v;
+    si[w] = i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < P1T / 32; k++) amax_merge(sv[0], si[0], sv[k], si[k]);
+  }
+  __syncthreads();
+  v = sv[0];
+  i = si[0];
+  __syncthreads();
+}
+
+// Jacobi rotation R (column-major R11, R21, R12, R22) with R^* E R = diag(l1, l2)
+__device__ void herm2_jacobi_dev(double a, double2 b, double c, double2* R, double* l1, double* l2) {
+  const double ab = c_abs(b);
+  if (ab == 0.0) {
+    R[0] = c_mk(1, 0); R[1] = c_mk(0, 0); R[2] = c_mk(0, 0); R[3] = c_mk(1, 0);
+    *l1 = a; *l2 = c;
+    return;
+  }
+  const double2 e = c_mk(__ddiv_rn(b.x, ab), __ddiv_rn(b.y, ab));
+  const double tau = __ddiv_rn(__dsub_rn(c, a), __dmul_rn(2.0, ab));
+  const double t = __ddiv_rn(tau >= 0.0 ? 1.0 : -1.0, __dadd_rn(fabs(tau), __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(tau, tau)))));
+  const double cs = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(t, t)))), sn = __dmul_rn(t, cs);
+  const double2 em = c_conj(e);
+  R[0] = c_mk(cs, 0.0);
+  R[1] = c_scale(em, -sn);
+  R[2] = c_mk(sn, 0.0);
+  R[3] = c_scale(em, cs);
+  *l1 = __dsub_rn(a, __dmul_rn(t, ab));
+  *l2 = __dadd_rn(c, __dmul_rn(t, ab));
+}
+
+// Build W_a (full Hermitian from the lower triangle of T_a) and the tolerance.
+__global__ void __launch_bounds__(P1T) k_build_T(P1Scr s, int NL) {
+  const int a = blockIdx.x, r = 2 * NL;
+  const double2* taa = s.Taa + (size_t)a * NL * NL;
+  const double2* tab = s.Tab + (size_t)a * NL * NL;
+  const double2* tbb = s.Tbb + (size_t)a * NL * NL;
+  double2* W = s.W + (size_t)a * r * r;
+  for (int e = threadIdx.x; e < r * r; e += P1T) {
+    const int i = e % r, j = e / r;
+    const int ii = i >= j ? i : j, jj = i >= j ? j : i;  // lower-triangle source (ii >= jj)
+    double2 v;
+    if (ii < NL) v = taa[ii + (size_t)jj * NL];
+    else if (jj >= NL) v = tbb[(ii - NL) + (size_t)(jj - NL) * NL];
+    else v = c_conj(tab[jj + (size_t)(ii - NL) * NL]);  // T_BA = T_AB^*
+    if (ii == jj) v.y = 0.0;
+    W[i + (size_t)j * r] = (i >= j) ? v : c_conj(v);
+  }
+}
+
+// HEBPJ of one T_a per CTA (in global memory, L2-resident).
+__global__ void __launch_bounds__(P1T) k_hebpj(P1Scr s, int NL) {
+  const int a = blockIdx.x, r = 2 * NL;
+  double2* W = s.W + (size_t)a * r * r;
+  double2* M = s.M + (size_t)a * r * r;
+  double2* Ra = s.R + (size_t)a * r * 4;
+  double* d = s.d + (size_t)a * r;
+  int* bsz = s.bsz + (size_t)a * r;
+  int* perm = s.perm + (size_t)a * r;
+  __shared__ double sv[P1T / 32];
+  __shared__ long long si[P1T / 32];
+  __shared__ double2 colk[2][256 * 2];   // saved pivot columns / L values (r <= 512)
+  __shared__ int sh_two, sh_err;
+  __shared__ double sh_tolz;
+  const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+  const double eps = 0x1p-53;
+  for (int i = threadIdx.x; i < r; i += P1T) perm[i] = i;
+  __syncthreads();
+  // tolerance r * eps * max|T| over the lower triangle
+  double tv = 0.0;
+  long long ti = 0;
+  for (int e = threadIdx.x; e < r * r; e += P1T) {
+    const int i = e % r, j = e / r;
+    if (i >= j) amax_merge(tv, ti, c_abs(W[i + (size_t)j * r]), 0);
+  }
+  block_amax(tv, ti, sv, si);
+  if (threadIdx.x == 0) {
+    sh_tolz = __dmul_rn(__dmul_rn((double)r, eps), tv);
+    sh_err = 0;
+  }
+  __syncthreads();
+  int k = 0;
+  while (k < r) {
+    // complete pivoting search
+    double mu1 = -1.0;
+    long long id = 0x7fffffffffffffffll;
+    for (int i = k + threadIdx.x; i < r; i += P1T) amax_merge(mu1, id, fabs(W[i + (size_t)i * r].x), i);
+    block_amax(mu1, id, sv, si);
+    double mu0 = 0.0;
+    long long oidx = 0x7fffffffffffffffll;
+    const long long rem = r - k;
+    for (long long e = threadIdx.x; e < rem * rem; e += P1T) {
+      const int j = k + (int)(e / rem), i = k + (int)(e % rem);
+      if (i > j) amax_merge(mu0, oidx, c_abs(W[i + (size_t)j * r]), (long long)j * r + i);
+    }
+    block_amax(mu0, oidx, sv, si);
+    const double mall = mu0 > mu1 ? mu0 : mu1;
+    if (!(mall > sh_tolz)) {
+      if (threadIdx.x == 0) sh_err = -7;
+      break;
+    }
+    const int two = !(mu1 >= __dmul_rn(alpha, mu0));
+    int src0 = (int)id, src1 = -1;
+    if (two) {
+      src0 = (int)(oidx / r);
+      src1 = (int)(oidx % r);
+    }
+    for (int b = 0; b < (two ? 2 : 1); b++) {
+      const int dst = k + b;
+      int sidx = b == 0 ? src0 : src1;
+      if (b == 1 && sidx == k) sidx = src0;
+      if (sidx != dst) {
+        // swap rows dst, sidx over all columns (rows of L for c < k live below the diagonal)
+        for (int c = threadIdx.x; c < r; c += P1T) {
+          const double2 t = W[dst + (size_t)c * r];
+          W[dst + (size_t)c * r] = W[sidx + (size_t)c * r];
+          W[sidx + (size_t)c * r] = t;
+        }
+        __syncthreads();
+        // swap columns dst, sidx over rows >= k (the live trailing block)
+        for (int i = k + threadIdx.x; i < r; i += P1T) {
+          const double2 t = W[i + (size_t)dst * r];
+          W[i + (size_t)dst * r] = W[i + (size_t)sidx * r];
+          W[i + (size_t)sidx * r] = t;
+        }
+        if (threadIdx.x == 0) {
+          const int t = perm[dst];
+          perm[dst] = perm[sidx];
+          perm[sidx] = t;
+        }
+        __syncthreads();
+      }
+    }
+    if (!two) {
+      const double dk = W[k + (size_t)k * r].x;
+      const double inv = __ddiv_rn(1.0, dk);
+      for (int i = k + 1 + threadIdx.x; i < r; i += P1T) colk[0][i] = W[i + (size_t)k * r];
+      __syncthreads();
+      const long long rm = r - k - 1;
+      for (long long e = threadIdx.x; e < rm * rm; e += P1T) {
+        const int i = k + 1 + (int)(e % rm), j = k + 1 + (int)(e / rm);
+        W[i + (size_t)j * r] = c_sub(W[i + (size_t)j * r], c_scale(c_mul(colk[0][i], c_conj(colk[0][j])), inv));
+      }
+      __syncthreads();
+      for (int i = k + 1 + threadIdx.x; i < r; i += P1T) W[i + (size_t)k * r] = c_scale(colk[0][i], inv);
+      if (threadIdx.x == 0) {
+        bsz[k] = 1;
+        d[k] = dk;
+      }
+      __syncthreads();
+      k += 1;
+    } else {
+      const double ea = W[k + (size_t)k * r].x, ec = W[(k + 1) + (size_t)(k + 1) * r].x;
+      const double2 eb = W[k + (size_t)(k + 1) * r];
+      const double det = __dsub_rn(__dmul_rn(ea, ec), c_abs2(eb));
+      const double inv = __ddiv_rn(1.0, det);
+      for (int i = k + 2 + threadIdx.x; i < r; i += P1T) {
+        const double2 w0 = W[i + (size_t)k * r], w1 = W[i + (size_t)(k + 1) * r];
+        colk[0][i] = w0;
+        colk[1][i] = w1;
+        const double2 l0 = c_scale(c_sub(c_scale(w0, ec), c_mul(w1, c_conj(eb))), inv);
+        const double2 l1 = c_scale(c_sub(c_scale(w1, ea), c_mul(w0, eb)), inv);
+        W[i + (size_t)k * r] = l0;   // L stored in place (the update reads colk)
+        W[i + (size_t)(k + 1) * r] = l1;
+      }
+      __syncthreads();
+      const long long rm = r - k - 2;
+      for (long long e = threadIdx.x; e < rm * rm; e += P1T) {
+        const int i = k + 2 + (int)(e % rm), j = k + 2 + (int)(e / rm);
+        const double2 t = c_add(c_mul(W[i + (size_t)k * r], c_conj(colk[0][j])),
+                                c_mul(W[i + (size_t)(k + 1) * r], c_conj(colk[1][j])));
+        W[i + (size_t)j * r] = c_sub(W[i + (size_t)j * r], t);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double l1, l2;
+        herm2_jacobi_dev(ea, eb, ec, &Ra[4 * k], &l1, &l2);
+        d[k] = l1;
+        d[k + 1] = l2;
+        bsz[k] = 2;
+        bsz[k + 1] = 0;
+      }
+      __syncthreads();
+      k += 2;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s.info[a] = sh_err;
+  if (sh_err) return;
+  // signs and sorted row positions (+ first, stable)
+  __shared__ int rowpos[512];
+  __shared__ signed char sgn[512];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < r; i++) sgn[i] = d[i] > 0.0 ? 1 : -1;
+    int np = 0;
+    for (int i = 0; i < r; i++)
+      if (sgn[i] > 0) rowpos[i] = np++;
+    int q = np;
+    for (int i = 0; i < r; i++)
+      if (sgn[i] < 0) rowpos[i] = q++;
+    s.npos[a] = np;
+  }
+  __syncthreads();
+  // Mtilde(rowpos(i), perm[l]) = row i of diag(|d|^1/2) R^* L^*, column l
+  for (int e = threadIdx.x; e < r * r; e += P1T) {
+    const int i = e % r, l = e / r;
+    auto Lh = [&](int row, int col) -> double2 {  // (L^*)(row, col) = conj(L(col, row))
+      if (row == col) return c_mk(1.0, 0.0);
+      if (col < row) return c_mk(0.0, 0.0);
+      return c_conj(W[col + (size_t)row * r]);
+    };
+    double2 y;
+    if (bsz[i] == 1) {
+      y = c_scale(Lh(i, l), __dsqrt_rn(fabs(d[i])));
+    } else if (bsz[i] == 2) {
+      const double2* R = &Ra[4 * i];
+      const double2 x0 = Lh(i, l), x1 = Lh(i + 1, l);
+      y = c_scale(c_add(c_mul(c_conj(R[0]), x0), c_mul(c_conj(R[1]), x1)), __dsqrt_rn(fabs(d[i])));
+    } else {
+      const double2* R = &Ra[4 * (i - 1)];
+      const double2 x0 = Lh(i - 1, l), x1 = Lh(i, l);
+      y = c_scale(c_add(c_mul(c_conj(R[2]), x0), c_mul(c_conj(R[3]), x1)), __dsqrt_rn(fabs(d[i])));
+    }
+    M[rowpos[i] + (size_t)perm[l] * r] = y;
+  }
+}
+
+// F rows of atom a (H~_a = [A_a; B_a], r x NG at row offset a*r) <- Mtilde_a H~_a, in place.
+constexpr int AM_TC = 8;  // columns per tile
+__global__ void __launch_bounds__(256) k_apply_M(P1Scr s, double2* F, long long ldm, int NL, long long NG) {
+  extern __shared__ double2 tile[];  // r x AM_TC
+  const int a = blockIdx.y, r = 2 * NL;
+  const long long c0 = (long long)blockIdx.x * AM_TC;
+  const int nc = (int)min((long long)AM_TC, NG - c0);
+  double2* Fa = F + (size_t)a * r;
+  for (int e = threadIdx.x; e < r * nc; e += 256) {
+    const int i = e % r, c = e / r;
+    tile[i + c * r] = Fa[i + (c0 + c) * ldm];
+  }
+  __syncthreads();
+  const double2* M = s.M + (size_t)a * r * r;
+  for (int e = threadIdx.x; e < r * nc; e += 256) {
+    const int i = e % r, c = e / r;
+    double re = 0.0, im = 0.0;
+    for (int l = 0; l < r; l++) {
+      const double2 mv = M[i + (size_t)l * r], hv = tile[l + c * r];
+      re = fma(mv.x, hv.x, fma(-mv.y, hv.y, re));
+      im = fma(mv.x, hv.y, fma(mv.y, hv.x, im));
+    }
+    Fa[i + (c0 + c) * ldm] = make_double2(re, im);
+  }
+}
+
+// Row destinations for the global sign sort and the sorted J.
+__global__ void k_p1_dest(P1Scr s, int NA, int NL, int* dest, int8_t* J, long long* npos_out) {
+  const int r = 2 * NL;
+  __shared__ long long P[1025], Nn[1025];
+  if (threadIdx.x == 0) {
+    long long p = 0, q = 0;
+    for (int a = 0; a < NA; a++) {
+      P[a] = p;
+      Nn[a] = q;
+      p += s.npos[a];
+      q += r - s.npos[a];
+    }
+    P[NA] = p;
+    *npos_out = p;
+  }
+  __syncthreads();
+  const long long np = P[NA];
+  for (long long g = threadIdx.x; g < (long long)NA * r; g += blockDim.x) {
+    const int a = (int)(g / r), i = (int)(g % r);
+    const int npa = s.npos[a];
+    const long long dd = i < npa ? P[a] + i : np + Nn[a] + (i - npa);
+    dest[g] = (int)dd;
+    J[dd] = i < npa ? 1 : -1;
+  }
+}
+
+__global__ void k_scale_UB(double2* G, long long ldm, const double* U, int NA, int NL, long long NG) {
+  const long long c = blockIdx.y;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)NA * NL;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int a = (int)(e / NL), l = (int)(e % NL);
+    double2* x = G + c * ldm + (size_t)a * 2 * NL + NL + l;
+    const double u = U[e];
+    *x = make_double2(x->x * u, x->y * u);
+  }
+}
+
+}  // namespace
+
+size_t phase1_scratch_bytes(int64_t m, int64_t n, int64_t nl) {
+  if (nl <= 0) return 0;
+  const int64_t NA = std::max<int64_t>(1, m / (2 * nl));
+  return carve_bytes(NA, nl) + 2 * 256;
+}
+
+ghsvd_status phase1_factor(Ctx* ctx, int64_t NA, int64_t NL, int64_t NG, const void* A, const void* B,
+                           const double* U, const void* TAA, const void* TAB, const void* TBB) {
+  const int64_t r = 2 * NL, m = NA * r;
+  if (r > 512 || NA > 1024) {
+    ctx->err = "factor: 2*NL must be <= 512 and NA <= 1024";
+    return GHSVD_E_INVALID_ARG;
+  }
+  if (carve_bytes(NA, NL) + 256 > ctx->L.scr_bytes) {
+    ctx->err = "factor: workspace scratch too small (create with nl >= NL)";
+    return GHSVD_E_WORKSPACE;
+  }
+  cudaStream_t st = ctx->stream;
+  P1Scr s = carve(ctx->scr, NA, NL);
+  long long* npos_dev = (long long*)((char*)s.info + al256((size_t)NA * 4));
+  // 1. stage inputs: [A_a; B_a] into the F buffer; T blocks and U into scratch
+  for (int64_t a = 0; a < NA; a++) {
+    GH_CUDA(cudaMemcpy2DAsync(ctx->F + a * r, (size_t)ctx->ldm * 16, (const double2*)A + a * NL * NG,
+                              (size_t)NL * 16, (size_t)NL * 16, (size_t)NG, cudaMemcpyDefault, st));
+    GH_CUDA(cudaMemcpy2DAsync(ctx->F + a * r + NL, (size_t)ctx->ldm * 16, (const double2*)B + a * NL * NG,
+                              (size_t)NL * 16, (size_t)NL * 16, (size_t)NG, cudaMemcpyDefault, st));
+  }
+  GH_CUDA(cudaMemcpyAsync(s.Taa, TAA, (size_t)NA * NL * NL * 16, cudaMemcpyDefault, st));
+  GH_CUDA(cudaMemcpyAsync(s.Tab, TAB, (size_t)NA * NL * NL * 16, cudaMemcpyDefault, st));
+  GH_CUDA(cudaMemcpyAsync(s.Tbb, TBB, (size_t)NA * NL * NL * 16, cudaMemcpyDefault, st));
+  GH_CUDA(cudaMemcpyAsync(s.U, U, (size_t)NA * NL * 8, cudaMemcpyDefault, st));
+  // 2. HEBPJ per atom
+  k_build_T<<<(unsigned)NA, P1T, 0, st>>>(s, (int)NL);
+  GH_CUDA(cudaGetLastError());
+  k_hebpj<<<(unsigned)NA, P1T, 0, st>>>(s, (int)NL);
+  GH_CUDA(cudaGetLastError());
+  std::vector<int> info((size_t)NA);
+  GH_CUDA(cudaMemcpyAsync(info.data(), s.info, (size_t)NA * 4, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  for (int64_t a = 0; a < NA; a++)
+    if (info[a]) {
+      ctx->err = "factor: T_a numerically singular (atom " + std::to_string(a) + ")";
+      return GHSVD_E_RANK_DEFICIENT;
+    }
+  // 3. F_a = Mtilde_a [A_a; B_a] in place
+  const size_t smem = (size_t)r * AM_TC * 16;
+  GH_CUDA(cudaFuncSetAttribute(k_apply_M, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 g3((unsigned)((NG + AM_TC - 1) / AM_TC), (unsigned)NA);
+  k_apply_M<<<g3, 256, smem, st>>>(s, ctx->F, ctx->ldm, (int)NL, NG);
+  GH_CUDA(cudaGetLastError());
+  // 4. global sign sort of F's rows: F buffer -> G buffer, then swap roles
+  k_p1_dest<<<1, 256, 0, st>>>(s, (int)NA, (int)NL, ctx->rowdest, ctx->J, npos_dev);
+  GH_CUDA(cudaGetLastError());
+  {
+    ghsvd_status e = launch_row_scatter(ctx, ctx->F, ctx->ldm, ctx->G, ctx->ldm, ctx->rowdest, m, NG);
+    if (e) return e;
+  }
+  std::swap(ctx->F, ctx->G);
+  // 5. G = [A_a; U_a B_a]
+  GH_CUDA(cudaMemsetAsync(ctx->G, 0, (size_t)ctx->ldm * (ctx->n_cap + 1) * 16, st));
+  for (int64_t a = 0; a < NA; a++) {
+    GH_CUDA(cudaMemcpy2DAsync(ctx->G + a * r, (size_t)ctx->ldm * 16, (const double2*)A + a * NL * NG,
+                              (size_t)NL * 16, (size_t)NL * 16, (size_t)NG, cudaMemcpyDefault, st));
+    GH_CUDA(cudaMemcpy2DAsync(ctx->G + a * r + NL, (size_t)ctx->ldm * 16, (const double2*)B + a * NL * NG,
+                              (size_t)NL * 16, (size_t)NL * 16, (size_t)NG, cudaMemcpyDefault, st));
+  }
+  dim3 g5((unsigned)std::min<int64_t>((NA * NL + 255) / 256, 64), (unsigned)NG);
+  k_scale_UB<<<g5, 256, 0, st>>>(ctx->G, ctx->ldm, s.U, (int)NA, (int)NL, NG);
+  GH_CUDA(cudaGetLastError());
+  long long npos = 0;
+  GH_CUDA(cudaMemcpyAsync(&npos, npos_dev, 8, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  ctx->npos = npos;
+  return GHSVD_OK;
+}
+
+}  // namespace ghsvd

@@ -1,0 +1,398 @@
+// pointwise.cu -- fused pointwise HZ step on sm_100a.
+//
+// One parallel step S_s of the round-robin ordering (Sec 6.3, Alg. 3
+// PAPER.md:1758-1814) is ONE launch: n/2 thread-block clusters, one per pivot
+// pair (p, q).  The C CTAs of a cluster split the m rows of the pair's four
+// columns f_p, f_q, g_p, g_q into contiguous slices; each CTA
+//   1. stages its slices in shared memory with TMA bulk copies
+//      (cp.async.bulk global->shared, mbarrier completion) -- one HBM read,
+//   2. forms its partial Grams (eq 6.1; J = diag(I_npos, -I) from the row sort),
+//      reduces them warp -> CTA, then across the cluster through DSMEM in fixed
+//      rank order (deterministic, identical in every CTA),
+//   3. computes the 2x2 transformation Z' (hz2x2.cuh, eqs 6.2-6.12) redundantly
+//      per CTA (bitwise identical inputs -> identical Z'),
+//   4. if Z' is applied: updates the slices in shared memory and writes them back
+//      with TMA bulk stores (one HBM write), then loads/updates/stores its slice
+//      of z'_p, z'_q (n rows) the same way ("two ZVROTMs of length m and one of
+//      length n").
+// Counters (all, big, max off-measure) are device atomics read once per sweep
+// (a5).  Per transformed pair the kernel moves the algorithmic minimum
+// 128 m + 64 n bytes (read + write F, G pair columns once; Z pair read + write),
+// per skipped pair 64 m bytes.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "hz2x2.cuh"
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace ghsvd {
+
+struct StepArgs {
+  double2* F;
+  double2* G;
+  double2* Z;
+  long long ldm, ldn;
+  long long m, n;
+  long long npos;
+  long long s;
+  long long cs;   // F/G rows per CTA slice
+  long long zs;   // Z rows per CTA slice
+  double tol;
+  int literal;
+  DevCounters* cnt;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// [a b] <- [a b] Z' for one row: a' = a z11 + b z21, b' = a z12 + b z22
+__device__ __forceinline__ void rot_row(double2& a, double2& b, const Cplx& z11, const Cplx& z21,
+                                        const Cplx& z12, const Cplx& z22) {
+  const double2 x = a, y = b;
+  a.x = fma(x.x, z11.re, fma(-x.y, z11.im, fma(y.x, z21.re, -y.y * z21.im)));
+  a.y = fma(x.x, z11.im, fma(x.y, z11.re, fma(y.x, z21.im, y.y * z21.re)));
+  b.x = fma(x.x, z12.re, fma(-x.y, z12.im, fma(y.x, z22.re, -y.y * z22.im)));
+  b.y = fma(x.x, z12.im, fma(x.y, z12.re, fma(y.x, z22.im, y.y * z22.re)));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_pair_step(StepArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ double red[NT / 32][8];
+  __shared__ double part[8];
+  __shared__ double tot[8];
+  __shared__ double zsh[8];
+  __shared__ int kind_sh;
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const long long pair = blockIdx.x / C;
+  long long p, q;
+  rr_pair(a.n, a.s, pair, &p, &q);
+
+  const long long r0 = (long long)rank * a.cs;
+  const long long r1 = min(a.m, r0 + a.cs);
+  const long long len = r1 > r0 ? r1 - r0 : 0;
+  const long long z0 = (long long)rank * a.zs;
+  const long long z1 = min(a.n, z0 + a.zs);
+  const long long zlen = z1 > z0 ? z1 - z0 : 0;
+
+  double2* sFp = reinterpret_cast<double2*>(smem_raw);
+  double2* sFq = sFp + a.cs;
+  double2* sGp = sFq + a.cs;
+  double2* sGq = sGp + a.cs;
+  double2* sZp = sGq + a.cs;
+  double2* sZq = sZp + a.zs;
+
+  double2* gFp = a.F + p * a.ldm + r0;
+  double2* gFq = a.F + q * a.ldm + r0;
+  double2* gGp = a.G + p * a.ldm + r0;
+  double2* gGq = a.G + q * a.ldm + r0;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned bytes = (unsigned)(len * 16);
+    mbar_expect_tx(&bar[0], 4u * bytes);
+    if (len > 0) {
+      bulk_g2s(sFp, gFp, bytes, &bar[0]);
+      bulk_g2s(sFq, gFq, bytes, &bar[0]);
+      bulk_g2s(sGp, gGp, bytes, &bar[0]);
+      bulk_g2s(sGq, gGq, bytes, &bar[0]);
+    }
+  }
+  mbar_wait(&bar[0], 0);
+
+  // ---- (6.1): partial Grams over this slice (fixed per-thread row order)
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long npos_loc = a.npos - r0;  // rows i < npos_loc have J = +1
+  for (long long i = tid; i < len; i += NT) {
+    const double2 fp = sFp[i], fq = sFq[i], gp = sGp[i], gq = sGq[i];
+    const double sgn = (i < npos_loc) ? 1.0 : -1.0;
+    acc[0] = fma(sgn, fma(fp.x, fp.x, fp.y * fp.y), acc[0]);
+    acc[1] = fma(sgn, fma(fq.x, fq.x, fq.y * fq.y), acc[1]);
+    acc[2] = fma(sgn, fma(fp.x, fq.x, fp.y * fq.y), acc[2]);   // Re conj(fp) fq
+    acc[3] = fma(sgn, fma(fp.x, fq.y, -fp.y * fq.x), acc[3]);  // Im conj(fp) fq
+    acc[4] = fma(gp.x, gp.x, fma(gp.y, gp.y, acc[4]));
+    acc[5] = fma(gq.x, gq.x, fma(gq.y, gq.y, acc[5]));
+    acc[6] = fma(gp.x, gq.x, fma(gp.y, gq.y, acc[6]));
+    acc[7] = fma(gp.x, gq.y, fma(-gp.y, gq.x, acc[7]));
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) red[warp][k] = acc[k];
+  }
+  __syncthreads();
+  if (tid < 8) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; w++) s += red[w][tid];
+    part[tid] = s;
+  }
+  // ---- cluster reduction through DSMEM, fixed rank order
+  if (C > 1) {
+    cluster.sync();
+    if (tid < 8) {
+      double s = 0.0;
+      for (int r = 0; r < C; r++) s += *cluster.map_shared_rank(&part[tid], r);
+      tot[tid] = s;
+    }
+    cluster_arrive_relaxed();  // remote reads done; waited on before exit
+  } else {
+    __syncthreads();
+    if (tid < 8) tot[tid] = part[tid];
+  }
+  __syncthreads();
+  // ---- (6.2)-(6.12): the 2x2 transformation
+  if (tid == 0) {
+    const HZOut z = hz2x2_dev(tot, a.tol, a.literal);
+    zsh[0] = z.z11.re; zsh[1] = z.z11.im; zsh[2] = z.z21.re; zsh[3] = z.z21.im;
+    zsh[4] = z.z12.re; zsh[5] = z.z12.im; zsh[6] = z.z22.re; zsh[7] = z.z22.im;
+    kind_sh = z.kind;
+    if (rank == 0) {
+      if (z.kind < 0) atomicCAS(&a.cnt->err, 0, z.kind);
+      if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
+        atomicAdd(&a.cnt->all, 1ull);
+        if (z.kind == KIND_BIG) atomicAdd(&a.cnt->big, 1ull);
+      }
+      atomicMax(&a.cnt->off_bits, (unsigned long long)__double_as_longlong(z.off));
+    }
+  }
+  __syncthreads();
+  const int kind = kind_sh;
+  if (kind == KIND_SMALL || kind == KIND_BIG) {
+    const Cplx z11{zsh[0], zsh[1]}, z21{zsh[2], zsh[3]}, z12{zsh[4], zsh[5]}, z22{zsh[6], zsh[7]};
+    if (tid == 0) {
+      const unsigned zb = (unsigned)(zlen * 16);
+      mbar_expect_tx(&bar[1], 2u * zb);
+      if (zlen > 0) {
+        bulk_g2s(sZp, a.Z + p * a.ldn + z0, zb, &bar[1]);
+        bulk_g2s(sZq, a.Z + q * a.ldn + z0, zb, &bar[1]);
+      }
+    }
+    for (long long i = tid; i < len; i += NT) {
+      double2 fp = sFp[i], fq = sFq[i], gp = sGp[i], gq = sGq[i];
+      rot_row(fp, fq, z11, z21, z12, z22);
+      rot_row(gp, gq, z11, z21, z12, z22);
+      sFp[i] = fp; sFq[i] = fq; sGp[i] = gp; sGq[i] = gq;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0 && len > 0) {
+      const unsigned bytes = (unsigned)(len * 16);
+      bulk_s2g(gFp, sFp, bytes);
+      bulk_s2g(gFq, sFq, bytes);
+      bulk_s2g(gGp, sGp, bytes);
+      bulk_s2g(gGq, sGq, bytes);
+      bulk_commit();
+    }
+    mbar_wait(&bar[1], 0);
+    for (long long i = tid; i < zlen; i += NT) {
+      double2 zp = sZp[i], zq = sZq[i];
+      rot_row(zp, zq, z11, z21, z12, z22);
+      sZp[i] = zp; sZq[i] = zq;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      if (zlen > 0) {
+        const unsigned zb = (unsigned)(zlen * 16);
+        bulk_s2g(a.Z + p * a.ldn + z0, sZp, zb);
+        bulk_s2g(a.Z + q * a.ldn + z0, sZq, zb);
+        bulk_commit();
+      }
+      bulk_wait_all();
+    }
+  }
+  if (C > 1) cluster_wait();
+}
+
+// ------------------------------------------------------------------ host side
+typedef void (*StepKernel)(StepArgs);
+
+static StepKernel pick_kernel(int threads) {
+  switch (threads) {
+    case 32: return k_pair_step<32>;
+    case 64: return k_pair_step<64>;
+    case 128: return k_pair_step<128>;
+    case 512: return k_pair_step<512>;
+    default: return k_pair_step<256>;
+  }
+}
+
+ghsvd_status pw_configure(Ctx* ctx) {
+  const int64_t m = ctx->m, n = ctx->n;
+  int C = ctx->o.cluster;
+  if (C <= 0) {
+    // smallest power-of-two cluster whose per-CTA slices fit ~100 KB of smem
+    C = 1;
+    while (C < 16) {
+      const int64_t cs = (m + C - 1) / C, zs = (n + C - 1) / C;
+      if ((4 * cs + 2 * zs) * 16 <= 100 * 1024) break;
+      C *= 2;
+    }
+  }
+  if (C != 1 && C != 2 && C != 4 && C != 8 && C != 16) {
+    ctx->err = "cluster must be 1, 2, 4, 8 or 16";
+    return GHSVD_E_INVALID_ARG;
+  }
+  const int64_t cs = (m + C - 1) / C, zs = (n + C - 1) / C;
+  int T = ctx->o.threads;
+  if (T <= 0) {
+    T = 256;
+    while (T > 32 && T / 2 >= cs) T /= 2;
+  }
+  if (T != 32 && T != 64 && T != 128 && T != 256 && T != 512) {
+    ctx->err = "threads must be 32, 64, 128, 256 or 512";
+    return GHSVD_E_INVALID_ARG;
+  }
+  const size_t smem = (size_t)(4 * cs + 2 * zs) * 16;
+  if (smem > 220 * 1024) {
+    ctx->err = "pointwise slices exceed shared memory; use a larger cluster";
+    return GHSVD_E_INVALID_ARG;
+  }
+  StepKernel k = pick_kernel(T);
+  GH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (C > 8) GH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  ctx->pw_cluster = C;
+  ctx->pw_threads = T;
+  ctx->pw_smem = smem;
+  return GHSVD_OK;
+}
+
+static ghsvd_status launch_step(Ctx* ctx, cudaStream_t st, int64_t s) {
+  StepArgs a;
+  a.F = ctx->F;
+  a.G = ctx->G;
+  a.Z = ctx->Z;
+  a.ldm = ctx->ldm;
+  a.ldn = ctx->ldn;
+  a.m = ctx->m;
+  a.n = ctx->n;
+  a.npos = ctx->npos;
+  a.s = s;
+  const int C = ctx->pw_cluster;
+  a.cs = (ctx->m + C - 1) / C;
+  a.zs = (ctx->n + C - 1) / C;
+  a.tol = (ctx->o.eps > 0 ? ctx->o.eps : 0x1p-53) * sqrt((double)ctx->n);
+  a.literal = ctx->o.criterion == GHSVD_CRIT_LITERAL;
+  a.cnt = ctx->cnt;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ctx->n / 2 * C), 1, 1);
+  cfg.blockDim = dim3(ctx->pw_threads, 1, 1);
+  cfg.dynamicSmemBytes = ctx->pw_smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GH_CUDA(cudaLaunchKernelEx(&cfg, pick_kernel(ctx->pw_threads), a));
+  return GHSVD_OK;
+}
+
+ghsvd_status pw_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
+  for (int64_t s = s0; s < s0 + ns; s++) {
+    ghsvd_status e = launch_step(ctx, ctx->stream, s);
+    if (e) return e;
+  }
+  return GHSVD_OK;
+}
+
+// Enqueue one full sweep (n-1 steps).  With use_graph the launches are
+// captured once per (buffers, shape, config) and replayed as a CUDA graph.
+ghsvd_status pw_sweep_launch(Ctx* ctx) {
+  if (!ctx->o.use_graph) return pw_run_steps(ctx, 0, ctx->n - 1);
+  const int64_t key = (int64_t)(uintptr_t)ctx->F ^ ((int64_t)ctx->n << 40) ^
+                      ((int64_t)ctx->pw_cluster << 56) ^ ((int64_t)ctx->pw_threads << 48) ^
+                      ctx->npos * 1315423911ll ^ ctx->m * 2654435761ll;
+  if (!ctx->graph || ctx->graph_key != key) {
+    if (ctx->graph) {
+      cudaGraphExecDestroy(ctx->graph);
+      ctx->graph = nullptr;
+    }
+    cudaGraph_t g;
+    GH_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    for (int64_t s = 0; s < ctx->n - 1; s++) {
+      ghsvd_status e = launch_step(ctx, ctx->cap_stream, s);
+      if (e) {
+        cudaStreamEndCapture(ctx->cap_stream, &g);
+        return e;
+      }
+    }
+    GH_CUDA(cudaStreamEndCapture(ctx->cap_stream, &g));
+    GH_CUDA(cudaGraphInstantiate(&ctx->graph, g, 0));
+    cudaGraphDestroy(g);
+    ctx->graph_key = key;
+  }
+  GH_CUDA(cudaGraphLaunch(ctx->graph, ctx->stream));
+  return GHSVD_OK;
+}
+
+}  // namespace ghsvd

@@ -1,0 +1,194 @@
+"""GPU parity of the pointwise sweep engine against the CPU oracle (through the C ABI).
+
+Tolerances: the device 2x2 routine is bitwise equal
+to the oracle's (same IEEE op sequence, C-8); single steps agree to ~1e-13 relative
+(reduction order differs); converged eigenvalues agree to 1e-9 relative on
+well-conditioned S and 1e-6 on ill-conditioned S (BASELINE north_star); sweep counts
+within +-1 (parity unpinned); residual <= 1e-12 n.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1907_08560_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+EPS = oracle.EPS
+
+
+@pytest.fixture(scope="module")
+def gh():
+    from paper_1907_08560_b200 import build, ghsvd
+    build.build()
+    return ghsvd
+
+
+def relerr(a, b):
+    a = np.sort(np.asarray(a))
+    b = np.sort(np.asarray(b))
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+def residual(F, J, G, lam, Z):
+    nf2 = np.linalg.norm(F) ** 2 + np.linalg.norm(G) ** 2
+    Hx = F.conj().T @ (J[:, None] * (F @ Z))
+    Sx = G.conj().T @ (G @ Z)
+    return float((np.linalg.norm(Hx - Sx * lam[None, :], axis=0) / (nf2 * np.linalg.norm(Z, axis=0))).max())
+
+
+# ------------------------------------------------------------------ 2x2 routine
+def _random_pivots(rng, count):
+    out = []
+    for i in range(count):
+        A = rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2))
+        S = A.conj().T @ A * 10.0 ** rng.uniform(-3, 3)
+        B = rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2))
+        H = B.conj().T @ np.diag(rng.choice([-1.0, 1.0], 2)) @ B * 10.0 ** rng.uniform(-3, 3)
+        out.append([H[0, 0].real, H[1, 1].real, H[0, 1].real, H[0, 1].imag,
+                    S[0, 0].real, S[1, 1].real, S[0, 1].real, S[0, 1].imag])
+    # branch cases: identity, skip, x = 0, h = v = 0, small, errors
+    tol = EPS * 8
+    out += [[1, 1, 0, 0, 1, 1, 0, 0], [0, 2, 0, 0, 1, 1, 0, 0], [1, 2, 0.1 * tol, 0, 1, 1, 0, 0],
+            [1, 2, 4 * tol, 0, 1, 1, 0, 0], [1, 3, 0.5, 0.2, 1, 1, 0, 0], [2, 2, 0.3, 0.4, 1, 1, 0.3, 0.4],
+            [1, 1, 0.5, 0, 1, 1, 0, 0], [1, 1, 0.5, 0, 0, 1, 0.1, 0], [1, 1, 0.5, 0, 1, 1, 1.0, 0],
+            [np.nan, 1, 0, 0, 1, 1, 0, 0], [1, 1, 0.5, 0, -1, 1, 0, 0]]
+    return np.array(out, dtype=np.float64)
+
+
+def test_device_hz2x2_bitwise_equals_oracle(gh):
+    """C-8: identical inputs -> bitwise identical Z' and kind on host (oracle) and device."""
+    ctx = gh.Context(16, 8)
+    rng = np.random.default_rng(1)
+    piv = _random_pivots(rng, 20000)
+    tol = EPS * np.sqrt(64)
+    for crit in (0, 1):
+        zd, kd = ctx.hz2x2_batch(piv, tol, crit)
+        for i in range(piv.shape[0]):
+            g = piv[i]
+            rc, Z, _ = oracle.hz2x2_raw(g[0], g[1], complex(g[2], g[3]), g[4], g[5], complex(g[6], g[7]), tol, crit)
+            assert rc == kd[i], (i, g, rc, kd[i])
+            if rc >= 2:
+                zo = np.array([Z[0, 0].real, Z[0, 0].imag, Z[1, 0].real, Z[1, 0].imag,
+                               Z[0, 1].real, Z[0, 1].imag, Z[1, 1].real, Z[1, 1].imag])
+                assert np.array_equal(zo.view(np.uint64), zd[i].view(np.uint64)), (i, g)
+    ctx.close()
+
+
+# ------------------------------------------------------------------ set/get factors
+def test_set_get_factors_sorts_rows_by_J(gh):
+    P = inputs.random_pencil(3, 37, 10, 0.4)
+    ctx = gh.Context(37, 10)
+    ctx.set_factors(P.F, P.J, P.G)
+    F, J, G, p2 = ctx.get_factors()
+    npos = int((P.J > 0).sum())
+    assert list(J) == [1] * npos + [-1] * (37 - npos)
+    order = np.concatenate([np.where(P.J > 0)[0], np.where(P.J < 0)[0]])
+    assert np.array_equal(F, P.F[order])       # stable partition, exact copy
+    assert np.array_equal(G, P.G)
+    assert list(p2) == list(range(10))
+    ctx.close()
+
+
+def test_bad_J_rejected(gh):
+    P = inputs.random_pencil(3, 16, 4, 0.4)
+    J = P.J.copy()
+    J[3] = 0
+    ctx = gh.Context(16, 4)
+    with pytest.raises(gh.GHSVDError):
+        ctx.set_factors(P.F, J, P.G)
+    ctx.close()
+
+
+# ------------------------------------------------------------------ single steps
+@pytest.mark.parametrize("m,n,cluster", [(64, 32, 1), (200, 64, 2), (333, 40, 4), (1000, 100, 8), (1030, 48, 16),
+                                         (17, 16, 1)])
+def test_steps_match_oracle(gh, m, n, cluster):
+    """a1-a4 parity: after each of the first steps the GPU's F', G', Z' equal the oracle's
+    elementwise (same inputs from get_factors, same pair ordering); ragged m and all
+    cluster sizes (slices crossing tile/cluster boundaries)."""
+    P = inputs.random_pencil(100 + m, m, n, 0.45)
+    ctx = gh.Context(m, n, cluster=cluster)
+    ctx.set_factors(P.F, P.J, P.G)
+    F0, J0, G0, _ = ctx.get_factors()
+    Zo = np.eye(n, dtype=complex)
+    Fo, Go = F0, G0
+    for s in range(min(n - 1, 5)):
+        a_gpu, b_gpu = ctx.run_steps(s, 1)
+        Fo, Go, Zo, a, b = oracle.hz_steps(Fo, J0, Go, Zo, s, 1)
+        Fg, Gg, Zg = ctx.transformed(m, n)
+        scale = np.abs(F0).max()
+        assert np.abs(Fg - Fo).max() <= 1e-12 * scale * max(1, s + 1)
+        assert np.abs(Gg - Go).max() <= 1e-12 * np.abs(G0).max() * max(1, s + 1)
+        assert np.abs(Zg - Zo).max() <= 1e-12 * max(1, s + 1)
+        assert (a_gpu, b_gpu) == (a, b)
+    ctx.close()
+
+
+# ------------------------------------------------------------------ full sweeps
+def _gpu_run(gh, P, **kw):
+    m, n = P.F.shape
+    ctx = gh.Context(m, n, **kw)
+    ctx.set_factors(P.F, P.J, P.G)
+    F0, J0, G0, _ = ctx.get_factors()
+    st = ctx.sweep()
+    lam, sf, sg, Z = ctx.extract()
+    ctx.close()
+    return F0, J0, G0, st, lam, sf, sg, Z
+
+
+def _oracle_run(F0, J0, G0, n):
+    Fo, Go, Zp, sto = oracle.hz_pointwise(F0, J0, G0)
+    lo, sfo, sgo, Zo = oracle.extract(Fo, J0, Go, Zp)
+    return sto, lo[:n], Zo
+
+
+@pytest.mark.parametrize("which,m,n", [("gsvd", 512, 256), ("hyp", 300, 128), ("hyp", 97, 33), ("rand", 250, 64)])
+def test_converged_eigenvalues_match_oracle(gh, which, m, n):
+    if which == "gsvd":
+        P = inputs.known_gsvd(1, m, n)                 # config 1 at full size
+    elif which == "hyp":
+        P = inputs.known_hyperbolic(7 + n, m, n, 0.4)
+    else:
+        P = inputs.random_pencil(9, m, n, 0.5)
+    F0, J0, G0, st, lam, sf, sg, Z = _gpu_run(gh, P)
+    sto, lo, _ = _oracle_run(F0, J0, G0, n)
+    assert st["converged"] and sto["converged"]
+    assert abs(st["sweeps"] - sto["sweeps"]) <= 1
+    assert relerr(lam, lo) <= 1e-9
+    if P.lam_true is not None:
+        assert relerr(lam, P.lam_true) <= 1e-9
+    assert residual(P.F, P.J, P.G, lam, Z) <= 1e-12 * n
+    assert np.allclose(sf ** 2 + sg ** 2, 1.0, atol=8 * EPS)
+
+
+def test_graph_and_plain_launches_bitwise_equal(gh):
+    """The CUDA-graph replay and plain launches run the same kernels: bitwise equal results
+    (and the engine is deterministic run to run)."""
+    P = inputs.known_hyperbolic(21, 160, 64, 0.5)
+    r1 = _gpu_run(gh, P, use_graph=True)
+    r2 = _gpu_run(gh, P, use_graph=False)
+    r3 = _gpu_run(gh, P, use_graph=True)
+    for a, b, c in zip(r1[4:], r2[4:], r3[4:]):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert r1[3]["transforms_all"] == r2[3]["transforms_all"]
+
+
+def test_singular_G_reports_indefinite(gh):
+    P = inputs.random_pencil(5, 40, 8, 0.5)
+    G = P.G.copy()
+    G[:, 3] = 0.0                                   # zero column: s_pp = 0 (C-9)
+    ctx = gh.Context(40, 8)
+    ctx.set_factors(P.F, P.J, G)
+    with pytest.raises(gh.GHSVDError) as e:
+        ctx.sweep()
+    assert e.value.status == -6
+    ctx.close()
+
+
+def test_state_machine(gh):
+    ctx = gh.Context(16, 8)
+    with pytest.raises(gh.GHSVDError) as e:
+        ctx.sweep()
+    assert e.value.status == -2
+    ctx.close()

@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(P1T) k_hebpj(P1Scr s, int NL) {
         herm2_jacobi_dev(ea, eb, ec, &Ra[4 * k], &l1, &l2);
         d[k] = l1;
         d[k + 1] = l2;
+        W[(k + 1) + (size_t)k * r] = c_mk(0.0, 0.0);  // L's 2x2 diagonal block is I
         bsz[k] = 2;
         bsz[k + 1] = 0;
       }

@@ -70,6 +70,8 @@ typedef struct {
   int cluster;         /* pointwise: CTAs per column pair (0 = auto; 1,2,4,8,16) */
   int threads;         /* pointwise: threads per CTA (0 = auto) */
   int use_graph;       /* capture each sweep's steps in a CUDA graph (default 1) */
+  int kernel;          /* pointwise step kernel: 0 = auto (= 2), 1 = one cluster per pair, TMA-staged slices;
+                          2 = two-pass through L2 (default); 3 = persistent pipelined TMA */
 } ghsvd_options;
 
 typedef struct {
@@ -83,6 +85,7 @@ typedef struct {
   uint64_t launches;          /* sweep-kernel launches issued (pointwise: sweeps * (n-1)) */
   uint64_t alg_bytes;         /* algorithmic HBM bytes of the sweeps: per transformed pair
                                  128m+64n, per skipped pair 64m */
+  double alg_flops;           /* algorithmic FP64 flops (blocked: Hermitian block Grams + updates) */
   double max_offdiag_last;    /* max scaled off-diagonal measure seen in the last sweep */
   uint64_t all_per_sweep[64]; /* per-sweep counters (first 64 sweeps) */
   uint64_t big_per_sweep[64];

@@ -1,8 +1,576 @@
+// blocked.cu -- Level-2 blocked HZ (BO / FB variants), Sec 6.4
+// (lines 1815-2040); SURVEY 8(a) row a6, and the slot bookkeeping of a7.
+//
+// Partition (Sec 6.4.1): nblk (even) block columns of widths w or w-1,
+// non-increasing.  Outer ordering: round-robin over block columns (reading
+// C-11).  Per block step s, for every block pair (bp, bq) owned by this rank:
+//   k_blk_gram   H_blk = F_pair^* J F_pair, S_blk = G_pair^* G_pair (k x k,
+//                k = w_p + w_q <= 64), lower-triangle 8x8 tiles on the FP64
+//                tensor cores (mma.sync m8n8k4 f64 = DMMA), J fused into the
+//                B operand, split over row chunks (deterministic sum later);
+//   k_blk_pivot  one CTA: sum the partials, HEBPJ(H_blk) -> F^ (Sec 4.2-4.3),
+//                pivoted Cholesky(S_blk) -> G^, border to
+//                even order, inner Level-1 one-sided HZ sweep(s) in shared
+//                memory (BO: 1 sweep; FB: until no transformation, <= 30)
+//                accumulating Z_blk (Sec 6.4.2); counters;
+//   k_blk_update F_pair <- F_pair Z_blk, G_pair <- G_pair Z_blk, Z_pair <-
+//                Z_pair Z_blk in place, row tiles on DMMA (Sec 6.4.3, the
+//                paper's three ZGEMMs; no shadow copy is needed on one GPU
+//                because every CTA reads its row tile before writing it).
+// Multi-GPU (comm.cpp) exchanges block columns between the steps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "hebpj.cuh"
+#include "hz2x2.cuh"
 #include "internal.h"
+
 namespace ghsvd {
-size_t blk_scratch_bytes(const ghsvd_options*, int64_t, int64_t) { return 0; }
-ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats*) {
-  ctx->err = "blocked: not implemented yet";
-  return GHSVD_E_STATE;
+
+namespace {
+
+constexpr int KM = 64;          // max block-pivot order 2w
+constexpr int RT = 32;          // rows per staged tile
+constexpr int GS = RT + 4;      // Gram tile column stride (double2), conflict-free fragments
+constexpr int US = RT + 2;      // update tile column stride
+constexpr int ZS = KM + 4;      // Z_blk column stride in smem
+constexpr int NT_G = 256, NT_P = 512, NT_U = 256;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct BlkArgs {
+  double2* F;
+  double2* G;
+  double2* Z;
+  long long ldm, ldn, m, n, npos;
+  int nblk, s, slot0, npairs;
+  const int* bstart;
+  const int* bwidth;
+  int nsplit;
+  long long split_rows;     // rows per split (multiple of RT)
+  double2* gpart;           // [pair][hs][split][KM*KM]
+  double2* zblk;            // [pair][KM*KM]
+  int* applied;             // [pair]
+  DevCounters* cnt;
+  double eps;
+  int literal;
+  int inner_sweeps;
+};
+
+__device__ __forceinline__ void pair_cols(const BlkArgs& a, int pl, int& c0p, int& wp, int& c0q, int& wq) {
+  long long bp, bq;
+  rr_pair(a.nblk, a.s, a.slot0 + pl, &bp, &bq);
+  c0p = a.bstart[bp];
+  wp = a.bwidth[bp];
+  c0q = a.bstart[bq];
+  wq = a.bwidth[bq];
+}
+
+// global column of pivot column c (c < wp: block p, else block q), -1 if padding
+__device__ __forceinline__ long long gcol(int c, int c0p, int wp, int c0q, int wq) {
+  if (c < wp) return c0p + c;
+  if (c < wp + wq) return c0q + (c - wp);
+  return -1;
+}
+
+// lower-triangle 8x8 tile list (I >= J) of a KM x KM matrix
+__constant__ signed char kTileI[36] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5,
+                                       5, 5, 5, 6, 6, 6, 6, 6, 6, 6, 7, 7, 7, 7, 7, 7, 7, 7};
+__constant__ signed char kTileJ[36] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2,
+                                       3, 4, 5, 0, 1, 2, 3, 4, 5, 6, 0, 1, 2, 3, 4, 5, 6, 7};
+
+// ---------------------------------------------------------------- Gram (DMMA)
+__global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
+  extern __shared__ __align__(128) double2 gsm[];  // [2][KM][GS]
+  const int pl = blockIdx.x, hs = blockIdx.y, split = blockIdx.z;
+  int c0p, wp, c0q, wq;
+  pair_cols(a, pl, c0p, wp, c0q, wq);
+  const double2* X = hs == 0 ? a.F : a.G;
+  const long long r_begin = (long long)split * a.split_rows;
+  const long long r_end = min(a.m, r_begin + a.split_rows);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double cre[5][2], cim[5][2];
+#pragma unroll
+  for (int t = 0; t < 5; t++) cre[t][0] = cre[t][1] = cim[t][0] = cim[t][1] = 0.0;
+  const int ntile = warp + 32 < 36 ? 5 : 4;
+  auto load_stage = [&](int st, long long r0) {
+    double2* T = gsm + (size_t)st * KM * GS;
+    for (int e = tid; e < KM * RT; e += NT_G) {
+      const int c = e / RT, r = e % RT;
+      const long long gc = gcol(c, c0p, wp, c0q, wq);
+      const long long gr = r0 + r;
+      const bool ok = gc >= 0 && gr < r_end;
+      cp_async16(&T[c * GS + r], ok ? (const void*)(X + gc * a.ldm + gr) : (const void*)X, ok);
+    }
+    cp_commit();
+  };
+  if (r_begin < r_end) load_stage(0, r_begin);
+  int st = 0;
+  for (long long r0 = r_begin; r0 < r_end; r0 += RT, st ^= 1) {
+    const bool more = r0 + RT < r_end;
+    if (more) load_stage(st ^ 1, r0 + RT);
+    if (more) cp_wait<1>(); else cp_wait<0>();
+    __syncthreads();
+    const double2* T = gsm + (size_t)st * KM * GS;
+#pragma unroll
+    for (int kk = 0; kk < RT; kk += 4) {
+      const int row = kk + (lane & 3);
+      const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
+#pragma unroll
+      for (int t = 0; t < 5; t++) {
+        if (t < ntile) {
+          const int tt = warp + 8 * t;
+          const int I = kTileI[tt], J = kTileJ[tt];
+          const double2 x = T[(8 * I + (lane >> 2)) * GS + row];   // A = X^H (row i, k)
+          const double2 y = T[(8 * J + (lane >> 2)) * GS + row];   // B = J X (k, col j)
+          const double yr = sg * y.x, yi = sg * y.y;
+          dmma(cre[t][0], cre[t][1], x.x, yr);
+          dmma(cre[t][0], cre[t][1], x.y, yi);
+          dmma(cim[t][0], cim[t][1], x.x, yi);
+          dmma(cim[t][0], cim[t][1], -x.y, yr);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
+#pragma unroll
+  for (int t = 0; t < 5; t++) {
+    if (t < ntile) {
+      const int tt = warp + 8 * t;
+      const int I = kTileI[tt], J = kTileJ[tt];
+      const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
+      out[i + (size_t)j * KM] = make_double2(cre[t][0], cim[t][0]);
+      out[i + (size_t)(j + 1) * KM] = make_double2(cre[t][1], cim[t][1]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- block pivot
+__global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
+  extern __shared__ __align__(128) double2 psm[];  // W0 | F^ | G^  (KM*KM each)
+  double2* W0 = psm;
+  double2* Fh = psm + KM * KM;
+  double2* Gh = psm + 2 * KM * KM;
+  __shared__ signed char Jh[KM];
+  __shared__ int np_sh;
+  __shared__ unsigned long long cnt_all, cnt_big, sweep_all;
+  __shared__ int err_sh;
+  const int pl = blockIdx.x, tid = threadIdx.x;
+  int c0p, wp, c0q, wq;
+  pair_cols(a, pl, c0p, wp, c0q, wq);
+  const int k = wp + wq;
+  const int kb = k + (k & 1);
+  if (tid == 0) {
+    cnt_all = cnt_big = sweep_all = 0;
+    err_sh = 0;
+  }
+  for (int e = tid; e < KM * KM; e += NT_P) {
+    Fh[e] = make_double2(0, 0);
+    Gh[e] = make_double2(0, 0);
+  }
+  // H_blk = sum of split partials (lower triangle), full Hermitian in W0
+  const double2* gp = a.gpart + ((size_t)pl * 2) * a.nsplit * (KM * KM);
+  auto gather = [&](int hs) {
+    const double2* base = gp + (size_t)hs * a.nsplit * (KM * KM);
+    for (int e = tid; e < k * k; e += NT_P) {
+      const int i = e % k, j = e / k;
+      const int ii = i >= j ? i : j, jj = i >= j ? j : i;
+      double2 v = make_double2(0, 0);
+      for (int sp = 0; sp < a.nsplit; sp++) {
+        const double2 x = base[(size_t)sp * (KM * KM) + ii + (size_t)jj * KM];
+        v.x += x.x;
+        v.y += x.y;
+      }
+      if (ii == jj) v.y = 0.0;
+      W0[i + j * KM] = (i >= j) ? v : make_double2(v.x, -v.y);
+    }
+    __syncthreads();
+  };
+  gather(0);
+  // HEBPJ tolerance k * eps * max |H| (lower triangle), as the oracle
+  double tv = 0.0;
+  long long ti = 0;
+  for (int e = tid; e < k * k; e += NT_P) {
+    const int i = e % k, j = e / k;
+    if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W0[i + j * KM]), 0);
+  }
+  hb::block_amax<NT_P>(tv, ti);
+  const double tolz = __dmul_rn(__dmul_rn((double)k, 0x1p-53), tv);
+  int rc = hb::hebpj_dev<NT_P, KM>(W0, k, KM, Fh, KM, Jh, &np_sh, tolz);
+  if (rc) {
+    if (tid == 0) atomicCAS(&a.cnt->err, 0, -7);
+    if (tid == 0) a.applied[pl] = 0;
+    return;
+  }
+  gather(1);
+  rc = hb::pchol_dev<NT_P, KM>(W0, k, KM, Gh, KM);
+  if (rc) {
+    if (tid == 0) atomicCAS(&a.cnt->err, 0, -6);
+    if (tid == 0) a.applied[pl] = 0;
+    return;
+  }
+  // border to even order (Sec 6.3.2) and Z_blk = I
+  if (tid == 0 && kb != k) {
+    Fh[k + k * KM] = make_double2(1, 0);
+    Gh[k + k * KM] = make_double2(1, 0);
+    Jh[k] = 1;
+  }
+  for (int e = tid; e < KM * KM; e += NT_P) {
+    const int i = e % KM, j = e / KM;
+    W0[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  // inner Level-1 sweeps: one warp per pivot pair, kb/2 pairs per step
+  const int warp = tid >> 5, lane = tid & 31;
+  const double tol = a.eps * sqrt((double)kb);       // C-7: n = block-pivot order
+  for (int sw = 0; sw < a.inner_sweeps; sw++) {
+    unsigned long long sw_all = 0, sw_big = 0;
+    for (int s = 0; s < kb - 1; s++) {
+      for (int pr = warp; pr < kb / 2; pr += NT_P / 32) {
+        long long p, q;
+        rr_pair(kb, s, pr, &p, &q);
+        double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = lane; i < kb; i += 32) {
+          const double2 fp = Fh[i + p * KM], fq = Fh[i + q * KM], gpp = Gh[i + p * KM], gq = Gh[i + q * KM];
+          const double sg = (double)Jh[i];
+          g[0] += sg * (fp.x * fp.x + fp.y * fp.y);
+          g[1] += sg * (fq.x * fq.x + fq.y * fq.y);
+          g[2] += sg * (fp.x * fq.x + fp.y * fq.y);
+          g[3] += sg * (fp.x * fq.y - fp.y * fq.x);
+          g[4] += gpp.x * gpp.x + gpp.y * gpp.y;
+          g[5] += gq.x * gq.x + gq.y * gq.y;
+          g[6] += gpp.x * gq.x + gpp.y * gq.y;
+          g[7] += gpp.x * gq.y - gpp.y * gq.x;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; c++)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) g[c] += __shfl_xor_sync(0xffffffffu, g[c], o);
+        HZOut z{};
+        if (lane == 0) z = hz2x2_dev(g, tol, a.literal);
+        double zz[8] = {z.z11.re, z.z11.im, z.z21.re, z.z21.im, z.z12.re, z.z12.im, z.z22.re, z.z22.im};
+#pragma unroll
+        for (int c = 0; c < 8; c++) zz[c] = __shfl_sync(0xffffffffu, zz[c], 0);
+        const int kind = __shfl_sync(0xffffffffu, lane == 0 ? z.kind : 0, 0);
+        if (kind < 0) {
+          if (lane == 0) atomicCAS(&err_sh, 0, kind);
+          continue;
+        }
+        if (kind != KIND_SMALL && kind != KIND_BIG) continue;
+        if (lane == 0) {
+          sw_all++;
+          if (kind == KIND_BIG) sw_big++;
+        }
+        const double2 z11 = make_double2(zz[0], zz[1]), z21 = make_double2(zz[2], zz[3]);
+        const double2 z12 = make_double2(zz[4], zz[5]), z22 = make_double2(zz[6], zz[7]);
+        auto rot = [&](double2* M) {
+          for (int i = lane; i < kb; i += 32) {
+            const double2 x = M[i + p * KM], y = M[i + q * KM];
+            M[i + p * KM] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
+                                         x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
+            M[i + q * KM] = make_double2(x.x * z12.x - x.y * z12.y + y.x * z22.x - y.y * z22.y,
+                                         x.x * z12.y + x.y * z12.x + y.x * z22.y + y.y * z22.x);
+          }
+        };
+        rot(Fh);
+        rot(Gh);
+        rot(W0);
+      }
+      __syncthreads();
+    }
+    // per-sweep totals; FB stops on a sweep without transformations (C-3)
+    if (lane == 0) {
+      atomicAdd(&sweep_all, sw_all);
+      atomicAdd(&cnt_all, sw_all);
+      atomicAdd(&cnt_big, sw_big);
+    }
+    __syncthreads();
+    const unsigned long long this_sweep = sweep_all;
+    __syncthreads();
+    if (tid == 0) sweep_all = 0;
+    __syncthreads();
+    if (this_sweep == 0) break;
+  }
+  if (err_sh) {
+    if (tid == 0) atomicCAS(&a.cnt->err, 0, err_sh);
+  }
+  double2* zo = a.zblk + (size_t)pl * (KM * KM);
+  for (int e = tid; e < KM * KM; e += NT_P) zo[e] = W0[e];
+  if (tid == 0) {
+    a.applied[pl] = cnt_all > 0;
+    atomicAdd(&a.cnt->all, cnt_all);
+    atomicAdd(&a.cnt->big, cnt_big);
+  }
+}
+
+// ---------------------------------------------------------------- update (DMMA)
+// grid (pair, tile): tiles [0, tF) rows of F, [tF, 2 tF) rows of G, [2 tF, 2 tF + tZ) rows of Z
+__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tZ) {
+  extern __shared__ __align__(128) double2 usm[];  // X tile [KM][US] | Z_blk [KM][ZS]
+  const int pl = blockIdx.x, tile = blockIdx.y;
+  if (!a.applied[pl]) return;
+  int c0p, wp, c0q, wq;
+  pair_cols(a, pl, c0p, wp, c0q, wq);
+  const int k = wp + wq;
+  double2* X;
+  long long ld, rows, r0;
+  if (tile < tF) {
+    X = a.F; ld = a.ldm; rows = a.m; r0 = (long long)tile * RT;
+  } else if (tile < 2 * tF) {
+    X = a.G; ld = a.ldm; rows = a.m; r0 = (long long)(tile - tF) * RT;
+  } else {
+    X = a.Z; ld = a.ldn; rows = a.n; r0 = (long long)(tile - 2 * tF) * RT;
+  }
+  double2* Xt = usm;
+  double2* Zb = usm + KM * US;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < KM * RT; e += NT_U) {
+    const int c = e / RT, r = e % RT;
+    const long long gc = gcol(c, c0p, wp, c0q, wq);
+    const bool ok = gc >= 0 && r0 + r < rows;
+    cp_async16(&Xt[c * US + r], ok ? (const void*)(X + gc * ld + r0 + r) : (const void*)X, ok);
+  }
+  const double2* zsrc = a.zblk + (size_t)pl * (KM * KM);
+  for (int e = tid; e < KM * KM; e += NT_U) {
+    const int i = e % KM, j = e / KM;
+    cp_async16(&Zb[j * ZS + i], zsrc + e, i < k && j < k);
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  // out (RT x KM) = Xt (RT x KM) Z_blk (KM x KM): 4 x 8 tiles of 8x8, 4 per warp
+  double ore[4][2], oim[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; t++) ore[t][0] = ore[t][1] = oim[t][0] = oim[t][1] = 0.0;
+  const int I = warp & 3;          // row tile
+  const int J0 = (warp >> 2) * 4;  // first of 4 column tiles
+  const int kend = (k + 3) & ~3;
+  for (int kk = 0; kk < kend; kk += 4) {
+    const double2 x = Xt[(kk + (lane & 3)) * US + 8 * I + (lane >> 2)];  // A(i, k)
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const double2 z = Zb[(8 * (J0 + t) + (lane >> 2)) * ZS + kk + (lane & 3)];  // B(k, j)
+      dmma(ore[t][0], ore[t][1], x.x, z.x);
+      dmma(ore[t][0], ore[t][1], -x.y, z.y);
+      dmma(oim[t][0], oim[t][1], x.x, z.y);
+      dmma(oim[t][0], oim[t][1], x.y, z.x);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const int i = 8 * I + (lane >> 2), j = 8 * (J0 + t) + 2 * (lane & 3);
+    Xt[j * US + i] = make_double2(ore[t][0], oim[t][0]);
+    Xt[(j + 1) * US + i] = make_double2(ore[t][1], oim[t][1]);
+  }
+  __syncthreads();
+  for (int e = tid; e < KM * RT; e += NT_U) {
+    const int c = e / RT, r = e % RT;
+    const long long gc = gcol(c, c0p, wp, c0q, wq);
+    if (gc >= 0 && r0 + r < rows) X[gc * ld + r0 + r] = Xt[c * US + r];
+  }
+}
+
+__global__ void k_blk_partition(int* bstart, int* bwidth, int nblk, long long n) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const long long w = (n + nblk - 1) / nblk;
+  const long long nbig = n - (long long)nblk * (w - 1);
+  long long c = 0;
+  for (int b = 0; b < nblk; b++) {
+    bwidth[b] = (int)(b < nbig ? w : w - 1);
+    bstart[b] = (int)c;
+    c += bwidth[b];
+  }
+}
+
+size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+int auto_nblk(int64_t n, const ghsvd_options* o) {
+  if (o->nblocks > 0) return o->nblocks;
+  int64_t nb = (n + 31) / 32;      // width w <= 32 -> block pivots of order <= 64
+  nb += nb & 1;
+  const int64_t P = std::max(1, o->world_size);
+  nb = round_up(nb, 2 * P);
+  return (int)std::max<int64_t>(2, nb);
+}
+
+constexpr int MAX_SPLIT = 16;
+
+struct BlkPlan {
+  int nblk, K, slot0, nsplit;
+  long long split_rows;
+};
+
+BlkPlan make_plan(const Ctx* ctx) {
+  BlkPlan p;
+  p.nblk = auto_nblk(ctx->n, &ctx->o);
+  const int P = std::max(1, ctx->o.world_size);
+  p.K = p.nblk / 2 / P;
+  p.slot0 = ctx->o.rank * p.K;
+  const long long target = 4 * 148;
+  p.nsplit = (int)std::min<long long>(MAX_SPLIT, std::max<long long>(1, (target + 2 * p.K - 1) / (2 * p.K)));
+  const long long rows_per = (ctx->m + p.nsplit - 1) / p.nsplit;
+  p.split_rows = round_up(std::max<long long>(rows_per, 1), RT);
+  p.nsplit = (int)((ctx->m + p.split_rows - 1) / p.split_rows);
+  return p;
+}
+
+}  // namespace
+
+size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
+  const int64_t nb = auto_nblk(n + 1, o) + 2;
+  const int64_t K = nb / 2;
+  return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)K * KM * KM * 16) + al256((size_t)K * 4) +
+         2 * al256((size_t)nb * 4) + 4096;
+}
+
+// in comm.cpp
+ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart_h, const int* bwidth_h);
+ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c);
+
+ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
+  BlkPlan pl = make_plan(ctx);
+  if (pl.nblk % 2 || pl.nblk < 2 || pl.nblk > ctx->n || pl.K < 1 ||
+      pl.nblk % (2 * std::max(1, ctx->o.world_size))) {
+    ctx->err = "blocked: nblocks must be even, <= n and a multiple of 2*world_size";
+    return GHSVD_E_INVALID_ARG;
+  }
+  const int64_t w = (ctx->n + pl.nblk - 1) / pl.nblk;
+  if (2 * w > KM) {
+    ctx->err = "blocked: block width " + std::to_string(w) + " > 32 (increase nblocks)";
+    return GHSVD_E_INVALID_ARG;
+  }
+  if (blk_scratch_bytes(&ctx->o, ctx->m, ctx->n) > ctx->L.scr_bytes) {
+    ctx->err = "blocked: workspace scratch too small (create the context with a blocked variant)";
+    return GHSVD_E_WORKSPACE;
+  }
+  cudaStream_t str = ctx->stream;
+  char* p = ctx->scr;
+  BlkArgs a;
+  a.gpart = (double2*)p; p += al256((size_t)pl.K * 2 * MAX_SPLIT * KM * KM * 16);
+  a.zblk = (double2*)p; p += al256((size_t)pl.K * KM * KM * 16);
+  a.applied = (int*)p; p += al256((size_t)pl.K * 4);
+  int* bstart = (int*)p; p += al256((size_t)(pl.nblk + 2) * 4);
+  int* bwidth = (int*)p; p += al256((size_t)(pl.nblk + 2) * 4);
+  k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
+  GH_CUDA(cudaGetLastError());
+  std::vector<int> bs_h(pl.nblk), bw_h(pl.nblk);
+  GH_CUDA(cudaMemcpyAsync(bs_h.data(), bstart, pl.nblk * 4, cudaMemcpyDeviceToHost, str));
+  GH_CUDA(cudaMemcpyAsync(bw_h.data(), bwidth, pl.nblk * 4, cudaMemcpyDeviceToHost, str));
+  a.F = ctx->F;
+  a.G = ctx->G;
+  a.Z = ctx->Z;
+  a.ldm = ctx->ldm;
+  a.ldn = ctx->ldn;
+  a.m = ctx->m;
+  a.n = ctx->n;
+  a.npos = ctx->npos;
+  a.nblk = pl.nblk;
+  a.slot0 = pl.slot0;
+  a.npairs = pl.K;
+  a.bstart = bstart;
+  a.bwidth = bwidth;
+  a.nsplit = pl.nsplit;
+  a.split_rows = pl.split_rows;
+  a.cnt = ctx->cnt;
+  a.eps = ctx->o.eps;
+  a.literal = ctx->o.criterion == GHSVD_CRIT_LITERAL;
+  a.inner_sweeps = ctx->o.variant == GHSVD_BLOCKED_FB ? 30 : 1;
+  const size_t smem_g = (size_t)2 * KM * GS * 16;
+  const size_t smem_p = (size_t)3 * KM * KM * 16;
+  const size_t smem_u = (size_t)(KM * US + KM * ZS) * 16;
+  GH_CUDA(cudaFuncSetAttribute(k_blk_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u));
+  const int tF = (int)((ctx->m + RT - 1) / RT), tZ = (int)((ctx->n + RT - 1) / RT);
+  const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
+  // algorithmic flops per block pair (Hermitian Grams k(k+1)/2 m each, updates k^2 (2m+n))
+  GH_CUDA(cudaStreamSynchronize(str));
+  const bool multi = ctx->o.world_size > 1;
+  GH_CUDA(cudaEventRecord(ctx->ev0, str));
+  for (int sw = 0; sw < ctx->o.max_sweeps; sw++) {
+    GH_CUDA(cudaMemsetAsync(ctx->cnt, 0, sizeof(DevCounters), str));
+    GH_CUDA(cudaEventRecord(ctx->ev2, str));
+    for (int s = 0; s < pl.nblk - 1; s++) {
+      a.s = s;
+      k_blk_gram<<<dim3(pl.K, 2, pl.nsplit), NT_G, smem_g, str>>>(a);
+      k_blk_pivot<<<pl.K, NT_P, smem_p, str>>>(a);
+      k_blk_update<<<dim3(pl.K, 2 * tF + tZ), NT_U, smem_u, str>>>(a, tF, tZ);
+      GH_CUDA(cudaGetLastError());
+      if (multi) {
+        const int s_next = (s + 1) % (pl.nblk - 1);
+        ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data());
+        if (e) return e;
+      }
+    }
+    GH_CUDA(cudaEventRecord(ctx->ev3, str));
+    DevCounters c;
+    GH_CUDA(cudaMemcpyAsync(&c, ctx->cnt, sizeof(c), cudaMemcpyDeviceToHost, str));
+    GH_CUDA(cudaStreamSynchronize(str));
+    if (multi) {
+      ghsvd_status e = comm_allreduce_counters(ctx, &c);
+      if (e) return e;
+    }
+    if (c.err) {
+      ctx->err = c.err == -7 ? "blocked: rank-deficient block pivot (HEBPJ)"
+                 : c.err == -6 ? "blocked: indefinite / singular S block pivot"
+                               : "blocked: non-finite value in a block pivot";
+      return c.err == -7 ? GHSVD_E_RANK_DEFICIENT : c.err == -6 ? GHSVD_E_INDEFINITE_S : GHSVD_E_NONFINITE;
+    }
+    float kms = 0;
+    GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
+    st->kernel_seconds += kms * 1e-3;
+    st->launches += (uint64_t)3 * (pl.nblk - 1);
+    if (sw < 64) {
+      st->all_per_sweep[sw] = c.all;
+      st->big_per_sweep[sw] = c.big;
+    }
+    st->sweeps = sw + 1;
+    st->pairs_visited += pairs;
+    st->transforms_all += c.all;
+    st->transforms_big += c.big;
+    if (c.big == 0) {
+      st->converged = 1;
+      break;
+    }
+  }
+  GH_CUDA(cudaEventRecord(ctx->ev1, str));
+  GH_CUDA(cudaEventSynchronize(ctx->ev1));
+  float ms = 0;
+  GH_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  st->seconds = ms * 1e-3;
+  // algorithmic flops: per sweep sum over block pairs of 8 [k(k+1) m + k^2 (2m + n)] (re+im FMAs x2)
+  double fl = 0.0;
+  for (int s = 0; s < pl.nblk - 1; s++)
+    for (int kk = 0; kk < pl.nblk / 2; kk++) {
+      long long bp, bq;
+      rr_pair(pl.nblk, s, kk, &bp, &bq);
+      const double kq = bw_h[bp] + bw_h[bq];
+      fl += 8.0 * (kq * (kq + 1) * ctx->m + kq * kq * (2.0 * ctx->m + ctx->n));
+    }
+  st->alg_flops = fl * st->sweeps / std::max(1, ctx->o.world_size);
+  // HBM bytes the blocked sweep must move per block step: Grams read F, G pairs once,
+  // updates read + write F, G, Z pairs once
+  st->alg_bytes = (uint64_t)((double)st->sweeps * (pl.nblk - 1) / std::max(1, ctx->o.world_size) *
+                             16.0 * (double)ctx->n * (2.0 * ctx->m + 2.0 * (2.0 * ctx->m + ctx->n)));
+  return GHSVD_OK;
+}
+
 }  // namespace ghsvd

@@ -1,0 +1,301 @@
+// hebpj.cuh -- CTA-wide Hermitian indefinite factorisation with complete pivoting
+// (HEBPJ, Sec 4.2-4.3, eq 4.3) and diagonally pivoted Cholesky
+// (PAPER.md:1920-1932), as __device__ routines run by one thread block on a
+// matrix in global or shared memory.  Used by Phase 1 (T_a, order 2 N_L) and by
+// the blocked variant's block pivots (order 2w, Sec 6.4.2).
+//
+// hebpj_dev: W (r x r, ld, full Hermitian; overwritten: L below the diagonal)
+//   -> M (r x r, ld) with T = M^* diag(J) M, rows sorted + before - ;
+//   Bunch-Parlett pivoting, alpha = (1 + sqrt 17)/8, smallest-index ties;
+//   2x2 pivots diagonalised by a Jacobi rotation, rows scaled by |d|^1/2.
+// pchol_dev: S (r x r, ld, full Hermitian; overwritten) -> Gh = L^* P.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ghsvd {
+namespace hb {
+
+__device__ __forceinline__ double2 mk(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ double2 add(double2 a, double2 b) { return mk(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 sub(double2 a, double2 b) { return mk(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 mul(double2 a, double2 b) {
+  return mk(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 conj(double2 a) { return mk(a.x, -a.y); }
+__device__ __forceinline__ double2 scale(double2 a, double s) { return mk(__dmul_rn(a.x, s), __dmul_rn(a.y, s)); }
+__device__ __forceinline__ double cabs(double2 a) { return __dsqrt_rn(__dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y))); }
+__device__ __forceinline__ double cabs2(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+
+__device__ __forceinline__ void amax_merge(double& v, long long& i, double v2, long long i2) {
+  if (v2 > v || (v2 == v && i2 < i)) {
+    v = v2;
+    i = i2;
+  }
+}
+
+template <int NT>
+__device__ void block_amax(double& v, long long& i) {
+  __shared__ double sv[NT / 32];
+  __shared__ long long si[NT / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    amax_merge(v, i, v2, i2);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[w] = v;
+    si[w] = i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < NT / 32; k++) amax_merge(sv[0], si[0], sv[k], si[k]);
+  }
+  __syncthreads();
+  v = sv[0];
+  i = si[0];
+  __syncthreads();
+}
+
+// Jacobi rotation R (column-major R11, R21, R12, R22) with R^* E R = diag(l1, l2)
+__device__ inline void herm2_jacobi(double a, double2 b, double c, double2* R, double* l1, double* l2) {
+  const double ab = cabs(b);
+  if (ab == 0.0) {
+    R[0] = mk(1, 0); R[1] = mk(0, 0); R[2] = mk(0, 0); R[3] = mk(1, 0);
+    *l1 = a; *l2 = c;
+    return;
+  }
+  const double2 e = mk(__ddiv_rn(b.x, ab), __ddiv_rn(b.y, ab));
+  const double tau = __ddiv_rn(__dsub_rn(c, a), __dmul_rn(2.0, ab));
+  const double t = __ddiv_rn(tau >= 0.0 ? 1.0 : -1.0,
+                             __dadd_rn(fabs(tau), __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(tau, tau)))));
+  const double cs = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(t, t)))), sn = __dmul_rn(t, cs);
+  const double2 em = conj(e);
+  R[0] = mk(cs, 0.0);
+  R[1] = scale(em, -sn);
+  R[2] = mk(sn, 0.0);
+  R[3] = scale(em, cs);
+  *l1 = __dsub_rn(a, __dmul_rn(t, ab));
+  *l2 = __dadd_rn(c, __dmul_rn(t, ab));
+}
+
+// Returns 0 or -7 (rank deficient).  All NT threads of the block must call it.
+// tolz: pivots with max |entry| <= tolz stop the factorisation (rank deficiency).
+template <int NT, int RMAX>
+__device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long ldmo, signed char* Jout,
+                         int* npos_out, double tolz) {
+  __shared__ int perm[RMAX];
+  __shared__ int bsz[RMAX];
+  __shared__ double d[RMAX];
+  __shared__ double2 Rk[RMAX * 2];  // 4 per 2x2 pivot (stored at 2*k .. 2*k+3 for pivot k)
+  __shared__ double2 colk[2][RMAX];
+  __shared__ int rowpos[RMAX];
+  __shared__ signed char sgn[RMAX];
+  __shared__ int err_sh;
+  const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+  for (int i = threadIdx.x; i < r; i += NT) perm[i] = i;
+  if (threadIdx.x == 0) err_sh = 0;
+  __syncthreads();
+  int k = 0;
+  while (k < r) {
+    double mu1 = -1.0;
+    long long id = 0x7fffffffffffffffll;
+    for (int i = k + threadIdx.x; i < r; i += NT) amax_merge(mu1, id, fabs(W[i + i * ldw].x), i);
+    block_amax<NT>(mu1, id);
+    double mu0 = 0.0;
+    long long oidx = 0x7fffffffffffffffll;
+    const long long rem = r - k;
+    for (long long e = threadIdx.x; e < rem * rem; e += NT) {
+      const int j = k + (int)(e / rem), i = k + (int)(e % rem);
+      if (i > j) amax_merge(mu0, oidx, cabs(W[i + j * ldw]), (long long)j * r + i);
+    }
+    block_amax<NT>(mu0, oidx);
+    const double mall = mu0 > mu1 ? mu0 : mu1;
+    if (!(mall > tolz)) {
+      if (threadIdx.x == 0) err_sh = -7;
+      __syncthreads();
+      break;
+    }
+    const int two = !(mu1 >= __dmul_rn(alpha, mu0));
+    int src0 = (int)id, src1 = -1;
+    if (two) {
+      src0 = (int)(oidx / r);
+      src1 = (int)(oidx % r);
+    }
+    for (int b = 0; b < (two ? 2 : 1); b++) {
+      const int dst = k + b;
+      int s = b == 0 ? src0 : src1;
+      if (b == 1 && s == k) s = src0;
+      if (s != dst) {
+        for (int c = threadIdx.x; c < r; c += NT) {
+          const double2 t = W[dst + c * ldw];
+          W[dst + c * ldw] = W[s + c * ldw];
+          W[s + c * ldw] = t;
+        }
+        __syncthreads();
+        for (int i = k + threadIdx.x; i < r; i += NT) {
+          const double2 t = W[i + dst * ldw];
+          W[i + dst * ldw] = W[i + s * ldw];
+          W[i + s * ldw] = t;
+        }
+        if (threadIdx.x == 0) {
+          const int t = perm[dst];
+          perm[dst] = perm[s];
+          perm[s] = t;
+        }
+        __syncthreads();
+      }
+    }
+    if (!two) {
+      const double dk = W[k + k * ldw].x;
+      const double inv = __ddiv_rn(1.0, dk);
+      for (int i = k + 1 + threadIdx.x; i < r; i += NT) colk[0][i] = W[i + k * ldw];
+      __syncthreads();
+      const long long rm = r - k - 1;
+      for (long long e = threadIdx.x; e < rm * rm; e += NT) {
+        const int i = k + 1 + (int)(e % rm), j = k + 1 + (int)(e / rm);
+        W[i + j * ldw] = sub(W[i + j * ldw], scale(mul(colk[0][i], conj(colk[0][j])), inv));
+      }
+      __syncthreads();
+      for (int i = k + 1 + threadIdx.x; i < r; i += NT) W[i + k * ldw] = scale(colk[0][i], inv);
+      if (threadIdx.x == 0) {
+        bsz[k] = 1;
+        d[k] = dk;
+      }
+      __syncthreads();
+      k += 1;
+    } else {
+      const double ea = W[k + k * ldw].x, ec = W[(k + 1) + (k + 1) * ldw].x;
+      const double2 eb = W[k + (k + 1) * ldw];
+      const double det = __dsub_rn(__dmul_rn(ea, ec), cabs2(eb));
+      const double inv = __ddiv_rn(1.0, det);
+      for (int i = k + 2 + threadIdx.x; i < r; i += NT) {
+        const double2 w0 = W[i + k * ldw], w1 = W[i + (k + 1) * ldw];
+        colk[0][i] = w0;
+        colk[1][i] = w1;
+        W[i + k * ldw] = scale(sub(scale(w0, ec), mul(w1, conj(eb))), inv);
+        W[i + (k + 1) * ldw] = scale(sub(scale(w1, ea), mul(w0, eb)), inv);
+      }
+      __syncthreads();
+      const long long rm = r - k - 2;
+      for (long long e = threadIdx.x; e < rm * rm; e += NT) {
+        const int i = k + 2 + (int)(e % rm), j = k + 2 + (int)(e / rm);
+        const double2 t = add(mul(W[i + k * ldw], conj(colk[0][j])), mul(W[i + (k + 1) * ldw], conj(colk[1][j])));
+        W[i + j * ldw] = sub(W[i + j * ldw], t);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double l1, l2;
+        herm2_jacobi(ea, eb, ec, &Rk[2 * k], &l1, &l2);
+        d[k] = l1;
+        d[k + 1] = l2;
+        bsz[k] = 2;
+        bsz[k + 1] = 0;
+        W[(k + 1) + k * ldw] = mk(0.0, 0.0);  // L's 2x2 diagonal block is I
+      }
+      __syncthreads();
+      k += 2;
+    }
+  }
+  if (err_sh) return err_sh;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < r; i++) sgn[i] = d[i] > 0.0 ? 1 : -1;
+    int np = 0;
+    for (int i = 0; i < r; i++)
+      if (sgn[i] > 0) rowpos[i] = np++;
+    int q = np;
+    for (int i = 0; i < r; i++)
+      if (sgn[i] < 0) rowpos[i] = q++;
+    *npos_out = np;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < r; i += NT) Jout[rowpos[i]] = sgn[i];
+  // Mtilde(rowpos(i), perm[l]) = row i of diag(|d|^1/2) R^* L^*, column l
+  for (int e = threadIdx.x; e < r * r; e += NT) {
+    const int i = e % r, l = e / r;
+    auto Lh = [&](int row, int col) -> double2 {  // (L^*)(row, col) = conj(L(col, row))
+      if (row == col) return mk(1.0, 0.0);
+      if (col < row) return mk(0.0, 0.0);
+      return conj(W[col + row * ldw]);
+    };
+    double2 y;
+    if (bsz[i] == 1) {
+      y = scale(Lh(i, l), __dsqrt_rn(fabs(d[i])));
+    } else if (bsz[i] == 2) {
+      const double2* R = &Rk[2 * i];
+      y = scale(add(mul(conj(R[0]), Lh(i, l)), mul(conj(R[1]), Lh(i + 1, l))), __dsqrt_rn(fabs(d[i])));
+    } else {
+      const double2* R = &Rk[2 * (i - 1)];
+      y = scale(add(mul(conj(R[2]), Lh(i - 1, l)), mul(conj(R[3]), Lh(i, l))), __dsqrt_rn(fabs(d[i])));
+    }
+    M[rowpos[i] + perm[l] * ldmo] = y;
+  }
+  __syncthreads();
+  return 0;
+}
+
+// Diagonally pivoted Cholesky: P S P^T = L L^*, Gh = L^* P (column perm[l] of Gh
+// is column l of L^*).  S overwritten (L below/on the diagonal).  Returns 0 or -6.
+template <int NT, int RMAX>
+__device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long long ldg) {
+  __shared__ int perm[RMAX];
+  __shared__ int err_sh;
+  __shared__ int pv_sh;
+  for (int i = threadIdx.x; i < r; i += NT) perm[i] = i;
+  if (threadIdx.x == 0) err_sh = 0;
+  __syncthreads();
+  for (int k = 0; k < r; k++) {
+    if (threadIdx.x == 0) {
+      int pv = k;
+      for (int i = k + 1; i < r; i++)
+        if (S[i + i * lds].x > S[pv + pv * lds].x) pv = i;
+      pv_sh = pv;
+      if (!(S[pv + pv * lds].x > 0.0)) err_sh = -6;
+    }
+    __syncthreads();
+    if (err_sh) return err_sh;
+    const int pv = pv_sh;
+    if (pv != k) {
+      for (int c = threadIdx.x; c < r; c += NT) {
+        const double2 t = S[k + c * lds];
+        S[k + c * lds] = S[pv + c * lds];
+        S[pv + c * lds] = t;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < r; i += NT) {
+        if (i < k) continue;  // columns >= k hold the live matrix; L (cols < k) rows were swapped above
+        const double2 t = S[i + k * lds];
+        S[i + k * lds] = S[i + pv * lds];
+        S[i + pv * lds] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = perm[k];
+        perm[k] = perm[pv];
+        perm[pv] = t;
+      }
+      __syncthreads();
+    }
+    const double lkk = __dsqrt_rn(S[k + k * lds].x);
+    const double inv = __ddiv_rn(1.0, lkk);
+    __syncthreads();
+    for (int i = k + 1 + threadIdx.x; i < r; i += NT) S[i + k * lds] = scale(S[i + k * lds], inv);
+    if (threadIdx.x == 0) S[k + k * lds] = mk(lkk, 0.0);
+    __syncthreads();
+    const long long rm = r - k - 1;
+    for (long long e = threadIdx.x; e < rm * rm; e += NT) {
+      const int i = k + 1 + (int)(e % rm), j = k + 1 + (int)(e / rm);
+      S[i + j * lds] = sub(S[i + j * lds], mul(S[i + k * lds], conj(S[j + k * lds])));
+    }
+    __syncthreads();
+  }
+  // Gh(i, perm[l]) = (L^*)(i, l) = conj(L(l, i)) for l >= i, else 0
+  for (int e = threadIdx.x; e < r * r; e += NT) {
+    const int i = e % r, l = e / r;
+    Gh[i + perm[l] * ldg] = l >= i ? conj(S[l + i * lds]) : mk(0.0, 0.0);
+  }
+  __syncthreads();
+  return 0;
+}
+
+}  // namespace hb
+}  // namespace ghsvd

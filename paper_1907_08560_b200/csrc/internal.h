@@ -55,6 +55,9 @@ struct Ctx {
   int* rowdest;                  // m+1 row destinations (row sort)
   // pointwise launch configuration
   int pw_cluster, pw_threads;
+  bool pw_pipe;
+  int pw_kind;
+  int64_t pw_nclusters;           // clusters launched per step
   size_t pw_smem;
   // graph cache
   cudaGraphExec_t graph;

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "hebpj.cuh"
 #include "internal.h"
 
 namespace ghsvd {
@@ -147,181 +148,26 @@ __global__ void __launch_bounds__(P1T) k_build_T(P1Scr s, int NL) {
   }
 }
 
-// HEBPJ of one T_a per CTA (in global memory, L2-resident).
+// HEBPJ of one T_a per CTA (in global memory, L2-resident), hebpj.cuh.
 __global__ void __launch_bounds__(P1T) k_hebpj(P1Scr s, int NL) {
   const int a = blockIdx.x, r = 2 * NL;
   double2* W = s.W + (size_t)a * r * r;
   double2* M = s.M + (size_t)a * r * r;
-  double2* Ra = s.R + (size_t)a * r * 4;
-  double* d = s.d + (size_t)a * r;
-  int* bsz = s.bsz + (size_t)a * r;
-  int* perm = s.perm + (size_t)a * r;
-  __shared__ double sv[P1T / 32];
-  __shared__ long long si[P1T / 32];
-  __shared__ double2 colk[2][256 * 2];   // saved pivot columns / L values (r <= 512)
-  __shared__ int sh_two, sh_err;
-  __shared__ double sh_tolz;
-  const double alpha = (1.0 + sqrt(17.0)) / 8.0;
-  const double eps = 0x1p-53;
-  for (int i = threadIdx.x; i < r; i += P1T) perm[i] = i;
-  __syncthreads();
+  __shared__ signed char Jloc[512];
+  __shared__ int np_sh;
   // tolerance r * eps * max|T| over the lower triangle
   double tv = 0.0;
   long long ti = 0;
   for (int e = threadIdx.x; e < r * r; e += P1T) {
     const int i = e % r, j = e / r;
-    if (i >= j) amax_merge(tv, ti, c_abs(W[i + (size_t)j * r]), 0);
+    if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W[i + (size_t)j * r]), 0);
   }
-  block_amax(tv, ti, sv, si);
+  hb::block_amax<P1T>(tv, ti);
+  const double tolz = __dmul_rn(__dmul_rn((double)r, 0x1p-53), tv);
+  const int rc = hb::hebpj_dev<P1T, 512>(W, r, r, M, r, Jloc, &np_sh, tolz);
   if (threadIdx.x == 0) {
-    sh_tolz = __dmul_rn(__dmul_rn((double)r, eps), tv);
-    sh_err = 0;
-  }
-  __syncthreads();
-  int k = 0;
-  while (k < r) {
-    // complete pivoting search
-    double mu1 = -1.0;
-    long long id = 0x7fffffffffffffffll;
-    for (int i = k + threadIdx.x; i < r; i += P1T) amax_merge(mu1, id, fabs(W[i + (size_t)i * r].x), i);
-    block_amax(mu1, id, sv, si);
-    double mu0 = 0.0;
-    long long oidx = 0x7fffffffffffffffll;
-    const long long rem = r - k;
-    for (long long e = threadIdx.x; e < rem * rem; e += P1T) {
-      const int j = k + (int)(e / rem), i = k + (int)(e % rem);
-      if (i > j) amax_merge(mu0, oidx, c_abs(W[i + (size_t)j * r]), (long long)j * r + i);
-    }
-    block_amax(mu0, oidx, sv, si);
-    const double mall = mu0 > mu1 ? mu0 : mu1;
-    if (!(mall > sh_tolz)) {
-      if (threadIdx.x == 0) sh_err = -7;
-      break;
-    }
-    const int two = !(mu1 >= __dmul_rn(alpha, mu0));
-    int src0 = (int)id, src1 = -1;
-    if (two) {
-      src0 = (int)(oidx / r);
-      src1 = (int)(oidx % r);
-    }
-    for (int b = 0; b < (two ? 2 : 1); b++) {
-      const int dst = k + b;
-      int sidx = b == 0 ? src0 : src1;
-      if (b == 1 && sidx == k) sidx = src0;
-      if (sidx != dst) {
-        // swap rows dst, sidx over all columns (rows of L for c < k live below the diagonal)
-        for (int c = threadIdx.x; c < r; c += P1T) {
-          const double2 t = W[dst + (size_t)c * r];
-          W[dst + (size_t)c * r] = W[sidx + (size_t)c * r];
-          W[sidx + (size_t)c * r] = t;
-        }
-        __syncthreads();
-        // swap columns dst, sidx over rows >= k (the live trailing block)
-        for (int i = k + threadIdx.x; i < r; i += P1T) {
-          const double2 t = W[i + (size_t)dst * r];
-          W[i + (size_t)dst * r] = W[i + (size_t)sidx * r];
-          W[i + (size_t)sidx * r] = t;
-        }
-        if (threadIdx.x == 0) {
-          const int t = perm[dst];
-          perm[dst] = perm[sidx];
-          perm[sidx] = t;
-        }
-        __syncthreads();
-      }
-    }
-    if (!two) {
-      const double dk = W[k + (size_t)k * r].x;
-      const double inv = __ddiv_rn(1.0, dk);
-      for (int i = k + 1 + threadIdx.x; i < r; i += P1T) colk[0][i] = W[i + (size_t)k * r];
-      __syncthreads();
-      const long long rm = r - k - 1;
-      for (long long e = threadIdx.x; e < rm * rm; e += P1T) {
-        const int i = k + 1 + (int)(e % rm), j = k + 1 + (int)(e / rm);
-        W[i + (size_t)j * r] = c_sub(W[i + (size_t)j * r], c_scale(c_mul(colk[0][i], c_conj(colk[0][j])), inv));
-      }
-      __syncthreads();
-      for (int i = k + 1 + threadIdx.x; i < r; i += P1T) W[i + (size_t)k * r] = c_scale(colk[0][i], inv);
-      if (threadIdx.x == 0) {
-        bsz[k] = 1;
-        d[k] = dk;
-      }
-      __syncthreads();
-      k += 1;
-    } else {
-      const double ea = W[k + (size_t)k * r].x, ec = W[(k + 1) + (size_t)(k + 1) * r].x;
-      const double2 eb = W[k + (size_t)(k + 1) * r];
-      const double det = __dsub_rn(__dmul_rn(ea, ec), c_abs2(eb));
-      const double inv = __ddiv_rn(1.0, det);
-      for (int i = k + 2 + threadIdx.x; i < r; i += P1T) {
-        const double2 w0 = W[i + (size_t)k * r], w1 = W[i + (size_t)(k + 1) * r];
-        colk[0][i] = w0;
-        colk[1][i] = w1;
-        const double2 l0 = c_scale(c_sub(c_scale(w0, ec), c_mul(w1, c_conj(eb))), inv);
-        const double2 l1 = c_scale(c_sub(c_scale(w1, ea), c_mul(w0, eb)), inv);
-        W[i + (size_t)k * r] = l0;   // L stored in place (the update reads colk)
-        W[i + (size_t)(k + 1) * r] = l1;
-      }
-      __syncthreads();
-      const long long rm = r - k - 2;
-      for (long long e = threadIdx.x; e < rm * rm; e += P1T) {
-        const int i = k + 2 + (int)(e % rm), j = k + 2 + (int)(e / rm);
-        const double2 t = c_add(c_mul(W[i + (size_t)k * r], c_conj(colk[0][j])),
-                                c_mul(W[i + (size_t)(k + 1) * r], c_conj(colk[1][j])));
-        W[i + (size_t)j * r] = c_sub(W[i + (size_t)j * r], t);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double l1, l2;
-        herm2_jacobi_dev(ea, eb, ec, &Ra[4 * k], &l1, &l2);
-        d[k] = l1;
-        d[k + 1] = l2;
-        W[(k + 1) + (size_t)k * r] = c_mk(0.0, 0.0);  // L's 2x2 diagonal block is I
-        bsz[k] = 2;
-        bsz[k + 1] = 0;
-      }
-      __syncthreads();
-      k += 2;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) s.info[a] = sh_err;
-  if (sh_err) return;
-  // signs and sorted row positions (+ first, stable)
-  __shared__ int rowpos[512];
-  __shared__ signed char sgn[512];
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < r; i++) sgn[i] = d[i] > 0.0 ? 1 : -1;
-    int np = 0;
-    for (int i = 0; i < r; i++)
-      if (sgn[i] > 0) rowpos[i] = np++;
-    int q = np;
-    for (int i = 0; i < r; i++)
-      if (sgn[i] < 0) rowpos[i] = q++;
-    s.npos[a] = np;
-  }
-  __syncthreads();
-  // Mtilde(rowpos(i), perm[l]) = row i of diag(|d|^1/2) R^* L^*, column l
-  for (int e = threadIdx.x; e < r * r; e += P1T) {
-    const int i = e % r, l = e / r;
-    auto Lh = [&](int row, int col) -> double2 {  // (L^*)(row, col) = conj(L(col, row))
-      if (row == col) return c_mk(1.0, 0.0);
-      if (col < row) return c_mk(0.0, 0.0);
-      return c_conj(W[col + (size_t)row * r]);
-    };
-    double2 y;
-    if (bsz[i] == 1) {
-      y = c_scale(Lh(i, l), __dsqrt_rn(fabs(d[i])));
-    } else if (bsz[i] == 2) {
-      const double2* R = &Ra[4 * i];
-      const double2 x0 = Lh(i, l), x1 = Lh(i + 1, l);
-      y = c_scale(c_add(c_mul(c_conj(R[0]), x0), c_mul(c_conj(R[1]), x1)), __dsqrt_rn(fabs(d[i])));
-    } else {
-      const double2* R = &Ra[4 * (i - 1)];
-      const double2 x0 = Lh(i - 1, l), x1 = Lh(i, l);
-      y = c_scale(c_add(c_mul(c_conj(R[2]), x0), c_mul(c_conj(R[3]), x1)), __dsqrt_rn(fabs(d[i])));
-    }
-    M[rowpos[i] + (size_t)perm[l] * r] = y;
+    s.info[a] = rc;
+    s.npos[a] = rc ? 0 : np_sh;
   }
 }
 

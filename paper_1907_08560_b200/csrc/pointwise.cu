@@ -271,10 +271,353 @@ __global__ void __launch_bounds__(NT) k_pair_step(StepArgs a) {
   if (C > 1) cluster_wait();
 }
 
+// Persistent, software-pipelined variant: a fixed set of clusters (as many as
+// are co-resident) walks the step's pairs pair = cluster_id + it * nclusters;
+// each CTA double-buffers its slices so the TMA load of pair it+1 is in flight
+// while pair it is reduced, transformed, updated and stored.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_pair_step_pipe(StepArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar[3];
+  __shared__ double red[NT / 32][8];
+  __shared__ double part[2][8];
+  __shared__ double tot[8];
+  __shared__ double zsh[8];
+  __shared__ int kind_sh;
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const long long nclusters = gridDim.x / C;
+  const long long cid = blockIdx.x / C;
+  const long long npairs = a.n / 2;
+
+  const long long r0 = (long long)rank * a.cs;
+  const long long r1 = min(a.m, r0 + a.cs);
+  const long long len = r1 > r0 ? r1 - r0 : 0;
+  const long long z0 = (long long)rank * a.zs;
+  const long long z1 = min(a.n, z0 + a.zs);
+  const long long zlen = z1 > z0 ? z1 - z0 : 0;
+  const unsigned bytes = (unsigned)(len * 16), zb = (unsigned)(zlen * 16);
+
+  double2* buf0 = reinterpret_cast<double2*>(smem_raw);
+  double2* buf1 = buf0 + 4 * a.cs;
+  double2* sZp = buf1 + 4 * a.cs;
+  double2* sZq = sZp + a.zs;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue_load = [&](long long pr, double2* buf, unsigned long long* b) {
+    long long p, q;
+    rr_pair(a.n, a.s, pr, &p, &q);
+    mbar_expect_tx(b, 4u * bytes);
+    if (len > 0) {
+      bulk_g2s(buf, a.F + p * a.ldm + r0, bytes, b);
+      bulk_g2s(buf + a.cs, a.F + q * a.ldm + r0, bytes, b);
+      bulk_g2s(buf + 2 * a.cs, a.G + p * a.ldm + r0, bytes, b);
+      bulk_g2s(buf + 3 * a.cs, a.G + q * a.ldm + r0, bytes, b);
+    }
+  };
+
+  if (tid == 0 && cid < npairs) issue_load(cid, buf0, &bar[0]);
+  unsigned zpar = 0;
+  const long long npos_loc = a.npos - r0;
+  int it = 0;
+  for (long long pair = cid; pair < npairs; pair += nclusters, it++) {
+    const int b = it & 1;
+    double2* buf = b ? buf1 : buf0;
+    const long long nxt = pair + nclusters;
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous stores done reading smem
+      fence_proxy_async();
+      if (nxt < npairs) issue_load(nxt, b ? buf0 : buf1, &bar[b ^ 1]);
+    }
+    mbar_wait(&bar[b], (unsigned)((it >> 1) & 1));
+    long long p, q;
+    rr_pair(a.n, a.s, pair, &p, &q);
+    double2* sFp = buf;
+    double2* sFq = buf + a.cs;
+    double2* sGp = buf + 2 * a.cs;
+    double2* sGq = buf + 3 * a.cs;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (long long i = tid; i < len; i += NT) {
+      const double2 fp = sFp[i], fq = sFq[i], gp = sGp[i], gq = sGq[i];
+      const double sgn = (i < npos_loc) ? 1.0 : -1.0;
+      acc[0] = fma(sgn, fma(fp.x, fp.x, fp.y * fp.y), acc[0]);
+      acc[1] = fma(sgn, fma(fq.x, fq.x, fq.y * fq.y), acc[1]);
+      acc[2] = fma(sgn, fma(fp.x, fq.x, fp.y * fq.y), acc[2]);
+      acc[3] = fma(sgn, fma(fp.x, fq.y, -fp.y * fq.x), acc[3]);
+      acc[4] = fma(gp.x, gp.x, fma(gp.y, gp.y, acc[4]));
+      acc[5] = fma(gq.x, gq.x, fma(gq.y, gq.y, acc[5]));
+      acc[6] = fma(gp.x, gq.x, fma(gp.y, gq.y, acc[6]));
+      acc[7] = fma(gp.x, gq.y, fma(-gp.y, gq.x, acc[7]));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; k++) red[warp][k] = acc[k];
+    }
+    __syncthreads();
+    if (tid < 8) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NT / 32; w++) s += red[w][tid];
+      part[b][tid] = s;
+    }
+    if (C > 1) {
+      cluster.sync();
+      if (tid < 8) {
+        double s = 0.0;
+        for (int r = 0; r < C; r++) s += *cluster.map_shared_rank(&part[b][tid], r);
+        tot[tid] = s;
+      }
+    } else {
+      __syncthreads();
+      if (tid < 8) tot[tid] = part[b][tid];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const HZOut z = hz2x2_dev(tot, a.tol, a.literal);
+      zsh[0] = z.z11.re; zsh[1] = z.z11.im; zsh[2] = z.z21.re; zsh[3] = z.z21.im;
+      zsh[4] = z.z12.re; zsh[5] = z.z12.im; zsh[6] = z.z22.re; zsh[7] = z.z22.im;
+      kind_sh = z.kind;
+      if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
+        if (zlen > 0) {
+          mbar_expect_tx(&bar[2], 2u * zb);
+          bulk_g2s(sZp, a.Z + p * a.ldn + z0, zb, &bar[2]);
+          bulk_g2s(sZq, a.Z + q * a.ldn + z0, zb, &bar[2]);
+        } else {
+          mbar_expect_tx(&bar[2], 0u);
+        }
+      }
+      if (rank == 0) {
+        if (z.kind < 0) atomicCAS(&a.cnt->err, 0, z.kind);
+        if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
+          atomicAdd(&a.cnt->all, 1ull);
+          if (z.kind == KIND_BIG) atomicAdd(&a.cnt->big, 1ull);
+        }
+        atomicMax(&a.cnt->off_bits, (unsigned long long)__double_as_longlong(z.off));
+      }
+    }
+    __syncthreads();
+    const int kind = kind_sh;
+    if (kind == KIND_SMALL || kind == KIND_BIG) {
+      const Cplx z11{zsh[0], zsh[1]}, z21{zsh[2], zsh[3]}, z12{zsh[4], zsh[5]}, z22{zsh[6], zsh[7]};
+      for (long long i = tid; i < len; i += NT) {
+        double2 fp = sFp[i], fq = sFq[i], gp = sGp[i], gq = sGq[i];
+        rot_row(fp, fq, z11, z21, z12, z22);
+        rot_row(gp, gq, z11, z21, z12, z22);
+        sFp[i] = fp; sFq[i] = fq; sGp[i] = gp; sGq[i] = gq;
+      }
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0 && len > 0) {
+        bulk_s2g(a.F + p * a.ldm + r0, sFp, bytes);
+        bulk_s2g(a.F + q * a.ldm + r0, sFq, bytes);
+        bulk_s2g(a.G + p * a.ldm + r0, sGp, bytes);
+        bulk_s2g(a.G + q * a.ldm + r0, sGq, bytes);
+        bulk_commit();
+      }
+      mbar_wait(&bar[2], zpar);
+      zpar ^= 1u;
+      for (long long i = tid; i < zlen; i += NT) {
+        double2 zp = sZp[i], zq = sZq[i];
+        rot_row(zp, zq, z11, z21, z12, z22);
+        sZp[i] = zp; sZq[i] = zq;
+      }
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0 && zlen > 0) {
+        bulk_s2g(a.Z + p * a.ldn + z0, sZp, zb);
+        bulk_s2g(a.Z + q * a.ldn + z0, sZq, zb);
+        bulk_commit();
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+  if (C > 1) cluster.sync();  // no CTA leaves while a peer may still read its part[]
+}
+
+// Two-pass variant (no shared-memory staging): pass 1 streams the slice from HBM
+// forming the Grams (loads marked L2::evict_last so the lines stay in L2), pass 2
+// re-reads the slice from L2, applies Z' and streams it back.  No smem for data ->
+// occupancy is bounded by registers, so more pairs are in flight per SM to hide
+// the per-pair reduce -> transform latency.  HBM traffic stays 128m+64n per
+// transformed pair when the in-flight slices fit in L2 (126 MB).
+struct C2 {
+  double2 a, b;  // two consecutive rows
+};
+__device__ __forceinline__ C2 ld2_keep(const double2* p) {  // 32-B load, keep in L2
+  unsigned long long x0, x1, x2, x3;
+  asm volatile("ld.global.L1::no_allocate.L2::evict_last.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3)
+               : "l"(p));
+  C2 r;
+  r.a = make_double2(__longlong_as_double(x0), __longlong_as_double(x1));
+  r.b = make_double2(__longlong_as_double(x2), __longlong_as_double(x3));
+  return r;
+}
+__device__ __forceinline__ C2 ld2_last(const double2* p) {  // 32-B load, last use
+  unsigned long long x0, x1, x2, x3;
+  asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3)
+               : "l"(p));
+  C2 r;
+  r.a = make_double2(__longlong_as_double(x0), __longlong_as_double(x1));
+  r.b = make_double2(__longlong_as_double(x2), __longlong_as_double(x3));
+  return r;
+}
+__device__ __forceinline__ void st2(double2* p, const C2& v) {
+  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(__double_as_longlong(v.a.x)),
+               "l"(__double_as_longlong(v.a.y)), "l"(__double_as_longlong(v.b.x)), "l"(__double_as_longlong(v.b.y))
+               : "memory");
+}
+__device__ __forceinline__ void gram_row(double* acc, const double2& fp, const double2& fq, const double2& gp,
+                                         const double2& gq, double sgn) {
+  acc[0] = fma(sgn, fma(fp.x, fp.x, fp.y * fp.y), acc[0]);
+  acc[1] = fma(sgn, fma(fq.x, fq.x, fq.y * fq.y), acc[1]);
+  acc[2] = fma(sgn, fma(fp.x, fq.x, fp.y * fq.y), acc[2]);
+  acc[3] = fma(sgn, fma(fp.x, fq.y, -fp.y * fq.x), acc[3]);
+  acc[4] = fma(gp.x, gp.x, fma(gp.y, gp.y, acc[4]));
+  acc[5] = fma(gq.x, gq.x, fma(gq.y, gq.y, acc[5]));
+  acc[6] = fma(gp.x, gq.x, fma(gp.y, gq.y, acc[6]));
+  acc[7] = fma(gp.x, gq.y, fma(-gp.y, gq.x, acc[7]));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_pair_step_2p(StepArgs a) {
+  __shared__ double red[NT / 32][8];
+  __shared__ double part[8];
+  __shared__ double tot[8];
+  __shared__ double zsh[8];
+  __shared__ int kind_sh;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const long long pair = blockIdx.x / C;
+  long long p, q;
+  rr_pair(a.n, a.s, pair, &p, &q);
+  const long long r0 = (long long)rank * a.cs;
+  const long long r1 = min(a.m, r0 + a.cs);
+  const long long z0 = (long long)rank * a.zs;
+  const long long z1 = min(a.n, z0 + a.zs);
+  double2* Fp = a.F + p * a.ldm;
+  double2* Fq = a.F + q * a.ldm;
+  double2* Gp = a.G + p * a.ldm;
+  double2* Gq = a.G + q * a.ldm;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // rows in pairs (2i, 2i+1): r0 even (cs even), ld multiple of 16 -> 32-B aligned
+  const long long h0 = r0 >> 1, h1 = (r1 + 1) >> 1;
+#pragma unroll 2
+  for (long long h = h0 + tid; h < h1; h += NT) {
+    const C2 fp = ld2_keep(Fp + 2 * h), fq = ld2_keep(Fq + 2 * h), gp = ld2_keep(Gp + 2 * h), gq = ld2_keep(Gq + 2 * h);
+    gram_row(acc, fp.a, fq.a, gp.a, gq.a, (2 * h < a.npos) ? 1.0 : -1.0);
+    gram_row(acc, fp.b, fq.b, gp.b, gq.b, (2 * h + 1 < a.npos) ? 1.0 : -1.0);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) red[warp][k] = acc[k];
+  }
+  __syncthreads();
+  if (tid < 8) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; w++) s += red[w][tid];
+    part[tid] = s;
+  }
+  if (C > 1) {
+    cluster.sync();
+    if (tid < 8) {
+      double s = 0.0;
+      for (int r = 0; r < C; r++) s += *cluster.map_shared_rank(&part[tid], r);
+      tot[tid] = s;
+    }
+    cluster_arrive_relaxed();
+  } else {
+    __syncthreads();
+    if (tid < 8) tot[tid] = part[tid];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const HZOut z = hz2x2_dev(tot, a.tol, a.literal);
+    zsh[0] = z.z11.re; zsh[1] = z.z11.im; zsh[2] = z.z21.re; zsh[3] = z.z21.im;
+    zsh[4] = z.z12.re; zsh[5] = z.z12.im; zsh[6] = z.z22.re; zsh[7] = z.z22.im;
+    kind_sh = z.kind;
+    if (rank == 0) {
+      if (z.kind < 0) atomicCAS(&a.cnt->err, 0, z.kind);
+      if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
+        atomicAdd(&a.cnt->all, 1ull);
+        if (z.kind == KIND_BIG) atomicAdd(&a.cnt->big, 1ull);
+      }
+      atomicMax(&a.cnt->off_bits, (unsigned long long)__double_as_longlong(z.off));
+    }
+  }
+  __syncthreads();
+  const int kind = kind_sh;
+  if (kind == KIND_SMALL || kind == KIND_BIG) {
+    const Cplx z11{zsh[0], zsh[1]}, z21{zsh[2], zsh[3]}, z12{zsh[4], zsh[5]}, z22{zsh[6], zsh[7]};
+#pragma unroll 2
+    for (long long h = h0 + tid; h < h1; h += NT) {
+      C2 fp = ld2_last(Fp + 2 * h), fq = ld2_last(Fq + 2 * h), gp = ld2_last(Gp + 2 * h), gq = ld2_last(Gq + 2 * h);
+      rot_row(fp.a, fq.a, z11, z21, z12, z22);
+      rot_row(fp.b, fq.b, z11, z21, z12, z22);
+      rot_row(gp.a, gq.a, z11, z21, z12, z22);
+      rot_row(gp.b, gq.b, z11, z21, z12, z22);
+      st2(Fp + 2 * h, fp); st2(Fq + 2 * h, fq); st2(Gp + 2 * h, gp); st2(Gq + 2 * h, gq);
+    }
+    double2* Zp = a.Z + p * a.ldn;
+    double2* Zq = a.Z + q * a.ldn;
+#pragma unroll 2
+    for (long long i = z0 + tid; i < z1; i += NT) {
+      double2 zp = Zp[i], zq = Zq[i];
+      rot_row(zp, zq, z11, z21, z12, z22);
+      Zp[i] = zp; Zq[i] = zq;
+    }
+  }
+  if (C > 1) cluster_wait();
+}
+
 // ------------------------------------------------------------------ host side
 typedef void (*StepKernel)(StepArgs);
 
-static StepKernel pick_kernel(int threads) {
+static StepKernel pick_kernel(int threads, int kind) {
+  if (kind == 2) {
+    switch (threads) {
+      case 32: return k_pair_step_2p<32>;
+      case 64: return k_pair_step_2p<64>;
+      case 128: return k_pair_step_2p<128>;
+      case 512: return k_pair_step_2p<512>;
+      default: return k_pair_step_2p<256>;
+    }
+  }
+  if (kind == 3) {
+    switch (threads) {
+      case 32: return k_pair_step_pipe<32>;
+      case 64: return k_pair_step_pipe<64>;
+      case 128: return k_pair_step_pipe<128>;
+      case 512: return k_pair_step_pipe<512>;
+      default: return k_pair_step_pipe<256>;
+    }
+  }
   switch (threads) {
     case 32: return k_pair_step<32>;
     case 64: return k_pair_step<64>;
@@ -286,13 +629,23 @@ static StepKernel pick_kernel(int threads) {
 
 ghsvd_status pw_configure(Ctx* ctx) {
   const int64_t m = ctx->m, n = ctx->n;
+  // kernel kinds (ghsvd_options.kernel): 1 = one cluster per pair (TMA staging),
+  // 2 = two-pass through L2 (no staging, default), 3 = persistent pipelined TMA
+  const int kk = ctx->o.kernel == 0 ? 2 : ctx->o.kernel;
+  if (kk < 1 || kk > 3) {
+    ctx->err = "kernel must be 0..3";
+    return GHSVD_E_INVALID_ARG;
+  }
+  const bool pipe = kk == 3;
+  const int nbuf = kk == 3 ? 8 : (kk == 1 ? 4 : 0);   // F/G slice buffers (x cs) per CTA
   int C = ctx->o.cluster;
   if (C <= 0) {
-    // smallest power-of-two cluster whose per-CTA slices fit ~100 KB of smem
+    // smallest power-of-two cluster whose per-CTA slices fit the smem budget
+    const int64_t budget = pipe ? 200 * 1024 : 100 * 1024;
     C = 1;
     while (C < 16) {
       const int64_t cs = (m + C - 1) / C, zs = (n + C - 1) / C;
-      if ((4 * cs + 2 * zs) * 16 <= 100 * 1024) break;
+      if ((nbuf * cs + (nbuf ? 2 * zs : 0)) * 16 <= budget || (nbuf == 0 && C == 8)) break;
       C *= 2;
     }
   }
@@ -300,7 +653,7 @@ ghsvd_status pw_configure(Ctx* ctx) {
     ctx->err = "cluster must be 1, 2, 4, 8 or 16";
     return GHSVD_E_INVALID_ARG;
   }
-  const int64_t cs = (m + C - 1) / C, zs = (n + C - 1) / C;
+  const int64_t cs = round_up((m + C - 1) / C, 2), zs = (n + C - 1) / C;
   int T = ctx->o.threads;
   if (T <= 0) {
     T = 256;
@@ -310,17 +663,40 @@ ghsvd_status pw_configure(Ctx* ctx) {
     ctx->err = "threads must be 32, 64, 128, 256 or 512";
     return GHSVD_E_INVALID_ARG;
   }
-  const size_t smem = (size_t)(4 * cs + 2 * zs) * 16;
+  const size_t smem = nbuf ? (size_t)(nbuf * cs + 2 * zs) * 16 : 0;
   if (smem > 220 * 1024) {
     ctx->err = "pointwise slices exceed shared memory; use a larger cluster";
     return GHSVD_E_INVALID_ARG;
   }
-  StepKernel k = pick_kernel(T);
+  StepKernel k = pick_kernel(T, kk);
   GH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (C > 8) GH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   ctx->pw_cluster = C;
   ctx->pw_threads = T;
   ctx->pw_smem = smem;
+  ctx->pw_pipe = pipe;
+  ctx->pw_kind = kk;
+  ctx->pw_nclusters = n / 2;
+  if (pipe) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n / 2 * C), 1, 1);
+    cfg.blockDim = dim3(T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    GH_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+    if (ncl < 1) {
+      ctx->err = "pointwise: no cluster of this shape fits on the device";
+      return GHSVD_E_INVALID_ARG;
+    }
+    ctx->pw_nclusters = std::min<int64_t>(ncl, n / 2);
+  }
   return GHSVD_OK;
 }
 
@@ -336,13 +712,13 @@ static ghsvd_status launch_step(Ctx* ctx, cudaStream_t st, int64_t s) {
   a.npos = ctx->npos;
   a.s = s;
   const int C = ctx->pw_cluster;
-  a.cs = (ctx->m + C - 1) / C;
+  a.cs = round_up((ctx->m + C - 1) / C, 2);
   a.zs = (ctx->n + C - 1) / C;
   a.tol = (ctx->o.eps > 0 ? ctx->o.eps : 0x1p-53) * sqrt((double)ctx->n);
   a.literal = ctx->o.criterion == GHSVD_CRIT_LITERAL;
   a.cnt = ctx->cnt;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(ctx->n / 2 * C), 1, 1);
+  cfg.gridDim = dim3((unsigned)(ctx->pw_nclusters * C), 1, 1);
   cfg.blockDim = dim3(ctx->pw_threads, 1, 1);
   cfg.dynamicSmemBytes = ctx->pw_smem;
   cfg.stream = st;
@@ -353,7 +729,7 @@ static ghsvd_status launch_step(Ctx* ctx, cudaStream_t st, int64_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  GH_CUDA(cudaLaunchKernelEx(&cfg, pick_kernel(ctx->pw_threads), a));
+  GH_CUDA(cudaLaunchKernelEx(&cfg, pick_kernel(ctx->pw_threads, ctx->pw_kind), a));
   return GHSVD_OK;
 }
 
@@ -370,7 +746,7 @@ ghsvd_status pw_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
 ghsvd_status pw_sweep_launch(Ctx* ctx) {
   if (!ctx->o.use_graph) return pw_run_steps(ctx, 0, ctx->n - 1);
   const int64_t key = (int64_t)(uintptr_t)ctx->F ^ ((int64_t)ctx->n << 40) ^
-                      ((int64_t)ctx->pw_cluster << 56) ^ ((int64_t)ctx->pw_threads << 48) ^
+                      ((int64_t)ctx->pw_cluster << 56) ^ ((int64_t)ctx->pw_threads << 48) ^ ((int64_t)ctx->pw_kind << 45) ^
                       ctx->npos * 1315423911ll ^ ctx->m * 2654435761ll;
   if (!ctx->graph || ctx->graph_key != key) {
     if (ctx->graph) {

@@ -47,7 +47,7 @@ class Options(ctypes.Structure):
                 ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("variant", ctypes.c_int),
                 ("ordering", ctypes.c_int), ("nblocks", ctypes.c_int), ("max_sweeps", ctypes.c_int),
                 ("criterion", ctypes.c_int), ("eps", ctypes.c_double), ("cluster", ctypes.c_int),
-                ("threads", ctypes.c_int), ("use_graph", ctypes.c_int)]
+                ("threads", ctypes.c_int), ("use_graph", ctypes.c_int), ("kernel", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
                 ("transforms_all", ctypes.c_uint64), ("transforms_big", ctypes.c_uint64),
                 ("seconds", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
                 ("launches", ctypes.c_uint64), ("alg_bytes", ctypes.c_uint64),
-                ("max_offdiag_last", ctypes.c_double),
+                ("alg_flops", ctypes.c_double), ("max_offdiag_last", ctypes.c_double),
                 ("all_per_sweep", ctypes.c_uint64 * 64), ("big_per_sweep", ctypes.c_uint64 * 64)]
 
     def todict(self):
@@ -64,7 +64,7 @@ class Stats(ctypes.Structure):
                 "pairs_visited": int(self.pairs_visited), "transforms_all": int(self.transforms_all),
                 "transforms_big": int(self.transforms_big), "seconds": self.seconds,
                 "kernel_seconds": self.kernel_seconds, "launches": int(self.launches),
-                "alg_bytes": int(self.alg_bytes),
+                "alg_bytes": int(self.alg_bytes), "alg_flops": self.alg_flops,
                 "max_offdiag_last": self.max_offdiag_last,
                 "all_per_sweep": [int(v) for v in self.all_per_sweep[:k]],
                 "big_per_sweep": [int(v) for v in self.big_per_sweep[:k]]}
@@ -152,7 +152,7 @@ class Context:
     def __init__(self, m: int, n: int, nl: int = 0, *, variant: str = "pointwise", device: int = 0,
                  stream=None, world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  nblocks: int = 0, max_sweeps: int = 30, criterion: str = "relative", eps: float = 0.0,
-                 cluster: int = 0, threads: int = 0, use_graph: bool = True):
+                 cluster: int = 0, threads: int = 0, use_graph: bool = True, kernel: int = 0):
         import torch
         L = load()
         self._L = L
@@ -176,6 +176,7 @@ class Context:
         o.cluster = cluster
         o.threads = threads
         o.use_graph = 1 if use_graph else 0
+        o.kernel = kernel
         self.opts = o
         nbytes = L.ghsvd_workspace_bytes(ctypes.byref(o), m, n, nl)
         if nbytes == 0:

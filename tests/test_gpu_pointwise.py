@@ -101,14 +101,15 @@ def test_bad_J_rejected(gh):
 
 
 # ------------------------------------------------------------------ single steps
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 @pytest.mark.parametrize("m,n,cluster", [(64, 32, 1), (200, 64, 2), (333, 40, 4), (1000, 100, 8), (1030, 48, 16),
                                          (17, 16, 1)])
-def test_steps_match_oracle(gh, m, n, cluster):
+def test_steps_match_oracle(gh, m, n, cluster, kernel):
     """a1-a4 parity: after each of the first steps the GPU's F', G', Z' equal the oracle's
     elementwise (same inputs from get_factors, same pair ordering); ragged m and all
     cluster sizes (slices crossing tile/cluster boundaries)."""
     P = inputs.random_pencil(100 + m, m, n, 0.45)
-    ctx = gh.Context(m, n, cluster=cluster)
+    ctx = gh.Context(m, n, cluster=cluster, kernel=kernel)
     ctx.set_factors(P.F, P.J, P.G)
     F0, J0, G0, _ = ctx.get_factors()
     Zo = np.eye(n, dtype=complex)
@@ -160,6 +161,13 @@ def test_converged_eigenvalues_match_oracle(gh, which, m, n):
         assert relerr(lam, P.lam_true) <= 1e-9
     assert residual(P.F, P.J, P.G, lam, Z) <= 1e-12 * n
     assert np.allclose(sf ** 2 + sg ** 2, 1.0, atol=8 * EPS)
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3])
+def test_kernel_variants_converge(gh, kernel):
+    P = inputs.known_hyperbolic(31, 300, 96, 0.5)
+    F0, J0, G0, st, lam, sf, sg, Z = _gpu_run(gh, P, kernel=kernel)
+    assert st["converged"] and relerr(lam, P.lam_true) <= 1e-9
 
 
 def test_graph_and_plain_launches_bitwise_equal(gh):

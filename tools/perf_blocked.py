@@ -1,0 +1,17 @@
+"""Time blocked BO sweeps on config 3 (exploration)."""
+import json, os, sys, warnings
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1907_08560_b200 import build, ghsvd, inputs
+build.build()
+warnings.simplefilter("ignore")
+kind, at = inputs.make_config(3, backend="torch")
+NA, NL, NG = at.A.shape
+sweeps = int(os.environ.get("SWEEPS", "1"))
+for nb in [int(x) for x in os.environ.get("NBLK", "128").split(",")]:
+    ctx = ghsvd.Context(2 * NA * NL, NG, NL, variant="bo", nblocks=nb, max_sweeps=sweeps)
+    ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    st = ctx.sweep()
+    print(json.dumps({"nblk": nb, "sweeps": st["sweeps"], "converged": st["converged"], "kernel_s": st["kernel_seconds"],
+                      "s_per_sweep": st["kernel_seconds"] / st["sweeps"], "TFLOPs": st["alg_flops"] / st["kernel_seconds"] / 1e12,
+                      "big": st["big_per_sweep"]}), flush=True)
+    ctx.close()

@@ -24,16 +24,16 @@ if "--peaks" in sys.argv:
 kind, at = inputs.make_config(3, backend="torch")
 NA, NL, NG = at.A.shape
 m, n = 2 * NA * NL, NG
-cfgs = [(8, 256), (16, 256), (4, 512), (16, 128), (8, 512)]
+cfgs = [(8, 256, 2), (8, 128, 2), (4, 256, 2), (16, 256, 2), (8, 512, 2), (4, 512, 2), (8, 256, 1)]
 for arg in sys.argv[1:]:
     if arg.startswith("--cfg="):
         cfgs = [tuple(int(x) for x in c.split("x")) for c in arg[6:].split(",")]
-for C, T in cfgs:
-    ctx = ghsvd.Context(m, n, NL, cluster=C, threads=T, max_sweeps=1)
+for C, T, K in cfgs:
+    ctx = ghsvd.Context(m, n, NL, cluster=C, threads=T, max_sweeps=1, kernel=K)
     ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
     import warnings; warnings.simplefilter("ignore")
     st = ctx.sweep()
     gbs = st["alg_bytes"] / st["kernel_seconds"] / 1e9
-    print(json.dumps({"C": C, "T": T, "sweep_s": st["kernel_seconds"], "GBs": gbs,
+    print(json.dumps({"C": C, "T": T, "K": K, "sweep_s": st["kernel_seconds"], "GBs": gbs,
                       "us_per_launch": st["kernel_seconds"] / st["launches"] * 1e6}), flush=True)
     ctx.close()

@@ -1,0 +1,22 @@
+"""Run a few pointwise step launches on config 3 (for ncu captures of k_pair_step).
+usage: python tools/profile_step.py [--kernel K] [--cluster C] [--threads T] [--steps S]"""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1907_08560_b200 import build, ghsvd, inputs
+ap = argparse.ArgumentParser()
+ap.add_argument("--kernel", type=int, default=1)
+ap.add_argument("--cluster", type=int, default=0)
+ap.add_argument("--threads", type=int, default=0)
+ap.add_argument("--steps", type=int, default=3)
+a = ap.parse_args()
+build.build()
+kind, at = inputs.make_config(3, backend="torch")
+NA, NL, NG = at.A.shape
+ctx = ghsvd.Context(2 * NA * NL, NG, NL, kernel=a.kernel, cluster=a.cluster, threads=a.threads)
+ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(torch.cuda.current_stream())
+ctx.run_steps(0, a.steps)
+e1.record(torch.cuda.current_stream()); torch.cuda.synchronize()
+print("steps", a.steps, "ms/step", e0.elapsed_time(e1) / a.steps)

@@ -72,6 +72,7 @@ typedef struct {
   int use_graph;       /* capture each sweep's steps in a CUDA graph (default 1) */
   int kernel;          /* pointwise step kernel: 0 = auto (= 2), 1 = one cluster per pair, TMA-staged slices;
                           2 = two-pass through L2 (default); 3 = persistent pipelined TMA */
+  int detail_timing;   /* blocked: CUDA events around every kernel (fills t_* in ghsvd_stats) */
 } ghsvd_options;
 
 typedef struct {
@@ -86,6 +87,9 @@ typedef struct {
   uint64_t alg_bytes;         /* algorithmic HBM bytes of the sweeps: per transformed pair
                                  128m+64n, per skipped pair 64m */
   double alg_flops;           /* algorithmic FP64 flops (blocked: Hermitian block Grams + updates) */
+  double t_gram, t_pivot, t_update, t_exchange;  /* blocked: summed device time per kernel kind
+                                                    (CUDA events, only if opts.detail_timing) */
+  double flops_gram, flops_update;               /* blocked: algorithmic flops of those kernels */
   double max_offdiag_last;    /* max scaled off-diagonal measure seen in the last sweep */
   uint64_t all_per_sweep[64]; /* per-sweep counters (first 64 sweeps) */
   uint64_t big_per_sweep[64];
@@ -166,6 +170,20 @@ ghsvd_status ghsvd_get_transformed(ghsvd_ctx ctx, void* F, int64_t ldf, void* G,
  * < 0 error).  All three are DEVICE pointers.  tol = eps*sqrt(n). */
 ghsvd_status ghsvd_hz2x2_batch(ghsvd_ctx ctx, int64_t count, const double* in, double tol,
                                int criterion, double* out, int* kind);
+
+/* Multi-GPU helpers (blocked variant, Sec 6.4.3).  Host-only,
+ * no GPU needed.  Rank r owns round-robin slots [r K, (r+1) K) of each block step,
+ * K = nblk / (2 world).
+ * ghsvd_block_owner: rank owning block column b in block step s (-1 on bad args).
+ * ghsvd_exchange_plan: blocks `rank` sends (to send_peer) / receives (from recv_peer)
+ *   between block steps s and s_next; arrays of nblk entries; 0 or -1.
+ * ghsvd_nccl_unique_id: 128-byte ncclUniqueId for opts.nccl_id (rank 0 creates it and
+ *   broadcasts it); 0, or -4 if NCCL cannot be loaded. */
+int ghsvd_block_owner(int nblk, int world, int s, int b);
+int ghsvd_exchange_plan(int nblk, int world, int rank, int s, int s_next, int64_t* send_blk,
+                        int64_t* send_peer, int64_t* nsend, int64_t* recv_blk, int64_t* recv_peer,
+                        int64_t* nrecv);
+int ghsvd_nccl_unique_id(void* out128);
 
 const char* ghsvd_last_error(ghsvd_ctx ctx);
 void ghsvd_destroy(ghsvd_ctx ctx);

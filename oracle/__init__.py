@@ -93,6 +93,9 @@ def lib():
         L.or_hz_blocked.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, I64, Ci, D, Ci, Ci, Ci,
                                     ctypes.POINTER(_Stats)]
         L.or_extract.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, P, P, P, P, I64]
+        L.or_block_partition.argtypes = [I64, I64, P, P]
+        L.or_block_pair.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, I64, I64, I64, I64, Ci, D, Ci,
+                                    ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.or_hebpj.argtypes = [I64, P, I64, P, I64, P, ctypes.POINTER(I64)]
         L.or_pchol.argtypes = [I64, P, I64, P, I64]
         L.or_factor.argtypes = [I64, I64, I64, P, P, P, P, P, P, P, P, P]
@@ -182,6 +185,26 @@ def hz_blocked(F, J, G, nblk, inner_sweeps=1, eps=EPS, criterion=CRIT_RELATIVE, 
                              inner_sweeps, eps, criterion, cmax, nthreads, ctypes.byref(st)),
          "hz_blocked")
     return F, G, Z, st.todict()
+
+
+def block_partition(n, nblk):
+    start = np.zeros(nblk, np.int64)
+    width = np.zeros(nblk, np.int64)
+    _chk(lib().or_block_partition(n, nblk, _ptr(start), _ptr(width)), "block_partition")
+    return start, width
+
+
+def block_pair(F, J, G, Z, p0, wp, q0, wq, inner_sweeps=1, eps=EPS, criterion=CRIT_RELATIVE):
+    """One block pivot IN PLACE on Fortran-ordered complex128 arrays F, G (m x n), Z (n x n).
+    Returns (all, big)."""
+    for X in (F, G, Z):
+        assert X.dtype == np.complex128 and X.flags.f_contiguous
+    J = np.ascontiguousarray(J, dtype=np.int8)
+    m, n = F.shape
+    a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+    _chk(lib().or_block_pair(m, n, _ptr(F), m, _ptr(J), _ptr(G), m, _ptr(Z), n, p0, wp, q0, wq, inner_sweeps,
+                             eps, criterion, ctypes.byref(a), ctypes.byref(b)), "block_pair")
+    return a.value, b.value
 
 
 def extract(F, J, G, Zp):

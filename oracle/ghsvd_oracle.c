@@ -615,6 +615,20 @@ done:
   return rc;
 }
 
+int or_block_partition(int64_t n, int64_t nblk, int64_t *start, int64_t *width) {
+  if (nblk < 1 || nblk > n) return OR_E_ARG;
+  block_part(n, nblk, start, width);
+  return OR_OK;
+}
+
+int or_block_pair(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
+                  orc *G, int64_t ldg, orc *Z, int64_t ldz, int64_t p0, int64_t wp,
+                  int64_t q0, int64_t wq, int inner_sweeps, double eps, int criterion,
+                  int64_t *all, int64_t *big) {
+  return block_pivot(m, n, F, ldf, J, G, ldg, Z, ldz, p0, wp, q0, wq, inner_sweeps, eps,
+                     criterion, all, big);
+}
+
 int or_hz_blocked(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
                   orc *G, int64_t ldg, orc *Z, int64_t ldz, int64_t nblk,
                   int inner_sweeps, double eps, int criterion, int cmax,

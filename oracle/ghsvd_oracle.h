@@ -83,6 +83,14 @@ int or_hz_blocked(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
                   int inner_sweeps, double eps, int criterion, int cmax,
                   int nthreads, or_stats *st);
 
+/* The Sec 6.4.1 partition (widths w or w-1, non-increasing) and one block pivot
+ * (Sec 6.4.2-6.4.3) of block columns [p0, p0+wp) and [q0, q0+wq), in place. */
+int or_block_partition(int64_t n, int64_t nblk, int64_t *start, int64_t *width);
+int or_block_pair(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
+                  orc *G, int64_t ldg, orc *Z, int64_t ldz, int64_t p0, int64_t wp,
+                  int64_t q0, int64_t wq, int inner_sweeps, double eps, int criterion,
+                  int64_t *all, int64_t *big);
+
 /* Outputs of Sec. 6.1.7 and eq (3.2). */
 int or_extract(int64_t m, int64_t n, const orc *F, int64_t ldf, const int8_t *J,
                const orc *G, int64_t ldg, const orc *Zp, int64_t ldzp,

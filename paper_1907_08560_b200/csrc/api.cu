@@ -178,6 +178,8 @@ void ghsvd_destroy(ghsvd_ctx h) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+  if (ctx->aux_stream2) cudaStreamDestroy(ctx->aux_stream2);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
@@ -451,6 +453,9 @@ ghsvd_status ghsvd_extract(ghsvd_ctx h, double* lambda, double* sigma_f, double*
   CTX_CUDA(cudaSetDevice(ctx->o.device));
   TRY(prepare(ctx));
   TRY(launch_extract(ctx));
+  if (ctx->o.world_size > 1 && ctx->state == 2 && !ctx->blk_start.empty())
+    TRY(comm_finalize_outputs(ctx, (int)ctx->blk_start.size(), ctx->blk_start.data(), ctx->blk_width.data(),
+                              ctx->lam, ctx->sf, ctx->sg, ctx->Z2, ctx->ldn));
   const int64_t n = ctx->n_user;
   if (lambda) CTX_CUDA(cudaMemcpyAsync(lambda, ctx->lam, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
   if (sigma_f) CTX_CUDA(cudaMemcpyAsync(sigma_f, ctx->sf, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));

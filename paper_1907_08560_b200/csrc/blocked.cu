@@ -60,6 +60,7 @@ struct BlkArgs {
   double2* Z;
   long long ldm, ldn, m, n, npos;
   int nblk, s, slot0, npairs;
+  int pair0;                // first local pair handled by this launch (blockIdx.x offset)
   const int* bstart;
   const int* bwidth;
   int nsplit;
@@ -98,7 +99,7 @@ __constant__ signed char kTileJ[36] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3,
 // ---------------------------------------------------------------- Gram (DMMA)
 __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
   extern __shared__ __align__(128) double2 gsm[];  // [2][KM][GS]
-  const int pl = blockIdx.x, hs = blockIdx.y, split = blockIdx.z;
+  const int pl = a.pair0 + blockIdx.x, hs = blockIdx.y, split = blockIdx.z;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
   const double2* X = hs == 0 ? a.F : a.G;
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
   __shared__ int np_sh;
   __shared__ unsigned long long cnt_all, cnt_big, sweep_all;
   __shared__ int err_sh;
-  const int pl = blockIdx.x, tid = threadIdx.x;
+  const int pl = a.pair0 + blockIdx.x, tid = threadIdx.x;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
   const int k = wp + wq;
@@ -237,17 +238,20 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
     W0[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
-  // inner Level-1 sweeps: one warp per pivot pair, kb/2 pairs per step
+  // inner Level-1 sweeps: one HALF-warp per pivot pair, so the kb/2 <= 32 transforms of
+  // a step are computed concurrently by the 32 half-warps of the CTA
   const int warp = tid >> 5, lane = tid & 31;
+  const int hw = lane >> 4, hl = lane & 15, lead = hw << 4;
+  const unsigned hmask = hw ? 0xffff0000u : 0x0000ffffu;
   const double tol = a.eps * sqrt((double)kb);       // C-7: n = block-pivot order
   for (int sw = 0; sw < a.inner_sweeps; sw++) {
     unsigned long long sw_all = 0, sw_big = 0;
     for (int s = 0; s < kb - 1; s++) {
-      for (int pr = warp; pr < kb / 2; pr += NT_P / 32) {
+      for (int pr = 2 * warp + hw; pr < kb / 2; pr += NT_P / 16) {
         long long p, q;
         rr_pair(kb, s, pr, &p, &q);
         double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i = lane; i < kb; i += 32) {
+        for (int i = hl; i < kb; i += 16) {
           const double2 fp = Fh[i + p * KM], fq = Fh[i + q * KM], gpp = Gh[i + p * KM], gq = Gh[i + q * KM];
           const double sg = (double)Jh[i];
           g[0] += sg * (fp.x * fp.x + fp.y * fp.y);
@@ -262,26 +266,26 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
 #pragma unroll
         for (int c = 0; c < 8; c++)
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) g[c] += __shfl_xor_sync(0xffffffffu, g[c], o);
+          for (int o = 8; o > 0; o >>= 1) g[c] += __shfl_xor_sync(hmask, g[c], o);
         HZOut z{};
-        if (lane == 0) z = hz2x2_dev(g, tol, a.literal);
+        if (hl == 0) z = hz2x2_dev(g, tol, a.literal);
         double zz[8] = {z.z11.re, z.z11.im, z.z21.re, z.z21.im, z.z12.re, z.z12.im, z.z22.re, z.z22.im};
 #pragma unroll
-        for (int c = 0; c < 8; c++) zz[c] = __shfl_sync(0xffffffffu, zz[c], 0);
-        const int kind = __shfl_sync(0xffffffffu, lane == 0 ? z.kind : 0, 0);
+        for (int c = 0; c < 8; c++) zz[c] = __shfl_sync(hmask, zz[c], lead);
+        const int kind = __shfl_sync(hmask, hl == 0 ? z.kind : 0, lead);
         if (kind < 0) {
-          if (lane == 0) atomicCAS(&err_sh, 0, kind);
+          if (hl == 0) atomicCAS(&err_sh, 0, kind);
           continue;
         }
         if (kind != KIND_SMALL && kind != KIND_BIG) continue;
-        if (lane == 0) {
+        if (hl == 0) {
           sw_all++;
           if (kind == KIND_BIG) sw_big++;
         }
         const double2 z11 = make_double2(zz[0], zz[1]), z21 = make_double2(zz[2], zz[3]);
         const double2 z12 = make_double2(zz[4], zz[5]), z22 = make_double2(zz[6], zz[7]);
         auto rot = [&](double2* M) {
-          for (int i = lane; i < kb; i += 32) {
+          for (int i = hl; i < kb; i += 16) {
             const double2 x = M[i + p * KM], y = M[i + q * KM];
             M[i + p * KM] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
                                          x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
       __syncthreads();
     }
     // per-sweep totals; FB stops on a sweep without transformations (C-3)
-    if (lane == 0) {
+    if (hl == 0) {
       atomicAdd(&sweep_all, sw_all);
       atomicAdd(&cnt_all, sw_all);
       atomicAdd(&cnt_big, sw_big);
@@ -322,9 +326,10 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
 
 // ---------------------------------------------------------------- update (DMMA)
 // grid (pair, tile): tiles [0, tF) rows of F, [tF, 2 tF) rows of G, [2 tF, 2 tF + tZ) rows of Z
-__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tZ) {
+__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tZ, int tile0) {
   extern __shared__ __align__(128) double2 usm[];  // X tile [KM][US] | Z_blk [KM][ZS]
-  const int pl = blockIdx.x, tile = blockIdx.y;
+  const int pl = a.pair0 + blockIdx.x, tile = tile0 + blockIdx.y;
+  (void)tZ;
   if (!a.applied[pl]) return;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
@@ -437,8 +442,8 @@ BlkPlan make_plan(const Ctx* ctx) {
 size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
   const int64_t nb = auto_nblk(n + 1, o) + 2;
   const int64_t K = nb / 2;
-  return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)K * KM * KM * 16) + al256((size_t)K * 4) +
-         2 * al256((size_t)nb * 4) + 4096;
+  return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)2 * K * KM * KM * 16) +
+         al256((size_t)2 * K * 4) + 2 * al256((size_t)nb * 4) + 4096;
 }
 
 // in comm.cpp
@@ -465,8 +470,8 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   char* p = ctx->scr;
   BlkArgs a;
   a.gpart = (double2*)p; p += al256((size_t)pl.K * 2 * MAX_SPLIT * KM * KM * 16);
-  a.zblk = (double2*)p; p += al256((size_t)pl.K * KM * KM * 16);
-  a.applied = (int*)p; p += al256((size_t)pl.K * 4);
+  a.zblk = (double2*)p; p += al256((size_t)2 * pl.K * KM * KM * 16);   // double-buffered by step parity
+  a.applied = (int*)p; p += al256((size_t)2 * pl.K * 4);
   int* bstart = (int*)p; p += al256((size_t)(pl.nblk + 2) * 4);
   int* bwidth = (int*)p; p += al256((size_t)(pl.nblk + 2) * 4);
   k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
@@ -474,6 +479,9 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   std::vector<int> bs_h(pl.nblk), bw_h(pl.nblk);
   GH_CUDA(cudaMemcpyAsync(bs_h.data(), bstart, pl.nblk * 4, cudaMemcpyDeviceToHost, str));
   GH_CUDA(cudaMemcpyAsync(bw_h.data(), bwidth, pl.nblk * 4, cudaMemcpyDeviceToHost, str));
+  GH_CUDA(cudaStreamSynchronize(str));
+  ctx->blk_start = bs_h;
+  ctx->blk_width = bw_h;
   a.F = ctx->F;
   a.G = ctx->G;
   a.Z = ctx->Z;
@@ -501,34 +509,113 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   GH_CUDA(cudaFuncSetAttribute(k_blk_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u));
   const int tF = (int)((ctx->m + RT - 1) / RT), tZ = (int)((ctx->n + RT - 1) / RT);
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
-  // algorithmic flops per block pair (Hermitian Grams k(k+1)/2 m each, updates k^2 (2m+n))
   GH_CUDA(cudaStreamSynchronize(str));
   const bool multi = ctx->o.world_size > 1;
+  const bool timing = ctx->o.detail_timing != 0;
+  // The Z' update of step s (aux stream) overlaps the Gram + pivot of step s+1: Z is
+  // touched by no other kernel, and Z_blk / applied are double-buffered by step parity.
+  if (!ctx->aux_stream) GH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+  if (!ctx->aux_stream2) GH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream2, cudaStreamNonBlocking));
+  cudaStream_t aux = ctx->aux_stream;
+  // the step's pairs are split in two halves on two streams so that one half's
+  // latency-bound pivot kernel overlaps the other half's Gram / update kernels
+  const int nh = pl.K >= 2 ? 2 : 1;
+  const int KA = nh == 2 ? pl.K / 2 : pl.K;
+  cudaStream_t hs_st[2] = {str, ctx->aux_stream2};
+  const int h_pair0[2] = {0, KA}, h_np[2] = {KA, pl.K - KA};
+  const int nst = pl.nblk - 1;
+  std::vector<cudaEvent_t> ev_piv(2), ev_fg(2), ev_zdone(2), tev;
+  for (int i = 0; i < 2; i++) {
+    GH_CUDA(cudaEventCreateWithFlags(&ev_piv[i], cudaEventDisableTiming));
+    GH_CUDA(cudaEventCreateWithFlags(&ev_fg[i], cudaEventDisableTiming));
+    GH_CUDA(cudaEventCreateWithFlags(&ev_zdone[i], cudaEventDisableTiming));
+  }
+  if (timing) {
+    tev.resize((size_t)nst * 8);
+    for (auto& e : tev) GH_CUDA(cudaEventCreate(&e));
+  }
+  auto destroy_events = [&]() {
+    for (auto e : ev_piv) cudaEventDestroy(e);
+    for (auto e : ev_fg) cudaEventDestroy(e);
+    for (auto e : ev_zdone) cudaEventDestroy(e);
+    for (auto e : tev) cudaEventDestroy(e);
+  };
+  double2* zblk0 = a.zblk;
+  int* applied0 = a.applied;
+  // algorithmic flops per block step (Hermitian Grams k(k+1)/2 m each; updates k^2 (2m+n))
+  std::vector<double> fl_gram(nst, 0.0), fl_upd(nst, 0.0);
+  for (int s = 0; s < nst; s++)
+    for (int kk = pl.slot0; kk < pl.slot0 + pl.K; kk++) {
+      long long bp, bq;
+      rr_pair(pl.nblk, s, kk, &bp, &bq);
+      const double kq = bw_h[bp] + bw_h[bq];
+      fl_gram[s] += 8.0 * kq * (kq + 1) * ctx->m;
+      fl_upd[s] += 8.0 * kq * kq * (2.0 * ctx->m + ctx->n);
+    }
   GH_CUDA(cudaEventRecord(ctx->ev0, str));
   for (int sw = 0; sw < ctx->o.max_sweeps; sw++) {
     GH_CUDA(cudaMemsetAsync(ctx->cnt, 0, sizeof(DevCounters), str));
     GH_CUDA(cudaEventRecord(ctx->ev2, str));
-    for (int s = 0; s < pl.nblk - 1; s++) {
+    if (nh == 2) GH_CUDA(cudaStreamWaitEvent(hs_st[1], ctx->ev2, 0));
+    for (int s = 0; s < nst; s++) {
+      const int b = s & 1;
       a.s = s;
-      k_blk_gram<<<dim3(pl.K, 2, pl.nsplit), NT_G, smem_g, str>>>(a);
-      k_blk_pivot<<<pl.K, NT_P, smem_p, str>>>(a);
-      k_blk_update<<<dim3(pl.K, 2 * tF + tZ), NT_U, smem_u, str>>>(a, tF, tZ);
+      a.zblk = zblk0 + (size_t)b * pl.K * KM * KM;
+      a.applied = applied0 + (size_t)b * pl.K;
+      // the Grams of step s read block columns updated by both halves in step s-1
+      if (nh == 2 && s > 0) {
+        GH_CUDA(cudaStreamWaitEvent(hs_st[0], ev_fg[1], 0));
+        GH_CUDA(cudaStreamWaitEvent(hs_st[1], ev_fg[0], 0));
+      }
+      for (int h = 0; h < nh; h++) {
+        cudaStream_t sh = hs_st[h];
+        a.pair0 = h_pair0[h];
+        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 0], sh));
+        k_blk_gram<<<dim3(h_np[h], 2, pl.nsplit), NT_G, smem_g, sh>>>(a);
+        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 1], sh));
+        // Z_blk buffer b was last read by the Z update of step s-2
+        if (s >= 2 || sw > 0) GH_CUDA(cudaStreamWaitEvent(sh, ev_zdone[b], 0));
+        k_blk_pivot<<<h_np[h], NT_P, smem_p, sh>>>(a);
+        GH_CUDA(cudaEventRecord(ev_piv[h], sh));
+        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
+        k_blk_update<<<dim3(h_np[h], 2 * tF), NT_U, smem_u, sh>>>(a, tF, tZ, 0);
+        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 3], sh));
+        GH_CUDA(cudaEventRecord(ev_fg[h], sh));
+      }
+      // Z' update of all pairs of step s on the aux stream (overlaps step s+1)
+      a.pair0 = 0;
+      for (int h = 0; h < nh; h++) GH_CUDA(cudaStreamWaitEvent(aux, ev_piv[h], 0));
+      k_blk_update<<<dim3(pl.K, tZ), NT_U, smem_u, aux>>>(a, tF, tZ, 2 * tF);
+      GH_CUDA(cudaEventRecord(ev_zdone[b], aux));
       GH_CUDA(cudaGetLastError());
       if (multi) {
-        const int s_next = (s + 1) % (pl.nblk - 1);
+        // block columns (F, G and Z) leave only after every update of step s
+        if (nh == 2) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[1], 0));
+        GH_CUDA(cudaStreamWaitEvent(str, ev_zdone[b], 0));
+        const int s_next = (s + 1) % nst;
         ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data());
-        if (e) return e;
+        if (e) {
+          destroy_events();
+          return e;
+        }
+        GH_CUDA(cudaEventRecord(ev_fg[0], str));  // half 1 of step s+1 waits for the exchange
       }
     }
+    if (nh == 2) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[1], 0));
+    GH_CUDA(cudaStreamWaitEvent(str, ev_zdone[(nst - 1) & 1], 0));
     GH_CUDA(cudaEventRecord(ctx->ev3, str));
     DevCounters c;
     GH_CUDA(cudaMemcpyAsync(&c, ctx->cnt, sizeof(c), cudaMemcpyDeviceToHost, str));
     GH_CUDA(cudaStreamSynchronize(str));
     if (multi) {
       ghsvd_status e = comm_allreduce_counters(ctx, &c);
-      if (e) return e;
+      if (e) {
+        destroy_events();
+        return e;
+      }
     }
     if (c.err) {
+      destroy_events();
       ctx->err = c.err == -7 ? "blocked: rank-deficient block pivot (HEBPJ)"
                  : c.err == -6 ? "blocked: indefinite / singular S block pivot"
                                : "blocked: non-finite value in a block pivot";
@@ -537,7 +624,22 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     float kms = 0;
     GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
     st->kernel_seconds += kms * 1e-3;
-    st->launches += (uint64_t)3 * (pl.nblk - 1);
+    st->launches += (uint64_t)4 * nst;
+    for (int s = 0; s < nst; s++) {
+      st->flops_gram += fl_gram[s];
+      st->flops_update += fl_upd[s];
+      if (timing) {
+        for (int h = 0; h < nh; h++) {
+          float t0 = 0, t1 = 0, t2 = 0;
+          GH_CUDA(cudaEventElapsedTime(&t0, tev[8 * s + 4 * h + 0], tev[8 * s + 4 * h + 1]));
+          GH_CUDA(cudaEventElapsedTime(&t1, tev[8 * s + 4 * h + 1], tev[8 * s + 4 * h + 2]));
+          GH_CUDA(cudaEventElapsedTime(&t2, tev[8 * s + 4 * h + 2], tev[8 * s + 4 * h + 3]));
+          st->t_gram += t0 * 1e-3;
+          st->t_pivot += t1 * 1e-3;
+          st->t_update += t2 * 1e-3;
+        }
+      }
+    }
     if (sw < 64) {
       st->all_per_sweep[sw] = c.all;
       st->big_per_sweep[sw] = c.big;
@@ -553,19 +655,12 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   }
   GH_CUDA(cudaEventRecord(ctx->ev1, str));
   GH_CUDA(cudaEventSynchronize(ctx->ev1));
+  destroy_events();
   float ms = 0;
   GH_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   st->seconds = ms * 1e-3;
-  // algorithmic flops: per sweep sum over block pairs of 8 [k(k+1) m + k^2 (2m + n)] (re+im FMAs x2)
-  double fl = 0.0;
-  for (int s = 0; s < pl.nblk - 1; s++)
-    for (int kk = 0; kk < pl.nblk / 2; kk++) {
-      long long bp, bq;
-      rr_pair(pl.nblk, s, kk, &bp, &bq);
-      const double kq = bw_h[bp] + bw_h[bq];
-      fl += 8.0 * (kq * (kq + 1) * ctx->m + kq * kq * (2.0 * ctx->m + ctx->n));
-    }
-  st->alg_flops = fl * st->sweeps / std::max(1, ctx->o.world_size);
+  // algorithmic flops of this rank: per block pair 8 [k(k+1) m + k^2 (2m + n)]
+  st->alg_flops = st->flops_gram + st->flops_update;
   // HBM bytes the blocked sweep must move per block step: Grams read F, G pairs once,
   // updates read + write F, G, Z pairs once
   st->alg_bytes = (uint64_t)((double)st->sweeps * (pl.nblk - 1) / std::max(1, ctx->o.world_size) *

@@ -1,16 +1,272 @@
+// comm.cpp -- multi-GPU layer of the blocked variant.
+//
+// P ranks (one per GPU) run the Level-2 round-robin over nblk = 2 P K block
+// columns; rank r owns slots [r K, (r+1) K) of every block step (a slot holds one
+// block pair).  Every rank keeps full-size F, G, Z buffers, but only the block
+// columns it currently owns are up to date.  After block step s the block columns
+// whose owner changes for step s' are moved with grouped ncclSend / ncclRecv
+// (the paper's physical block-column exchange, over
+// NVLink/NVSwitch), and once per sweep the counters are combined with
+// ncclAllReduce so every rank takes the same stop decision.
+// NCCL is loaded with dlopen("libnccl.so.2") (torch's copy when torch is loaded),
+// so the library itself has no link-time NCCL dependency.
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
 #include "internal.h"
+
 namespace ghsvd {
-ghsvd_status comm_init(Ctx* ctx) {
-  ctx->err = "multi-GPU: not implemented yet";
-  return GHSVD_E_NCCL;
+
+// ------------------------------------------------------------------ schedule
+// Round-robin pair of slot k in step s (same closed form as hz2x2.cuh rr_pair).
+static void rr(long long n, long long s, long long k, long long* p, long long* q) {
+  long long a, b;
+  if (k == 0) {
+    a = n - 1;
+    b = s;
+  } else {
+    const long long r = n - 1;
+    a = (s + k) % r;
+    b = ((s - k) % r + r) % r;
+  }
+  *p = a < b ? a : b;
+  *q = a < b ? b : a;
 }
-void comm_destroy(Ctx*) {}
-ghsvd_status comm_exchange(Ctx* ctx, int, int, int, const int*, const int*) {
-  ctx->err = "multi-GPU: not implemented yet";
-  return GHSVD_E_NCCL;
+
+// owner[b] = rank owning block b in step s
+static void owners(int nblk, int world, int s, std::vector<int>& own) {
+  own.assign(nblk, -1);
+  const int K = nblk / 2 / world;
+  for (int k = 0; k < nblk / 2; k++) {
+    long long p, q;
+    rr(nblk, s, k, &p, &q);
+    own[p] = own[q] = k / K;
+  }
 }
-ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters*) {
-  ctx->err = "multi-GPU: not implemented yet";
-  return GHSVD_E_NCCL;
-}
+
 }  // namespace ghsvd
+
+extern "C" {
+
+// Rank owning block column b in block step s (nblk even, world | nblk/2).  -1 on bad args.
+int ghsvd_block_owner(int nblk, int world, int s, int b) {
+  if (nblk < 2 || (nblk & 1) || world < 1 || (nblk / 2) % world || s < 0 || s > nblk - 2 || b < 0 || b >= nblk)
+    return -1;
+  std::vector<int> own;
+  ghsvd::owners(nblk, world, s, own);
+  return own[b];
+}
+
+// Exchange plan of `rank` between block steps s and s_next: blocks it sends
+// (send_blk[i] to send_peer[i]) and receives (recv_blk[i] from recv_peer[i]),
+// in increasing block order.  Arrays must hold nblk entries.  Returns 0 / -1.
+int ghsvd_exchange_plan(int nblk, int world, int rank, int s, int s_next, int64_t* send_blk, int64_t* send_peer,
+                        int64_t* nsend, int64_t* recv_blk, int64_t* recv_peer, int64_t* nrecv) {
+  if (nblk < 2 || (nblk & 1) || world < 1 || (nblk / 2) % world || rank < 0 || rank >= world || s < 0 ||
+      s > nblk - 2 || s_next < 0 || s_next > nblk - 2)
+    return -1;
+  std::vector<int> o1, o2;
+  ghsvd::owners(nblk, world, s, o1);
+  ghsvd::owners(nblk, world, s_next, o2);
+  int64_t ns = 0, nr = 0;
+  for (int b = 0; b < nblk; b++) {
+    if (o1[b] == rank && o2[b] != rank) {
+      send_blk[ns] = b;
+      send_peer[ns] = o2[b];
+      ns++;
+    }
+    if (o2[b] == rank && o1[b] != rank) {
+      recv_blk[nr] = b;
+      recv_peer[nr] = o1[b];
+      nr++;
+    }
+  }
+  *nsend = ns;
+  *nrecv = nr;
+  return 0;
+}
+
+}  // extern "C"
+
+namespace ghsvd {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static Nccl* nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (tried) return n.h ? &n : nullptr;
+  tried = true;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names) {
+    n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (n.h) break;
+  }
+  if (!n.h) return nullptr;
+  n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
+  n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
+  n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+  n.Send = (decltype(n.Send))dlsym(n.h, "ncclSend");
+  n.Recv = (decltype(n.Recv))dlsym(n.h, "ncclRecv");
+  n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
+  n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
+  n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
+  n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
+  if (!n.GetUniqueId || !n.CommInitRank || !n.Send || !n.Recv || !n.GroupStart || !n.GroupEnd || !n.AllReduce) {
+    dlclose(n.h);
+    n.h = nullptr;
+    return nullptr;
+  }
+  return &n;
+}
+
+#define NCCL_CALL(x)                                                                            \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) {                                                                    \
+      ctx->err = std::string(#x) + ": " + (N->GetErrorString ? N->GetErrorString(r_) : "error"); \
+      return GHSVD_E_NCCL;                                                                      \
+    }                                                                                           \
+  } while (0)
+
+ghsvd_status comm_init(Ctx* ctx) {
+  Nccl* N = nccl();
+  if (!N) {
+    ctx->err = "multi-GPU: libnccl.so.2 could not be loaded";
+    return GHSVD_E_NCCL;
+  }
+  ncclUniqueId id;
+  memcpy(&id, ctx->o.nccl_id, sizeof(id));
+  ncclComm_t c;
+  NCCL_CALL(N->CommInitRank(&c, ctx->o.world_size, id, ctx->o.rank));
+  ctx->comm = c;
+  return GHSVD_OK;
+}
+
+void comm_destroy(Ctx* ctx) {
+  Nccl* N = nccl();
+  if (N && ctx->comm && N->CommDestroy) N->CommDestroy((ncclComm_t)ctx->comm);
+  ctx->comm = nullptr;
+}
+
+// Move the block columns (F, G: m rows; Z: n rows) whose owner changes between
+// block steps s_now and s_next.  A block column is contiguous in each buffer.
+ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart, const int* bwidth) {
+  Nccl* N = nccl();
+  if (!N || !ctx->comm) {
+    ctx->err = "multi-GPU: no communicator";
+    return GHSVD_E_NCCL;
+  }
+  std::vector<int64_t> sb(nblk), sp(nblk), rb(nblk), rp(nblk);
+  int64_t ns = 0, nr = 0;
+  if (ghsvd_exchange_plan(nblk, ctx->o.world_size, ctx->o.rank, s_now, s_next, sb.data(), sp.data(), &ns, rb.data(),
+                          rp.data(), &nr)) {
+    ctx->err = "multi-GPU: bad exchange plan arguments";
+    return GHSVD_E_INVALID_ARG;
+  }
+  if (ns == 0 && nr == 0) return GHSVD_OK;
+  ncclComm_t comm = (ncclComm_t)ctx->comm;
+  cudaStream_t st = ctx->stream;
+  NCCL_CALL(N->GroupStart());
+  auto xfer = [&](int64_t b, int peer, bool send) -> ncclResult_t {
+    const size_t w = (size_t)bwidth[b];
+    double2* bufs[3] = {ctx->F + (size_t)bstart[b] * ctx->ldm, ctx->G + (size_t)bstart[b] * ctx->ldm,
+                        ctx->Z + (size_t)bstart[b] * ctx->ldn};
+    const size_t cnt[3] = {w * ctx->ldm * 2, w * ctx->ldm * 2, w * ctx->ldn * 2};  // doubles
+    for (int t = 0; t < 3; t++) {
+      ncclResult_t r = send ? N->Send(bufs[t], cnt[t], ncclFloat64, peer, comm, st)
+                            : N->Recv(bufs[t], cnt[t], ncclFloat64, peer, comm, st);
+      if (r != ncclSuccess) return r;
+    }
+    return ncclSuccess;
+  };
+  for (int64_t i = 0; i < ns; i++) NCCL_CALL(xfer(sb[i], (int)sp[i], true));
+  for (int64_t i = 0; i < nr; i++) NCCL_CALL(xfer(rb[i], (int)rp[i], false));
+  NCCL_CALL(N->GroupEnd());
+  return GHSVD_OK;
+}
+
+// Sum all/big, max off, min err over ranks (one small allreduce group per sweep).
+ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c) {
+  Nccl* N = nccl();
+  if (!N || !ctx->comm) {
+    ctx->err = "multi-GPU: no communicator";
+    return GHSVD_E_NCCL;
+  }
+  ncclComm_t comm = (ncclComm_t)ctx->comm;
+  cudaStream_t st = ctx->stream;
+  DevCounters* d = ctx->cnt;  // device copy (already holds this rank's values)
+  NCCL_CALL(N->GroupStart());
+  NCCL_CALL(N->AllReduce(&d->all, &d->all, 2, ncclUint64, ncclSum, comm, st));
+  NCCL_CALL(N->AllReduce(&d->off_bits, &d->off_bits, 1, ncclUint64, ncclMax, comm, st));
+  NCCL_CALL(N->AllReduce(&d->err, &d->err, 1, ncclInt32, ncclMin, comm, st));
+  NCCL_CALL(N->GroupEnd());
+  GH_CUDA(cudaMemcpyAsync(c, d, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  return GHSVD_OK;
+}
+
+// Complete the extracted outputs on every rank: zero the columns this rank does
+// not own after the final exchange (ownership of block step 0), then sum.
+ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam, double* sf,
+                                   double* sg, double2* Zout, int64_t ldz) {
+  Nccl* N = nccl();
+  if (!N || !ctx->comm) {
+    ctx->err = "multi-GPU: no communicator";
+    return GHSVD_E_NCCL;
+  }
+  std::vector<int> own;
+  owners(nblk, ctx->o.world_size, 0, own);
+  cudaStream_t st = ctx->stream;
+  for (int b = 0; b < nblk; b++) {
+    if (own[b] == ctx->o.rank) continue;
+    const size_t c0 = (size_t)bstart[b], w = (size_t)bwidth[b];
+    GH_CUDA(cudaMemsetAsync(lam + c0, 0, w * 8, st));
+    GH_CUDA(cudaMemsetAsync(sf + c0, 0, w * 8, st));
+    GH_CUDA(cudaMemsetAsync(sg + c0, 0, w * 8, st));
+    GH_CUDA(cudaMemsetAsync(Zout + c0 * ldz, 0, w * ldz * 16, st));
+  }
+  ncclComm_t comm = (ncclComm_t)ctx->comm;
+  const size_t n = (size_t)ctx->n;
+  NCCL_CALL(N->GroupStart());
+  NCCL_CALL(N->AllReduce(lam, lam, n, ncclFloat64, ncclSum, comm, st));
+  NCCL_CALL(N->AllReduce(sf, sf, n, ncclFloat64, ncclSum, comm, st));
+  NCCL_CALL(N->AllReduce(sg, sg, n, ncclFloat64, ncclSum, comm, st));
+  NCCL_CALL(N->AllReduce(Zout, Zout, n * ldz * 2, ncclFloat64, ncclSum, comm, st));
+  NCCL_CALL(N->GroupEnd());
+  return GHSVD_OK;
+}
+
+}  // namespace ghsvd
+
+extern "C" {
+
+// Fill 128 bytes with a fresh ncclUniqueId (rank 0 calls this and broadcasts it).
+// Returns 0, or -4 if NCCL cannot be loaded.
+int ghsvd_nccl_unique_id(void* out128) {
+  ghsvd::Nccl* N = ghsvd::nccl();
+  if (!N || !out128) return -4;
+  ncclUniqueId id;
+  if (N->GetUniqueId(&id) != ncclSuccess) return -4;
+  memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+}  // extern "C"

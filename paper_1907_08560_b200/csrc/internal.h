@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/ghsvd.h"
 
@@ -29,6 +30,8 @@ struct Ctx {
   ghsvd_options o;
   cudaStream_t stream;
   cudaStream_t cap_stream;    // private stream for graph capture
+  cudaStream_t aux_stream;    // blocked: Z' updates overlapped with the next step
+  cudaStream_t aux_stream2;   // blocked: second half of each step's block pairs
   char* ws;
   size_t ws_bytes;
   Layout L;
@@ -63,6 +66,8 @@ struct Ctx {
   cudaGraphExec_t graph;
   int64_t graph_n, graph_key;
   cudaEvent_t ev0, ev1, ev2, ev3;
+  // blocked partition of the last blocked sweep (host copies)
+  std::vector<int> blk_start, blk_width;
   // multi-GPU
   void* comm;                    // ncclComm_t (opaque)
   std::string err;
@@ -104,5 +109,8 @@ size_t phase2_scratch_bytes(int64_t m, int64_t n);
 // blocked.cu
 ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st);
 size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n);
+// comm.cpp
+ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam,
+                                   double* sf, double* sg, double2* Zout, int64_t ldz);
 
 }  // namespace ghsvd

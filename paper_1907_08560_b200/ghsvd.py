@@ -33,7 +33,8 @@ CRITERIA = {"relative": 0, "literal": 1}
 EXPORTS = ["ghsvd_default_options", "ghsvd_workspace_bytes", "ghsvd_create", "ghsvd_factor",
            "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors", "ghsvd_sweep", "ghsvd_run_steps",
            "ghsvd_extract", "ghsvd_get_transformed", "ghsvd_hz2x2_batch", "ghsvd_last_error",
-           "ghsvd_destroy", "ghsvd_version"]
+           "ghsvd_destroy", "ghsvd_version", "ghsvd_block_owner", "ghsvd_exchange_plan",
+           "ghsvd_nccl_unique_id"]
 
 
 class GHSVDError(RuntimeError):
@@ -47,7 +48,8 @@ class Options(ctypes.Structure):
                 ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("variant", ctypes.c_int),
                 ("ordering", ctypes.c_int), ("nblocks", ctypes.c_int), ("max_sweeps", ctypes.c_int),
                 ("criterion", ctypes.c_int), ("eps", ctypes.c_double), ("cluster", ctypes.c_int),
-                ("threads", ctypes.c_int), ("use_graph", ctypes.c_int), ("kernel", ctypes.c_int)]
+                ("threads", ctypes.c_int), ("use_graph", ctypes.c_int), ("kernel", ctypes.c_int),
+                ("detail_timing", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -55,7 +57,10 @@ class Stats(ctypes.Structure):
                 ("transforms_all", ctypes.c_uint64), ("transforms_big", ctypes.c_uint64),
                 ("seconds", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
                 ("launches", ctypes.c_uint64), ("alg_bytes", ctypes.c_uint64),
-                ("alg_flops", ctypes.c_double), ("max_offdiag_last", ctypes.c_double),
+                ("alg_flops", ctypes.c_double), ("t_gram", ctypes.c_double), ("t_pivot", ctypes.c_double),
+                ("t_update", ctypes.c_double), ("t_exchange", ctypes.c_double),
+                ("flops_gram", ctypes.c_double), ("flops_update", ctypes.c_double),
+                ("max_offdiag_last", ctypes.c_double),
                 ("all_per_sweep", ctypes.c_uint64 * 64), ("big_per_sweep", ctypes.c_uint64 * 64)]
 
     def todict(self):
@@ -65,6 +70,9 @@ class Stats(ctypes.Structure):
                 "transforms_big": int(self.transforms_big), "seconds": self.seconds,
                 "kernel_seconds": self.kernel_seconds, "launches": int(self.launches),
                 "alg_bytes": int(self.alg_bytes), "alg_flops": self.alg_flops,
+                "t_gram": self.t_gram, "t_pivot": self.t_pivot, "t_update": self.t_update,
+                "t_exchange": self.t_exchange, "flops_gram": self.flops_gram,
+                "flops_update": self.flops_update,
                 "max_offdiag_last": self.max_offdiag_last,
                 "all_per_sweep": [int(v) for v in self.all_per_sweep[:k]],
                 "big_per_sweep": [int(v) for v in self.big_per_sweep[:k]]}
@@ -103,6 +111,9 @@ def load():
     L.ghsvd_destroy.argtypes = [P]
     L.ghsvd_destroy.restype = None
     L.ghsvd_version.restype = ctypes.c_char_p
+    L.ghsvd_block_owner.argtypes = [Ci, Ci, Ci, Ci]
+    L.ghsvd_exchange_plan.argtypes = [Ci, Ci, Ci, Ci, Ci, P, P, P, P, P, P]
+    L.ghsvd_nccl_unique_id.argtypes = [P]
     for f in ("ghsvd_create", "ghsvd_factor", "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors",
               "ghsvd_sweep", "ghsvd_run_steps", "ghsvd_extract", "ghsvd_get_transformed", "ghsvd_hz2x2_batch"):
         getattr(L, f).restype = ctypes.c_int
@@ -152,7 +163,8 @@ class Context:
     def __init__(self, m: int, n: int, nl: int = 0, *, variant: str = "pointwise", device: int = 0,
                  stream=None, world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  nblocks: int = 0, max_sweeps: int = 30, criterion: str = "relative", eps: float = 0.0,
-                 cluster: int = 0, threads: int = 0, use_graph: bool = True, kernel: int = 0):
+                 cluster: int = 0, threads: int = 0, use_graph: bool = True, kernel: int = 0,
+                 detail_timing: bool = False):
         import torch
         L = load()
         self._L = L
@@ -177,6 +189,7 @@ class Context:
         o.threads = threads
         o.use_graph = 1 if use_graph else 0
         o.kernel = kernel
+        o.detail_timing = 1 if detail_timing else 0
         self.opts = o
         nbytes = L.ghsvd_workspace_bytes(ctypes.byref(o), m, n, nl)
         if nbytes == 0:
@@ -333,6 +346,33 @@ class Context:
                                               ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(kind.data_ptr())),
                     "hz2x2_batch")
         return out.cpu().numpy(), kind.cpu().numpy()
+
+
+def block_owner(nblk: int, world: int, s: int, b: int) -> int:
+    return load().ghsvd_block_owner(nblk, world, s, b)
+
+
+def exchange_plan(nblk: int, world: int, rank: int, s: int, s_next: int):
+    """-> (sends [(block, peer)], recvs [(block, peer)]) between block steps s and s_next."""
+    L = load()
+    arr = [np.zeros(nblk, np.int64) for _ in range(4)]
+    ns, nr = ctypes.c_int64(), ctypes.c_int64()
+    rc = L.ghsvd_exchange_plan(nblk, world, rank, s, s_next, *[a.ctypes.data_as(ctypes.c_void_p) for a in arr[:2]],
+                               ctypes.byref(ns), *[a.ctypes.data_as(ctypes.c_void_p) for a in arr[2:]],
+                               ctypes.byref(nr))
+    if rc != 0:
+        raise GHSVDError(-1, "exchange_plan: bad arguments")
+    sends = list(zip(arr[0][:ns.value].tolist(), arr[1][:ns.value].tolist()))
+    recvs = list(zip(arr[2][:nr.value].tolist(), arr[3][:nr.value].tolist()))
+    return sends, recvs
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = load().ghsvd_nccl_unique_id(buf)
+    if rc != 0:
+        raise GHSVDError(rc, "ncclGetUniqueId failed (NCCL not loadable)")
+    return buf.raw
 
 
 def version() -> str:

@@ -8,10 +8,13 @@ kind, at = inputs.make_config(3, backend="torch")
 NA, NL, NG = at.A.shape
 sweeps = int(os.environ.get("SWEEPS", "1"))
 for nb in [int(x) for x in os.environ.get("NBLK", "128").split(",")]:
-    ctx = ghsvd.Context(2 * NA * NL, NG, NL, variant="bo", nblocks=nb, max_sweeps=sweeps)
+    ctx = ghsvd.Context(2 * NA * NL, NG, NL, variant="bo", nblocks=nb, max_sweeps=sweeps, detail_timing=True)
     ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
     st = ctx.sweep()
     print(json.dumps({"nblk": nb, "sweeps": st["sweeps"], "converged": st["converged"], "kernel_s": st["kernel_seconds"],
                       "s_per_sweep": st["kernel_seconds"] / st["sweeps"], "TFLOPs": st["alg_flops"] / st["kernel_seconds"] / 1e12,
-                      "big": st["big_per_sweep"]}), flush=True)
+                      "t_gram": st["t_gram"], "t_pivot": st["t_pivot"], "t_update": st["t_update"],
+                      "TF_gram": st["flops_gram"] / max(st["t_gram"], 1e-12) / 1e12,
+                      "TF_update": st["flops_update"] / max(st["t_update"], 1e-12) / 1e12,
+                      "big": st["big_per_sweep"][-3:]}), flush=True)
     ctx.close()

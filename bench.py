@@ -163,18 +163,53 @@ def run_reference(args):
     return 0
 
 
+def measure_zgemm_peak(dev) -> float:
+    """Live FP64 tensor-core roofline denominator: cuBLAS ZGEMM (complex128) TFLOP/s,
+    best of 5 at 4096^3 (MEASURED_PEAKS.json has no FP64 figure)."""
+    import torch
+    a = torch.randn(4096, 4096, dtype=torch.complex128, device=dev)
+    b = torch.randn(4096, 4096, dtype=torch.complex128, device=dev)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize(dev)
+    best = 1e30
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(5):
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    del a, b
+    return 8.0 * 4096 ** 3 / best / 1e12
+
+
+def _ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu summary, if any."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        k = d.get("kernels", {}).get(kernel)
+        return None if k is None else k.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     from paper_1907_08560_b200 import build, ghsvd, inputs
     ws, rank, local = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        if args.variant == "pointwise":
+            args.variant = "bo"                     # only the blocked variant shards (DESIGN.md 7)
     build.build()
     stream = torch.cuda.Stream(dev)
     cfg = inputs.CONFIGS[args.config]
+    blocked = args.variant in ("bo", "fb")
+    zgemm_peak = measure_zgemm_peak(dev) if blocked else None
     # ---- inputs (seeded, synthetic) and Phase 1 on the device
     kind, payload = make_factors(args.config, "torch")
     if kind == "atoms":
@@ -184,9 +219,16 @@ def run_ours(args):
     else:
         m, n = payload.F.shape
         nl = 0
+    nccl_id = None
+    if ws > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(ghsvd.nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
     ctx = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=args.max_sweeps,
-                        cluster=args.cluster, threads=args.threads, nblocks=args.nblocks)
-    t0 = time.perf_counter()
+                        cluster=args.cluster, threads=args.threads, nblocks=args.nblocks, world_size=ws,
+                        rank=rank, nccl_id=nccl_id, detail_timing=blocked)
     phase1_s = None
     with torch.cuda.stream(stream):
         if kind == "atoms":
@@ -199,7 +241,7 @@ def run_ours(args):
         else:
             ctx.set_factors(payload.F, payload.J, payload.G)
         mb, nb = ctx.factor_shape()
-        # pinned host copies of the starting factors (e2e inputs) and device copies
+        # pinned host copies of the starting factors: the e2e inputs of every step
         Fh = torch.empty((nb, mb), dtype=torch.complex128, pin_memory=True).t()
         Gh = torch.empty((nb, mb), dtype=torch.complex128, pin_memory=True).t()
         Jh = torch.empty(mb, dtype=torch.int8, pin_memory=True)
@@ -210,14 +252,16 @@ def run_ours(args):
     sg_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
 
     def one_step():
+        """e2e: H2D of F, J, G (pinned) -> Phase 3 to convergence -> D2H of lambda, Sigma_F, Sigma_G.
+        value: the sweep alone (factors resident in HBM)."""
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         with torch.cuda.stream(stream):
             e[0].record(stream)
-            ctx.set_factors(Fh, Jh, Gh)                 # H2D from pinned host
+            ctx.set_factors(Fh, Jh, Gh)
             e[1].record(stream)
-            st = ctx.sweep()                            # Phase 3 to convergence
+            st = ctx.sweep()
             e[2].record(stream)
-            ctx.extract(want_z=False, out=(lam_h, sf_h, sg_h, None))   # D2H of the result
+            ctx.extract(want_z=False, out=(lam_h, sf_h, sg_h, None))
             e[3].record(stream)
         stream.synchronize()
         return st, e[1].elapsed_time(e[2]) * 1e-3, e[0].elapsed_time(e[3]) * 1e-3
@@ -244,30 +288,54 @@ def run_ours(args):
         t = torch.tensor([value, e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         value, e2e = float(t[0]), float(t[1])
-    kern_s = sum(s["kernel_seconds"] for s in stats)
-    alg = sum(s["alg_bytes"] for s in stats)
     launches = sum(s["launches"] for s in stats)
     sweeps = stats[-1]["sweeps"]
     pairs = stats[-1]["pairs_visited"]
     peaks = _peaks()
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = alg / kern_s / 1e9 if kern_s > 0 else 0.0
+    if blocked:
+        t_upd = sum(s["t_update"] for s in stats)
+        f_upd = sum(s["flops_update"] for s in stats)
+        t_gr = sum(s["t_gram"] for s in stats)
+        f_gr = sum(s["flops_gram"] for s in stats)
+        t_pv = sum(s["t_pivot"] for s in stats)
+        n_upd = sum(s["launches"] for s in stats) // 4 * 2   # FG + Z update launches
+        ach = f_upd / t_upd / 1e12 if t_upd > 0 else 0.0
+        roof = {"bound": "tensor", "achieved": ach, "peak": zgemm_peak, "unit": "TFLOP/s",
+                "frac": ach / zgemm_peak, "traffic": _ncu_traffic("k_blk_update"), "kernel": "k_blk_update",
+                "alg_flops_per_launch": f_upd / max(n_upd, 1), "avg_launch_us": t_upd / max(n_upd, 1) * 1e6,
+                "peak_source": "cuBLAS ZGEMM 4096^3 measured live in this run (FP64 DMMA; MEASURED_PEAKS.json "
+                               "has no FP64 figure)",
+                "others": {"k_blk_gram": {"achieved": f_gr / t_gr / 1e12 if t_gr else 0.0,
+                                          "frac": (f_gr / t_gr / 1e12) / zgemm_peak if t_gr else 0.0,
+                                          "seconds": t_gr},
+                           "k_blk_update": {"seconds": t_upd},
+                           "k_blk_pivot": {"seconds": t_pv, "bound": "latency (serial HEBPJ/Cholesky/inner sweep)"}},
+                "whole_step_tflops": sum(s["alg_flops"] for s in stats) / sum(s["kernel_seconds"] for s in stats) / 1e12}
+    else:
+        kern_s = sum(s["kernel_seconds"] for s in stats)
+        alg = sum(s["alg_bytes"] for s in stats)
+        peak = peaks.get("hbm_gbs", 6650.0)
+        achieved = alg / kern_s / 1e9 if kern_s > 0 else 0.0
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": _ncu_traffic("k_pair_step_2p"), "kernel": "k_pair_step_2p",
+                "alg_bytes_per_launch": alg / max(launches, 1), "avg_launch_us": kern_s / max(launches, 1) * 1e6,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
     if rank != 0:
+        ctx.close()
+        if ws > 1:
+            torch.distributed.destroy_process_group()
         return 0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak" if ws > 1 else "weak",
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant,
-                   "cluster": ctx.opts.cluster, "l2": "inputs (1.6 GB) larger than L2", "phase2": "skipped"},
-        "sweeps": sweeps, "converged": stats[-1]["converged"],
+        "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant, "max_sweeps": args.max_sweeps,
+                   "l2": "inputs (1.6 GB) larger than L2 (126 MB)", "phase2": "skipped (ill-conditioned G, PAPER.md:925)"},
+        "sweeps": sweeps, "converged": stats[-1]["converged"], "big_per_sweep_tail": stats[-1]["big_per_sweep"][-4:],
+        "seconds_per_sweep": value / max(sweeps, 1),
         "pair_updates_per_s": pairs / value, "transforms_per_s": stats[-1]["transforms_all"] / value,
         "phase1_seconds": phase1_s,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": "k_pair_step", "alg_bytes_per_launch": alg / max(launches, 1),
-                     "avg_launch_us": kern_s / max(launches, 1) * 1e6,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback"},
+        "roofline": roof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(2 * mb * nb * 16 + mb),
                 "d2h_bytes_per_step": int(3 * n * 8)},
         "gpu_launches": int(launches),
@@ -292,14 +360,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--variant", default="pointwise", choices=["pointwise", "bo", "fb"])
+    ap.add_argument("--variant", default="bo", choices=["pointwise", "bo", "fb"])
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--nblocks", type=int, default=0)
-    ap.add_argument("--max-sweeps", type=int, default=30)
+    ap.add_argument("--max-sweeps", type=int, default=64,
+                    help="C_max; config 3 (S condition 1e12) needs ~36 sweeps, beyond the paper's usual 30")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=15.0)
-    ap.add_argument("--ref-sweeps", type=int, default=20,
+    ap.add_argument("--ref-sweeps", type=int, default=36,
                     help="sweep count used to extrapolate the oracle sample in --impl reference")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -68,6 +68,10 @@ struct BlkArgs {
   double2* gpart;           // [pair][hs][split][KM*KM]
   double2* zblk;            // [pair][KM*KM]
   int* applied;             // [pair]
+  double2* fhat;            // [pair][KM*KM]  F^ from HEBPJ
+  double2* ghat;            // [pair][KM*KM]  G^ from pivoted Cholesky
+  signed char* jhat;        // [pair][KM]     J^
+  int* fact_ok;             // [pair][2]
   DevCounters* cnt;
   double eps;
   int literal;
@@ -164,13 +168,63 @@ __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
 }
 
 // ---------------------------------------------------------------- block pivot
+// k_blk_factor: grid (pairs, 2).  y = 0: H_blk -> HEBPJ -> F^ (and J^);  y = 1:
+// S_blk -> diagonally pivoted Cholesky -> G^.  The two factorizations of a pair
+// run as separate, concurrent CTAs; F^, G^ go to L2-resident scratch.
+constexpr int NT_F = 256;
+__global__ void __launch_bounds__(NT_F) k_blk_factor(BlkArgs a) {
+  extern __shared__ __align__(128) double2 fsm[];  // W (KM*KM)
+  double2* W = fsm;
+  __shared__ int np_sh;
+  const int pl = a.pair0 + blockIdx.x, which = blockIdx.y, tid = threadIdx.x;
+  int c0p, wp, c0q, wq;
+  pair_cols(a, pl, c0p, wp, c0q, wq);
+  const int k = wp + wq;
+  // sum of split partials (lower triangle), full Hermitian in W
+  const double2* base = a.gpart + ((size_t)pl * 2 + which) * a.nsplit * (KM * KM);
+  for (int e = tid; e < k * k; e += NT_F) {
+    const int i = e % k, j = e / k;
+    const int ii = i >= j ? i : j, jj = i >= j ? j : i;
+    double2 v = make_double2(0, 0);
+    for (int sp = 0; sp < a.nsplit; sp++) {
+      const double2 x = base[(size_t)sp * (KM * KM) + ii + (size_t)jj * KM];
+      v.x += x.x;
+      v.y += x.y;
+    }
+    if (ii == jj) v.y = 0.0;
+    W[i + j * KM] = (i >= j) ? v : make_double2(v.x, -v.y);
+  }
+  __syncthreads();
+  double2* out = (which == 0 ? a.fhat : a.ghat) + (size_t)pl * (KM * KM);
+  int rc;
+  if (which == 0) {
+    // HEBPJ tolerance k * eps * max |H| (lower triangle), as the oracle
+    double tv = 0.0;
+    long long ti = 0;
+    for (int e = tid; e < k * k; e += NT_F) {
+      const int i = e % k, j = e / k;
+      if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W[i + j * KM]), 0);
+    }
+    hb::block_amax<NT_F>(tv, ti);
+    const double tolz = __dmul_rn(__dmul_rn((double)k, 0x1p-53), tv);
+    rc = hb::hebpj_dev<NT_F, KM>(W, k, KM, out, KM, a.jhat + (size_t)pl * KM, &np_sh, tolz);
+  } else {
+    rc = hb::pchol_dev<NT_F, KM>(W, k, KM, out, KM);
+  }
+  if (tid == 0) {
+    a.fact_ok[pl * 2 + which] = rc == 0;
+    if (rc) atomicCAS(&a.cnt->err, 0, which == 0 ? -7 : -6);
+  }
+}
+
+// k_blk_pivot: one CTA per pair: F^, G^, J^ -> shared memory, border to even order
+// (Sec 6.3.2), inner Level-1 sweep(s) accumulating Z_blk.
 __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
-  extern __shared__ __align__(128) double2 psm[];  // W0 | F^ | G^  (KM*KM each)
+  extern __shared__ __align__(128) double2 psm[];  // W0 (Z_blk) | F^ | G^  (KM*KM each)
   double2* W0 = psm;
   double2* Fh = psm + KM * KM;
   double2* Gh = psm + 2 * KM * KM;
   __shared__ signed char Jh[KM];
-  __shared__ int np_sh;
   __shared__ unsigned long long cnt_all, cnt_big, sweep_all;
   __shared__ int err_sh;
   const int pl = a.pair0 + blockIdx.x, tid = threadIdx.x;
@@ -178,64 +232,30 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
   pair_cols(a, pl, c0p, wp, c0q, wq);
   const int k = wp + wq;
   const int kb = k + (k & 1);
+  if (!a.fact_ok[2 * pl] || !a.fact_ok[2 * pl + 1]) {
+    if (tid == 0) a.applied[pl] = 0;
+    return;
+  }
   if (tid == 0) {
     cnt_all = cnt_big = sweep_all = 0;
     err_sh = 0;
   }
+  const double2* fsrc = a.fhat + (size_t)pl * (KM * KM);
+  const double2* gsrc = a.ghat + (size_t)pl * (KM * KM);
   for (int e = tid; e < KM * KM; e += NT_P) {
-    Fh[e] = make_double2(0, 0);
-    Gh[e] = make_double2(0, 0);
+    const int i = e % KM, j = e / KM;
+    const bool in = i < k && j < k;
+    Fh[e] = in ? fsrc[e] : make_double2(0, 0);
+    Gh[e] = in ? gsrc[e] : make_double2(0, 0);
+    W0[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);   // Z_blk = I
   }
-  // H_blk = sum of split partials (lower triangle), full Hermitian in W0
-  const double2* gp = a.gpart + ((size_t)pl * 2) * a.nsplit * (KM * KM);
-  auto gather = [&](int hs) {
-    const double2* base = gp + (size_t)hs * a.nsplit * (KM * KM);
-    for (int e = tid; e < k * k; e += NT_P) {
-      const int i = e % k, j = e / k;
-      const int ii = i >= j ? i : j, jj = i >= j ? j : i;
-      double2 v = make_double2(0, 0);
-      for (int sp = 0; sp < a.nsplit; sp++) {
-        const double2 x = base[(size_t)sp * (KM * KM) + ii + (size_t)jj * KM];
-        v.x += x.x;
-        v.y += x.y;
-      }
-      if (ii == jj) v.y = 0.0;
-      W0[i + j * KM] = (i >= j) ? v : make_double2(v.x, -v.y);
-    }
-    __syncthreads();
-  };
-  gather(0);
-  // HEBPJ tolerance k * eps * max |H| (lower triangle), as the oracle
-  double tv = 0.0;
-  long long ti = 0;
-  for (int e = tid; e < k * k; e += NT_P) {
-    const int i = e % k, j = e / k;
-    if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W0[i + j * KM]), 0);
-  }
-  hb::block_amax<NT_P>(tv, ti);
-  const double tolz = __dmul_rn(__dmul_rn((double)k, 0x1p-53), tv);
-  int rc = hb::hebpj_dev<NT_P, KM>(W0, k, KM, Fh, KM, Jh, &np_sh, tolz);
-  if (rc) {
-    if (tid == 0) atomicCAS(&a.cnt->err, 0, -7);
-    if (tid == 0) a.applied[pl] = 0;
-    return;
-  }
-  gather(1);
-  rc = hb::pchol_dev<NT_P, KM>(W0, k, KM, Gh, KM);
-  if (rc) {
-    if (tid == 0) atomicCAS(&a.cnt->err, 0, -6);
-    if (tid == 0) a.applied[pl] = 0;
-    return;
-  }
-  // border to even order (Sec 6.3.2) and Z_blk = I
+  for (int i = tid; i < KM; i += NT_P) Jh[i] = i < k ? a.jhat[(size_t)pl * KM + i] : (signed char)1;
+  __syncthreads();
+  // border to even order (Sec 6.3.2)
   if (tid == 0 && kb != k) {
     Fh[k + k * KM] = make_double2(1, 0);
     Gh[k + k * KM] = make_double2(1, 0);
     Jh[k] = 1;
-  }
-  for (int e = tid; e < KM * KM; e += NT_P) {
-    const int i = e % KM, j = e / KM;
-    W0[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
   // inner Level-1 sweeps: one HALF-warp per pivot pair, so the kb/2 <= 32 transforms of
@@ -443,7 +463,8 @@ size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
   const int64_t nb = auto_nblk(n + 1, o) + 2;
   const int64_t K = nb / 2;
   return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)2 * K * KM * KM * 16) +
-         al256((size_t)2 * K * 4) + 2 * al256((size_t)nb * 4) + 4096;
+         al256((size_t)2 * K * 4) + 2 * al256((size_t)nb * 4) + 2 * al256((size_t)K * KM * KM * 16) +
+         al256((size_t)K * KM) + al256((size_t)2 * K * 4) + 4096;
 }
 
 // in comm.cpp
@@ -474,6 +495,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   a.applied = (int*)p; p += al256((size_t)2 * pl.K * 4);
   int* bstart = (int*)p; p += al256((size_t)(pl.nblk + 2) * 4);
   int* bwidth = (int*)p; p += al256((size_t)(pl.nblk + 2) * 4);
+  a.fhat = (double2*)p; p += al256((size_t)pl.K * KM * KM * 16);
+  a.ghat = (double2*)p; p += al256((size_t)pl.K * KM * KM * 16);
+  a.jhat = (signed char*)p; p += al256((size_t)pl.K * KM);
+  a.fact_ok = (int*)p; p += al256((size_t)2 * pl.K * 4);
   k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
   GH_CUDA(cudaGetLastError());
   std::vector<int> bs_h(pl.nblk), bw_h(pl.nblk);
@@ -506,6 +531,8 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   const size_t smem_u = (size_t)(KM * US + KM * ZS) * 16;
   GH_CUDA(cudaFuncSetAttribute(k_blk_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_g));
   GH_CUDA(cudaFuncSetAttribute(k_blk_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+  const size_t smem_f = (size_t)KM * KM * 16;
+  GH_CUDA(cudaFuncSetAttribute(k_blk_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
   GH_CUDA(cudaFuncSetAttribute(k_blk_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u));
   const int tF = (int)((ctx->m + RT - 1) / RT), tZ = (int)((ctx->n + RT - 1) / RT);
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
@@ -575,6 +602,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 1], sh));
         // Z_blk buffer b was last read by the Z update of step s-2
         if (s >= 2 || sw > 0) GH_CUDA(cudaStreamWaitEvent(sh, ev_zdone[b], 0));
+        k_blk_factor<<<dim3(h_np[h], 2), NT_F, smem_f, sh>>>(a);
         k_blk_pivot<<<h_np[h], NT_P, smem_p, sh>>>(a);
         GH_CUDA(cudaEventRecord(ev_piv[h], sh));
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
@@ -624,7 +652,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     float kms = 0;
     GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
     st->kernel_seconds += kms * 1e-3;
-    st->launches += (uint64_t)4 * nst;
+    st->launches += (uint64_t)(4 * nh + 1) * nst;
     for (int s = 0; s < nst; s++) {
       st->flops_gram += fl_gram[s];
       st->flops_update += fl_upd[s];

@@ -57,6 +57,38 @@ __device__ void block_amax(double& v, long long& i) {
   __syncthreads();
 }
 
+// two independent (value, index) argmax reductions with one set of barriers
+template <int NT>
+__device__ void block_amax2(double& v, long long& i, double& u, long long& j) {
+  __shared__ double sv[2][NT / 32];
+  __shared__ long long si[2][NT / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    const double u2 = __shfl_xor_sync(0xffffffffu, u, o);
+    const long long j2 = __shfl_xor_sync(0xffffffffu, j, o);
+    amax_merge(v, i, v2, i2);
+    amax_merge(u, j, u2, j2);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[0][w] = v;
+    si[0][w] = i;
+    sv[1][w] = u;
+    si[1][w] = j;
+  }
+  __syncthreads();
+  v = sv[0][0];
+  i = si[0][0];
+  u = sv[1][0];
+  j = si[1][0];
+  for (int k = 1; k < NT / 32; k++) {  // every thread reduces the NT/32 partials (same order)
+    amax_merge(v, i, sv[0][k], si[0][k]);
+    amax_merge(u, j, sv[1][k], si[1][k]);
+  }
+  __syncthreads();
+}
+
 // Jacobi rotation R (column-major R11, R21, R12, R22) with R^* E R = diag(l1, l2)
 __device__ inline void herm2_jacobi(double a, double2 b, double c, double2* R, double* l1, double* l2) {
   const double ab = cabs(b);
@@ -101,7 +133,6 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
     double mu1 = -1.0;
     long long id = 0x7fffffffffffffffll;
     for (int i = k + threadIdx.x; i < r; i += NT) amax_merge(mu1, id, fabs(W[i + i * ldw].x), i);
-    block_amax<NT>(mu1, id);
     double mu0 = 0.0;
     long long oidx = 0x7fffffffffffffffll;
     const long long rem = r - k;
@@ -109,7 +140,7 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
       const int j = k + (int)(e / rem), i = k + (int)(e % rem);
       if (i > j) amax_merge(mu0, oidx, cabs(W[i + j * ldw]), (long long)j * r + i);
     }
-    block_amax<NT>(mu0, oidx);
+    block_amax2<NT>(mu1, id, mu0, oidx);
     const double mall = mu0 > mu1 ? mu0 : mu1;
     if (!(mall > tolz)) {
       if (threadIdx.x == 0) err_sh = -7;

@@ -282,3 +282,42 @@ def test_reduce_then_sweep_same_eigenvalues():
     Fo, Go, Zp, _ = oracle.hz_pointwise(Fs, Js, Gs)
     l2, *_ = oracle.extract(Fo, Js, Go, Zp)
     assert relerr(l2, l1) < 1e-9
+
+
+# -------------------------------------------------------------- block pivots
+@pytest.mark.parametrize("n,nblk", [(64, 8), (64, 6), (67, 10), (33, 2), (100, 16)])
+def test_block_partition_definition(n, nblk):
+    """Sec 6.4.1: exactly nblk block columns of widths w or w-1
+    (w = ceil(n/nblk)), non-increasing, covering 0..n-1 contiguously."""
+    start, width = oracle.block_partition(n, nblk)
+    w = -(-n // nblk)
+    assert len(width) == nblk and width.sum() == n
+    assert set(width.tolist()) <= {w, w - 1} and all(np.diff(width) <= 0)
+    assert start[0] == 0 and np.array_equal(start[1:], np.cumsum(width)[:-1])
+
+
+def test_block_pair_fb_diagonalises_and_is_a_congruence():
+    """Sec 6.4.2-6.4.3: with the inner level iterated to convergence (FB) the pair's block
+    columns become mutually J-orthogonal / orthogonal, the other columns are untouched, and
+    the update is the congruence F_pair <- F_pair Z_blk accumulated into Z."""
+    P = inputs.known_hyperbolic(71, 80, 24, 0.5)
+    F = np.asfortranarray(P.F.copy())
+    G = np.asfortranarray(P.G.copy())
+    Z = np.asfortranarray(np.eye(24, dtype=np.complex128))
+    cols = list(range(4, 10)) + list(range(15, 20))          # blocks [4,10) and [15,20): order 11 (bordered)
+    a, b = oracle.block_pair(F, P.J, G, Z, 4, 6, 15, 5, inner_sweeps=30)
+    assert a > 0
+    Fp, Gp = F[:, cols], G[:, cols]
+    H = Fp.conj().T @ (P.J[:, None] * Fp)
+    S = Gp.conj().T @ Gp
+    dh, ds = np.sqrt(np.abs(np.diag(H))), np.sqrt(np.diag(S).real)
+    offH = np.abs(H) / np.outer(dh, dh)
+    offS = np.abs(S) / np.outer(ds, ds)
+    np.fill_diagonal(offH, 0)
+    np.fill_diagonal(offS, 0)
+    assert offH.max() < 1e-10 and offS.max() < 1e-12
+    others = [c for c in range(24) if c not in cols]
+    assert np.array_equal(F[:, others], P.F[:, others]) and np.array_equal(G[:, others], P.G[:, others])
+    Zb = Z[np.ix_(cols, cols)]
+    assert np.linalg.norm(F[:, cols] - P.F[:, cols] @ Zb) / np.linalg.norm(F[:, cols]) < 1e-12
+    assert np.linalg.norm(G[:, cols] - P.G[:, cols] @ Zb) / np.linalg.norm(G[:, cols]) < 1e-12

@@ -128,7 +128,9 @@ ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* 
 /* Optional Phase 2 (Sec 5, eq 5.1): JQR of F with diagonal + partial pivoting,
  * hyperbolic Householder reflectors and (J,I) URV 2x2 pivots; G prepermuted by
  * P2 and reduced by Householder QR (R kept, diag real >= 0).  Afterwards
- * m = n.  flags: reserved, pass 0. */
+ * m = n.  May follow a ghsvd_get_factors (which then exported the Phase-1
+ * factors); at most once per problem, before ghsvd_sweep.  flags: reserved, 0.
+ * Errors: GHSVD_E_RANK_DEFICIENT on a degenerate JQR pivot or rank-deficient G. */
 ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
 
 /* Export the factors the sweep will start from (after factor/set_factors,
@@ -145,9 +147,10 @@ ghsvd_status ghsvd_get_factors(ghsvd_ctx ctx, int64_t* m, int64_t* n, void* F, i
  * (may be NULL) receives counters and device time. */
 ghsvd_status ghsvd_sweep(ghsvd_ctx ctx, ghsvd_stats* out);
 
-/* Diagnostic: run only steps [s0, s0+ns) of the pointwise round-robin sweep
- * on the current factors (Z' initialised to I on the first call after
- * factor/set_factors).  *all / *big receive the transformations applied. */
+/* Diagnostic: run only steps [s0, s0+ns) of the round-robin sweep on the current
+ * factors (Z' initialised to I on the first call after factor/set_factors):
+ * pointwise steps in [0, n-2], or for the blocked variants block steps in
+ * [0, nblk-2] (single rank).  *all / *big receive the transformations applied. */
 ghsvd_status ghsvd_run_steps(ghsvd_ctx ctx, int64_t s0, int64_t ns, uint64_t* all, uint64_t* big);
 
 /* Outputs of Sec 6.1.7 and eq (3.2): for each column i,

@@ -50,12 +50,8 @@ static Layout make_layout(const ghsvd_options* o, int64_t m, int64_t n, int64_t 
   L.off_G = off; off += fg;
   L.off_Z = off; off += z;
   L.off_Z2 = off; off += z;
-  if (blocked) {
-    L.off_F2 = off; off += fg;
-    L.off_G2 = off; off += fg;
-  } else {
-    L.off_F2 = L.off_G2 = (size_t)-1;
-  }
+  // no shadow copies of F, G: the blocked updates are in place
+  L.off_F2 = L.off_G2 = (size_t)-1;
   size_t scr = phase2_scratch_bytes(m, n);
   if (nl > 0) scr = std::max(scr, phase1_scratch_bytes(m, n, nl));
   if (blocked) scr = std::max(scr, blk_scratch_bytes(o, m, n));
@@ -158,7 +154,9 @@ ghsvd_status ghsvd_create(const ghsvd_options* opts, int64_t m, int64_t n, int64
     delete h;
     return GHSVD_E_CUDA;
   }
-  if (opts->world_size > 1) {
+  // a communicator is built whenever an id is given (also for world_size == 1, which
+  // runs the NCCL code path with a single rank)
+  if (opts->world_size > 1 || (opts->nccl_id && opts->variant != GHSVD_POINTWISE)) {
     ghsvd_status s = comm_init(ctx);
     if (s != GHSVD_OK) {
       delete h;
@@ -262,14 +260,21 @@ ghsvd_status ghsvd_factor(ghsvd_ctx h, int64_t NA, int64_t NL, int64_t NG, const
 ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
   if (!h) return GHSVD_E_INVALID_ARG;
   Ctx* ctx = &h->c;
-  if (ctx->state != 1 || ctx->bordered || ctx->z_init) {
-    ctx->err = "reduce: must follow factor/set_factors and precede sweep/get_factors";
+  if (ctx->state != 1 || ctx->have_p2) {
+    ctx->err = "reduce: must follow factor/set_factors (once) and precede sweep";
     return GHSVD_E_STATE;
   }
   (void)flags;
   CTX_CUDA(cudaSetDevice(ctx->o.device));
+  // a get_factors before reduce may have bordered the factors and set Z' = I: reduce works
+  // on the unbordered m_user x n_user factors, zeroes both buffers, and bordering / Z' are
+  // redone by the next prepare()
+  ctx->m = ctx->m_user;
+  ctx->n = ctx->n_user;
   TRY(phase2_reduce(ctx));
   ctx->have_p2 = true;
+  ctx->bordered = false;
+  ctx->z_init = false;
   return GHSVD_OK;
 }
 
@@ -364,12 +369,17 @@ ghsvd_status ghsvd_run_steps(ghsvd_ctx h, int64_t s0, int64_t ns, uint64_t* all,
   }
   CTX_CUDA(cudaSetDevice(ctx->o.device));
   TRY(prepare(ctx));
-  if (s0 < 0 || ns < 0 || s0 + ns > ctx->n - 1) {
+  const bool blocked = ctx->o.variant != GHSVD_POINTWISE;
+  if (!blocked && (s0 < 0 || ns < 0 || s0 + ns > ctx->n - 1)) {
     ctx->err = "run_steps: step range outside [0, n-2]";
     return GHSVD_E_INVALID_ARG;
   }
   CTX_CUDA(cudaMemsetAsync(ctx->cnt, 0, sizeof(DevCounters), ctx->stream));
-  TRY(pw_run_steps(ctx, s0, ns));
+  if (blocked) {
+    TRY(blk_run_steps(ctx, s0, ns));  // block steps of the Level-2 round-robin
+  } else {
+    TRY(pw_run_steps(ctx, s0, ns));
+  }
   DevCounters c;
   CTX_CUDA(cudaMemcpyAsync(&c, ctx->cnt, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
   CTX_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -453,7 +463,7 @@ ghsvd_status ghsvd_extract(ghsvd_ctx h, double* lambda, double* sigma_f, double*
   CTX_CUDA(cudaSetDevice(ctx->o.device));
   TRY(prepare(ctx));
   TRY(launch_extract(ctx));
-  if (ctx->o.world_size > 1 && ctx->state == 2 && !ctx->blk_start.empty())
+  if (ctx->comm && ctx->state == 2 && !ctx->blk_start.empty())
     TRY(comm_finalize_outputs(ctx, (int)ctx->blk_start.size(), ctx->blk_start.data(), ctx->blk_width.data(),
                               ctx->lam, ctx->sf, ctx->sg, ctx->Z2, ctx->ldn));
   const int64_t n = ctx->n_user;

@@ -108,6 +108,7 @@ ghsvd_status phase2_reduce(Ctx* ctx);
 size_t phase2_scratch_bytes(int64_t m, int64_t n);
 // blocked.cu
 ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st);
+ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns);
 size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n);
 // comm.cpp
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam,

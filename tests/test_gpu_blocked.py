@@ -82,3 +82,19 @@ def test_blocked_deterministic(gh):
     r1 = run_gpu(gh, P, "bo", 6)
     r2 = run_gpu(gh, P, "bo", 6)
     assert np.array_equal(r1[4], r2[4]) and np.array_equal(r1[5], r2[5])
+
+
+def test_nccl_path_single_rank_bitwise(gh):
+    """The multi-GPU code path (ncclCommInitRank, per-step exchange plan, per-sweep
+    ncclAllReduce of the counters, output allreduce) run with a one-rank communicator must
+    give bitwise the single-GPU result."""
+    P = inputs.known_hyperbolic(16, 160, 128, 0.5)
+    ref = run_gpu(gh, P, "bo", 8)
+    m, n = P.F.shape
+    ctx = gh.Context(m, n, variant="bo", nblocks=8, nccl_id=gh.nccl_unique_id())
+    ctx.set_factors(P.F, P.J, P.G)
+    st = ctx.sweep()
+    lam, sf, sg, Z = ctx.extract()
+    ctx.close()
+    assert st["sweeps"] == ref[3]["sweeps"]
+    assert np.array_equal(lam, ref[4]) and np.array_equal(Z, ref[5])

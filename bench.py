@@ -136,7 +136,7 @@ def cpu_baseline_sample(F0, J0, G0, sweeps: int, budget_s: float = 15.0):
     return {"value": per_step * (n - 1) * sweeps, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"round-robin steps 1..{ns} (of {n - 1}) of the first pointwise sweep on the full {m}x{n} "
                       f"factors, {per_step:.4f} s/step (array-copy overhead {copy_s:.2f} s removed), extrapolated "
-                      f"x{n - 1} steps x {sweeps} sweeps (the GPU run's sweep count)",
+                      f"x{n - 1} steps x {sweeps} sweeps (sweep count of the GPU solve of this config)",
             "seconds_measured": t1 + t2 + tn}
 
 
@@ -237,6 +237,7 @@ def run_ours(args):
                         cluster=args.cluster, threads=args.threads, nblocks=args.nblocks, world_size=ws,
                         rank=rank, nccl_id=nccl_id, detail_timing=blocked)
     phase1_s = None
+    phase2_s = None
     with torch.cuda.stream(stream):
         if kind == "atoms":
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -245,6 +246,10 @@ def run_ours(args):
             ev[1].record(stream)
             stream.synchronize()
             phase1_s = ev[0].elapsed_time(ev[1]) * 1e-3
+            if "reduce" in cfg.get("entry", ""):
+                t0 = time.perf_counter()
+                ctx.reduce()                            # Phase 2 (config 2 recipe)
+                phase2_s = time.perf_counter() - t0
         else:
             ctx.set_factors(payload.F, payload.J, payload.G)
         mb, nb = ctx.factor_shape()
@@ -332,16 +337,18 @@ def run_ours(args):
         if ws > 1:
             torch.distributed.destroy_process_group()
         return 0
+    metric = METRIC if args.config == 3 else f"GHSVD time-to-converge (s) c128 N_G={n} (config {args.config})"
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "metric": metric, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant, "max_sweeps": args.max_sweeps,
-                   "l2": "inputs (1.6 GB) larger than L2 (126 MB)", "phase2": "skipped (ill-conditioned G, PAPER.md:925)"},
+                   "l2": f"inputs ({2 * mb * nb * 16 / 1e9:.2f} GB) vs L2 126 MB",
+                   "phase2": "applied" if phase2_s is not None else "skipped (config recipe; PAPER.md:925 for ill-conditioned G)"},
         "sweeps": sweeps, "converged": stats[-1]["converged"], "big_per_sweep_tail": stats[-1]["big_per_sweep"][-4:],
         "seconds_per_sweep": value / max(sweeps, 1),
         "pair_updates_per_s": pairs / value, "transforms_per_s": stats[-1]["transforms_all"] / value,
-        "phase1_seconds": phase1_s,
+        "phase1_seconds": phase1_s, "phase2_seconds": phase2_s,
         "roofline": roof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(2 * mb * nb * 16 + mb),
                 "d2h_bytes_per_step": int(3 * n * 8)},

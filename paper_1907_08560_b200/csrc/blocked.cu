@@ -20,6 +20,8 @@
 // Multi-GPU (comm.cpp) exchanges block columns between the steps.
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -348,78 +350,78 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
 
 // ---------------------------------------------------------------- update (DMMA)
 // grid (pair, tile): tiles [0, tF) rows of F, [tF, 2 tF) rows of G, [2 tF, 2 tF + tZ) rows of Z
-__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tZ, int tile0) {
+__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile0, int tile_end, int tpc) {
   extern __shared__ __align__(128) double2 usm[];  // X tile [KM][US] | Z_blk [KM][ZS]
-  const int pl = a.pair0 + blockIdx.x, tile = tile0 + blockIdx.y;
-  (void)tZ;
+  const int pl = a.pair0 + blockIdx.x;
   if (!a.applied[pl]) return;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
   const int k = wp + wq;
-  double2* X;
-  long long ld, rows, r0;
-  if (tile < tF) {
-    X = a.F; ld = a.ldm; rows = a.m; r0 = (long long)tile * RT;
-  } else if (tile < 2 * tF) {
-    X = a.G; ld = a.ldm; rows = a.m; r0 = (long long)(tile - tF) * RT;
-  } else {
-    X = a.Z; ld = a.ldn; rows = a.n; r0 = (long long)(tile - 2 * tF) * RT;
-  }
   double2* Xt = usm;
   double2* Zb = usm + KM * US;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < KM * RT; e += NT_U) {
-    const int c = e / RT, r = e % RT;
-    const long long gc = gcol(c, c0p, wp, c0q, wq);
-    const bool ok = gc >= 0 && r0 + r < rows;
-    cp_async16(&Xt[c * US + r], ok ? (const void*)(X + gc * ld + r0 + r) : (const void*)X, ok);
-  }
+  // Z_blk loaded once per CTA and reused for its tpc row tiles
   const double2* zsrc = a.zblk + (size_t)pl * (KM * KM);
   for (int e = tid; e < KM * KM; e += NT_U) {
     const int i = e % KM, j = e / KM;
     cp_async16(&Zb[j * ZS + i], zsrc + e, i < k && j < k);
   }
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-  // out (RT x KM) = Xt (RT x KM) Z_blk (KM x KM): 4 x 8 tiles of 8x8, 4 per warp.
-  // Complex product by the 3M (Gauss) scheme on DMMA: P1 = Xr Zr, P2 = Xi Zi,
-  // P3 = (Xr + Xi)(Zr + Zi); out = (P1 - P2) + i (P3 - P1 - P2): 3 real DMMAs per
-  // 8x8x4 complex step instead of 4 (normwise error bound of the same order).
-  double p1[4][2], p2[4][2], p3[4][2];
-#pragma unroll
-  for (int t = 0; t < 4; t++) p1[t][0] = p1[t][1] = p2[t][0] = p2[t][1] = p3[t][0] = p3[t][1] = 0.0;
-  const int I = warp & 3;          // row tile
+  const int I = warp & 3;          // row tile of 8 rows within the 32-row tile
   const int J0 = (warp >> 2) * 4;  // first of 4 column tiles
   const int kend = (k + 3) & ~3;
-  for (int kk = 0; kk < kend; kk += 4) {
-    const double2 x = Xt[(kk + (lane & 3)) * US + 8 * I + (lane >> 2)];  // A(i, k)
-    const double xs = x.x + x.y;
+  for (int tt = 0; tt < tpc; tt++) {
+    const int tile = tile0 + blockIdx.y * tpc + tt;
+    if (tile >= tile_end) break;
+    double2* X;
+    long long ld, rows, r0;
+    if (tile < tF) {
+      X = a.F; ld = a.ldm; rows = a.m; r0 = (long long)tile * RT;
+    } else if (tile < 2 * tF) {
+      X = a.G; ld = a.ldm; rows = a.m; r0 = (long long)(tile - tF) * RT;
+    } else {
+      X = a.Z; ld = a.ldn; rows = a.n; r0 = (long long)(tile - 2 * tF) * RT;
+    }
+    for (int e = tid; e < KM * RT; e += NT_U) {
+      const int c = e / RT, r = e % RT;
+      const long long gc = gcol(c, c0p, wp, c0q, wq);
+      const bool ok = gc >= 0 && r0 + r < rows;
+      cp_async16(&Xt[c * US + r], ok ? (const void*)(X + gc * ld + r0 + r) : (const void*)X, ok);
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    // out (RT x KM) = Xt (RT x KM) Z_blk (KM x KM): 4 x 8 tiles of 8x8, 4 per warp.
+    // Complex product by the 3M (Gauss) scheme on DMMA: P1 = Xr Zr, P2 = Xi Zi,
+    // P3 = (Xr + Xi)(Zr + Zi); out = (P1 - P2) + i (P3 - P1 - P2): 3 real DMMAs per
+    // 8x8x4 complex step instead of 4 (normwise error bound of the same order).
+    double p1[4][2], p2[4][2], p3[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; t++) p1[t][0] = p1[t][1] = p2[t][0] = p2[t][1] = p3[t][0] = p3[t][1] = 0.0;
+    for (int kk = 0; kk < kend; kk += 4) {
+      const double2 x = Xt[(kk + (lane & 3)) * US + 8 * I + (lane >> 2)];  // A(i, k)
+      const double xs = x.x + x.y;
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const double2 z = Zb[(8 * (J0 + t) + (lane >> 2)) * ZS + kk + (lane & 3)];  // B(k, j)
+        dmma(p1[t][0], p1[t][1], x.x, z.x);
+        dmma(p2[t][0], p2[t][1], x.y, z.y);
+        dmma(p3[t][0], p3[t][1], xs, z.x + z.y);
+      }
+    }
+    __syncthreads();
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-      const double2 z = Zb[(8 * (J0 + t) + (lane >> 2)) * ZS + kk + (lane & 3)];  // B(k, j)
-      dmma(p1[t][0], p1[t][1], x.x, z.x);
-      dmma(p2[t][0], p2[t][1], x.y, z.y);
-      dmma(p3[t][0], p3[t][1], xs, z.x + z.y);
+      const int i = 8 * I + (lane >> 2), j = 8 * (J0 + t) + 2 * (lane & 3);
+      Xt[j * US + i] = make_double2(p1[t][0] - p2[t][0], p3[t][0] - p1[t][0] - p2[t][0]);
+      Xt[(j + 1) * US + i] = make_double2(p1[t][1] - p2[t][1], p3[t][1] - p1[t][1] - p2[t][1]);
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < 4; t++) {
-    const int i = 8 * I + (lane >> 2), j = 8 * (J0 + t) + 2 * (lane & 3);
-    double ore[2], oim[2];
-    for (int e = 0; e < 2; e++) {
-      ore[e] = p1[t][e] - p2[t][e];
-      oim[e] = p3[t][e] - p1[t][e] - p2[t][e];
+    __syncthreads();
+    for (int e = tid; e < KM * RT; e += NT_U) {
+      const int c = e / RT, r = e % RT;
+      const long long gc = gcol(c, c0p, wp, c0q, wq);
+      if (gc >= 0 && r0 + r < rows) X[gc * ld + r0 + r] = Xt[c * US + r];
     }
-    Xt[j * US + i] = make_double2(ore[0], oim[0]);
-    Xt[(j + 1) * US + i] = make_double2(ore[1], oim[1]);
-  }
-  __syncthreads();
-  for (int e = tid; e < KM * RT; e += NT_U) {
-    const int c = e / RT, r = e % RT;
-    const long long gc = gcol(c, c0p, wp, c0q, wq);
-    if (gc >= 0 && r0 + r < rows) X[gc * ld + r0 + r] = Xt[c * US + r];
+    __syncthreads();
   }
 }
 
@@ -436,6 +438,12 @@ __global__ void k_blk_partition(int* bstart, int* bwidth, int nblk, long long n)
 }
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+// tuning knobs (experiments only; defaults are the measured best)
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
 
 int auto_nblk(int64_t n, const ghsvd_options* o) {
   if (o->nblocks > 0) return o->nblocks;
@@ -461,6 +469,7 @@ BlkPlan make_plan(const Ctx* ctx) {
   p.slot0 = ctx->o.rank * p.K;
   const long long target = 4 * 148;
   p.nsplit = (int)std::min<long long>(MAX_SPLIT, std::max<long long>(1, (target + 2 * p.K - 1) / (2 * p.K)));
+  if (env_int("GHSVD_NSPLIT", 0) > 0) p.nsplit = std::min(MAX_SPLIT, env_int("GHSVD_NSPLIT", 0));
   const long long rows_per = (ctx->m + p.nsplit - 1) / p.nsplit;
   p.split_rows = round_up(std::max<long long>(rows_per, 1), RT);
   p.nsplit = (int)((ctx->m + p.split_rows - 1) / p.split_rows);
@@ -580,7 +589,7 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
     k_blk_gram<<<dim3(S.pl.K, 2, S.pl.nsplit), NT_G, S.smem_g, str>>>(a);
     k_blk_factor<<<dim3(S.pl.K, 2), NT_F, S.smem_f, str>>>(a);
     k_blk_pivot<<<S.pl.K, NT_P, S.smem_p, str>>>(a);
-    k_blk_update<<<dim3(S.pl.K, 2 * S.tF + S.tZ), NT_U, S.smem_u, str>>>(a, S.tF, S.tZ, 0);
+    k_blk_update<<<dim3(S.pl.K, 2 * S.tF + S.tZ), NT_U, S.smem_u, str>>>(a, S.tF, 0, 2 * S.tF + S.tZ, 1);
     GH_CUDA(cudaGetLastError());
   }
   return GHSVD_OK;
@@ -598,6 +607,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   const std::vector<int>& bw_h = S.bw_h;
   const size_t smem_g = S.smem_g, smem_p = S.smem_p, smem_f = S.smem_f, smem_u = S.smem_u;
   const int tF = S.tF, tZ = S.tZ;
+  const int tpc = env_int("GHSVD_UPD_TPC", 1);   // row tiles per update CTA (1..8 measured equal)
   cudaStream_t str = ctx->stream;
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
   GH_CUDA(cudaStreamSynchronize(str));
@@ -670,14 +680,14 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         k_blk_pivot<<<h_np[h], NT_P, smem_p, sh>>>(a);
         GH_CUDA(cudaEventRecord(ev_piv[h], sh));
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
-        k_blk_update<<<dim3(h_np[h], 2 * tF), NT_U, smem_u, sh>>>(a, tF, tZ, 0);
+        k_blk_update<<<dim3(h_np[h], (2 * tF + tpc - 1) / tpc), NT_U, smem_u, sh>>>(a, tF, 0, 2 * tF, tpc);
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 3], sh));
         GH_CUDA(cudaEventRecord(ev_fg[h], sh));
       }
       // Z' update of all pairs of step s on the aux stream (overlaps step s+1)
       a.pair0 = 0;
       for (int h = 0; h < nh; h++) GH_CUDA(cudaStreamWaitEvent(aux, ev_piv[h], 0));
-      k_blk_update<<<dim3(pl.K, tZ), NT_U, smem_u, aux>>>(a, tF, tZ, 2 * tF);
+      k_blk_update<<<dim3(pl.K, (tZ + tpc - 1) / tpc), NT_U, smem_u, aux>>>(a, tF, 2 * tF, 2 * tF + tZ, tpc);
       GH_CUDA(cudaEventRecord(ev_zdone[b], aux));
       GH_CUDA(cudaGetLastError());
       if (multi) {

@@ -23,28 +23,15 @@ namespace ghsvd {
 
 namespace {
 
-__device__ __forceinline__ double2 c_mk(double a, double b) { return make_double2(a, b); }
-__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return c_mk(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
-__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return c_mk(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
-__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
-  return c_mk(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
-}
-__device__ __forceinline__ double2 c_conj(double2 a) { return c_mk(a.x, -a.y); }
-__device__ __forceinline__ double2 c_scale(double2 a, double s) { return c_mk(__dmul_rn(a.x, s), __dmul_rn(a.y, s)); }
-__device__ __forceinline__ double c_abs(double2 a) { return __dsqrt_rn(__dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y))); }
-__device__ __forceinline__ double c_abs2(double2 a) { return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)); }
+__device__ __forceinline__ double2 c_conj(double2 a) { return make_double2(a.x, -a.y); }
 
 struct P1Scr {
-  double2* Taa;   // NA * NL*NL staging
+  double2* Taa;   // NA * NL*NL staging of the T blocks
   double2* Tab;
   double2* Tbb;
   double* U;      // NA * NL
   double2* W;     // NA * r*r working matrix (L stored below the diagonal)
   double2* M;     // NA * r*r output Mtilde_a
-  double2* R;     // NA * r * 4 Jacobi rotations of 2x2 pivots
-  double* d;      // NA * r   pivot values / eigenvalues
-  int* bsz;       // NA * r   1, 2 (first of a pair), 0 (second of a pair)
-  int* perm;      // NA * r
   int* npos;      // NA
   int* info;      // NA  (0 ok, -7 rank deficient)
 };
@@ -61,10 +48,6 @@ P1Scr carve(char* base, int64_t NA, int64_t NL) {
   s.U = (double*)p; p += al256((size_t)NA * NL * 8);
   s.W = (double2*)p; p += al256((size_t)NA * r * r * 16);
   s.M = (double2*)p; p += al256((size_t)NA * r * r * 16);
-  s.R = (double2*)p; p += al256((size_t)NA * r * 4 * 16);
-  s.d = (double*)p; p += al256((size_t)NA * r * 8);
-  s.bsz = (int*)p; p += al256((size_t)NA * r * 4);
-  s.perm = (int*)p; p += al256((size_t)NA * r * 4);
   s.npos = (int*)p; p += al256((size_t)NA * 4);
   s.info = (int*)p; p += al256((size_t)NA * 4);
   return s;
@@ -73,61 +56,10 @@ P1Scr carve(char* base, int64_t NA, int64_t NL) {
 size_t carve_bytes(int64_t NA, int64_t NL) {
   const int64_t r = 2 * NL;
   return 3 * al256((size_t)NA * NL * NL * 16) + al256((size_t)NA * NL * 8) + 2 * al256((size_t)NA * r * r * 16) +
-         al256((size_t)NA * r * 64) + al256((size_t)NA * r * 8) + 2 * al256((size_t)NA * r * 4) +
          2 * al256((size_t)NA * 4) + 256;
 }
 
 constexpr int P1T = 256;
-
-// (value, index) argmax keeping the smallest index among equal maxima.
-__device__ __forceinline__ void amax_merge(double& v, long long& i, double v2, long long i2) {
-  if (v2 > v || (v2 == v && i2 < i)) {
-    v = v2;
-    i = i2;
-  }
-}
-
-__device__ void block_amax(double& v, long long& i, double* sv, long long* si) {
-  for (int o = 16; o > 0; o >>= 1) {
-    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
-    amax_merge(v, i, v2, i2);
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sv[w] = v;
-    si[w] = i;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < P1T / 32; k++) amax_merge(sv[0], si[0], sv[k], si[k]);
-  }
-  __syncthreads();
-  v = sv[0];
-  i = si[0];
-  __syncthreads();
-}
-
-// Jacobi rotation R (column-major R11, R21, R12, R22) with R^* E R = diag(l1, l2)
-__device__ void herm2_jacobi_dev(double a, double2 b, double c, double2* R, double* l1, double* l2) {
-  const double ab = c_abs(b);
-  if (ab == 0.0) {
-    R[0] = c_mk(1, 0); R[1] = c_mk(0, 0); R[2] = c_mk(0, 0); R[3] = c_mk(1, 0);
-    *l1 = a; *l2 = c;
-    return;
-  }
-  const double2 e = c_mk(__ddiv_rn(b.x, ab), __ddiv_rn(b.y, ab));
-  const double tau = __ddiv_rn(__dsub_rn(c, a), __dmul_rn(2.0, ab));
-  const double t = __ddiv_rn(tau >= 0.0 ? 1.0 : -1.0, __dadd_rn(fabs(tau), __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(tau, tau)))));
-  const double cs = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(t, t)))), sn = __dmul_rn(t, cs);
-  const double2 em = c_conj(e);
-  R[0] = c_mk(cs, 0.0);
-  R[1] = c_scale(em, -sn);
-  R[2] = c_mk(sn, 0.0);
-  R[3] = c_scale(em, cs);
-  *l1 = __dsub_rn(a, __dmul_rn(t, ab));
-  *l2 = __dadd_rn(c, __dmul_rn(t, ab));
-}
 
 // Build W_a (full Hermitian from the lower triangle of T_a) and the tolerance.
 __global__ void __launch_bounds__(P1T) k_build_T(P1Scr s, int NL) {

@@ -339,8 +339,6 @@ __global__ void __launch_bounds__(T2) k_qr_prep(double2* G, long long ld, long l
 __global__ void k_qr_gather(const double2* G, long long ld, double2* out, long long ldo, long long n,
                             const long long* p2) {
   const long long j = blockIdx.x;
-  __shared__ double2 ph_dummy;
-  (void)ph_dummy;
   for (long long i = threadIdx.x; i < n; i += blockDim.x)
     out[i + j * ldo] = i <= j ? G[i + p2[j] * ld] : cmk(0, 0);
 }

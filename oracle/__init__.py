@@ -94,6 +94,8 @@ def lib():
                                     ctypes.POINTER(_Stats)]
         L.or_extract.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, P, P, P, P, I64]
         L.or_block_partition.argtypes = [I64, I64, P, P]
+        L.or_hz_pointwise_inv.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, P, I64, D, Ci, Ci, Ci,
+                                          ctypes.POINTER(_Stats)]
         L.or_block_pair.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, I64, I64, I64, I64, Ci, D, Ci,
                                     ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.or_hebpj.argtypes = [I64, P, I64, P, I64, P, ctypes.POINTER(I64)]
@@ -158,6 +160,22 @@ def hz_pointwise(F, J, G, eps=EPS, criterion=CRIT_RELATIVE, cmax=30, nthreads=0)
     _chk(lib().or_hz_pointwise(m, n, _ptr(F), m, _ptr(J), _ptr(G), m, _ptr(Z), n, eps, criterion,
                                cmax, nthreads, ctypes.byref(st)), "hz_pointwise")
     return F, G, Z, st.todict()
+
+
+def hz_pointwise_inv(F, J, G, eps=EPS, criterion=CRIT_RELATIVE, cmax=30, nthreads=1):
+    """Algorithm 2 also accumulating W = Z'^{-1} (n even).  Returns (F', G', Z', W, stats).
+    Single-threaded: the row updates of W are not disjoint across the pairs of a step in
+    memory order (they are in index space), kept sequential for clarity."""
+    F = _cf(F)
+    G = _cf(G)
+    J = np.ascontiguousarray(J, dtype=np.int8)
+    m, n = F.shape
+    Z = np.zeros((n, n), dtype=np.complex128, order="F")
+    W = np.zeros((n, n), dtype=np.complex128, order="F")
+    st = _Stats()
+    _chk(lib().or_hz_pointwise_inv(m, n, _ptr(F), m, _ptr(J), _ptr(G), m, _ptr(Z), n, _ptr(W), n, eps,
+                                   criterion, cmax, nthreads, ctypes.byref(st)), "hz_pointwise_inv")
+    return F, G, Z, W, st.todict()
 
 
 def hz_steps(F, J, G, Z, s0, ns, eps=EPS, criterion=CRIT_RELATIVE, nthreads=0):

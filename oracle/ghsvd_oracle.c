@@ -174,6 +174,24 @@ static void rot_cols(int64_t len, orc *xp, orc *xq, const orc z[4]) {
   }
 }
 
+/* Optional accumulation of Z'^{-1}: when Z' <- Z' E (E = Z'hat
+ * at (p, q)), Z'^{-1} <- E^{-1} Z'^{-1}, i.e. rows p and q of W = Z'^{-1} are replaced
+ * by Z'hat^{-1} [w_p; w_q], Z'hat^{-1} = (1/det) [[z22, -z12], [-z21, z11]]. */
+static orc *g_winv = NULL;
+static int64_t g_ldw = 0, g_nw = 0;
+
+static void rot_rows_inv(orc *W, int64_t ldw, int64_t nw, int64_t p, int64_t q, const orc z[4]) {
+  /* z = {z11, z21, z12, z22} */
+  orc det = csub(cmul(z[0], z[3]), cmul(z[2], z[1]));
+  orc a = cdiv(z[3], det), b = cdiv(cscale(z[2], -1.0), det);
+  orc c = cdiv(cscale(z[1], -1.0), det), d = cdiv(z[0], det);
+  for (int64_t j = 0; j < nw; j++) {
+    orc wp = EL(W, ldw, p, j), wq = EL(W, ldw, q, j);
+    EL(W, ldw, p, j) = cadd(cmul(a, wp), cmul(b, wq));
+    EL(W, ldw, q, j) = cadd(cmul(c, wp), cmul(d, wq));
+  }
+}
+
 /* One parallel step s of the ordering (Alg. 3 body): Grams (6.1) in one pass,
  * transform, updates of F, G (m rows) and Z (nz rows). */
 static int hz_step(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
@@ -215,6 +233,7 @@ static int hz_step(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
     rot_cols(m, fp, fq, z);
     rot_cols(m, gp, gq, z);
     rot_cols(nz, &EL(Z, ldz, 0, p), &EL(Z, ldz, 0, q), z);
+    if (g_winv && nz == g_nw) rot_rows_inv(g_winv, g_ldw, g_nw, p, q, z);
     a_all += 1;
     if (kind == OR_K_BIG) a_big += 1;
   }
@@ -307,6 +326,21 @@ int or_hz_pointwise(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
   }
   free(Fb); free(Gb); free(Zb); free(Jb);
   return e;
+}
+
+/* Algorithm 2 also accumulating W = Z'^{-1} (n even; W initialised to I). */
+int or_hz_pointwise_inv(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
+                        orc *G, int64_t ldg, orc *Z, int64_t ldz, orc *W, int64_t ldw,
+                        double eps, int criterion, int cmax, int nthreads, or_stats *st) {
+  if ((n & 1) || ldw < n) return OR_E_ARG;
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) EL(W, ldw, i, j) = cmk(i == j ? 1.0 : 0.0, 0.0);
+  g_winv = W;
+  g_ldw = ldw;
+  g_nw = n;
+  int rc = or_hz_pointwise(m, n, F, ldf, J, G, ldg, Z, ldz, eps, criterion, cmax, nthreads, st);
+  g_winv = NULL;
+  return rc;
 }
 
 /* ------------------------------------------------------------- extract */

@@ -67,6 +67,12 @@ int or_hz_pointwise(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
                     orc *G, int64_t ldg, orc *Z, int64_t ldz, double eps,
                     int criterion, int cmax, int nthreads, or_stats *st);
 
+/* As or_hz_pointwise (n even) and also accumulating W = Z'^{-1} by applying each
+ * 2x2 inverse to rows p, q from the left; X = Sigma W. */
+int or_hz_pointwise_inv(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
+                        orc *G, int64_t ldg, orc *Z, int64_t ldz, orc *W, int64_t ldw,
+                        double eps, int criterion, int cmax, int nthreads, or_stats *st);
+
 /* Run only steps [s0, s0+ns) of one pointwise sweep on (F,G,Z) in place
  * (Z not reset).  n must be even.  Counters accumulated into *all, *big. */
 int or_hz_steps(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,

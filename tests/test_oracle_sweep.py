@@ -321,3 +321,34 @@ def test_block_pair_fb_diagonalises_and_is_a_congruence():
     Zb = Z[np.ix_(cols, cols)]
     assert np.linalg.norm(F[:, cols] - P.F[:, cols] @ Zb) / np.linalg.norm(F[:, cols]) < 1e-12
     assert np.linalg.norm(G[:, cols] - P.G[:, cols] @ Zb) / np.linalg.norm(G[:, cols]) < 1e-12
+
+
+# ------------------------------------------------ NEXT-1: accumulated Z'^{-1}
+@pytest.mark.parametrize("which,m,n", [("hyp", 96, 64), ("gsvd", 128, 64), ("rand", 70, 40)])
+def test_accumulated_inverse_and_eq71_errors(which, m, n):
+    """W = Z'^{-1} accumulated by the 2x2 inverses from the left.
+    Pins: W Z' = I (definition of the inverse, numpy matmul); the GHSVD (3.1) with
+    X = Sigma W reproduces the inputs, i.e. the eq (7.1) relative errors
+    ||F - U Sigma_F X||_F / ||F||_F and ||G - V Sigma_G X||_F / ||G||_F are at the level
+    the paper reports (7.98e-14 ... 8.23e-13)."""
+    if which == "hyp":
+        P = inputs.known_hyperbolic(81, m, n, 0.5)
+    elif which == "gsvd":
+        P = inputs.known_gsvd(82, m, n)
+    else:
+        P = inputs.random_pencil(83, m, n, 0.5)
+    F, G, Zp, W, st = oracle.hz_pointwise_inv(P.F, P.J, P.G)
+    F2, G2, Zp2, st2 = oracle.hz_pointwise(P.F, P.J, P.G, nthreads=1)
+    assert np.array_equal(F, F2) and np.array_equal(Zp, Zp2)      # same iteration
+    assert np.abs(W @ Zp - np.eye(n)).max() < 1e-10
+    lam, sf, sg, Z = oracle.extract(F, P.J, G, Zp)
+    sfp = np.sqrt(np.abs(np.einsum("ij,i,ij->j", F.conj(), P.J, F).real))
+    sgp = np.linalg.norm(G, axis=0)
+    sig = np.sqrt(sfp ** 2 + sgp ** 2)
+    U = F / sfp[None, :]
+    V = G / sgp[None, :]
+    X = sig[:, None] * W                                           # X = Sigma Z'^{-1}
+    assert np.abs(Z @ X - np.eye(n)).max() < 1e-9                  # X = Z^{-1}
+    eF = np.linalg.norm(P.F - U @ (sf[:, None] * X)) / np.linalg.norm(P.F)
+    eG = np.linalg.norm(P.G - V @ (sg[:, None] * X)) / np.linalg.norm(P.G)
+    assert eF < 1e-12 and eG < 1e-12

@@ -73,6 +73,10 @@ typedef struct {
   int kernel;          /* pointwise step kernel: 0 = auto (= 2), 1 = one cluster per pair, TMA-staged slices;
                           2 = two-pass through L2 (default); 3 = persistent pipelined TMA */
   int detail_timing;   /* blocked: CUDA events around every kernel (fills t_* in ghsvd_stats) */
+  int want_x;          /* also accumulate W = Z'^{-1} during the sweep so that ghsvd_extract_x
+                          can return X = Z^{-1} = Sigma Z'^{-1} (NEXT-1):
+                          pointwise by 2x2 inverses, blocked by block-pivot inverses.
+                          Costs one more n x n buffer and its updates.  Pointwise kernel 2 only. */
 } ghsvd_options;
 
 typedef struct {
@@ -161,6 +165,12 @@ ghsvd_status ghsvd_run_steps(ghsvd_ctx ctx, int64_t s0, int64_t ns, uint64_t* al
  * global column index of each output column (identity on one GPU). */
 ghsvd_status ghsvd_extract(ghsvd_ctx ctx, double* lambda, double* sigma_f, double* sigma_g,
                            void* Z, int64_t ldz, int64_t* col_ids);
+
+/* X = Z^{-1} = Sigma Z'^{-1}, the right generalized singular vectors of (3.1)
+ * (F = U Sigma_F X, G = V Sigma_G X), with columns permuted back by P2
+ * (X~ = X P2^T).  n x n (ldx >= n), host or device.  Requires opts.want_x and a
+ * completed sweep; GHSVD_E_STATE otherwise. */
+ghsvd_status ghsvd_extract_x(ghsvd_ctx ctx, void* X, int64_t ldx);
 
 /* Copy the current transformed factors F', G' (m x n) to F, G (NULL = skip). */
 ghsvd_status ghsvd_get_transformed(ghsvd_ctx ctx, void* F, int64_t ldf, void* G, int64_t ldg,

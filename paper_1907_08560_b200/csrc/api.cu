@@ -50,6 +50,12 @@ static Layout make_layout(const ghsvd_options* o, int64_t m, int64_t n, int64_t 
   L.off_G = off; off += fg;
   L.off_Z = off; off += z;
   L.off_Z2 = off; off += z;
+  if (o->want_x) {
+    L.off_W = off; off += z;
+    L.off_X = off; off += z;
+  } else {
+    L.off_W = L.off_X = (size_t)-1;
+  }
   // no shadow copies of F, G: the blocked updates are in place
   L.off_F2 = L.off_G2 = (size_t)-1;
   size_t scr = phase2_scratch_bytes(m, n);
@@ -85,6 +91,9 @@ void ghsvd_default_options(ghsvd_options* o) {
   o->cluster = 0;
   o->threads = 0;
   o->use_graph = 1;
+  o->kernel = 0;
+  o->detail_timing = 0;
+  o->want_x = 0;
 }
 
 static bool opts_ok(const ghsvd_options* o) {
@@ -133,6 +142,8 @@ ghsvd_status ghsvd_create(const ghsvd_options* opts, int64_t m, int64_t n, int64
   ctx->Z2 = (double2*)(ctx->ws + L.off_Z2);
   ctx->F2 = L.off_F2 == (size_t)-1 ? nullptr : (double2*)(ctx->ws + L.off_F2);
   ctx->G2 = L.off_G2 == (size_t)-1 ? nullptr : (double2*)(ctx->ws + L.off_G2);
+  ctx->W = L.off_W == (size_t)-1 ? nullptr : (double2*)(ctx->ws + L.off_W);
+  ctx->Xo = L.off_X == (size_t)-1 ? nullptr : (double2*)(ctx->ws + L.off_X);
   ctx->scr = ctx->ws + L.off_scr;
   char* p = ctx->ws + L.off_misc;
   ctx->cnt = (DevCounters*)p; p += al(sizeof(DevCounters));
@@ -306,6 +317,7 @@ static ghsvd_status prepare(Ctx* ctx) {
     ctx->n = ctx->n_user;
   }
   TRY(launch_set_identity(ctx, ctx->Z, ctx->ldn, ctx->n));
+  if (ctx->W) TRY(launch_set_identity(ctx, ctx->W, ctx->ldn, ctx->n));
   TRY(pw_configure(ctx));
   CTX_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->z_init = true;
@@ -465,7 +477,7 @@ ghsvd_status ghsvd_extract(ghsvd_ctx h, double* lambda, double* sigma_f, double*
   TRY(launch_extract(ctx));
   if (ctx->comm && ctx->state == 2 && !ctx->blk_start.empty())
     TRY(comm_finalize_outputs(ctx, (int)ctx->blk_start.size(), ctx->blk_start.data(), ctx->blk_width.data(),
-                              ctx->lam, ctx->sf, ctx->sg, ctx->Z2, ctx->ldn));
+                              ctx->lam, ctx->sf, ctx->sg, ctx->Z2, ctx->ldn, ctx->o.want_x ? ctx->Xo : nullptr));
   const int64_t n = ctx->n_user;
   if (lambda) CTX_CUDA(cudaMemcpyAsync(lambda, ctx->lam, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
   if (sigma_f) CTX_CUDA(cudaMemcpyAsync(sigma_f, ctx->sf, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
@@ -477,6 +489,29 @@ ghsvd_status ghsvd_extract(ghsvd_ctx h, double* lambda, double* sigma_f, double*
   if (col_ids) {
     for (int64_t i = 0; i < n; i++) col_ids[i] = i;
   }
+  return GHSVD_OK;
+}
+
+ghsvd_status ghsvd_extract_x(ghsvd_ctx h, void* X, int64_t ldx) {
+  if (!h) return GHSVD_E_INVALID_ARG;
+  Ctx* ctx = &h->c;
+  if (!ctx->o.want_x || !ctx->W || ctx->state != 2) {
+    ctx->err = "extract_x: needs opts.want_x and a completed sweep";
+    return GHSVD_E_STATE;
+  }
+  if (!X || ldx < ctx->n_user) {
+    ctx->err = "extract_x: bad X / ldx";
+    return GHSVD_E_INVALID_ARG;
+  }
+  CTX_CUDA(cudaSetDevice(ctx->o.device));
+  TRY(launch_extract(ctx));
+  if (ctx->comm && !ctx->blk_start.empty())
+    TRY(comm_finalize_outputs(ctx, (int)ctx->blk_start.size(), ctx->blk_start.data(), ctx->blk_width.data(),
+                              ctx->lam, ctx->sf, ctx->sg, ctx->Z2, ctx->ldn, ctx->Xo));
+  const int64_t n = ctx->n_user;
+  CTX_CUDA(cudaMemcpy2DAsync(X, (size_t)ldx * 16, ctx->Xo, (size_t)ctx->ldn * 16, (size_t)n * 16, (size_t)n,
+                             cudaMemcpyDefault, ctx->stream));
+  CTX_CUDA(cudaStreamSynchronize(ctx->stream));
   return GHSVD_OK;
 }
 

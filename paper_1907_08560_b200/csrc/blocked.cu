@@ -74,6 +74,8 @@ struct BlkArgs {
   double2* ghat;            // [pair][KM*KM]  G^ from pivoted Cholesky
   signed char* jhat;        // [pair][KM]     J^
   int* fact_ok;             // [pair][2]
+  double2* zinvT;           // [pair][KM*KM] (Z_blk^{-1})^T if want_x, else nullptr
+  double2* W;               // want_x: W^T = (Z'^{-1})^T (n rows, ld ldn)
   DevCounters* cnt;
   double eps;
   int literal;
@@ -346,11 +348,76 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
     atomicAdd(&a.cnt->all, cnt_all);
     atomicAdd(&a.cnt->big, cnt_big);
   }
+  if (a.zinvT && cnt_all > 0) {
+    // NEXT-1: (Z_blk^{-1})^T for the W^T update, Gauss-Jordan with partial pivoting on
+    // [Fh | Gh] = [Z_blk | I] (F^, G^ are no longer needed after the inner sweep)
+    __syncthreads();
+    for (int e = tid; e < KM * KM; e += NT_P) {
+      const int i = e % KM, j = e / KM;
+      Fh[e] = W0[e];
+      Gh[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    }
+    __shared__ int piv_sh;
+    __syncthreads();
+    for (int c = 0; c < kb; c++) {
+      if (tid == 0) {
+        int pv = c;
+        double best = -1.0;
+        for (int i = c; i < kb; i++) {
+          const double2 v = Fh[i + c * KM];
+          const double av = v.x * v.x + v.y * v.y;
+          if (av > best) { best = av; pv = i; }
+        }
+        piv_sh = pv;
+      }
+      __syncthreads();
+      const int pv = piv_sh;
+      if (pv != c) {
+        for (int j = tid; j < KM; j += NT_P) {
+          double2 t = Fh[c + j * KM]; Fh[c + j * KM] = Fh[pv + j * KM]; Fh[pv + j * KM] = t;
+          t = Gh[c + j * KM]; Gh[c + j * KM] = Gh[pv + j * KM]; Gh[pv + j * KM] = t;
+        }
+        __syncthreads();
+      }
+      const double2 d = Fh[c + c * KM];
+      const double dd = d.x * d.x + d.y * d.y;
+      const double2 inv = make_double2(d.x / dd, -d.y / dd);
+      __syncthreads();
+      for (int j = tid; j < KM; j += NT_P) {   // scale row c
+        const double2 f = Fh[c + j * KM], g = Gh[c + j * KM];
+        Fh[c + j * KM] = make_double2(f.x * inv.x - f.y * inv.y, f.x * inv.y + f.y * inv.x);
+        Gh[c + j * KM] = make_double2(g.x * inv.x - g.y * inv.y, g.x * inv.y + g.y * inv.x);
+      }
+      __syncthreads();
+      for (int e = tid; e < kb * KM; e += NT_P) {   // eliminate column c from the other rows
+        const int i = e % kb, j = e / kb;
+        if (i == c) continue;
+        const double2 f = Fh[i + c * KM];
+        const double2 rf = Fh[c + j * KM], rg = Gh[c + j * KM];
+        const double2 uf = make_double2(f.x * rf.x - f.y * rf.y, f.x * rf.y + f.y * rf.x);
+        const double2 ug = make_double2(f.x * rg.x - f.y * rg.y, f.x * rg.y + f.y * rg.x);
+        if (j != c) Fh[i + j * KM] = make_double2(Fh[i + j * KM].x - uf.x, Fh[i + j * KM].y - uf.y);
+        Gh[i + j * KM] = make_double2(Gh[i + j * KM].x - ug.x, Gh[i + j * KM].y - ug.y);
+      }
+      __syncthreads();
+      for (int i = tid; i < kb; i += NT_P)
+        if (i != c) Fh[i + c * KM] = make_double2(0.0, 0.0);
+      __syncthreads();
+    }
+    double2* wo = a.zinvT + (size_t)pl * (KM * KM);
+    for (int e = tid; e < KM * KM; e += NT_P) {
+      const int i = e % KM, j = e / KM;
+      wo[e] = Gh[j + i * KM];   // transpose (no conjugation)
+    }
+  }
 }
 
 // ---------------------------------------------------------------- update (DMMA)
 // grid (pair, tile): tiles [0, tF) rows of F, [tF, 2 tF) rows of G, [2 tF, 2 tF + tZ) rows of Z
-__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile0, int tile_end, int tpc) {
+// wmode = 1: the tiles are row tiles of W^T (n rows) and the right factor is
+// (Z_blk^{-1})^T (NEXT-1 accumulation of Z'^{-1}).
+__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile0, int tile_end, int tpc,
+                                                     int wmode) {
   extern __shared__ __align__(128) double2 usm[];  // X tile [KM][US] | Z_blk [KM][ZS]
   const int pl = a.pair0 + blockIdx.x;
   if (!a.applied[pl]) return;
@@ -361,7 +428,7 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
   double2* Zb = usm + KM * US;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // Z_blk loaded once per CTA and reused for its tpc row tiles
-  const double2* zsrc = a.zblk + (size_t)pl * (KM * KM);
+  const double2* zsrc = (wmode ? a.zinvT : a.zblk) + (size_t)pl * (KM * KM);
   for (int e = tid; e < KM * KM; e += NT_U) {
     const int i = e % KM, j = e / KM;
     cp_async16(&Zb[j * ZS + i], zsrc + e, i < k && j < k);
@@ -374,7 +441,9 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
     if (tile >= tile_end) break;
     double2* X;
     long long ld, rows, r0;
-    if (tile < tF) {
+    if (wmode) {
+      X = a.W; ld = a.ldn; rows = a.n; r0 = (long long)(tile - tile0) * RT;
+    } else if (tile < tF) {
       X = a.F; ld = a.ldm; rows = a.m; r0 = (long long)tile * RT;
     } else if (tile < 2 * tF) {
       X = a.G; ld = a.ldm; rows = a.m; r0 = (long long)(tile - tF) * RT;
@@ -483,7 +552,8 @@ size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
   const int64_t K = nb / 2;
   return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)2 * K * KM * KM * 16) +
          al256((size_t)2 * K * 4) + 2 * al256((size_t)nb * 4) + 2 * al256((size_t)K * KM * KM * 16) +
-         al256((size_t)K * KM) + al256((size_t)2 * K * 4) + 4096;
+         al256((size_t)K * KM) + al256((size_t)2 * K * 4) + (o->want_x ? al256((size_t)2 * K * KM * KM * 16) : 0) +
+         4096;
 }
 
 // in comm.cpp
@@ -527,6 +597,12 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   a.ghat = (double2*)p; p += al256((size_t)pl.K * KM * KM * 16);
   a.jhat = (signed char*)p; p += al256((size_t)pl.K * KM);
   a.fact_ok = (int*)p; p += al256((size_t)2 * pl.K * 4);
+  a.W = ctx->o.want_x ? ctx->W : nullptr;
+  if (a.W) {
+    a.zinvT = (double2*)p; p += al256((size_t)2 * pl.K * KM * KM * 16);   // double-buffered like zblk
+  } else {
+    a.zinvT = nullptr;
+  }
   k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
   GH_CUDA(cudaGetLastError());
   S.bs_h.assign(pl.nblk, 0);
@@ -589,7 +665,8 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
     k_blk_gram<<<dim3(S.pl.K, 2, S.pl.nsplit), NT_G, S.smem_g, str>>>(a);
     k_blk_factor<<<dim3(S.pl.K, 2), NT_F, S.smem_f, str>>>(a);
     k_blk_pivot<<<S.pl.K, NT_P, S.smem_p, str>>>(a);
-    k_blk_update<<<dim3(S.pl.K, 2 * S.tF + S.tZ), NT_U, S.smem_u, str>>>(a, S.tF, 0, 2 * S.tF + S.tZ, 1);
+    k_blk_update<<<dim3(S.pl.K, 2 * S.tF + S.tZ), NT_U, S.smem_u, str>>>(a, S.tF, 0, 2 * S.tF + S.tZ, 1, 0);
+    if (a.W) k_blk_update<<<dim3(S.pl.K, S.tZ), NT_U, S.smem_u, str>>>(a, S.tF, 0, S.tZ, 1, 1);
     GH_CUDA(cudaGetLastError());
   }
   return GHSVD_OK;
@@ -642,6 +719,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     for (auto e : tev) cudaEventDestroy(e);
   };
   double2* zblk0 = a.zblk;
+  double2* zinv0 = a.zinvT;
   int* applied0 = a.applied;
   // algorithmic flops per block step (Hermitian Grams k(k+1)/2 m each; updates k^2 (2m+n))
   std::vector<double> fl_gram(nst, 0.0), fl_upd(nst, 0.0);
@@ -662,6 +740,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       const int b = s & 1;
       a.s = s;
       a.zblk = zblk0 + (size_t)b * pl.K * KM * KM;
+      if (zinv0) a.zinvT = zinv0 + (size_t)b * pl.K * KM * KM;
       a.applied = applied0 + (size_t)b * pl.K;
       // the Grams of step s read block columns updated by both halves in step s-1
       if (nh == 2 && s > 0) {
@@ -680,14 +759,15 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         k_blk_pivot<<<h_np[h], NT_P, smem_p, sh>>>(a);
         GH_CUDA(cudaEventRecord(ev_piv[h], sh));
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
-        k_blk_update<<<dim3(h_np[h], (2 * tF + tpc - 1) / tpc), NT_U, smem_u, sh>>>(a, tF, 0, 2 * tF, tpc);
+        k_blk_update<<<dim3(h_np[h], (2 * tF + tpc - 1) / tpc), NT_U, smem_u, sh>>>(a, tF, 0, 2 * tF, tpc, 0);
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 3], sh));
         GH_CUDA(cudaEventRecord(ev_fg[h], sh));
       }
       // Z' update of all pairs of step s on the aux stream (overlaps step s+1)
       a.pair0 = 0;
       for (int h = 0; h < nh; h++) GH_CUDA(cudaStreamWaitEvent(aux, ev_piv[h], 0));
-      k_blk_update<<<dim3(pl.K, (tZ + tpc - 1) / tpc), NT_U, smem_u, aux>>>(a, tF, 2 * tF, 2 * tF + tZ, tpc);
+      k_blk_update<<<dim3(pl.K, (tZ + tpc - 1) / tpc), NT_U, smem_u, aux>>>(a, tF, 2 * tF, 2 * tF + tZ, tpc, 0);
+      if (a.W) k_blk_update<<<dim3(pl.K, (tZ + tpc - 1) / tpc), NT_U, smem_u, aux>>>(a, tF, 0, tZ, tpc, 1);
       GH_CUDA(cudaEventRecord(ev_zdone[b], aux));
       GH_CUDA(cudaGetLastError());
       if (multi) {

@@ -187,10 +187,12 @@ ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int*
   NCCL_CALL(N->GroupStart());
   auto xfer = [&](int64_t b, int peer, bool send) -> ncclResult_t {
     const size_t w = (size_t)bwidth[b];
-    double2* bufs[3] = {ctx->F + (size_t)bstart[b] * ctx->ldm, ctx->G + (size_t)bstart[b] * ctx->ldm,
-                        ctx->Z + (size_t)bstart[b] * ctx->ldn};
-    const size_t cnt[3] = {w * ctx->ldm * 2, w * ctx->ldm * 2, w * ctx->ldn * 2};  // doubles
-    for (int t = 0; t < 3; t++) {
+    double2* bufs[4] = {ctx->F + (size_t)bstart[b] * ctx->ldm, ctx->G + (size_t)bstart[b] * ctx->ldm,
+                        ctx->Z + (size_t)bstart[b] * ctx->ldn,
+                        ctx->o.want_x && ctx->W ? ctx->W + (size_t)bstart[b] * ctx->ldn : nullptr};
+    const size_t cnt[4] = {w * ctx->ldm * 2, w * ctx->ldm * 2, w * ctx->ldn * 2, w * ctx->ldn * 2};  // doubles
+    for (int t = 0; t < 4; t++) {
+      if (!bufs[t]) continue;
       ncclResult_t r = send ? N->Send(bufs[t], cnt[t], ncclFloat64, peer, comm, st)
                             : N->Recv(bufs[t], cnt[t], ncclFloat64, peer, comm, st);
       if (r != ncclSuccess) return r;
@@ -226,7 +228,7 @@ ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c) {
 // Complete the extracted outputs on every rank: zero the columns this rank does
 // not own after the final exchange (ownership of block step 0), then sum.
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam, double* sf,
-                                   double* sg, double2* Zout, int64_t ldz) {
+                                   double* sg, double2* Zout, int64_t ldz, double2* Xout) {
   Nccl* N = nccl();
   if (!N || !ctx->comm) {
     ctx->err = "multi-GPU: no communicator";
@@ -242,6 +244,8 @@ ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const 
     GH_CUDA(cudaMemsetAsync(sf + c0, 0, w * 8, st));
     GH_CUDA(cudaMemsetAsync(sg + c0, 0, w * 8, st));
     GH_CUDA(cudaMemsetAsync(Zout + c0 * ldz, 0, w * ldz * 16, st));
+    if (Xout)  // rows c0 .. c0+w-1 of X belong to this block column of W^T
+      GH_CUDA(cudaMemset2DAsync(Xout + c0, (size_t)ldz * 16, 0, w * 16, (size_t)ctx->n, st));
   }
   ncclComm_t comm = (ncclComm_t)ctx->comm;
   const size_t n = (size_t)ctx->n;
@@ -250,6 +254,7 @@ ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const 
   NCCL_CALL(N->AllReduce(sf, sf, n, ncclFloat64, ncclSum, comm, st));
   NCCL_CALL(N->AllReduce(sg, sg, n, ncclFloat64, ncclSum, comm, st));
   NCCL_CALL(N->AllReduce(Zout, Zout, n * ldz * 2, ncclFloat64, ncclSum, comm, st));
+  if (Xout) NCCL_CALL(N->AllReduce(Xout, Xout, n * ldz * 2, ncclFloat64, ncclSum, comm, st));
   NCCL_CALL(N->GroupEnd());
   return GHSVD_OK;
 }

@@ -16,9 +16,10 @@ __global__ void __launch_bounds__(NT) k_extract(const double2* __restrict__ F, c
                                                 const double2* __restrict__ Zp, double2* __restrict__ Zout,
                                                 long long ldm, long long ldn, long long m, long long n_rows,
                                                 long long npos, const long long* __restrict__ p2,
-                                                long long np2, double* lam, double* sf, double* sg) {
+                                                long long np2, double* lam, double* sf, double* sg,
+                                                const double2* __restrict__ Wt, double2* __restrict__ Xout) {
   __shared__ double red[NT / 32][2];
-  __shared__ double inv_sig;
+  __shared__ double inv_sig, sig_sh;
   const long long c = blockIdx.x;
   const double2* f = F + c * ldm;
   const double2* g = G + c * ldm;
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(NT) k_extract(const double2* __restrict__ F, c
     sf[c] = sfp / sig;
     sg[c] = sgp / sig;
     inv_sig = 1.0 / sig;
+    sig_sh = sig;
   }
   __syncthreads();
   const double is = inv_sig;
@@ -60,13 +62,25 @@ __global__ void __launch_bounds__(NT) k_extract(const double2* __restrict__ F, c
     const long long dr = (r < np2) ? p2[r] : r;
     zo[dr] = make_double2(v.x * is, v.y * is);
   }
+  if (Wt) {
+    // NEXT-1: X = Sigma Z'^{-1}; row c of X is Sigma_c times column c of W^T; columns
+    // permuted back by P2 (X~ = X P2^T)
+    const double sg_c = sig_sh;
+    const double2* w = Wt + c * ldn;
+    for (long long r = threadIdx.x; r < n_rows; r += NT) {
+      const double2 v = w[r];
+      const long long dr = (r < np2) ? p2[r] : r;
+      Xout[c + dr * ldn] = make_double2(v.x * sg_c, v.y * sg_c);
+    }
+  }
 }
 
 ghsvd_status launch_extract(Ctx* ctx) {
   const long long np2 = ctx->have_p2 ? ctx->n_user : 0;
   k_extract<256><<<(unsigned)ctx->n, 256, 0, ctx->stream>>>(
       ctx->F, ctx->G, ctx->Z, ctx->Z2, ctx->ldm, ctx->ldn, ctx->m, ctx->n, ctx->npos,
-      (const long long*)ctx->p2, np2, ctx->lam, ctx->sf, ctx->sg);
+      (const long long*)ctx->p2, np2, ctx->lam, ctx->sf, ctx->sg, ctx->o.want_x ? ctx->W : nullptr,
+      ctx->o.want_x ? ctx->Xo : nullptr);
   GH_CUDA(cudaGetLastError());
   return GHSVD_OK;
 }

@@ -22,7 +22,7 @@ struct DevCounters {
 
 // Layout of the caller-provided workspace (all offsets 256-B aligned).
 struct Layout {
-  size_t off_F, off_G, off_Z, off_F2, off_G2, off_Z2, off_scr, off_misc, total;
+  size_t off_F, off_G, off_Z, off_F2, off_G2, off_Z2, off_W, off_X, off_scr, off_misc, total;
   size_t scr_bytes;
 };
 
@@ -47,7 +47,9 @@ struct Ctx {
   bool have_p2;
   // device pointers into the workspace
   double2 *F, *G, *Z;            // current ("regular") factors
-  double2 *F2, *G2, *Z2;         // shadow buffers (blocked variant / out-of-place phases)
+  double2 *F2, *G2, *Z2;         // Z2: extraction output / Phase 2 temporary (F2, G2 unused)
+  double2* W;                    // want_x: W^T = (Z'^{-1})^T, updated like Z' (column pairs)
+  double2* Xo;                   // want_x: X output of the extraction
   char* scr;                     // scratch
   DevCounters* cnt;
   int8_t* J;                     // m signs (sorted form) for export
@@ -112,6 +114,6 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns);
 size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n);
 // comm.cpp
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam,
-                                   double* sf, double* sg, double2* Zout, int64_t ldz);
+                                   double* sf, double* sg, double2* Zout, int64_t ldz, double2* Xout);
 
 }  // namespace ghsvd

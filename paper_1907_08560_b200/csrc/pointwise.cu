@@ -44,6 +44,7 @@ struct StepArgs {
   double tol;
   int literal;
   DevCounters* cnt;
+  double2* W;     // want_x: W^T = (Z'^{-1})^T (n rows, ld ldn), or nullptr
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -592,6 +593,27 @@ __global__ void __launch_bounds__(NT) k_pair_step_2p(StepArgs a) {
       rot_row(zp, zq, z11, z21, z12, z22);
       Zp[i] = zp; Zq[i] = zq;
     }
+    if (a.W) {
+      // NEXT-1: W = Z'^{-1} <- Zhat'^{-1} W on rows p, q, i.e. the
+      // columns p, q of W^T times (Zhat'^{-1})^T = (1/det) [[z22, -z21], [-z12, z11]]
+      const double dre = (z11.re * z22.re - z11.im * z22.im) - (z12.re * z21.re - z12.im * z21.im);
+      const double dim = (z11.re * z22.im + z11.im * z22.re) - (z12.re * z21.im + z12.im * z21.re);
+      const double dd = dre * dre + dim * dim;
+      const Cplx idet{dre / dd, -dim / dd};
+      auto cm = [](const Cplx& x, const Cplx& y) {
+        return Cplx{x.re * y.re - x.im * y.im, x.re * y.im + x.im * y.re};
+      };
+      const Cplx i11 = cm(z22, idet), i22 = cm(z11, idet);
+      const Cplx m12 = cm(z12, idet), m21 = cm(z21, idet);
+      const Cplx i21{-m12.re, -m12.im}, i12{-m21.re, -m21.im};
+      double2* Wp = a.W + p * a.ldn;
+      double2* Wq = a.W + q * a.ldn;
+      for (long long i = z0 + tid; i < z1; i += NT) {
+        double2 wp = Wp[i], wq = Wq[i];
+        rot_row(wp, wq, i11, i21, i12, i22);
+        Wp[i] = wp; Wq[i] = wq;
+      }
+    }
   }
   if (C > 1) cluster_wait();
 }
@@ -637,6 +659,10 @@ ghsvd_status pw_configure(Ctx* ctx) {
     return GHSVD_E_INVALID_ARG;
   }
   const bool pipe = kk == 3;
+  if (ctx->o.want_x && kk != 2) {
+    ctx->err = "want_x needs the default pointwise kernel (2)";
+    return GHSVD_E_INVALID_ARG;
+  }
   const int nbuf = kk == 3 ? 8 : (kk == 1 ? 4 : 0);   // F/G slice buffers (x cs) per CTA
   int C = ctx->o.cluster;
   if (C <= 0) {
@@ -717,6 +743,7 @@ static ghsvd_status launch_step(Ctx* ctx, cudaStream_t st, int64_t s) {
   a.tol = (ctx->o.eps > 0 ? ctx->o.eps : 0x1p-53) * sqrt((double)ctx->n);
   a.literal = ctx->o.criterion == GHSVD_CRIT_LITERAL;
   a.cnt = ctx->cnt;
+  a.W = ctx->o.want_x ? ctx->W : nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ctx->pw_nclusters * C), 1, 1);
   cfg.blockDim = dim3(ctx->pw_threads, 1, 1);

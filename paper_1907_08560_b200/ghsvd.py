@@ -32,7 +32,7 @@ CRITERIA = {"relative": 0, "literal": 1}
 # every symbol include/ghsvd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ghsvd_default_options", "ghsvd_workspace_bytes", "ghsvd_create", "ghsvd_factor",
            "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors", "ghsvd_sweep", "ghsvd_run_steps",
-           "ghsvd_extract", "ghsvd_get_transformed", "ghsvd_hz2x2_batch", "ghsvd_last_error",
+           "ghsvd_extract", "ghsvd_extract_x", "ghsvd_get_transformed", "ghsvd_hz2x2_batch", "ghsvd_last_error",
            "ghsvd_destroy", "ghsvd_version", "ghsvd_block_owner", "ghsvd_exchange_plan",
            "ghsvd_nccl_unique_id"]
 
@@ -49,7 +49,7 @@ class Options(ctypes.Structure):
                 ("ordering", ctypes.c_int), ("nblocks", ctypes.c_int), ("max_sweeps", ctypes.c_int),
                 ("criterion", ctypes.c_int), ("eps", ctypes.c_double), ("cluster", ctypes.c_int),
                 ("threads", ctypes.c_int), ("use_graph", ctypes.c_int), ("kernel", ctypes.c_int),
-                ("detail_timing", ctypes.c_int)]
+                ("detail_timing", ctypes.c_int), ("want_x", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -105,6 +105,8 @@ def load():
     L.ghsvd_run_steps.argtypes = [P, I64, I64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     L.ghsvd_extract.argtypes = [P, P, P, P, P, I64, P]
     L.ghsvd_get_transformed.argtypes = [P, P, I64, P, I64, P, I64]
+    L.ghsvd_extract_x.argtypes = [P, P, I64]
+    L.ghsvd_extract_x.restype = ctypes.c_int
     L.ghsvd_hz2x2_batch.argtypes = [P, I64, P, D, Ci, P, P]
     L.ghsvd_last_error.argtypes = [P]
     L.ghsvd_last_error.restype = ctypes.c_char_p
@@ -164,7 +166,7 @@ class Context:
                  stream=None, world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  nblocks: int = 0, max_sweeps: int = 30, criterion: str = "relative", eps: float = 0.0,
                  cluster: int = 0, threads: int = 0, use_graph: bool = True, kernel: int = 0,
-                 detail_timing: bool = False):
+                 detail_timing: bool = False, want_x: bool = False):
         import torch
         L = load()
         self._L = L
@@ -190,6 +192,7 @@ class Context:
         o.use_graph = 1 if use_graph else 0
         o.kernel = kernel
         o.detail_timing = 1 if detail_timing else 0
+        o.want_x = 1 if want_x else 0
         self.opts = o
         nbytes = L.ghsvd_workspace_bytes(ctypes.byref(o), m, n, nl)
         if nbytes == 0:
@@ -324,6 +327,13 @@ class Context:
             pz, ldz = None, n
         self._check(self._L.ghsvd_extract(self._h, pl, ps, pg, pz, ldz, None), "extract")
         return lam, sf, sg, Z
+
+    def extract_x(self):
+        """X = Z^{-1} (n x n numpy), requires want_x=True and a completed sweep."""
+        n = self.n
+        X = np.zeros((n, n), np.complex128, order="F")
+        self._check(self._L.ghsvd_extract_x(self._h, X.ctypes.data_as(ctypes.c_void_p), n), "extract_x")
+        return X
 
     def transformed(self, m: int, n: int):
         """Current F', G', Z' (bordered sizes m, n) as numpy."""

@@ -235,7 +235,7 @@ def run_ours(args):
         nccl_id = bytes(idt.cpu().numpy().tobytes())
     ctx = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=args.max_sweeps,
                         cluster=args.cluster, threads=args.threads, nblocks=args.nblocks, world_size=ws,
-                        rank=rank, nccl_id=nccl_id, detail_timing=blocked)
+                        rank=rank, nccl_id=nccl_id, detail_timing=blocked, want_x=args.want_x)
     phase1_s = None
     phase2_s = None
     with torch.cuda.stream(stream):
@@ -343,6 +343,7 @@ def run_ours(args):
         "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant, "max_sweeps": args.max_sweeps,
+                   "want_x": bool(args.want_x),
                    "l2": f"inputs ({2 * mb * nb * 16 / 1e9:.2f} GB) vs L2 126 MB",
                    "phase2": "applied" if phase2_s is not None else "skipped (config recipe; PAPER.md:925 for ill-conditioned G)"},
         "sweeps": sweeps, "converged": stats[-1]["converged"], "big_per_sweep_tail": stats[-1]["big_per_sweep"][-4:],
@@ -381,6 +382,8 @@ def main():
     ap.add_argument("--max-sweeps", type=int, default=64,
                     help="C_max; config 3 (S condition 1e12) needs ~36 sweeps, beyond the paper's usual 30")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--want-x", action="store_true",
+                    help="also accumulate Z'^{-1} during the sweep (full GHSVD X, NEXT-1)")
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--ref-sweeps", type=int, default=36,
                     help="sweep count used to extrapolate the oracle sample in --impl reference")

@@ -79,3 +79,23 @@ def test_x_after_phase2_is_in_original_column_order(gh):
     LG = sg ** 2
     assert np.linalg.norm(X.conj().T @ (LF[:, None] * X) - H) / np.linalg.norm(H) < 1e-11
     assert np.linalg.norm(X.conj().T @ (LG[:, None] * X) - S) / np.linalg.norm(S) < 1e-11
+
+
+def test_dataset_c_gsvd_small_vs_oracle(gh):
+    """NEXT-3: dataset-C-like GSVD pair (J = I, Hermitian F, G with U(0,1) spectra,
+    PAPER.md:2252-2257) at n = 128: eigenvalues vs the oracle, full GSVD residuals."""
+    P = inputs.dataset_c(93, 128)
+    ctx = gh.Context(128, 128, variant="bo", want_x=True)
+    ctx.set_factors(P.F, P.J, P.G)
+    F0, J0, G0, _ = ctx.get_factors()
+    st = ctx.sweep()
+    lam, sf, sg, Z = ctx.extract()
+    X = ctx.extract_x()
+    Fc, Gc, _ = ctx.transformed(128, 128)
+    ctx.close()
+    Fo, Go, Zp, sto = oracle.hz_pointwise(F0, J0, G0)
+    lo, *_ = oracle.extract(Fo, J0, Go, Zp)
+    assert st["converged"] and np.all(lam > 0)
+    assert np.max(np.abs(np.sort(lam) - np.sort(lo)) / np.abs(np.sort(lo))) < 1e-9
+    eF, eG = eq71(F0, J0, G0, Fc, Gc, X, sf, sg)
+    assert eF < 1e-12 and eG < 1e-12

@@ -310,7 +310,8 @@ def run_ours(args):
         t_gr = sum(s["t_gram"] for s in stats)
         f_gr = sum(s["flops_gram"] for s in stats)
         t_pv = sum(s["t_pivot"] for s in stats)
-        n_upd = sum(s["launches"] for s in stats) // 4 * 2   # FG + Z update launches
+        # per block step: 2 Gram, 2 factor, 2 pivot, 2 F/G-update (two halves) + 1 Z'-update
+        n_upd = sum(s["launches"] for s in stats) // 9 * 3
         ach = f_upd / t_upd / 1e12 if t_upd > 0 else 0.0
         roof = {"bound": "tensor", "achieved": ach, "peak": zgemm_peak, "unit": "TFLOP/s",
                 "frac": ach / zgemm_peak, "traffic": _ncu_traffic("k_blk_update"), "kernel": "k_blk_update",

@@ -40,6 +40,7 @@ constexpr int GS = RT + 4;      // Gram tile column stride (double2), conflict-f
 constexpr int US = RT + 2;      // update tile column stride
 constexpr int ZS = KM + 4;      // Z_blk column stride in smem
 constexpr int NT_G = 256, NT_P = 512, NT_U = 256;
+constexpr int GSTAGES = 3;      // cp.async pipeline depth of the Gram kernel
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -106,7 +107,7 @@ __constant__ signed char kTileJ[36] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3,
 
 // ---------------------------------------------------------------- Gram (DMMA)
 __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
-  extern __shared__ __align__(128) double2 gsm[];  // [2][KM][GS]
+  extern __shared__ __align__(128) double2 gsm[];  // [GSTAGES][KM][GS]
   const int pl = a.pair0 + blockIdx.x, hs = blockIdx.y, split = blockIdx.z;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
@@ -115,38 +116,45 @@ __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
   const long long r_end = min(a.m, r_begin + a.split_rows);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // 4 real DMMAs per complex step (the Grams feed the block pivots directly; the 3M
-  // scheme measured no faster here and is kept to the update kernel)
+  // scheme measured no faster here and is kept to the update kernel).
+  // Exact load balance: warp w owns the lower tiles w, w+8, w+16, w+24 for all k-steps
+  // and one half (k-steps 0-3 or 4-7 of each 32-row stage) of tile 32 + w/2; the two
+  // halves are summed at the end.  36 tiles x 8 k-steps = 8 warps x 36 units.
   double cre[5][2], cim[5][2];
 #pragma unroll
   for (int t = 0; t < 5; t++) cre[t][0] = cre[t][1] = cim[t][0] = cim[t][1] = 0.0;
-  const int ntile = warp + 32 < 36 ? 5 : 4;
+  const int kh0 = (warp & 1) * (RT / 2);   // k-step half for the shared tile
   auto load_stage = [&](int st, long long r0) {
-    double2* T = gsm + (size_t)st * KM * GS;
-    for (int e = tid; e < KM * RT; e += NT_G) {
-      const int c = e / RT, r = e % RT;
-      const long long gc = gcol(c, c0p, wp, c0q, wq);
-      const long long gr = r0 + r;
-      const bool ok = gc >= 0 && gr < r_end;
-      cp_async16(&T[c * GS + r], ok ? (const void*)(X + gc * a.ldm + gr) : (const void*)X, ok);
+    if (r0 < r_end) {
+      double2* T = gsm + (size_t)st * KM * GS;
+      for (int e = tid; e < KM * RT; e += NT_G) {
+        const int c = e / RT, r = e % RT;
+        const long long gc = gcol(c, c0p, wp, c0q, wq);
+        const long long gr = r0 + r;
+        const bool ok = gc >= 0 && gr < r_end;
+        cp_async16(&T[c * GS + r], ok ? (const void*)(X + gc * a.ldm + gr) : (const void*)X, ok);
+      }
     }
-    cp_commit();
+    cp_commit();   // possibly empty: keeps one group per stage
   };
-  if (r_begin < r_end) load_stage(0, r_begin);
+  // GSTAGES-deep cp.async pipeline
+#pragma unroll
+  for (int p = 0; p < GSTAGES - 1; p++) load_stage(p, r_begin + (long long)p * RT);
   int st = 0;
-  for (long long r0 = r_begin; r0 < r_end; r0 += RT, st ^= 1) {
-    const bool more = r0 + RT < r_end;
-    if (more) load_stage(st ^ 1, r0 + RT);
-    if (more) cp_wait<1>(); else cp_wait<0>();
+  for (long long r0 = r_begin; r0 < r_end; r0 += RT) {
+    load_stage((st + GSTAGES - 1) % GSTAGES, r0 + (long long)(GSTAGES - 1) * RT);
+    cp_wait<GSTAGES - 1>();
     __syncthreads();
     const double2* T = gsm + (size_t)st * KM * GS;
 #pragma unroll
     for (int kk = 0; kk < RT; kk += 4) {
       const int row = kk + (lane & 3);
       const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
+      const bool half = kk >= kh0 && kk < kh0 + RT / 2;
 #pragma unroll
       for (int t = 0; t < 5; t++) {
-        if (t < ntile) {
-          const int tt = warp + 8 * t;
+        if (t < 4 || half) {
+          const int tt = t < 4 ? warp + 8 * t : 32 + (warp >> 1);
           const int I = kTileI[tt], J = kTileJ[tt];
           const double2 x = T[(8 * I + (lane >> 2)) * GS + row];   // A = X^H (row i, k)
           const double2 y = T[(8 * J + (lane >> 2)) * GS + row];   // B = J X (k, col j)
@@ -159,12 +167,30 @@ __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
       }
     }
     __syncthreads();
+    st = (st + 1) % GSTAGES;
+  }
+  cp_wait<0>();
+  __syncthreads();
+  // combine the two halves of the shared tiles (odd warp -> smem -> even warp)
+  double* red = reinterpret_cast<double*>(gsm);
+  if (warp & 1) {
+    red[((warp >> 1) * 32 + lane) * 4 + 0] = cre[4][0];
+    red[((warp >> 1) * 32 + lane) * 4 + 1] = cre[4][1];
+    red[((warp >> 1) * 32 + lane) * 4 + 2] = cim[4][0];
+    red[((warp >> 1) * 32 + lane) * 4 + 3] = cim[4][1];
+  }
+  __syncthreads();
+  if (!(warp & 1)) {
+    cre[4][0] += red[((warp >> 1) * 32 + lane) * 4 + 0];
+    cre[4][1] += red[((warp >> 1) * 32 + lane) * 4 + 1];
+    cim[4][0] += red[((warp >> 1) * 32 + lane) * 4 + 2];
+    cim[4][1] += red[((warp >> 1) * 32 + lane) * 4 + 3];
   }
   double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
 #pragma unroll
   for (int t = 0; t < 5; t++) {
-    if (t < ntile) {
-      const int tt = warp + 8 * t;
+    if (t < 4 || !(warp & 1)) {
+      const int tt = t < 4 ? warp + 8 * t : 32 + (warp >> 1);
       const int I = kTileI[tt], J = kTileJ[tt];
       const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
       out[i + (size_t)j * KM] = make_double2(cre[t][0], cim[t][0]);
@@ -632,7 +658,7 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   a.literal = ctx->o.criterion == GHSVD_CRIT_LITERAL;
   a.inner_sweeps = ctx->o.variant == GHSVD_BLOCKED_FB ? 30 : 1;
   a.pair0 = 0;
-  S.smem_g = (size_t)2 * KM * GS * 16;
+  S.smem_g = (size_t)GSTAGES * KM * GS * 16;
   S.smem_p = (size_t)3 * KM * KM * 16;
   S.smem_u = (size_t)(KM * US + KM * ZS) * 16;
   S.smem_f = (size_t)KM * KM * 16;

@@ -35,6 +35,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns
 
 
 def kname(s):
+    s = s.replace("(anonymous namespace)::", "")
     s = re.sub(r"\(.*", "", s)
     s = re.sub(r"^void\s+", "", s)
     s = re.sub(r"<.*", "", s)
@@ -89,11 +90,21 @@ def main():
     except Exception:
         summary = {"kernels": {}}
     for rep in a.rep:
+        per = collections.defaultdict(list)
         for d in parse_rep(rep):
-            k = d["kernel"]
             d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
-            d["source"] = rep
-            summary["kernels"][k] = d
+            per[d["kernel"]].append(d)
+        for k, ds in per.items():
+            # several launches of one kernel in a capture (e.g. the F/G and Z' updates of one
+            # block step): report the mean over the captured mix, keep each launch
+            m = {key: sum(x.get(key, 0.0) for x in ds) / len(ds)
+                 for key in ds[0] if isinstance(ds[0][key], float)}
+            m["kernel"] = k
+            m["captured_launches"] = len(ds)
+            m["per_launch"] = [{"duration": x.get("duration"), "dram_bytes": x["dram_bytes_per_launch"],
+                                "tensor_cycles_pct": x.get("tensor_cycles_pct")} for x in ds]
+            m["source"] = rep
+            summary["kernels"][k] = m
     if a.launches:
         summary["launch_list"] = parse_launches(a.launches)
         summary["launch_list_source"] = a.launches

@@ -1,5 +1,8 @@
-"""Run a few pointwise step launches on config 3 (for ncu captures of k_pair_step).
-usage: python tools/profile_step.py [--kernel K] [--cluster C] [--threads T] [--steps S]"""
+"""Run a few steps on config 3 (for ncu captures of k_pair_step / the k_blk_* kernels).
+usage: python tools/profile_step.py [--variant pointwise|bo] [--kernel K] [--cluster C]
+       [--threads T] [--steps S]
+A pointwise step is one k_pair_step launch; a blocked (bo) step is one block step =
+2 k_blk_gram + 2 k_blk_factor + 2 k_blk_pivot + 3 k_blk_update launches."""
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -9,11 +12,15 @@ ap.add_argument("--kernel", type=int, default=1)
 ap.add_argument("--cluster", type=int, default=0)
 ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--variant", default="pointwise")
 a = ap.parse_args()
 build.build()
 kind, at = inputs.make_config(3, backend="torch")
 NA, NL, NG = at.A.shape
-ctx = ghsvd.Context(2 * NA * NL, NG, NL, kernel=a.kernel, cluster=a.cluster, threads=a.threads)
+if a.variant == "pointwise":
+    ctx = ghsvd.Context(2 * NA * NL, NG, NL, kernel=a.kernel, cluster=a.cluster, threads=a.threads)
+else:
+    ctx = ghsvd.Context(2 * NA * NL, NG, NL, variant=a.variant)
 ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(torch.cuda.current_stream())

@@ -99,14 +99,39 @@ __device__ __forceinline__ long long gcol(int c, int c0p, int wp, int c0q, int w
   return -1;
 }
 
-// lower-triangle 8x8 tile list (I >= J) of a KM x KM matrix
-__constant__ signed char kTileI[36] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5,
-                                       5, 5, 5, 6, 6, 6, 6, 6, 6, 6, 7, 7, 7, 7, 7, 7, 7, 7};
-__constant__ signed char kTileJ[36] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2,
-                                       3, 4, 5, 0, 1, 2, 3, 4, 5, 6, 0, 1, 2, 3, 4, 5, 6, 7};
-
 // ---------------------------------------------------------------- Gram (DMMA)
-__global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
+// One CTA = one (pair, H|S, row split).  The 36 lower-triangle 8x8 output tiles of the
+// k x k Gram (k <= 64) are grouped by tile-row pairs {I, 7-I} (9 tiles each); warps
+// 2g, 2g+1 own group g and split every 32-row stage's 8 k-steps (even / odd).  Within
+// a k-step a warp loads the 8-g column fragments its 9 tiles need once (the A fragment
+// of tile row I is the B fragment of tile column I) and issues 36 DMMAs (exact 4M
+// complex product; J folded into the A operand).  The two k-halves are summed in a
+// fixed order at the end, so the result is deterministic.
+template <int GI>
+__device__ __forceinline__ void gram_tiles(const double2* T, int row, double sg, double (&acc)[9][4]) {
+  constexpr int IA = GI, IB = 7 - GI, NF = 8 - GI;
+  const int lane = threadIdx.x & 31;
+  double2 f[NF];
+#pragma unroll
+  for (int j = 0; j < NF; j++) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
+  // A operand of tile rows IA, IB: J_r conj(x): (ar, ai) with conj -> (+x.y used as -(-x.y))
+  const double aar = sg * f[IA].x, aai = sg * f[IA].y;
+  const double abr = sg * f[IB].x, abi = sg * f[IB].y;
+#pragma unroll
+  for (int t = 0; t < 9; t++) {
+    const bool ra = t <= IA;
+    const int J = ra ? t : t - IA - 1;
+    const double ar = ra ? aar : abr, ai = ra ? aai : abi;
+    const double2 y = f[J];
+    // conj(x) y = (xr yr + xi yi) + i (xr yi - xi yr)
+    dmma(acc[t][0], acc[t][1], ar, y.x);
+    dmma(acc[t][0], acc[t][1], ai, y.y);
+    dmma(acc[t][2], acc[t][3], ar, y.y);
+    dmma(acc[t][2], acc[t][3], -ai, y.x);
+  }
+}
+
+__global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
   extern __shared__ __align__(128) double2 gsm[];  // [GSTAGES][KM][GS]
   const int pl = a.pair0 + blockIdx.x, hs = blockIdx.y, split = blockIdx.z;
   int c0p, wp, c0q, wq;
@@ -115,15 +140,10 @@ __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
   const long long r_begin = (long long)split * a.split_rows;
   const long long r_end = min(a.m, r_begin + a.split_rows);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // 4 real DMMAs per complex step (the Grams feed the block pivots directly; the 3M
-  // scheme measured no faster here and is kept to the update kernel).
-  // Exact load balance: warp w owns the lower tiles w, w+8, w+16, w+24 for all k-steps
-  // and one half (k-steps 0-3 or 4-7 of each 32-row stage) of tile 32 + w/2; the two
-  // halves are summed at the end.  36 tiles x 8 k-steps = 8 warps x 36 units.
-  double cre[5][2], cim[5][2];
+  const int gi = warp >> 1, kh = warp & 1;
+  double acc[9][4];
 #pragma unroll
-  for (int t = 0; t < 5; t++) cre[t][0] = cre[t][1] = cim[t][0] = cim[t][1] = 0.0;
-  const int kh0 = (warp & 1) * (RT / 2);   // k-step half for the shared tile
+  for (int t = 0; t < 9; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
   auto load_stage = [&](int st, long long r0) {
     if (r0 < r_end) {
       double2* T = gsm + (size_t)st * KM * GS;
@@ -137,7 +157,6 @@ __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
     }
     cp_commit();   // possibly empty: keeps one group per stage
   };
-  // GSTAGES-deep cp.async pipeline
 #pragma unroll
   for (int p = 0; p < GSTAGES - 1; p++) load_stage(p, r_begin + (long long)p * RT);
   int st = 0;
@@ -147,23 +166,14 @@ __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
     __syncthreads();
     const double2* T = gsm + (size_t)st * KM * GS;
 #pragma unroll
-    for (int kk = 0; kk < RT; kk += 4) {
-      const int row = kk + (lane & 3);
+    for (int ks = 0; ks < RT / 4; ks += 2) {
+      const int row = 4 * (ks + kh) + (lane & 3);
       const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
-      const bool half = kk >= kh0 && kk < kh0 + RT / 2;
-#pragma unroll
-      for (int t = 0; t < 5; t++) {
-        if (t < 4 || half) {
-          const int tt = t < 4 ? warp + 8 * t : 32 + (warp >> 1);
-          const int I = kTileI[tt], J = kTileJ[tt];
-          const double2 x = T[(8 * I + (lane >> 2)) * GS + row];   // A = X^H (row i, k)
-          const double2 y = T[(8 * J + (lane >> 2)) * GS + row];   // B = J X (k, col j)
-          const double yr = sg * y.x, yi = sg * y.y;
-          dmma(cre[t][0], cre[t][1], x.x, yr);
-          dmma(cre[t][0], cre[t][1], x.y, yi);
-          dmma(cim[t][0], cim[t][1], x.x, yi);
-          dmma(cim[t][0], cim[t][1], -x.y, yr);
-        }
+      switch (gi) {   // warp-uniform
+        case 0: gram_tiles<0>(T, row, sg, acc); break;
+        case 1: gram_tiles<1>(T, row, sg, acc); break;
+        case 2: gram_tiles<2>(T, row, sg, acc); break;
+        default: gram_tiles<3>(T, row, sg, acc); break;
       }
     }
     __syncthreads();
@@ -171,31 +181,28 @@ __global__ void __launch_bounds__(NT_G) k_blk_gram(BlkArgs a) {
   }
   cp_wait<0>();
   __syncthreads();
-  // combine the two halves of the shared tiles (odd warp -> smem -> even warp)
+  // sum the two k-halves: odd warp -> smem -> even warp (fixed order)
   double* red = reinterpret_cast<double*>(gsm);
-  if (warp & 1) {
-    red[((warp >> 1) * 32 + lane) * 4 + 0] = cre[4][0];
-    red[((warp >> 1) * 32 + lane) * 4 + 1] = cre[4][1];
-    red[((warp >> 1) * 32 + lane) * 4 + 2] = cim[4][0];
-    red[((warp >> 1) * 32 + lane) * 4 + 3] = cim[4][1];
+  if (kh) {
+#pragma unroll
+    for (int t = 0; t < 9; t++)
+#pragma unroll
+      for (int c = 0; c < 4; c++) red[((gi * 9 + t) * 4 + c) * 32 + lane] = acc[t][c];
   }
   __syncthreads();
-  if (!(warp & 1)) {
-    cre[4][0] += red[((warp >> 1) * 32 + lane) * 4 + 0];
-    cre[4][1] += red[((warp >> 1) * 32 + lane) * 4 + 1];
-    cim[4][0] += red[((warp >> 1) * 32 + lane) * 4 + 2];
-    cim[4][1] += red[((warp >> 1) * 32 + lane) * 4 + 3];
-  }
+  if (kh) return;
+#pragma unroll
+  for (int t = 0; t < 9; t++)
+#pragma unroll
+    for (int c = 0; c < 4; c++) acc[t][c] += red[((gi * 9 + t) * 4 + c) * 32 + lane];
   double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
 #pragma unroll
-  for (int t = 0; t < 5; t++) {
-    if (t < 4 || !(warp & 1)) {
-      const int tt = t < 4 ? warp + 8 * t : 32 + (warp >> 1);
-      const int I = kTileI[tt], J = kTileJ[tt];
-      const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
-      out[i + (size_t)j * KM] = make_double2(cre[t][0], cim[t][0]);
-      out[i + (size_t)(j + 1) * KM] = make_double2(cre[t][1], cim[t][1]);
-    }
+  for (int t = 0; t < 9; t++) {
+    const int I = t <= gi ? gi : 7 - gi;
+    const int J = t <= gi ? t : t - gi - 1;
+    const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
+    out[i + (size_t)j * KM] = make_double2(acc[t][0], acc[t][2]);
+    out[i + (size_t)(j + 1) * KM] = make_double2(acc[t][1], acc[t][3]);
   }
 }
 
@@ -290,17 +297,25 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
     Jh[k] = 1;
   }
   __syncthreads();
-  // inner Level-1 sweeps: one HALF-warp per pivot pair, so the kb/2 <= 32 transforms of
-  // a step are computed concurrently by the 32 half-warps of the CTA
+  // inner Level-1 sweeps.  Per inner step: one HALF-warp per pivot pair forms the 8 pair
+  // Gram entries (eq 6.1) -> shared memory; warp 0 then evaluates the kb/2 <= 32 2x2
+  // transforms of the step one per LANE (the scalar routine runs once per pair instead
+  // of once per half-warp, which cuts the step's issued instructions several-fold);
+  // the half-warps then apply them to the column pairs of F^, G^ and Z_blk.
+  __shared__ double gsh[KM / 2][8];
+  __shared__ double zsh[KM / 2][8];
+  __shared__ int ksh[KM / 2];
   const int warp = tid >> 5, lane = tid & 31;
-  const int hw = lane >> 4, hl = lane & 15, lead = hw << 4;
+  const int hw = lane >> 4, hl = lane & 15;
   const unsigned hmask = hw ? 0xffff0000u : 0x0000ffffu;
   const double tol = a.eps * sqrt((double)kb);       // C-7: n = block-pivot order
+  unsigned long long w0_all = 0, w0_big = 0;          // warp-0 lane counters
   for (int sw = 0; sw < a.inner_sweeps; sw++) {
     unsigned long long sw_all = 0, sw_big = 0;
     for (int s = 0; s < kb - 1; s++) {
-      for (int pr = 2 * warp + hw; pr < kb / 2; pr += NT_P / 16) {
-        long long p, q;
+      const int pr = 2 * warp + hw;
+      long long p = 0, q = 0;
+      if (pr < kb / 2) {
         rr_pair(kb, s, pr, &p, &q);
         double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int i = hl; i < kb; i += 16) {
@@ -319,51 +334,71 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
         for (int c = 0; c < 8; c++)
 #pragma unroll
           for (int o = 8; o > 0; o >>= 1) g[c] += __shfl_xor_sync(hmask, g[c], o);
-        HZOut z{};
-        if (hl == 0) z = hz2x2_dev(g, tol, a.literal);
-        double zz[8] = {z.z11.re, z.z11.im, z.z21.re, z.z21.im, z.z12.re, z.z12.im, z.z22.re, z.z22.im};
+        if (hl < 8) {
+          double v = g[0];
 #pragma unroll
-        for (int c = 0; c < 8; c++) zz[c] = __shfl_sync(hmask, zz[c], lead);
-        const int kind = __shfl_sync(hmask, hl == 0 ? z.kind : 0, lead);
-        if (kind < 0) {
-          if (hl == 0) atomicCAS(&err_sh, 0, kind);
-          continue;
+          for (int c = 1; c < 8; c++) v = hl == c ? g[c] : v;
+          gsh[pr][hl] = v;
         }
-        if (kind != KIND_SMALL && kind != KIND_BIG) continue;
-        if (hl == 0) {
+      }
+      __syncthreads();
+      if (warp == 0 && lane < kb / 2) {
+        const HZOut z = hz2x2_dev(gsh[lane], tol, a.literal);
+        zsh[lane][0] = z.z11.re; zsh[lane][1] = z.z11.im; zsh[lane][2] = z.z21.re; zsh[lane][3] = z.z21.im;
+        zsh[lane][4] = z.z12.re; zsh[lane][5] = z.z12.im; zsh[lane][6] = z.z22.re; zsh[lane][7] = z.z22.im;
+        ksh[lane] = z.kind;
+        if (z.kind < 0) atomicCAS(&err_sh, 0, z.kind);
+        if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
           sw_all++;
-          if (kind == KIND_BIG) sw_big++;
+          if (z.kind == KIND_BIG) sw_big++;
         }
-        const double2 z11 = make_double2(zz[0], zz[1]), z21 = make_double2(zz[2], zz[3]);
-        const double2 z12 = make_double2(zz[4], zz[5]), z22 = make_double2(zz[6], zz[7]);
-        auto rot = [&](double2* M) {
-          for (int i = hl; i < kb; i += 16) {
-            const double2 x = M[i + p * KM], y = M[i + q * KM];
-            M[i + p * KM] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
-                                         x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
-            M[i + q * KM] = make_double2(x.x * z12.x - x.y * z12.y + y.x * z22.x - y.y * z22.y,
-                                         x.x * z12.y + x.y * z12.x + y.x * z22.y + y.y * z22.x);
-          }
-        };
-        rot(Fh);
-        rot(Gh);
-        rot(W0);
+      }
+      __syncthreads();
+      if (pr < kb / 2) {
+        const int kind = ksh[pr];
+        if (kind == KIND_SMALL || kind == KIND_BIG) {
+          const double2 z11 = make_double2(zsh[pr][0], zsh[pr][1]), z21 = make_double2(zsh[pr][2], zsh[pr][3]);
+          const double2 z12 = make_double2(zsh[pr][4], zsh[pr][5]), z22 = make_double2(zsh[pr][6], zsh[pr][7]);
+          auto rot = [&](double2* M) {
+            for (int i = hl; i < kb; i += 16) {
+              const double2 x = M[i + p * KM], y = M[i + q * KM];
+              M[i + p * KM] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
+                                           x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
+              M[i + q * KM] = make_double2(x.x * z12.x - x.y * z12.y + y.x * z22.x - y.y * z22.y,
+                                           x.x * z12.y + x.y * z12.x + y.x * z22.y + y.y * z22.x);
+            }
+          };
+          rot(Fh);
+          rot(Gh);
+          rot(W0);
+        }
       }
       __syncthreads();
     }
+    w0_all += sw_all;
+    w0_big += sw_big;
     // per-sweep totals; FB stops on a sweep without transformations (C-3)
-    if (hl == 0) {
-      atomicAdd(&sweep_all, sw_all);
-      atomicAdd(&cnt_all, sw_all);
-      atomicAdd(&cnt_big, sw_big);
+    if (warp == 0) {
+      unsigned long long t = sw_all;
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) sweep_all = t;
     }
     __syncthreads();
     const unsigned long long this_sweep = sweep_all;
     __syncthreads();
-    if (tid == 0) sweep_all = 0;
-    __syncthreads();
     if (this_sweep == 0) break;
   }
+  if (warp == 0) {
+    for (int o = 16; o > 0; o >>= 1) {
+      w0_all += __shfl_xor_sync(0xffffffffu, w0_all, o);
+      w0_big += __shfl_xor_sync(0xffffffffu, w0_big, o);
+    }
+    if (lane == 0) {
+      cnt_all = w0_all;
+      cnt_big = w0_big;
+    }
+  }
+  __syncthreads();
   if (err_sh) {
     if (tid == 0) atomicCAS(&a.cnt->err, 0, err_sh);
   }
@@ -562,8 +597,28 @@ BlkPlan make_plan(const Ctx* ctx) {
   const int P = std::max(1, ctx->o.world_size);
   p.K = p.nblk / 2 / P;
   p.slot0 = ctx->o.rank * p.K;
-  const long long target = 4 * 148;
-  p.nsplit = (int)std::min<long long>(MAX_SPLIT, std::max<long long>(1, (target + 2 * p.K - 1) / (2 * p.K)));
+  // Row split of the Gram launches, chosen against wave quantization: a launch covers
+  // M = 2 * (pairs per launch) matrices x nsplit CTAs with R CTAs resident at once;
+  // cost ~ waves x (32-row stages per CTA + fill/partial overhead).  Deterministic for a
+  // given (m, K, device) since the sum of the split partials has a fixed order.
+  int dev = 0, sms = 148, per_sm = 2;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long M = 2LL * (p.K >= 2 ? p.K / 2 : p.K);
+  const long long R = (long long)sms * per_sm;
+  long long best = -1;
+  double best_cost = 0.0;
+  for (int ns = 1; ns <= MAX_SPLIT; ns++) {
+    const long long rows = round_up((ctx->m + ns - 1) / ns, RT);
+    const int nseff = (int)((ctx->m + rows - 1) / rows);
+    if (nseff != ns) continue;
+    const double waves = (double)((M * ns + R - 1) / R);
+    const double cost = waves * (double)(rows / RT + 3);
+    if (best < 0 || cost < best_cost - 1e-9) {
+      best = ns;
+      best_cost = cost;
+    }
+  }
+  p.nsplit = (int)std::max<long long>(1, best);
   if (env_int("GHSVD_NSPLIT", 0) > 0) p.nsplit = std::min(MAX_SPLIT, env_int("GHSVD_NSPLIT", 0));
   const long long rows_per = (ctx->m + p.nsplit - 1) / p.nsplit;
   p.split_rows = round_up(std::max<long long>(rows_per, 1), RT);

@@ -113,9 +113,13 @@ __device__ inline void herm2_jacobi(double a, double2 b, double c, double2* R, d
 
 // Returns 0 or -7 (rank deficient).  All NT threads of the block must call it.
 // tolz: pivots with max |entry| <= tolz stop the factorisation (rank deficiency).
+// Loops are 2-D (warp -> column, lane -> row) with 32-bit indices: no integer
+// division in the O(r^2) passes of an elimination step.
 template <int NT, int RMAX>
 __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long ldmo, signed char* Jout,
                          int* npos_out, double tolz) {
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ int perm[RMAX];
   __shared__ int bsz[RMAX];
   __shared__ double d[RMAX];
@@ -135,11 +139,8 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
     for (int i = k + threadIdx.x; i < r; i += NT) amax_merge(mu1, id, fabs(W[i + i * ldw].x), i);
     double mu0 = 0.0;
     long long oidx = 0x7fffffffffffffffll;
-    const long long rem = r - k;
-    for (long long e = threadIdx.x; e < rem * rem; e += NT) {
-      const int j = k + (int)(e / rem), i = k + (int)(e % rem);
-      if (i > j) amax_merge(mu0, oidx, cabs(W[i + j * ldw]), (long long)j * r + i);
-    }
+    for (int j = k + warp; j < r; j += NW)
+      for (int i = j + 1 + lane; i < r; i += 32) amax_merge(mu0, oidx, cabs(W[i + j * ldw]), (long long)j * r + i);
     block_amax2<NT>(mu1, id, mu0, oidx);
     const double mall = mu0 > mu1 ? mu0 : mu1;
     if (!(mall > tolz)) {
@@ -182,10 +183,9 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
       const double inv = __ddiv_rn(1.0, dk);
       for (int i = k + 1 + threadIdx.x; i < r; i += NT) colk[0][i] = W[i + k * ldw];
       __syncthreads();
-      const long long rm = r - k - 1;
-      for (long long e = threadIdx.x; e < rm * rm; e += NT) {
-        const int i = k + 1 + (int)(e % rm), j = k + 1 + (int)(e / rm);
-        W[i + j * ldw] = sub(W[i + j * ldw], scale(mul(colk[0][i], conj(colk[0][j])), inv));
+      for (int j = k + 1 + warp; j < r; j += NW) {
+        const double2 cj = conj(colk[0][j]);
+        for (int i = k + 1 + lane; i < r; i += 32) W[i + j * ldw] = sub(W[i + j * ldw], scale(mul(colk[0][i], cj), inv));
       }
       __syncthreads();
       for (int i = k + 1 + threadIdx.x; i < r; i += NT) W[i + k * ldw] = scale(colk[0][i], inv);
@@ -208,11 +208,12 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
         W[i + (k + 1) * ldw] = scale(sub(scale(w1, ea), mul(w0, eb)), inv);
       }
       __syncthreads();
-      const long long rm = r - k - 2;
-      for (long long e = threadIdx.x; e < rm * rm; e += NT) {
-        const int i = k + 2 + (int)(e % rm), j = k + 2 + (int)(e / rm);
-        const double2 t = add(mul(W[i + k * ldw], conj(colk[0][j])), mul(W[i + (k + 1) * ldw], conj(colk[1][j])));
-        W[i + j * ldw] = sub(W[i + j * ldw], t);
+      for (int j = k + 2 + warp; j < r; j += NW) {
+        const double2 c0 = conj(colk[0][j]), c1 = conj(colk[1][j]);
+        for (int i = k + 2 + lane; i < r; i += 32) {
+          const double2 t = add(mul(W[i + k * ldw], c0), mul(W[i + (k + 1) * ldw], c1));
+          W[i + j * ldw] = sub(W[i + j * ldw], t);
+        }
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -242,24 +243,25 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
   __syncthreads();
   for (int i = threadIdx.x; i < r; i += NT) Jout[rowpos[i]] = sgn[i];
   // Mtilde(rowpos(i), perm[l]) = row i of diag(|d|^1/2) R^* L^*, column l
-  for (int e = threadIdx.x; e < r * r; e += NT) {
-    const int i = e % r, l = e / r;
-    auto Lh = [&](int row, int col) -> double2 {  // (L^*)(row, col) = conj(L(col, row))
-      if (row == col) return mk(1.0, 0.0);
-      if (col < row) return mk(0.0, 0.0);
-      return conj(W[col + row * ldw]);
-    };
-    double2 y;
-    if (bsz[i] == 1) {
-      y = scale(Lh(i, l), __dsqrt_rn(fabs(d[i])));
-    } else if (bsz[i] == 2) {
-      const double2* R = &Rk[2 * i];
-      y = scale(add(mul(conj(R[0]), Lh(i, l)), mul(conj(R[1]), Lh(i + 1, l))), __dsqrt_rn(fabs(d[i])));
-    } else {
-      const double2* R = &Rk[2 * (i - 1)];
-      y = scale(add(mul(conj(R[2]), Lh(i - 1, l)), mul(conj(R[3]), Lh(i, l))), __dsqrt_rn(fabs(d[i])));
+  for (int l = warp; l < r; l += NW) {
+    for (int i = lane; i < r; i += 32) {
+      auto Lh = [&](int row, int col) -> double2 {  // (L^*)(row, col) = conj(L(col, row))
+        if (row == col) return mk(1.0, 0.0);
+        if (col < row) return mk(0.0, 0.0);
+        return conj(W[col + row * ldw]);
+      };
+      double2 y;
+      if (bsz[i] == 1) {
+        y = scale(Lh(i, l), __dsqrt_rn(fabs(d[i])));
+      } else if (bsz[i] == 2) {
+        const double2* R = &Rk[2 * i];
+        y = scale(add(mul(conj(R[0]), Lh(i, l)), mul(conj(R[1]), Lh(i + 1, l))), __dsqrt_rn(fabs(d[i])));
+      } else {
+        const double2* R = &Rk[2 * (i - 1)];
+        y = scale(add(mul(conj(R[2]), Lh(i - 1, l)), mul(conj(R[3]), Lh(i, l))), __dsqrt_rn(fabs(d[i])));
+      }
+      M[rowpos[i] + perm[l] * ldmo] = y;
     }
-    M[rowpos[i] + perm[l] * ldmo] = y;
   }
   __syncthreads();
   return 0;
@@ -267,34 +269,45 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
 
 // Diagonally pivoted Cholesky: P S P^T = L L^*, Gh = L^* P (column perm[l] of Gh
 // is column l of L^*).  S overwritten (L below/on the diagonal).  Returns 0 or -6.
+// The pivot search (largest diagonal entry, smallest index on ties) is done
+// redundantly by every warp, so no barrier is spent on it.
 template <int NT, int RMAX>
 __device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long long ldg) {
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ int perm[RMAX];
-  __shared__ int err_sh;
-  __shared__ int pv_sh;
   for (int i = threadIdx.x; i < r; i += NT) perm[i] = i;
-  if (threadIdx.x == 0) err_sh = 0;
   __syncthreads();
   for (int k = 0; k < r; k++) {
-    if (threadIdx.x == 0) {
-      int pv = k;
-      for (int i = k + 1; i < r; i++)
-        if (S[i + i * lds].x > S[pv + pv * lds].x) pv = i;
-      pv_sh = pv;
-      if (!(S[pv + pv * lds].x > 0.0)) err_sh = -6;
+    double bv = 0.0;
+    int bi = 0x7fffffff;
+    for (int i = k + lane; i < r; i += 32) {
+      const double v = S[i + i * lds].x;
+      if (bi == 0x7fffffff || v > bv) {
+        bv = v;
+        bi = i;
+      }
     }
-    __syncthreads();
-    if (err_sh) return err_sh;
-    const int pv = pv_sh;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (i2 != 0x7fffffff && (bi == 0x7fffffff || v2 > bv || (v2 == bv && i2 < bi))) {
+        bv = v2;
+        bi = i2;
+      }
+    }
+    const int pv = bi == 0x7fffffff ? k : bi;
+    if (!(S[pv + pv * lds].x > 0.0)) return -6;   // uniform across the block
     if (pv != k) {
+      __syncthreads();   // every warp has finished its pivot search before rows move
       for (int c = threadIdx.x; c < r; c += NT) {
         const double2 t = S[k + c * lds];
         S[k + c * lds] = S[pv + c * lds];
         S[pv + c * lds] = t;
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < r; i += NT) {
-        if (i < k) continue;  // columns >= k hold the live matrix; L (cols < k) rows were swapped above
+      for (int i = k + threadIdx.x; i < r; i += NT) {  // columns >= k hold the live matrix
         const double2 t = S[i + k * lds];
         S[i + k * lds] = S[i + pv * lds];
         S[i + pv * lds] = t;
@@ -312,18 +325,15 @@ __device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long lon
     for (int i = k + 1 + threadIdx.x; i < r; i += NT) S[i + k * lds] = scale(S[i + k * lds], inv);
     if (threadIdx.x == 0) S[k + k * lds] = mk(lkk, 0.0);
     __syncthreads();
-    const long long rm = r - k - 1;
-    for (long long e = threadIdx.x; e < rm * rm; e += NT) {
-      const int i = k + 1 + (int)(e % rm), j = k + 1 + (int)(e / rm);
-      S[i + j * lds] = sub(S[i + j * lds], mul(S[i + k * lds], conj(S[j + k * lds])));
+    for (int j = k + 1 + warp; j < r; j += NW) {
+      const double2 cj = conj(S[j + k * lds]);
+      for (int i = k + 1 + lane; i < r; i += 32) S[i + j * lds] = sub(S[i + j * lds], mul(S[i + k * lds], cj));
     }
     __syncthreads();
   }
   // Gh(i, perm[l]) = (L^*)(i, l) = conj(L(l, i)) for l >= i, else 0
-  for (int e = threadIdx.x; e < r * r; e += NT) {
-    const int i = e % r, l = e / r;
-    Gh[i + perm[l] * ldg] = l >= i ? conj(S[l + i * lds]) : mk(0.0, 0.0);
-  }
+  for (int l = warp; l < r; l += NW)
+    for (int i = lane; i < r; i += 32) Gh[i + perm[l] * ldg] = l >= i ? conj(S[l + i * lds]) : mk(0.0, 0.0);
   __syncthreads();
   return 0;
 }

@@ -97,6 +97,12 @@ typedef struct {
   double max_offdiag_last;    /* max scaled off-diagonal measure seen in the last sweep */
   uint64_t all_per_sweep[64]; /* per-sweep counters (first 64 sweeps) */
   uint64_t big_per_sweep[64];
+  /* blocked, dominant kernel (k_blk_update over the F and G row tiles, medium-priority
+     stream): launches, algorithmic flops, and their summed device time (CUDA events on
+     the launching stream; only if opts.detail_timing).  The Z' row tiles run on a
+     low-priority stream that fills idle SMs and are excluded here. */
+  uint64_t launches_update_fg;
+  double flops_update_fg, t_update_fg;
 } ghsvd_stats;
 
 /* Fill *opts with the defaults described above (device 0, world_size 1). */

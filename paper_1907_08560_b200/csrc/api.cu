@@ -189,6 +189,11 @@ void ghsvd_destroy(ghsvd_ctx h) {
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
   if (ctx->aux_stream2) cudaStreamDestroy(ctx->aux_stream2);
+  for (cudaStream_t g : ctx->grp_streams) cudaStreamDestroy(g);
+  for (cudaStream_t h : ctx->hi_stream)
+    if (h) cudaStreamDestroy(h);
+  for (cudaStream_t h : ctx->mid_stream)
+    if (h) cudaStreamDestroy(h);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);

@@ -20,6 +20,7 @@
 // Multi-GPU (comm.cpp) exchanges block columns between the steps.
 #include <cuda_runtime.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -36,11 +37,13 @@ namespace {
 
 constexpr int KM = 64;          // max block-pivot order 2w
 constexpr int RT = 32;          // rows per staged tile
-constexpr int GS = RT + 4;      // Gram tile column stride (double2), conflict-free fragments
-constexpr int US = RT + 2;      // update tile column stride
+constexpr int GS = RT + 2;      // Gram tile column stride (double2), conflict-free fragments
 constexpr int ZS = KM + 4;      // Z_blk column stride in smem
 constexpr int NT_G = 256, NT_P = 512, NT_U = 256;
+constexpr int US = RT + 2;      // update tile column stride
 constexpr int GSTAGES = 3;      // cp.async pipeline depth of the Gram kernel
+constexpr int MAX_SPLIT = 16;   // max row splits of a Gram (partials summed in order)
+constexpr int TRACE_SLOTS = 48; // trace launch slots per block step
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -75,13 +78,30 @@ struct BlkArgs {
   double2* ghat;            // [pair][KM*KM]  G^ from pivoted Cholesky
   signed char* jhat;        // [pair][KM]     J^
   int* fact_ok;             // [pair][2]
+  int* gcnt;                // [pair][2] finished Gram splits (reset by the last one)
   double2* zinvT;           // [pair][KM*KM] (Z_blk^{-1})^T if want_x, else nullptr
   double2* W;               // want_x: W^T = (Z'^{-1})^T (n rows, ld ldn)
   DevCounters* cnt;
   double eps;
   int literal;
   int inner_sweeps;
+  unsigned long long* trace;  // GHSVD_TRACE: [launch id][first CTA start, last CTA end] (ns)
+  int trace_id;
 };
+
+// Launch tracing (GHSVD_TRACE=<csv path>, first sweep only): thread 0 of every CTA
+// folds %globaltimer into the launch's [min start, max end] with atomics.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_begin(const BlkArgs& a) {
+  if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[2 * a.trace_id], gtimer());
+}
+__device__ __forceinline__ void trace_end(const BlkArgs& a) {
+  if (a.trace && threadIdx.x == 0) atomicMax(&a.trace[2 * a.trace_id + 1], gtimer());
+}
 
 __device__ __forceinline__ void pair_cols(const BlkArgs& a, int pl, int& c0p, int& wp, int& c0q, int& wq) {
   long long bp, bq;
@@ -99,8 +119,67 @@ __device__ __forceinline__ long long gcol(int c, int c0p, int wp, int c0q, int w
   return -1;
 }
 
+// ---------------------------------------------------------------- block pivot
+// blk_factor (run by the last Gram CTA of a (pair, H|S), see k_blk_gram): sum the split
+// partials in fixed order; which = 0: H_blk -> HEBPJ -> F^ (and J^); which = 1: S_blk ->
+// diagonally pivoted Cholesky -> G^.  F^, G^ go to L2-resident scratch.
+constexpr int NT_F = 256;
+__device__ void blk_factor(const BlkArgs& a, int pl, int which, double2* W) {
+  __shared__ int np_sh;
+  const int tid = threadIdx.x;
+  int c0p, wp, c0q, wq;
+  pair_cols(a, pl, c0p, wp, c0q, wq);
+  const int k = wp + wq;
+  // sum of split partials (lower triangle, fixed split order), full Hermitian in W;
+  // L2 loads (__ldcg): the partials were written by other CTAs of this launch
+  const double2* base = a.gpart + ((size_t)pl * 2 + which) * a.nsplit * (KM * KM);
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int j = warp; j < k; j += NT_F / 32) {
+      for (int i = j + lane; i < k; i += 32) {
+        double2 x[MAX_SPLIT];
+#pragma unroll
+        for (int sp = 0; sp < MAX_SPLIT; sp++)
+          if (sp < a.nsplit) x[sp] = __ldcg(base + (size_t)sp * (KM * KM) + i + (size_t)j * KM);
+        double2 v = make_double2(0, 0);
+#pragma unroll
+        for (int sp = 0; sp < MAX_SPLIT; sp++)
+          if (sp < a.nsplit) {
+            v.x += x[sp].x;
+            v.y += x[sp].y;
+          }
+        if (i == j) v.y = 0.0;
+        W[i + j * KM] = v;
+        W[j + i * KM] = make_double2(v.x, -v.y);
+      }
+    }
+  }
+  __syncthreads();
+  double2* out = (which == 0 ? a.fhat : a.ghat) + (size_t)pl * (KM * KM);
+  int rc;
+  if (which == 0) {
+    // HEBPJ tolerance k * eps * max |H| (lower triangle), as the oracle
+    double tv = 0.0;
+    long long ti = 0;
+    for (int e = tid; e < k * k; e += NT_F) {
+      const int i = e % k, j = e / k;
+      if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W[i + j * KM]), 0);
+    }
+    hb::block_amax<NT_F>(tv, ti);
+    const double tolz = __dmul_rn(__dmul_rn((double)k, 0x1p-53), tv);
+    rc = hb::hebpj_dev<NT_F, KM>(W, k, KM, out, KM, a.jhat + (size_t)pl * KM, &np_sh, tolz);
+  } else {
+    rc = hb::pchol_dev<NT_F, KM>(W, k, KM, out, KM);
+  }
+  if (tid == 0) {
+    a.fact_ok[pl * 2 + which] = rc == 0;
+    if (rc) atomicCAS(&a.cnt->err, 0, which == 0 ? -7 : -6);
+  }
+}
+
 // ---------------------------------------------------------------- Gram (DMMA)
-// One CTA = one (pair, H|S, row split).  The 36 lower-triangle 8x8 output tiles of the
+// One CTA = one (row split, H|S, pair) (grid x = split fastest, so a pair's splits run
+// together and pairs complete progressively).  The 36 lower-triangle 8x8 output tiles of the
 // k x k Gram (k <= 64) are grouped by tile-row pairs {I, 7-I} (9 tiles each); warps
 // 2g, 2g+1 own group g and split every 32-row stage's 8 k-steps (even / odd).  Within
 // a k-step a warp loads the 8-g column fragments its 9 tiles need once (the A fragment
@@ -132,8 +211,9 @@ __device__ __forceinline__ void gram_tiles(const double2* T, int row, double sg,
 }
 
 __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
+  trace_begin(a);
   extern __shared__ __align__(128) double2 gsm[];  // [GSTAGES][KM][GS]
-  const int pl = a.pair0 + blockIdx.x, hs = blockIdx.y, split = blockIdx.z;
+  const int pl = a.pair0 + blockIdx.z, hs = blockIdx.y, split = blockIdx.x;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
   const double2* X = hs == 0 ? a.F : a.G;
@@ -190,75 +270,44 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
       for (int c = 0; c < 4; c++) red[((gi * 9 + t) * 4 + c) * 32 + lane] = acc[t][c];
   }
   __syncthreads();
-  if (kh) return;
+  if (!kh) {
 #pragma unroll
-  for (int t = 0; t < 9; t++)
+    for (int t = 0; t < 9; t++)
 #pragma unroll
-    for (int c = 0; c < 4; c++) acc[t][c] += red[((gi * 9 + t) * 4 + c) * 32 + lane];
-  double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
+      for (int c = 0; c < 4; c++) acc[t][c] += red[((gi * 9 + t) * 4 + c) * 32 + lane];
+    double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
 #pragma unroll
-  for (int t = 0; t < 9; t++) {
-    const int I = t <= gi ? gi : 7 - gi;
-    const int J = t <= gi ? t : t - gi - 1;
-    const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
-    out[i + (size_t)j * KM] = make_double2(acc[t][0], acc[t][2]);
-    out[i + (size_t)(j + 1) * KM] = make_double2(acc[t][1], acc[t][3]);
-  }
-}
-
-// ---------------------------------------------------------------- block pivot
-// k_blk_factor: grid (pairs, 2).  y = 0: H_blk -> HEBPJ -> F^ (and J^);  y = 1:
-// S_blk -> diagonally pivoted Cholesky -> G^.  The two factorizations of a pair
-// run as separate, concurrent CTAs; F^, G^ go to L2-resident scratch.
-constexpr int NT_F = 256;
-__global__ void __launch_bounds__(NT_F) k_blk_factor(BlkArgs a) {
-  extern __shared__ __align__(128) double2 fsm[];  // W (KM*KM)
-  double2* W = fsm;
-  __shared__ int np_sh;
-  const int pl = a.pair0 + blockIdx.x, which = blockIdx.y, tid = threadIdx.x;
-  int c0p, wp, c0q, wq;
-  pair_cols(a, pl, c0p, wp, c0q, wq);
-  const int k = wp + wq;
-  // sum of split partials (lower triangle), full Hermitian in W
-  const double2* base = a.gpart + ((size_t)pl * 2 + which) * a.nsplit * (KM * KM);
-  for (int e = tid; e < k * k; e += NT_F) {
-    const int i = e % k, j = e / k;
-    const int ii = i >= j ? i : j, jj = i >= j ? j : i;
-    double2 v = make_double2(0, 0);
-    for (int sp = 0; sp < a.nsplit; sp++) {
-      const double2 x = base[(size_t)sp * (KM * KM) + ii + (size_t)jj * KM];
-      v.x += x.x;
-      v.y += x.y;
+    for (int t = 0; t < 9; t++) {
+      const int I = t <= gi ? gi : 7 - gi;
+      const int J = t <= gi ? t : t - gi - 1;
+      const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
+      out[i + (size_t)j * KM] = make_double2(acc[t][0], acc[t][2]);
+      out[i + (size_t)(j + 1) * KM] = make_double2(acc[t][1], acc[t][3]);
     }
-    if (ii == jj) v.y = 0.0;
-    W[i + j * KM] = (i >= j) ? v : make_double2(v.x, -v.y);
+  }
+  // The last CTA of this (pair, H|S) to finish factorizes the summed Gram right away
+  // (threadfence-reduction pattern): no separate launch, and a pair's block pivot is
+  // formed while the Grams of later pairs are still streaming.
+  __shared__ int last_sh;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int t = atomicAdd(&a.gcnt[pl * 2 + hs], 1);
+    last_sh = t == a.nsplit - 1;
+    if (last_sh) a.gcnt[pl * 2 + hs] = 0;   // ready for the next block step
   }
   __syncthreads();
-  double2* out = (which == 0 ? a.fhat : a.ghat) + (size_t)pl * (KM * KM);
-  int rc;
-  if (which == 0) {
-    // HEBPJ tolerance k * eps * max |H| (lower triangle), as the oracle
-    double tv = 0.0;
-    long long ti = 0;
-    for (int e = tid; e < k * k; e += NT_F) {
-      const int i = e % k, j = e / k;
-      if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W[i + j * KM]), 0);
-    }
-    hb::block_amax<NT_F>(tv, ti);
-    const double tolz = __dmul_rn(__dmul_rn((double)k, 0x1p-53), tv);
-    rc = hb::hebpj_dev<NT_F, KM>(W, k, KM, out, KM, a.jhat + (size_t)pl * KM, &np_sh, tolz);
-  } else {
-    rc = hb::pchol_dev<NT_F, KM>(W, k, KM, out, KM);
+  if (last_sh) {
+    __threadfence();
+    blk_factor(a, pl, hs, gsm);
   }
-  if (tid == 0) {
-    a.fact_ok[pl * 2 + which] = rc == 0;
-    if (rc) atomicCAS(&a.cnt->err, 0, which == 0 ? -7 : -6);
-  }
+  trace_end(a);
 }
 
 // k_blk_pivot: one CTA per pair: F^, G^, J^ -> shared memory, border to even order
 // (Sec 6.3.2), inner Level-1 sweep(s) accumulating Z_blk.
 __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
+  trace_begin(a);
   extern __shared__ __align__(128) double2 psm[];  // W0 (Z_blk) | F^ | G^  (KM*KM each)
   double2* W0 = psm;
   double2* Fh = psm + KM * KM;
@@ -273,6 +322,7 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
   const int kb = k + (k & 1);
   if (!a.fact_ok[2 * pl] || !a.fact_ok[2 * pl + 1]) {
     if (tid == 0) a.applied[pl] = 0;
+    trace_end(a);
     return;
   }
   if (tid == 0) {
@@ -305,22 +355,29 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
   __shared__ double gsh[KM / 2][8];
   __shared__ double zsh[KM / 2][8];
   __shared__ int ksh[KM / 2];
+  __shared__ double Jd[KM];
+  for (int i = tid; i < KM; i += NT_P) Jd[i] = (double)Jh[i];
+  __syncthreads();
   const int warp = tid >> 5, lane = tid & 31;
   const int hw = lane >> 4, hl = lane & 15;
   const unsigned hmask = hw ? 0xffff0000u : 0x0000ffffu;
   const double tol = a.eps * sqrt((double)kb);       // C-7: n = block-pivot order
   unsigned long long w0_all = 0, w0_big = 0;          // warp-0 lane counters
+  const int pr = 2 * warp + hw;                        // this half-warp's pivot pair slot
+  const int b3 = (hl >> 3) & 1, b2 = (hl >> 2) & 1, b1 = (hl >> 1) & 1;
   for (int sw = 0; sw < a.inner_sweeps; sw++) {
     unsigned long long sw_all = 0, sw_big = 0;
     for (int s = 0; s < kb - 1; s++) {
-      const int pr = 2 * warp + hw;
-      long long p = 0, q = 0;
+      int p = 0, q = 0;
       if (pr < kb / 2) {
-        rr_pair(kb, s, pr, &p, &q);
+        rr_pair32(kb, s, pr, &p, &q);
+        // rows >= kb of F^, G^ are zero, so all KM rows are summed without guards
         double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i = hl; i < kb; i += 16) {
+#pragma unroll
+        for (int t = 0; t < KM / 16; t++) {
+          const int i = hl + 16 * t;
           const double2 fp = Fh[i + p * KM], fq = Fh[i + q * KM], gpp = Gh[i + p * KM], gq = Gh[i + q * KM];
-          const double sg = (double)Jh[i];
+          const double sg = Jd[i];
           g[0] += sg * (fp.x * fp.x + fp.y * fp.y);
           g[1] += sg * (fq.x * fq.x + fq.y * fq.y);
           g[2] += sg * (fp.x * fq.x + fp.y * fq.y);
@@ -330,20 +387,28 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
           g[6] += gpp.x * gq.x + gpp.y * gq.y;
           g[7] += gpp.x * gq.y - gpp.y * gq.x;
         }
+        // transpose-reduce of the 8 sums over the 16 lanes: after the offsets 8, 4, 2
+        // every lane keeps one value index (hl >> 1), offset 1 completes the sum
+        double h4[4], h2[2];
 #pragma unroll
-        for (int c = 0; c < 8; c++)
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) g[c] += __shfl_xor_sync(hmask, g[c], o);
-        if (hl < 8) {
-          double v = g[0];
-#pragma unroll
-          for (int c = 1; c < 8; c++) v = hl == c ? g[c] : v;
-          gsh[pr][hl] = v;
+        for (int j = 0; j < 4; j++) {
+          const double snd = b3 ? g[j] : g[j + 4];
+          const double kep = b3 ? g[j + 4] : g[j];
+          h4[j] = kep + __shfl_xor_sync(hmask, snd, 8);
         }
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          const double snd = b2 ? h4[j] : h4[j + 2];
+          const double kep = b2 ? h4[j + 2] : h4[j];
+          h2[j] = kep + __shfl_xor_sync(hmask, snd, 4);
+        }
+        double w = (b1 ? h2[1] : h2[0]) + __shfl_xor_sync(hmask, b1 ? h2[0] : h2[1], 2);
+        w += __shfl_xor_sync(hmask, w, 1);
+        if (!(hl & 1)) gsh[pr][hl >> 1] = w;
       }
       __syncthreads();
       if (warp == 0 && lane < kb / 2) {
-        const HZOut z = hz2x2_dev(gsh[lane], tol, a.literal);
+        const HZOut z = hz2x2_core(gsh[lane], tol, a.literal);
         zsh[lane][0] = z.z11.re; zsh[lane][1] = z.z11.im; zsh[lane][2] = z.z21.re; zsh[lane][3] = z.z21.im;
         zsh[lane][4] = z.z12.re; zsh[lane][5] = z.z12.im; zsh[lane][6] = z.z22.re; zsh[lane][7] = z.z22.im;
         ksh[lane] = z.kind;
@@ -360,7 +425,9 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
           const double2 z11 = make_double2(zsh[pr][0], zsh[pr][1]), z21 = make_double2(zsh[pr][2], zsh[pr][3]);
           const double2 z12 = make_double2(zsh[pr][4], zsh[pr][5]), z22 = make_double2(zsh[pr][6], zsh[pr][7]);
           auto rot = [&](double2* M) {
-            for (int i = hl; i < kb; i += 16) {
+#pragma unroll
+            for (int t = 0; t < KM / 16; t++) {
+              const int i = hl + 16 * t;
               const double2 x = M[i + p * KM], y = M[i + q * KM];
               M[i + p * KM] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
                                            x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
@@ -471,17 +538,30 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
       wo[e] = Gh[j + i * KM];   // transpose (no conjugation)
     }
   }
+  trace_end(a);
 }
 
 // ---------------------------------------------------------------- update (DMMA)
-// grid (pair, tile): tiles [0, tF) rows of F, [tF, 2 tF) rows of G, [2 tF, 2 tF + tZ) rows of Z
+// grid (pair, tile): tiles [0, tF) rows of F, [tF, 2 tF) rows of G, [2 tF, 2 tF + tZ) rows of Z.
+// Measured faster than three persistent variants (Z_blk loaded once per pair, the next
+// row tile prefetched, results stored from the accumulators): one CTA of 8 warps per SM
+// with double-buffered 64-row tiles, two CTAs per SM walking contiguous ranges, one CTA
+// of 16 warps with double-buffered 64-row tiles were 8-15 % slower.  ncu: the short-
+// lived CTAs of this form keep the DMMA sub-pipe 71 % busy; in the 16-warp variant the
+// (Zr + Zi) / (Xr + Xi) DADDs of the 3M scheme stall on the FP64 pipe the DMMAs occupy
+// (math-pipe stalls 50 % vs 24 %).
 // wmode = 1: the tiles are row tiles of W^T (n rows) and the right factor is
 // (Z_blk^{-1})^T (NEXT-1 accumulation of Z'^{-1}).
+template <bool M4>
 __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile0, int tile_end, int tpc,
                                                      int wmode) {
+  trace_begin(a);
   extern __shared__ __align__(128) double2 usm[];  // X tile [KM][US] | Z_blk [KM][ZS]
   const int pl = a.pair0 + blockIdx.x;
-  if (!a.applied[pl]) return;
+  if (!a.applied[pl]) {
+    trace_end(a);
+    return;
+  }
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
   const int k = wp + wq;
@@ -535,15 +615,25 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
         const double2 z = Zb[(8 * (J0 + t) + (lane >> 2)) * ZS + kk + (lane & 3)];  // B(k, j)
         dmma(p1[t][0], p1[t][1], x.x, z.x);
         dmma(p2[t][0], p2[t][1], x.y, z.y);
-        dmma(p3[t][0], p3[t][1], xs, z.x + z.y);
+        if (M4) {   // exact 4M product: Im accumulated directly, no additions in the loop
+          dmma(p3[t][0], p3[t][1], x.x, z.y);
+          dmma(p3[t][0], p3[t][1], x.y, z.x);
+        } else {
+          dmma(p3[t][0], p3[t][1], xs, z.x + z.y);
+        }
       }
     }
     __syncthreads();
 #pragma unroll
     for (int t = 0; t < 4; t++) {
       const int i = 8 * I + (lane >> 2), j = 8 * (J0 + t) + 2 * (lane & 3);
-      Xt[j * US + i] = make_double2(p1[t][0] - p2[t][0], p3[t][0] - p1[t][0] - p2[t][0]);
-      Xt[(j + 1) * US + i] = make_double2(p1[t][1] - p2[t][1], p3[t][1] - p1[t][1] - p2[t][1]);
+      if (M4) {
+        Xt[j * US + i] = make_double2(p1[t][0] - p2[t][0], p3[t][0]);
+        Xt[(j + 1) * US + i] = make_double2(p1[t][1] - p2[t][1], p3[t][1]);
+      } else {
+        Xt[j * US + i] = make_double2(p1[t][0] - p2[t][0], p3[t][0] - p1[t][0] - p2[t][0]);
+        Xt[(j + 1) * US + i] = make_double2(p1[t][1] - p2[t][1], p3[t][1] - p1[t][1] - p2[t][1]);
+      }
     }
     __syncthreads();
     for (int e = tid; e < KM * RT; e += NT_U) {
@@ -553,6 +643,7 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
     }
     __syncthreads();
   }
+  trace_end(a);
 }
 
 __global__ void k_blk_partition(int* bstart, int* bwidth, int nblk, long long n) {
@@ -584,7 +675,6 @@ int auto_nblk(int64_t n, const ghsvd_options* o) {
   return (int)std::max<int64_t>(2, nb);
 }
 
-constexpr int MAX_SPLIT = 16;
 
 struct BlkPlan {
   int nblk, K, slot0, nsplit;
@@ -634,7 +724,7 @@ size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
   return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)2 * K * KM * KM * 16) +
          al256((size_t)2 * K * 4) + 2 * al256((size_t)nb * 4) + 2 * al256((size_t)K * KM * KM * 16) +
          al256((size_t)K * KM) + al256((size_t)2 * K * 4) + (o->want_x ? al256((size_t)2 * K * KM * KM * 16) : 0) +
-         4096;
+         al256((size_t)(nb + 2) * TRACE_SLOTS * 16) + al256((size_t)2 * K * 4) + 4096;
 }
 
 // in comm.cpp
@@ -645,8 +735,10 @@ struct BlkSetup {
   BlkPlan pl;
   BlkArgs a;
   std::vector<int> bs_h, bw_h;
-  size_t smem_g, smem_p, smem_f, smem_u;
-  int tF, tZ;
+  size_t smem_g, smem_p, smem_u;
+  int tF, tZ, sms;
+  bool upd4m;
+  unsigned long long* trace_buf;
 };
 
 static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
@@ -678,13 +770,18 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   a.ghat = (double2*)p; p += al256((size_t)pl.K * KM * KM * 16);
   a.jhat = (signed char*)p; p += al256((size_t)pl.K * KM);
   a.fact_ok = (int*)p; p += al256((size_t)2 * pl.K * 4);
+  a.gcnt = (int*)p; p += al256((size_t)2 * pl.K * 4);
   a.W = ctx->o.want_x ? ctx->W : nullptr;
   if (a.W) {
     a.zinvT = (double2*)p; p += al256((size_t)2 * pl.K * KM * KM * 16);   // double-buffered like zblk
   } else {
     a.zinvT = nullptr;
   }
+  S.trace_buf = (unsigned long long*)p; p += al256((size_t)(pl.nblk + 2) * TRACE_SLOTS * 16);
+  a.trace = nullptr;
+  a.trace_id = 0;
   k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
+  GH_CUDA(cudaMemsetAsync(a.gcnt, 0, (size_t)2 * pl.K * 4, str));
   GH_CUDA(cudaGetLastError());
   S.bs_h.assign(pl.nblk, 0);
   S.bw_h.assign(pl.nblk, 0);
@@ -716,14 +813,30 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   S.smem_g = (size_t)GSTAGES * KM * GS * 16;
   S.smem_p = (size_t)3 * KM * KM * 16;
   S.smem_u = (size_t)(KM * US + KM * ZS) * 16;
-  S.smem_f = (size_t)KM * KM * 16;
   GH_CUDA(cudaFuncSetAttribute(k_blk_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
   GH_CUDA(cudaFuncSetAttribute(k_blk_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_p));
-  GH_CUDA(cudaFuncSetAttribute(k_blk_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_f));
-  GH_CUDA(cudaFuncSetAttribute(k_blk_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_u));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_u));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_u));
+  S.upd4m = env_int("GHSVD_UPD4M", 0) != 0;
   S.tF = (int)((ctx->m + RT - 1) / RT);
   S.tZ = (int)((ctx->n + RT - 1) / RT);
+  {
+    int dev = 0;
+    S.sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&S.sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   return GHSVD_OK;
+}
+
+// Update launch: pairs [pair0, pair0 + np), row tiles [tbeg, tend) (see k_blk_update).
+static void launch_update(const BlkSetup& S, BlkArgs a, int pair0, int np, int tbeg, int tend, int wmode,
+                          cudaStream_t st) {
+  a.pair0 = pair0;
+  if (np <= 0 || tend <= tbeg) return;
+  if (S.upd4m)
+    k_blk_update<true><<<dim3(np, tend - tbeg), NT_U, S.smem_u, st>>>(a, S.tF, tbeg, tend, 1, wmode);
+  else
+    k_blk_update<false><<<dim3(np, tend - tbeg), NT_U, S.smem_u, st>>>(a, S.tF, tbeg, tend, 1, wmode);
 }
 
 // Diagnostic: block steps [s0, s0+ns) of the first block sweep, one stream, no overlap.
@@ -743,13 +856,150 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
   BlkArgs a = S.a;
   for (int64_t s = s0; s < s0 + ns; s++) {
     a.s = (int)s;
-    k_blk_gram<<<dim3(S.pl.K, 2, S.pl.nsplit), NT_G, S.smem_g, str>>>(a);
-    k_blk_factor<<<dim3(S.pl.K, 2), NT_F, S.smem_f, str>>>(a);
+    k_blk_gram<<<dim3(S.pl.nsplit, 2, S.pl.K), NT_G, S.smem_g, str>>>(a);
     k_blk_pivot<<<S.pl.K, NT_P, S.smem_p, str>>>(a);
-    k_blk_update<<<dim3(S.pl.K, 2 * S.tF + S.tZ), NT_U, S.smem_u, str>>>(a, S.tF, 0, 2 * S.tF + S.tZ, 1, 0);
-    if (a.W) k_blk_update<<<dim3(S.pl.K, S.tZ), NT_U, S.smem_u, str>>>(a, S.tF, 0, S.tZ, 1, 1);
+    launch_update(S, a, 0, S.pl.K, 0, 2 * S.tF + S.tZ, 0, str);
+    if (a.W) launch_update(S, a, 0, S.pl.K, 0, S.tZ, 1, str);
     GH_CUDA(cudaGetLastError());
   }
+  return GHSVD_OK;
+}
+
+// One-GPU block sweep, pipelined over pair groups (Sec 6.4 run on one device).
+//
+// Round-robin dependency structure (reading C-11 applied to block columns): the block
+// columns of slot k at step s+1 are those of slots k-1 and k+1 at step s (slot 0 also
+// keeps the fixed column n-1, slot K-1 the column it shares with itself).  So the
+// slots are cut into G contiguous groups, each group's chain
+//     Gram -> factor -> pivot -> update (F, G and Z' rows)
+// runs on its own stream, and group g at step s waits only for the updates of groups
+// g-1, g, g+1 at step s-1.  While one group is in its latency-bound factor / inner
+// sweep phase the other groups' Gram and update kernels keep the tensor pipes busy,
+// and step s+1 of the first groups starts while the last groups finish step s.  The
+// per-pair work and its arithmetic are exactly those of the step-synchronous
+// schedule, so the results are bitwise identical to it.
+static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int G) {
+  BlkPlan& pl = S.pl;
+  BlkArgs a = S.a;
+  const size_t smem_g = S.smem_g, smem_p = S.smem_p;
+  const int tF = S.tF, tZ = S.tZ;
+  cudaStream_t str = ctx->stream;
+  const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
+  const int nst = pl.nblk - 1;
+  while ((int)ctx->grp_streams.size() < G) {
+    cudaStream_t t;
+    GH_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    ctx->grp_streams.push_back(t);
+  }
+  std::vector<int> g0(G + 1);
+  for (int g = 0; g <= G; g++) g0[g] = (int)((long long)g * pl.K / G);
+  std::vector<cudaEvent_t> ev_upd(2 * G), tev;
+  for (auto& e : ev_upd) GH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // detail timing: per (step, group) events around Gram, factor + pivot, update on the
+  // group's stream (kernels of other groups run concurrently inside these intervals)
+  const bool timing = ctx->o.detail_timing != 0;
+  if (timing) {
+    tev.resize((size_t)nst * G * 4);
+    for (auto& e : tev) GH_CUDA(cudaEventCreate(&e));
+  }
+  auto destroy_events = [&]() {
+    for (auto e : ev_upd) cudaEventDestroy(e);
+    for (auto e : tev) cudaEventDestroy(e);
+  };
+  double fl_gram_sweep = 0.0, fl_upd_sweep = 0.0;
+  for (int s = 0; s < nst; s++)
+    for (int kk = pl.slot0; kk < pl.slot0 + pl.K; kk++) {
+      long long bp, bq;
+      rr_pair(pl.nblk, s, kk, &bp, &bq);
+      const double kq = S.bw_h[bp] + S.bw_h[bq];
+      fl_gram_sweep += 8.0 * kq * (kq + 1) * ctx->m;
+      fl_upd_sweep += 8.0 * kq * kq * (2.0 * ctx->m + ctx->n);
+    }
+  GH_CUDA(cudaEventRecord(ctx->ev0, str));
+  for (int sw = 0; sw < ctx->o.max_sweeps; sw++) {
+    GH_CUDA(cudaMemsetAsync(ctx->cnt, 0, sizeof(DevCounters), str));
+    GH_CUDA(cudaEventRecord(ctx->ev2, str));
+    for (int g = 0; g < G; g++) GH_CUDA(cudaStreamWaitEvent(ctx->grp_streams[g], ctx->ev2, 0));
+    for (int s = 0; s < nst; s++) {
+      const int b = s & 1;
+      a.s = s;
+      for (int g = 0; g < G; g++) {
+        cudaStream_t sh = ctx->grp_streams[g];
+        const int np = g0[g + 1] - g0[g];
+        if (np <= 0) continue;
+        if (s > 0) {
+          if (g > 0) GH_CUDA(cudaStreamWaitEvent(sh, ev_upd[2 * (g - 1) + (b ^ 1)], 0));
+          if (g + 1 < G) GH_CUDA(cudaStreamWaitEvent(sh, ev_upd[2 * (g + 1) + (b ^ 1)], 0));
+        }
+        a.pair0 = g0[g];
+        cudaEvent_t* te = timing ? &tev[((size_t)s * G + g) * 4] : nullptr;
+        if (te) GH_CUDA(cudaEventRecord(te[0], sh));
+        k_blk_gram<<<dim3(pl.nsplit, 2, np), NT_G, smem_g, sh>>>(a);
+        if (te) GH_CUDA(cudaEventRecord(te[1], sh));
+        k_blk_pivot<<<np, NT_P, smem_p, sh>>>(a);
+        if (te) GH_CUDA(cudaEventRecord(te[2], sh));
+        launch_update(S, a, g0[g], np, 0, 2 * tF + tZ, 0, sh);
+        if (a.W) launch_update(S, a, g0[g], np, 0, tZ, 1, sh);
+        if (te) GH_CUDA(cudaEventRecord(te[3], sh));
+        GH_CUDA(cudaEventRecord(ev_upd[2 * g + b], sh));
+      }
+      GH_CUDA(cudaGetLastError());
+    }
+    for (int g = 0; g < G; g++)
+      if (g0[g + 1] > g0[g]) GH_CUDA(cudaStreamWaitEvent(str, ev_upd[2 * g + ((nst - 1) & 1)], 0));
+    GH_CUDA(cudaEventRecord(ctx->ev3, str));
+    DevCounters c;
+    GH_CUDA(cudaMemcpyAsync(&c, ctx->cnt, sizeof(c), cudaMemcpyDeviceToHost, str));
+    GH_CUDA(cudaStreamSynchronize(str));
+    if (c.err) {
+      destroy_events();
+      ctx->err = c.err == -7 ? "blocked: rank-deficient block pivot (HEBPJ)"
+                 : c.err == -6 ? "blocked: indefinite / singular S block pivot"
+                               : "blocked: non-finite value in a block pivot";
+      return c.err == -7 ? GHSVD_E_RANK_DEFICIENT : c.err == -6 ? GHSVD_E_INDEFINITE_S : GHSVD_E_NONFINITE;
+    }
+    float kms = 0;
+    GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
+    st->kernel_seconds += kms * 1e-3;
+    st->launches += (uint64_t)(a.W ? 4 : 3) * G * nst;
+    st->flops_gram += fl_gram_sweep;
+    st->flops_update += fl_upd_sweep;
+    st->flops_update_fg += fl_upd_sweep;   // F, G and Z' row tiles share one launch here
+    st->launches_update_fg += (uint64_t)G * nst;
+    if (timing) {
+      for (size_t i = 0; i < tev.size(); i += 4) {
+        float t0 = 0, t1 = 0, t2 = 0;
+        GH_CUDA(cudaEventElapsedTime(&t0, tev[i], tev[i + 1]));
+        GH_CUDA(cudaEventElapsedTime(&t1, tev[i + 1], tev[i + 2]));
+        GH_CUDA(cudaEventElapsedTime(&t2, tev[i + 2], tev[i + 3]));
+        st->t_gram += t0 * 1e-3;
+        st->t_pivot += t1 * 1e-3;
+        st->t_update += t2 * 1e-3;
+        st->t_update_fg += t2 * 1e-3;
+      }
+    }
+    if (sw < 64) {
+      st->all_per_sweep[sw] = c.all;
+      st->big_per_sweep[sw] = c.big;
+    }
+    st->sweeps = sw + 1;
+    st->pairs_visited += pairs;
+    st->transforms_all += c.all;
+    st->transforms_big += c.big;
+    if (c.big == 0) {
+      st->converged = 1;
+      break;
+    }
+  }
+  GH_CUDA(cudaEventRecord(ctx->ev1, str));
+  GH_CUDA(cudaEventSynchronize(ctx->ev1));
+  destroy_events();
+  float ms = 0;
+  GH_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  st->seconds = ms * 1e-3;
+  st->alg_flops = st->flops_gram + st->flops_update;
+  st->alg_bytes = (uint64_t)((double)st->sweeps * (pl.nblk - 1) * 16.0 * (double)ctx->n *
+                             (2.0 * ctx->m + 2.0 * (2.0 * ctx->m + ctx->n)));
   return GHSVD_OK;
 }
 
@@ -759,17 +1009,23 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     ghsvd_status e = blk_setup(ctx, S);
     if (e) return e;
   }
+  const bool multi = ctx->comm != nullptr;   // NCCL path (also exercised with one rank)
+  {
+    // one GPU: GHSVD_GROUPS=G >= 2 selects the pipelined pair-group schedule
+    // (blk_sweep_groups; measured 1-2 % slower than the two-stream schedule below on
+    // config 3, kept as an experiment)
+    const int G = std::min(S.pl.K, env_int("GHSVD_GROUPS", 0));
+    if (!multi && G >= 2) return blk_sweep_groups(ctx, st, S, G);
+  }
   BlkPlan& pl = S.pl;
   BlkArgs a = S.a;
   const std::vector<int>& bs_h = S.bs_h;
   const std::vector<int>& bw_h = S.bw_h;
-  const size_t smem_g = S.smem_g, smem_p = S.smem_p, smem_f = S.smem_f, smem_u = S.smem_u;
+  const size_t smem_g = S.smem_g, smem_p = S.smem_p;
   const int tF = S.tF, tZ = S.tZ;
-  const int tpc = env_int("GHSVD_UPD_TPC", 1);   // row tiles per update CTA (1..8 measured equal)
   cudaStream_t str = ctx->stream;
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
   GH_CUDA(cudaStreamSynchronize(str));
-  const bool multi = ctx->comm != nullptr;   // NCCL path (also exercised with one rank)
   const bool timing = ctx->o.detail_timing != 0;
   // The Z' update of step s (aux stream) overlaps the Gram + pivot of step s+1: Z is
   // touched by no other kernel, and Z_blk / applied are double-buffered by step parity.
@@ -780,11 +1036,40 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   // latency-bound pivot kernel overlaps the other half's Gram / update kernels
   const int nh = pl.K >= 2 ? 2 : 1;
   const int KA = nh == 2 ? pl.K / 2 : pl.K;
+  // Stream priorities steer the block scheduler (GHSVD_PRIO=0 disables, for comparison):
+  //   highest  factor / pivot (latency-bound): their CTAs are placed as soon as a Gram
+  //            or update CTA retires, so a half's block pivots start right after its
+  //            own Grams instead of queueing behind the other half's Gram CTAs;
+  //   medium   Gram and F, G update of each half (half 0 one level above half 1);
+  //   lowest   the Z' update (aux): it has a whole step of slack and fills the SMs the
+  //            latency-bound kernels leave idle.
+  const bool prio = env_int("GHSVD_PRIO", 1) != 0;
   cudaStream_t hs_st[2] = {str, ctx->aux_stream2};
+  cudaStream_t fp_st[2] = {str, ctx->aux_stream2};
+  if (prio) {
+    int lo = 0, hi = 0;
+    GH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int i = 0; i < 2; i++) {
+      // half 0 above half 1: its Grams finish first, so its block pivots overlap the
+      // Grams of half 1 and its update is ready when they end
+      const int mid = std::min(lo, hi + 1 + i);
+      if (!ctx->hi_stream[i]) GH_CUDA(cudaStreamCreateWithPriority(&ctx->hi_stream[i], cudaStreamNonBlocking, hi));
+      if (!ctx->mid_stream[i])
+        GH_CUDA(cudaStreamCreateWithPriority(&ctx->mid_stream[i], cudaStreamNonBlocking, mid));
+      fp_st[i] = ctx->hi_stream[i];
+      hs_st[i] = ctx->mid_stream[i];
+    }
+  } else {
+    fp_st[0] = hs_st[0];
+    fp_st[1] = hs_st[1];
+  }
   const int h_pair0[2] = {0, KA}, h_np[2] = {KA, pl.K - KA};
   const int nst = pl.nblk - 1;
-  std::vector<cudaEvent_t> ev_piv(2), ev_fg(2), ev_zdone(2), tev;
+  std::vector<cudaEvent_t> ev_piv(2), ev_fg(2), ev_zdone(2), ev_gr(2), tev;
+  cudaEvent_t ev_x;
+  GH_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
   for (int i = 0; i < 2; i++) {
+    GH_CUDA(cudaEventCreateWithFlags(&ev_gr[i], cudaEventDisableTiming));
     GH_CUDA(cudaEventCreateWithFlags(&ev_piv[i], cudaEventDisableTiming));
     GH_CUDA(cudaEventCreateWithFlags(&ev_fg[i], cudaEventDisableTiming));
     GH_CUDA(cudaEventCreateWithFlags(&ev_zdone[i], cudaEventDisableTiming));
@@ -797,13 +1082,15 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     for (auto e : ev_piv) cudaEventDestroy(e);
     for (auto e : ev_fg) cudaEventDestroy(e);
     for (auto e : ev_zdone) cudaEventDestroy(e);
+    for (auto e : ev_gr) cudaEventDestroy(e);
     for (auto e : tev) cudaEventDestroy(e);
+    cudaEventDestroy(ev_x);
   };
   double2* zblk0 = a.zblk;
   double2* zinv0 = a.zinvT;
   int* applied0 = a.applied;
   // algorithmic flops per block step (Hermitian Grams k(k+1)/2 m each; updates k^2 (2m+n))
-  std::vector<double> fl_gram(nst, 0.0), fl_upd(nst, 0.0);
+  std::vector<double> fl_gram(nst, 0.0), fl_upd(nst, 0.0), fl_upd_fg(nst, 0.0);
   for (int s = 0; s < nst; s++)
     for (int kk = pl.slot0; kk < pl.slot0 + pl.K; kk++) {
       long long bp, bq;
@@ -811,12 +1098,22 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       const double kq = bw_h[bp] + bw_h[bq];
       fl_gram[s] += 8.0 * kq * (kq + 1) * ctx->m;
       fl_upd[s] += 8.0 * kq * kq * (2.0 * ctx->m + ctx->n);
+      fl_upd_fg[s] += 8.0 * kq * kq * (2.0 * ctx->m);
     }
+  const char* trace_path = getenv("GHSVD_TRACE");
+  std::vector<unsigned long long> trace_h;
+  if (trace_path && *trace_path) {
+    trace_h.assign((size_t)nst * TRACE_SLOTS * 2, 0);
+    for (size_t i = 0; i < trace_h.size(); i += 2) trace_h[i] = ~0ull;
+    GH_CUDA(cudaMemcpyAsync(S.trace_buf, trace_h.data(), trace_h.size() * 8, cudaMemcpyHostToDevice, str));
+  }
   GH_CUDA(cudaEventRecord(ctx->ev0, str));
   for (int sw = 0; sw < ctx->o.max_sweeps; sw++) {
+    a.trace = (sw == 0 && !trace_h.empty()) ? S.trace_buf : nullptr;
     GH_CUDA(cudaMemsetAsync(ctx->cnt, 0, sizeof(DevCounters), str));
     GH_CUDA(cudaEventRecord(ctx->ev2, str));
-    if (nh == 2) GH_CUDA(cudaStreamWaitEvent(hs_st[1], ctx->ev2, 0));
+    for (int h = 0; h < nh; h++)
+      if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(hs_st[h], ctx->ev2, 0));
     for (int s = 0; s < nst; s++) {
       const int b = s & 1;
       a.s = s;
@@ -828,32 +1125,47 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         GH_CUDA(cudaStreamWaitEvent(hs_st[0], ev_fg[1], 0));
         GH_CUDA(cudaStreamWaitEvent(hs_st[1], ev_fg[0], 0));
       }
+      // multi-GPU: the exchange after step s-1 (on str) precedes every Gram of step s
+      if (multi && s > 0)
+        for (int h = 0; h < nh; h++)
+          if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(hs_st[h], ev_x, 0));
       for (int h = 0; h < nh; h++) {
         cudaStream_t sh = hs_st[h];
         a.pair0 = h_pair0[h];
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 0], sh));
-        k_blk_gram<<<dim3(h_np[h], 2, pl.nsplit), NT_G, smem_g, sh>>>(a);
+        a.trace_id = s * TRACE_SLOTS + 0 + h;
+        k_blk_gram<<<dim3(pl.nsplit, 2, h_np[h]), NT_G, smem_g, sh>>>(a);
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 1], sh));
+        cudaStream_t fs = fp_st[h];
+        if (fs != sh) {
+          GH_CUDA(cudaEventRecord(ev_gr[h], sh));
+          GH_CUDA(cudaStreamWaitEvent(fs, ev_gr[h], 0));
+        }
         // Z_blk buffer b was last read by the Z update of step s-2
-        if (s >= 2 || sw > 0) GH_CUDA(cudaStreamWaitEvent(sh, ev_zdone[b], 0));
-        k_blk_factor<<<dim3(h_np[h], 2), NT_F, smem_f, sh>>>(a);
-        k_blk_pivot<<<h_np[h], NT_P, smem_p, sh>>>(a);
-        GH_CUDA(cudaEventRecord(ev_piv[h], sh));
+        if (s >= 2 || sw > 0) GH_CUDA(cudaStreamWaitEvent(fs, ev_zdone[b], 0));
+        a.trace_id = s * TRACE_SLOTS + 4 + h;
+        k_blk_pivot<<<h_np[h], NT_P, smem_p, fs>>>(a);
+        GH_CUDA(cudaEventRecord(ev_piv[h], fs));
+        if (fs != sh) GH_CUDA(cudaStreamWaitEvent(sh, ev_piv[h], 0));
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
-        k_blk_update<<<dim3(h_np[h], (2 * tF + tpc - 1) / tpc), NT_U, smem_u, sh>>>(a, tF, 0, 2 * tF, tpc, 0);
+        a.trace_id = s * TRACE_SLOTS + 6 + h;
+        launch_update(S, a, h_pair0[h], h_np[h], 0, 2 * tF, 0, sh);
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 3], sh));
         GH_CUDA(cudaEventRecord(ev_fg[h], sh));
       }
       // Z' update of all pairs of step s on the aux stream (overlaps step s+1)
       a.pair0 = 0;
       for (int h = 0; h < nh; h++) GH_CUDA(cudaStreamWaitEvent(aux, ev_piv[h], 0));
-      k_blk_update<<<dim3(pl.K, (tZ + tpc - 1) / tpc), NT_U, smem_u, aux>>>(a, tF, 2 * tF, 2 * tF + tZ, tpc, 0);
-      if (a.W) k_blk_update<<<dim3(pl.K, (tZ + tpc - 1) / tpc), NT_U, smem_u, aux>>>(a, tF, 0, tZ, tpc, 1);
+      a.trace_id = s * TRACE_SLOTS + 8;
+      launch_update(S, a, 0, pl.K, 2 * tF, 2 * tF + tZ, 0, aux);
+      a.trace_id = s * TRACE_SLOTS + 9;
+      if (a.W) launch_update(S, a, 0, pl.K, 0, tZ, 1, aux);
       GH_CUDA(cudaEventRecord(ev_zdone[b], aux));
       GH_CUDA(cudaGetLastError());
       if (multi) {
         // block columns (F, G and Z) leave only after every update of step s
-        if (nh == 2) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[1], 0));
+        for (int h = 0; h < nh; h++)
+          if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[h], 0));
         GH_CUDA(cudaStreamWaitEvent(str, ev_zdone[b], 0));
         const int s_next = (s + 1) % nst;
         ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data());
@@ -861,10 +1173,12 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
           destroy_events();
           return e;
         }
-        GH_CUDA(cudaEventRecord(ev_fg[0], str));  // half 1 of step s+1 waits for the exchange
+        GH_CUDA(cudaEventRecord(ev_x, str));
+        if (hs_st[0] == str) GH_CUDA(cudaEventRecord(ev_fg[0], str));  // half 1 of step s+1 waits for it
       }
     }
-    if (nh == 2) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[1], 0));
+    for (int h = 0; h < nh; h++)
+      if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[h], 0));
     GH_CUDA(cudaStreamWaitEvent(str, ev_zdone[(nst - 1) & 1], 0));
     GH_CUDA(cudaEventRecord(ctx->ev3, str));
     DevCounters c;
@@ -884,13 +1198,32 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
                                : "blocked: non-finite value in a block pivot";
       return c.err == -7 ? GHSVD_E_RANK_DEFICIENT : c.err == -6 ? GHSVD_E_INDEFINITE_S : GHSVD_E_NONFINITE;
     }
+    if (sw == 0 && !trace_h.empty()) {
+      GH_CUDA(cudaMemcpy(trace_h.data(), S.trace_buf, trace_h.size() * 8, cudaMemcpyDeviceToHost));
+      if (FILE* f = fopen(trace_path, "w")) {
+        static const char* names[10] = {"gram0", "gram1", "factor0", "factor1", "pivot0",
+                                        "pivot1", "update0", "update1", "updateZ", "updateW"};
+        unsigned long long t0 = ~0ull;
+        for (size_t i = 0; i < trace_h.size(); i += 2) t0 = std::min(t0, trace_h[i]);
+        fprintf(f, "step,kernel,start_ns,end_ns\n");
+        for (int s = 0; s < nst; s++)
+          for (int k = 0; k < 10; k++) {
+            const unsigned long long b0 = trace_h[2 * ((size_t)s * TRACE_SLOTS + k)];
+            const unsigned long long b1 = trace_h[2 * ((size_t)s * TRACE_SLOTS + k) + 1];
+            if (b0 != ~0ull && b1 >= b0) fprintf(f, "%d,%s,%llu,%llu\n", s, names[k], b0 - t0, b1 - t0);
+          }
+        fclose(f);
+      }
+    }
     float kms = 0;
     GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
     st->kernel_seconds += kms * 1e-3;
-    st->launches += (uint64_t)(4 * nh + 1) * nst;
+    st->launches += (uint64_t)(3 * nh + (a.W ? 2 : 1)) * nst;
+    st->launches_update_fg += (uint64_t)nh * nst;
     for (int s = 0; s < nst; s++) {
       st->flops_gram += fl_gram[s];
       st->flops_update += fl_upd[s];
+      st->flops_update_fg += fl_upd_fg[s];
       if (timing) {
         for (int h = 0; h < nh; h++) {
           float t0 = 0, t1 = 0, t2 = 0;
@@ -900,6 +1233,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
           st->t_gram += t0 * 1e-3;
           st->t_pivot += t1 * 1e-3;
           st->t_update += t2 * 1e-3;
+          st->t_update_fg += t2 * 1e-3;
         }
       }
     }

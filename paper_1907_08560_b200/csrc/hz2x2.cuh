@@ -43,7 +43,10 @@ struct HZOut {
 };
 
 // g[8] = {hpp, hqq, hpq.re, hpq.im, spp, sqq, spq.re, spq.im}
-static __device__ __noinline__ HZOut hz2x2_dev(const double* g, double tol, int literal) {
+// hz2x2_core is the inlinable body (used where one warp evaluates many pairs);
+// hz2x2_dev is the same routine behind a call boundary (keeps register pressure of
+// the streaming kernels low).  Both execute the identical IEEE operation sequence.
+__device__ __forceinline__ HZOut hz2x2_core(const double* g, double tol, int literal) {
   HZOut o;
   o.z11 = Cplx{1.0, 0.0};
   o.z21 = Cplx{0.0, 0.0};
@@ -146,6 +149,10 @@ static __device__ __noinline__ HZOut hz2x2_dev(const double* g, double tol, int 
   return o;
 }
 
+static __device__ __noinline__ HZOut hz2x2_dev(const double* g, double tol, int literal) {
+  return hz2x2_core(g, tol, literal);
+}
+
 // Round-robin (circle) parallel ordering, reading C-11 of PAPER.md Sec 6.3:
 // step s in [0, n-2], slot k in [0, n/2-1]; returns p < q.
 __host__ __device__ __forceinline__ void rr_pair(long long n, long long s, long long k,
@@ -158,6 +165,23 @@ __host__ __device__ __forceinline__ void rr_pair(long long n, long long s, long 
     const long long r = n - 1;
     a = (s + k) % r;
     b = (s - k) % r;
+    if (b < 0) b += r;
+  }
+  *p = a < b ? a : b;
+  *q = a < b ? b : a;
+}
+
+// 32-bit form of rr_pair for the in-shared-memory inner sweeps (n <= 64).
+__device__ __forceinline__ void rr_pair32(int n, int s, int k, int* p, int* q) {
+  int a, b;
+  if (k == 0) {
+    a = n - 1;
+    b = s;
+  } else {
+    const int r = n - 1;
+    a = s + k;
+    if (a >= r) a -= r;
+    b = s - k;
     if (b < 0) b += r;
   }
   *p = a < b ? a : b;

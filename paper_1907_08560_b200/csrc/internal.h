@@ -32,6 +32,9 @@ struct Ctx {
   cudaStream_t cap_stream;    // private stream for graph capture
   cudaStream_t aux_stream;    // blocked: Z' updates overlapped with the next step
   cudaStream_t aux_stream2;   // blocked: second half of each step's block pairs
+  std::vector<cudaStream_t> grp_streams;  // blocked, one GPU: one stream per pair group
+  cudaStream_t hi_stream[2];  // blocked: high-priority streams of the latency-bound factor/pivot kernels
+  cudaStream_t mid_stream[2]; // blocked: medium-priority streams of the Gram / F,G-update kernels
   char* ws;
   size_t ws_bytes;
   Layout L;

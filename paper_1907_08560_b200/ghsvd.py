@@ -61,7 +61,9 @@ class Stats(ctypes.Structure):
                 ("t_update", ctypes.c_double), ("t_exchange", ctypes.c_double),
                 ("flops_gram", ctypes.c_double), ("flops_update", ctypes.c_double),
                 ("max_offdiag_last", ctypes.c_double),
-                ("all_per_sweep", ctypes.c_uint64 * 64), ("big_per_sweep", ctypes.c_uint64 * 64)]
+                ("all_per_sweep", ctypes.c_uint64 * 64), ("big_per_sweep", ctypes.c_uint64 * 64),
+                ("launches_update_fg", ctypes.c_uint64), ("flops_update_fg", ctypes.c_double),
+                ("t_update_fg", ctypes.c_double)]
 
     def todict(self):
         k = min(self.sweeps, 64)
@@ -73,6 +75,8 @@ class Stats(ctypes.Structure):
                 "t_gram": self.t_gram, "t_pivot": self.t_pivot, "t_update": self.t_update,
                 "t_exchange": self.t_exchange, "flops_gram": self.flops_gram,
                 "flops_update": self.flops_update,
+                "launches_update_fg": int(self.launches_update_fg),
+                "flops_update_fg": self.flops_update_fg, "t_update_fg": self.t_update_fg,
                 "max_offdiag_last": self.max_offdiag_last,
                 "all_per_sweep": [int(v) for v in self.all_per_sweep[:k]],
                 "big_per_sweep": [int(v) for v in self.big_per_sweep[:k]]}

@@ -1,6 +1,7 @@
 """Print per-launch durations from an ncu --metrics gpu__time_duration.sum --csv log.
 usage: python tools/launch_table.py gpurun_out/launches.csv [--sum]"""
 import collections
+import re
 import csv
 import sys
 
@@ -9,7 +10,7 @@ h = rows[0]
 ki, vi, gi, bi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Grid Size"), h.index("Block Size")
 agg = collections.OrderedDict()
 for r in rows[1:]:
-    name = r[ki].split("::")[-1].split("(")[0]
+    name = re.sub(r"<[^<>]*>$", "", re.sub(r"^void\s+", "", r[ki].replace("(anonymous namespace)", "<unnamed>").split("(")[0]).strip()).split("::")[-1]
     v = float(r[vi].replace(",", ""))
     if "--sum" in sys.argv:
         a = agg.setdefault(name, [0, 0.0])

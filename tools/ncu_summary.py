@@ -28,17 +28,17 @@ WANT = {
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_cycles_pct",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_cycles_pct",
-    "sm__inst_executed_pipe_tensor_op_dmma.avg.pct_of_peak_sustained_active": "dmma_pct",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_pct",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-9,
          "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
 
 
 def kname(s):
-    s = s.replace("(anonymous namespace)::", "")
-    s = re.sub(r"\(.*", "", s)
+    """'void ghsvd::<unnamed>::k_blk_update<false>(ghsvd::<unnamed>::BlkArgs, int)' -> 'k_blk_update'."""
+    s = s.replace("(anonymous namespace)", "<unnamed>").split("(")[0]
     s = re.sub(r"^void\s+", "", s)
-    s = re.sub(r"<.*", "", s)
+    s = re.sub(r"<[^<>]*>$", "", s.strip())
     return s.split("::")[-1]
 
 

@@ -210,6 +210,74 @@ __device__ __forceinline__ void gram_tiles(const double2* T, int row, double sg,
   }
 }
 
+// 3M variant (GHSVD_GRAM3M=1): warp 2g+h owns tiles [5h, 5h+5) ∩ [0, 9) of group g for
+// every k-step of a stage, so no cross-warp sum is needed; per k-step it loads the
+// fragments those tiles need and issues 3 DMMAs per tile: P1 = Ar Br, P2 = Ai Bi,
+// P3 = (Ar + Ai)(Br + Bi); Re = P1 - P2, Im = P3 - P1 - P2 (A = J conj(X)^T, B = X).
+template <int GI>
+struct G3 {
+  static constexpr int IA = GI, IB = 7 - GI;
+  static constexpr int row(int t) { return t <= IA ? IA : IB; }
+  static constexpr int col(int t) { return t <= IA ? t : t - IA - 1; }
+  static constexpr bool needB(int j, int t0, int t1) {
+    bool r = false;
+    for (int t = t0; t < t1; t++) r = r || col(t) == j;
+    return r;
+  }
+  static constexpr bool needA(int i, int t0, int t1) {
+    bool r = false;
+    for (int t = t0; t < t1; t++) r = r || row(t) == i;
+    return r;
+  }
+};
+
+template <int GI, int H>
+__device__ __forceinline__ void gram3_tiles(const double2* T, int row, double sg, double (&acc)[5][6]) {
+  using C = G3<GI>;
+  constexpr int T0 = H ? 5 : 0, T1 = H ? 9 : 5;
+  const int lane = threadIdx.x & 31;
+  double2 f[8];
+  double bs[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    if (C::needB(j, T0, T1) || C::needA(j, T0, T1)) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
+    if (C::needB(j, T0, T1)) bs[j] = f[j].x + f[j].y;
+  }
+  double ar[2] = {0, 0}, ai[2] = {0, 0}, as[2] = {0, 0};   // rows IA, IB
+  if (C::needA(C::IA, T0, T1)) {
+    ar[0] = sg * f[C::IA].x;
+    ai[0] = -(sg * f[C::IA].y);
+    as[0] = ar[0] + ai[0];
+  }
+  if (C::needA(C::IB, T0, T1)) {
+    ar[1] = sg * f[C::IB].x;
+    ai[1] = -(sg * f[C::IB].y);
+    as[1] = ar[1] + ai[1];
+  }
+#pragma unroll
+  for (int t = T0; t < T1; t++) {
+    const int r = C::row(t) == C::IA ? 0 : 1, J = C::col(t);
+    dmma(acc[t - T0][0], acc[t - T0][1], ar[r], f[J].x);
+    dmma(acc[t - T0][2], acc[t - T0][3], ai[r], f[J].y);
+    dmma(acc[t - T0][4], acc[t - T0][5], as[r], bs[J]);
+  }
+}
+
+template <int GI, int H>
+__device__ __forceinline__ void gram3_store(double2* out, const double (&acc)[5][6]) {
+  using C = G3<GI>;
+  constexpr int T0 = H ? 5 : 0, T1 = H ? 9 : 5;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int t = T0; t < T1; t++) {
+    const double* c = acc[t - T0];
+    const int i = 8 * C::row(t) + (lane >> 2), j = 8 * C::col(t) + 2 * (lane & 3);
+    out[i + (size_t)j * KM] = make_double2(c[0] - c[2], c[4] - c[0] - c[2]);
+    out[i + (size_t)(j + 1) * KM] = make_double2(c[1] - c[3], c[5] - c[1] - c[3]);
+  }
+}
+
+template <bool M3>
 __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
   trace_begin(a);
   extern __shared__ __align__(128) double2 gsm[];  // [GSTAGES][KM][GS]
@@ -221,9 +289,6 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
   const long long r_end = min(a.m, r_begin + a.split_rows);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gi = warp >> 1, kh = warp & 1;
-  double acc[9][4];
-#pragma unroll
-  for (int t = 0; t < 9; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
   auto load_stage = [&](int st, long long r0) {
     if (r0 < r_end) {
       double2* T = gsm + (size_t)st * KM * GS;
@@ -237,52 +302,96 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
     }
     cp_commit();   // possibly empty: keeps one group per stage
   };
+  // GSTAGES-deep cp.async pipeline over the split's 32-row stages; consume(T, r0).
+  // One barrier per stage: after it every warp has finished the previous stage, whose
+  // buffer is then refilled with the stage GSTAGES-1 ahead.
+  auto pipeline = [&](auto&& consume) {
 #pragma unroll
-  for (int p = 0; p < GSTAGES - 1; p++) load_stage(p, r_begin + (long long)p * RT);
-  int st = 0;
-  for (long long r0 = r_begin; r0 < r_end; r0 += RT) {
-    load_stage((st + GSTAGES - 1) % GSTAGES, r0 + (long long)(GSTAGES - 1) * RT);
-    cp_wait<GSTAGES - 1>();
+    for (int p = 0; p < GSTAGES - 1; p++) load_stage(p, r_begin + (long long)p * RT);
+    int st = 0;
+    for (long long r0 = r_begin; r0 < r_end; r0 += RT) {
+      cp_wait<GSTAGES - 2>();
+      __syncthreads();
+      load_stage((st + GSTAGES - 1) % GSTAGES, r0 + (long long)(GSTAGES - 1) * RT);
+      consume(gsm + (size_t)st * KM * GS, r0);
+      st = (st + 1) % GSTAGES;
+    }
+    cp_wait<0>();
     __syncthreads();
-    const double2* T = gsm + (size_t)st * KM * GS;
+  };
+  double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
+  if constexpr (M3) {
+    double acc[5][6];
 #pragma unroll
-    for (int ks = 0; ks < RT / 4; ks += 2) {
-      const int row = 4 * (ks + kh) + (lane & 3);
-      const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
-      switch (gi) {   // warp-uniform
-        case 0: gram_tiles<0>(T, row, sg, acc); break;
-        case 1: gram_tiles<1>(T, row, sg, acc); break;
-        case 2: gram_tiles<2>(T, row, sg, acc); break;
-        default: gram_tiles<3>(T, row, sg, acc); break;
+    for (int t = 0; t < 5; t++)
+#pragma unroll
+      for (int c = 0; c < 6; c++) acc[t][c] = 0.0;
+    pipeline([&](const double2* T, long long r0) {
+#pragma unroll
+      for (int ks = 0; ks < RT / 4; ks++) {
+        const int row = 4 * ks + (lane & 3);
+        const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
+        switch (warp) {   // warp-uniform
+          case 0: gram3_tiles<0, 0>(T, row, sg, acc); break;
+          case 1: gram3_tiles<0, 1>(T, row, sg, acc); break;
+          case 2: gram3_tiles<1, 0>(T, row, sg, acc); break;
+          case 3: gram3_tiles<1, 1>(T, row, sg, acc); break;
+          case 4: gram3_tiles<2, 0>(T, row, sg, acc); break;
+          case 5: gram3_tiles<2, 1>(T, row, sg, acc); break;
+          case 6: gram3_tiles<3, 0>(T, row, sg, acc); break;
+          default: gram3_tiles<3, 1>(T, row, sg, acc); break;
+        }
       }
+    });
+    switch (warp) {
+      case 0: gram3_store<0, 0>(out, acc); break;
+      case 1: gram3_store<0, 1>(out, acc); break;
+      case 2: gram3_store<1, 0>(out, acc); break;
+      case 3: gram3_store<1, 1>(out, acc); break;
+      case 4: gram3_store<2, 0>(out, acc); break;
+      case 5: gram3_store<2, 1>(out, acc); break;
+      case 6: gram3_store<3, 0>(out, acc); break;
+      default: gram3_store<3, 1>(out, acc); break;
+    }
+  } else {
+    double acc[9][4];
+#pragma unroll
+    for (int t = 0; t < 9; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
+    pipeline([&](const double2* T, long long r0) {
+#pragma unroll
+      for (int ks = 0; ks < RT / 4; ks += 2) {
+        const int row = 4 * (ks + kh) + (lane & 3);
+        const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
+        switch (gi) {   // warp-uniform
+          case 0: gram_tiles<0>(T, row, sg, acc); break;
+          case 1: gram_tiles<1>(T, row, sg, acc); break;
+          case 2: gram_tiles<2>(T, row, sg, acc); break;
+          default: gram_tiles<3>(T, row, sg, acc); break;
+        }
+      }
+    });
+    // sum the two k-halves: odd warp -> smem -> even warp (fixed order)
+    double* red = reinterpret_cast<double*>(gsm);
+    if (kh) {
+#pragma unroll
+      for (int t = 0; t < 9; t++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) red[((gi * 9 + t) * 4 + c) * 32 + lane] = acc[t][c];
     }
     __syncthreads();
-    st = (st + 1) % GSTAGES;
-  }
-  cp_wait<0>();
-  __syncthreads();
-  // sum the two k-halves: odd warp -> smem -> even warp (fixed order)
-  double* red = reinterpret_cast<double*>(gsm);
-  if (kh) {
+    if (!kh) {
 #pragma unroll
-    for (int t = 0; t < 9; t++)
+      for (int t = 0; t < 9; t++)
 #pragma unroll
-      for (int c = 0; c < 4; c++) red[((gi * 9 + t) * 4 + c) * 32 + lane] = acc[t][c];
-  }
-  __syncthreads();
-  if (!kh) {
+        for (int c = 0; c < 4; c++) acc[t][c] += red[((gi * 9 + t) * 4 + c) * 32 + lane];
 #pragma unroll
-    for (int t = 0; t < 9; t++)
-#pragma unroll
-      for (int c = 0; c < 4; c++) acc[t][c] += red[((gi * 9 + t) * 4 + c) * 32 + lane];
-    double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
-#pragma unroll
-    for (int t = 0; t < 9; t++) {
-      const int I = t <= gi ? gi : 7 - gi;
-      const int J = t <= gi ? t : t - gi - 1;
-      const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
-      out[i + (size_t)j * KM] = make_double2(acc[t][0], acc[t][2]);
-      out[i + (size_t)(j + 1) * KM] = make_double2(acc[t][1], acc[t][3]);
+      for (int t = 0; t < 9; t++) {
+        const int I = t <= gi ? gi : 7 - gi;
+        const int J = t <= gi ? t : t - gi - 1;
+        const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
+        out[i + (size_t)j * KM] = make_double2(acc[t][0], acc[t][2]);
+        out[i + (size_t)(j + 1) * KM] = make_double2(acc[t][1], acc[t][3]);
+      }
     }
   }
   // The last CTA of this (pair, H|S) to finish factorizes the summed Gram right away
@@ -623,25 +732,24 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
         }
       }
     }
-    __syncthreads();
+    // accumulators -> global (each 8-lane group writes 8 consecutive rows of a column);
+    // every warp has read the whole tile and the tile's rows of these columns belong to
+    // this CTA alone, so no barrier is needed before the in-place stores
+    const long long row = r0 + 8 * I + (lane >> 2);
+    if (row < rows) {
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
-      const int i = 8 * I + (lane >> 2), j = 8 * (J0 + t) + 2 * (lane & 3);
-      if (M4) {
-        Xt[j * US + i] = make_double2(p1[t][0] - p2[t][0], p3[t][0]);
-        Xt[(j + 1) * US + i] = make_double2(p1[t][1] - p2[t][1], p3[t][1]);
-      } else {
-        Xt[j * US + i] = make_double2(p1[t][0] - p2[t][0], p3[t][0] - p1[t][0] - p2[t][0]);
-        Xt[(j + 1) * US + i] = make_double2(p1[t][1] - p2[t][1], p3[t][1] - p1[t][1] - p2[t][1]);
+      for (int t = 0; t < 4; t++) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int j = 8 * (J0 + t) + 2 * (lane & 3) + h;
+          const long long gc = gcol(j, c0p, wp, c0q, wq);
+          if (gc < 0) continue;
+          X[gc * ld + row] = M4 ? make_double2(p1[t][h] - p2[t][h], p3[t][h])
+                                : make_double2(p1[t][h] - p2[t][h], p3[t][h] - p1[t][h] - p2[t][h]);
+        }
       }
     }
-    __syncthreads();
-    for (int e = tid; e < KM * RT; e += NT_U) {
-      const int c = e / RT, r = e % RT;
-      const long long gc = gcol(c, c0p, wp, c0q, wq);
-      if (gc >= 0 && r0 + r < rows) X[gc * ld + r0 + r] = Xt[c * US + r];
-    }
-    __syncthreads();
+    __syncthreads();   // tile buffer reusable (tpc > 1)
   }
   trace_end(a);
 }
@@ -737,7 +845,7 @@ struct BlkSetup {
   std::vector<int> bs_h, bw_h;
   size_t smem_g, smem_p, smem_u;
   int tF, tZ, sms;
-  bool upd4m;
+  bool upd4m, gram3m;
   unsigned long long* trace_buf;
 };
 
@@ -813,7 +921,9 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   S.smem_g = (size_t)GSTAGES * KM * GS * 16;
   S.smem_p = (size_t)3 * KM * KM * 16;
   S.smem_u = (size_t)(KM * US + KM * ZS) * 16;
-  GH_CUDA(cudaFuncSetAttribute(k_blk_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
+  S.gram3m = env_int("GHSVD_GRAM3M", 1) != 0;
   GH_CUDA(cudaFuncSetAttribute(k_blk_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_p));
   GH_CUDA(cudaFuncSetAttribute(k_blk_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_u));
   GH_CUDA(cudaFuncSetAttribute(k_blk_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_u));
@@ -826,6 +936,14 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&S.sms, cudaDevAttrMultiProcessorCount, dev);
   }
   return GHSVD_OK;
+}
+
+// Gram launch over pairs [a.pair0, a.pair0 + np): grid (row split, H|S, pair).
+static void launch_gram(const BlkSetup& S, const BlkArgs& a, int np, cudaStream_t st) {
+  if (S.gram3m)
+    k_blk_gram<true><<<dim3(S.pl.nsplit, 2, np), NT_G, S.smem_g, st>>>(a);
+  else
+    k_blk_gram<false><<<dim3(S.pl.nsplit, 2, np), NT_G, S.smem_g, st>>>(a);
 }
 
 // Update launch: pairs [pair0, pair0 + np), row tiles [tbeg, tend) (see k_blk_update).
@@ -856,7 +974,7 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
   BlkArgs a = S.a;
   for (int64_t s = s0; s < s0 + ns; s++) {
     a.s = (int)s;
-    k_blk_gram<<<dim3(S.pl.nsplit, 2, S.pl.K), NT_G, S.smem_g, str>>>(a);
+    launch_gram(S, a, S.pl.K, str);
     k_blk_pivot<<<S.pl.K, NT_P, S.smem_p, str>>>(a);
     launch_update(S, a, 0, S.pl.K, 0, 2 * S.tF + S.tZ, 0, str);
     if (a.W) launch_update(S, a, 0, S.pl.K, 0, S.tZ, 1, str);
@@ -881,7 +999,7 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
 static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int G) {
   BlkPlan& pl = S.pl;
   BlkArgs a = S.a;
-  const size_t smem_g = S.smem_g, smem_p = S.smem_p;
+  const size_t smem_p = S.smem_p;
   const int tF = S.tF, tZ = S.tZ;
   cudaStream_t str = ctx->stream;
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
@@ -934,7 +1052,7 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
         a.pair0 = g0[g];
         cudaEvent_t* te = timing ? &tev[((size_t)s * G + g) * 4] : nullptr;
         if (te) GH_CUDA(cudaEventRecord(te[0], sh));
-        k_blk_gram<<<dim3(pl.nsplit, 2, np), NT_G, smem_g, sh>>>(a);
+        launch_gram(S, a, np, sh);
         if (te) GH_CUDA(cudaEventRecord(te[1], sh));
         k_blk_pivot<<<np, NT_P, smem_p, sh>>>(a);
         if (te) GH_CUDA(cudaEventRecord(te[2], sh));
@@ -1021,7 +1139,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   BlkArgs a = S.a;
   const std::vector<int>& bs_h = S.bs_h;
   const std::vector<int>& bw_h = S.bw_h;
-  const size_t smem_g = S.smem_g, smem_p = S.smem_p;
+  const size_t smem_p = S.smem_p;
   const int tF = S.tF, tZ = S.tZ;
   cudaStream_t str = ctx->stream;
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
@@ -1134,7 +1252,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         a.pair0 = h_pair0[h];
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 0], sh));
         a.trace_id = s * TRACE_SLOTS + 0 + h;
-        k_blk_gram<<<dim3(pl.nsplit, 2, h_np[h]), NT_G, smem_g, sh>>>(a);
+        launch_gram(S, a, h_np[h], sh);
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 1], sh));
         cudaStream_t fs = fp_st[h];
         if (fs != sh) {

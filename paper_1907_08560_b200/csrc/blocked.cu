@@ -59,6 +59,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_wait_dyn(int n) {   // n in [0, 3]
+  switch (n) {
+    case 0: cp_wait<0>(); break;
+    case 1: cp_wait<1>(); break;
+    case 2: cp_wait<2>(); break;
+    default: cp_wait<3>(); break;
+  }
+}
 
 struct BlkArgs {
   double2* F;
@@ -327,7 +335,9 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
 #pragma unroll
       for (int c = 0; c < 6; c++) acc[t][c] = 0.0;
     pipeline([&](const double2* T, long long r0) {
-#pragma unroll
+      // not unrolled: the 8 warp-specialized tile sets are already 8 code paths, and
+      // unrolling them 8x overflowed the instruction cache (ncu: 22 % no_inst stalls)
+#pragma unroll 1
       for (int ks = 0; ks < RT / 4; ks++) {
         const int row = 4 * ks + (lane & 3);
         const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
@@ -358,7 +368,7 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
 #pragma unroll
     for (int t = 0; t < 9; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
     pipeline([&](const double2* T, long long r0) {
-#pragma unroll
+#pragma unroll 1
       for (int ks = 0; ks < RT / 4; ks += 2) {
         const int row = 4 * (ks + kh) + (lane & 3);
         const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
@@ -677,38 +687,41 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
   double2* Xt = usm;
   double2* Zb = usm + KM * US;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // Z_blk loaded once per CTA and reused for its tpc row tiles
   const double2* zsrc = (wmode ? a.zinvT : a.zblk) + (size_t)pl * (KM * KM);
-  for (int e = tid; e < KM * KM; e += NT_U) {
-    const int i = e % KM, j = e / KM;
-    cp_async16(&Zb[j * ZS + i], zsrc + e, i < k && j < k);
-  }
   const int I = warp & 3;          // row tile of 8 rows within the 32-row tile
   const int J0 = (warp >> 2) * 4;  // first of 4 column tiles
   const int kend = (k + 3) & ~3;
-  for (int tt = 0; tt < tpc; tt++) {
-    const int tile = tile0 + blockIdx.y * tpc + tt;
-    if (tile >= tile_end) break;
-    double2* X;
-    long long ld, rows, r0;
-    if (wmode) {
-      X = a.W; ld = a.ldn; rows = a.n; r0 = (long long)(tile - tile0) * RT;
-    } else if (tile < tF) {
-      X = a.F; ld = a.ldm; rows = a.m; r0 = (long long)tile * RT;
-    } else if (tile < 2 * tF) {
-      X = a.G; ld = a.ldm; rows = a.m; r0 = (long long)(tile - tF) * RT;
-    } else {
-      X = a.Z; ld = a.ldn; rows = a.n; r0 = (long long)(tile - 2 * tF) * RT;
+  const int tile = tile0 + blockIdx.y;
+  double2* X;
+  long long ld, rows, r0;
+  if (wmode) {
+    X = a.W; ld = a.ldn; rows = a.n; r0 = (long long)(tile - tile0) * RT;
+  } else if (tile < tF) {
+    X = a.F; ld = a.ldm; rows = a.m; r0 = (long long)tile * RT;
+  } else if (tile < 2 * tF) {
+    X = a.G; ld = a.ldm; rows = a.m; r0 = (long long)(tile - tF) * RT;
+  } else {
+    X = a.Z; ld = a.ldn; rows = a.n; r0 = (long long)(tile - 2 * tF) * RT;
+  }
+  // Loads in NPH phases (tile columns and Z_blk rows [ph*KPH, +KPH) per cp.async group)
+  // would let the DMMAs over the first k-range start early; measured on config 3:
+  // NPH = 1: 1472 us, 2: 1488 us, 4: 1528 us per full-step launch, so one phase.
+  constexpr int NPH = 1, KPH = KM / NPH;
+#pragma unroll
+  for (int ph = 0; ph < NPH; ph++) {
+    for (int e = tid; e < KPH * KM; e += NT_U) {
+      const int i = ph * KPH + e % KPH, j = e / KPH;
+      cp_async16(&Zb[j * ZS + i], zsrc + i + (size_t)j * KM, i < k && j < k);
     }
-    for (int e = tid; e < KM * RT; e += NT_U) {
-      const int c = e / RT, r = e % RT;
+    for (int e = tid; e < KPH * RT; e += NT_U) {
+      const int c = ph * KPH + e / RT, r = e % RT;
       const long long gc = gcol(c, c0p, wp, c0q, wq);
       const bool ok = gc >= 0 && r0 + r < rows;
       cp_async16(&Xt[c * US + r], ok ? (const void*)(X + gc * ld + r0 + r) : (const void*)X, ok);
     }
     cp_commit();
-    cp_wait<0>();
-    __syncthreads();
+  }
+  {
     // out (RT x KM) = Xt (RT x KM) Z_blk (KM x KM): 4 x 8 tiles of 8x8, 4 per warp.
     // Complex product by the 3M (Gauss) scheme on DMMA: P1 = Xr Zr, P2 = Xi Zi,
     // P3 = (Xr + Xi)(Zr + Zi); out = (P1 - P2) + i (P3 - P1 - P2): 3 real DMMAs per
@@ -716,7 +729,11 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
     double p1[4][2], p2[4][2], p3[4][2];
 #pragma unroll
     for (int t = 0; t < 4; t++) p1[t][0] = p1[t][1] = p2[t][0] = p2[t][1] = p3[t][0] = p3[t][1] = 0.0;
-    for (int kk = 0; kk < kend; kk += 4) {
+#pragma unroll
+    for (int ph = 0; ph < NPH; ph++) {
+      cp_wait_dyn(NPH - 1 - ph);   // every phase is waited for, even past kend
+      __syncthreads();
+      for (int kk = ph * KPH; kk < min(kend, (ph + 1) * KPH); kk += 4) {
       const double2 x = Xt[(kk + (lane & 3)) * US + 8 * I + (lane >> 2)];  // A(i, k)
       const double xs = x.x + x.y;
 #pragma unroll
@@ -731,6 +748,7 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
           dmma(p3[t][0], p3[t][1], xs, z.x + z.y);
         }
       }
+    }
     }
     // accumulators -> global (each 8-lane group writes 8 consecutive rows of a column);
     // every warp has read the whole tile and the tile's rows of these columns belong to
@@ -749,7 +767,6 @@ __global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile
         }
       }
     }
-    __syncthreads();   // tile buffer reusable (tpc > 1)
   }
   trace_end(a);
 }

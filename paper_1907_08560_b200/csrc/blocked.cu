@@ -818,7 +818,10 @@ BlkPlan make_plan(const Ctx* ctx) {
   // given (m, K, device) since the sum of the split partials has a fixed order.
   int dev = 0, sms = 148, per_sm = 2;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long M = 2LL * (p.K >= 2 ? p.K / 2 : p.K);
+  // M from the GLOBAL pair count, so the split (and the partial-sum order) is the same
+  // for every world size: a P-GPU run stays bitwise equal to the 1-GPU run
+  const long long Kg = p.nblk / 2;
+  const long long M = 2LL * (Kg >= 2 ? Kg / 2 : Kg);
   const long long R = (long long)sms * per_sm;
   long long best = -1;
   double best_cost = 0.0;

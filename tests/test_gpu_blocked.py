@@ -98,3 +98,52 @@ def test_nccl_path_single_rank_bitwise(gh):
     ctx.close()
     assert st["sweeps"] == ref[3]["sweeps"]
     assert np.array_equal(lam, ref[4]) and np.array_equal(Z, ref[5])
+
+
+def _run_env(gh, monkeypatch, P, env, nblocks=8):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    try:
+        return run_gpu(gh, P, "bo", nblocks)
+    finally:
+        for k in env:
+            monkeypatch.delenv(k, raising=False)
+
+
+def test_schedules_bitwise(gh, monkeypatch):
+    """The step schedules (two halves with stream priorities: default; without priorities;
+    pipelined pair groups) run identical per-pair arithmetic, so lambda and Z must agree
+    bitwise (blocked scheduling)."""
+    P = inputs.known_hyperbolic(17, 192, 160, 0.5)
+    ref = _run_env(gh, monkeypatch, P, {}, nblocks=10)
+    for env in ({"GHSVD_PRIO": "0"}, {"GHSVD_GROUPS": "2"}, {"GHSVD_GROUPS": "5"}):
+        r = _run_env(gh, monkeypatch, P, env, nblocks=10)
+        assert r[3]["sweeps"] == ref[3]["sweeps"], env
+        assert np.array_equal(r[4], ref[4]) and np.array_equal(r[5], ref[5]), env
+
+
+@pytest.mark.parametrize("env", [{"GHSVD_GRAM3M": "0"}, {"GHSVD_UPD4M": "1"}])
+def test_product_variants_match_oracle(gh, monkeypatch, env):
+    """Exact 4M block Grams / exact 4M updates (the default uses the 3M scheme for both)
+    reach the same eigenvalues as the oracle (1e-9) and the known spectrum."""
+    P = inputs.known_hyperbolic(14, 96, 64, 0.4)
+    F0, J0, G0, st, lam, Z = _run_env(gh, monkeypatch, P, env, nblocks=4)
+    Fo, Go, Zp, sto = oracle.hz_blocked(F0, J0, G0, 4, inner_sweeps=1)
+    lo, *_ = oracle.extract(Fo, J0, Go, Zp)
+    assert st["converged"] and abs(st["sweeps"] - sto["sweeps"]) <= 1
+    assert relerr(lam, lo) <= 1e-9 and relerr(lam, P.lam_true) <= 1e-9
+
+
+def test_trace_csv(gh, monkeypatch, tmp_path):
+    """GHSVD_TRACE writes the first sweep's launch timeline: every block step has its
+    Gram, pivot and update launches with end >= start."""
+    import csv
+    path = tmp_path / "trace.csv"
+    P = inputs.known_hyperbolic(18, 160, 128, 0.5)
+    _run_env(gh, monkeypatch, P, {"GHSVD_TRACE": str(path)}, nblocks=8)
+    rows = list(csv.DictReader(open(path)))
+    steps = {int(r["step"]) for r in rows}
+    assert steps == set(range(7))
+    kinds = {r["kernel"] for r in rows}
+    assert {"gram0", "gram1", "pivot0", "pivot1", "update0", "update1", "updateZ"} <= kinds
+    assert all(int(r["end_ns"]) >= int(r["start_ns"]) for r in rows)

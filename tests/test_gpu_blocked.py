@@ -147,3 +147,22 @@ def test_trace_csv(gh, monkeypatch, tmp_path):
     kinds = {r["kernel"] for r in rows}
     assert {"gram0", "gram1", "pivot0", "pivot1", "update0", "update1", "updateZ"} <= kinds
     assert all(int(r["end_ns"]) >= int(r["start_ns"]) for r in rows)
+
+
+@pytest.mark.parametrize("m,n", [(4, 2), (5, 3), (6, 4), (9, 5), (40, 7)])
+@pytest.mark.parametrize("variant", ["pointwise", "bo"])
+def test_tiny_pencils_match_oracle(gh, m, n, variant):
+    """Degenerate sizes: a single pivot pair (n = 2), odd n (bordering, C-10), block
+    widths of 1-2 columns; eigenvalues vs the oracle's pointwise sweep and residuals."""
+    P = inputs.random_pencil(300 + 10 * m + n, m, n, 0.5)
+    ctx = gh.Context(m, n, variant=variant)
+    ctx.set_factors(P.F, P.J, P.G)
+    F0, J0, G0, _ = ctx.get_factors()
+    st = ctx.sweep()
+    lam, sf, sg, Z = ctx.extract()
+    ctx.close()
+    Fo, Go, Zp, sto = oracle.hz_pointwise(F0, J0, G0)
+    lo, *_ = oracle.extract(Fo, J0, Go, Zp)
+    assert st["converged"]
+    assert relerr(lam, lo[:n]) <= 1e-9
+    assert residual(P.F, P.J, P.G, lam, Z) <= 1e-12 * max(n, 8)

@@ -485,6 +485,19 @@ __device__ __forceinline__ void st2(double2* p, const C2& v) {
                "l"(__double_as_longlong(v.a.y)), "l"(__double_as_longlong(v.b.x)), "l"(__double_as_longlong(v.b.y))
                : "memory");
 }
+// 32-B store whose L2 lines are marked evict-first, so the written-back rotated rows do
+// not displace the evict-last rows other pairs still have to re-read in pass 2
+__device__ __forceinline__ void st2_ef(double2* p, const C2& v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+               "l"(__double_as_longlong(v.a.x)), "l"(__double_as_longlong(v.a.y)), "l"(__double_as_longlong(v.b.x)),
+               "l"(__double_as_longlong(v.b.y)), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void gram_row(double* acc, const double2& fp, const double2& fq, const double2& gp,
                                          const double2& gq, double sgn) {
   acc[0] = fma(sgn, fma(fp.x, fp.x, fp.y * fp.y), acc[0]);
@@ -576,14 +589,18 @@ __global__ void __launch_bounds__(NT) k_pair_step_2p(StepArgs a) {
   const int kind = kind_sh;
   if (kind == KIND_SMALL || kind == KIND_BIG) {
     const Cplx z11{zsh[0], zsh[1]}, z21{zsh[2], zsh[3]}, z12{zsh[4], zsh[5]}, z22{zsh[6], zsh[7]};
+    // pass 2 walks the rows in reverse: the most recently loaded (most likely still in
+    // L2) first; stores are marked evict-first
+    const unsigned long long pol = policy_evict_first();
+    const long long hl = h0 + tid + ((h1 - 1 - h0 - tid) / NT) * NT;   // this thread's last row pair
 #pragma unroll 2
-    for (long long h = h0 + tid; h < h1; h += NT) {
+    for (long long h = hl; h >= h0 + tid && h < h1; h -= NT) {
       C2 fp = ld2_last(Fp + 2 * h), fq = ld2_last(Fq + 2 * h), gp = ld2_last(Gp + 2 * h), gq = ld2_last(Gq + 2 * h);
       rot_row(fp.a, fq.a, z11, z21, z12, z22);
       rot_row(fp.b, fq.b, z11, z21, z12, z22);
       rot_row(gp.a, gq.a, z11, z21, z12, z22);
       rot_row(gp.b, gq.b, z11, z21, z12, z22);
-      st2(Fp + 2 * h, fp); st2(Fq + 2 * h, fq); st2(Gp + 2 * h, gp); st2(Gq + 2 * h, gq);
+      st2_ef(Fp + 2 * h, fp, pol); st2_ef(Fq + 2 * h, fq, pol); st2_ef(Gp + 2 * h, gp, pol); st2_ef(Gq + 2 * h, gq, pol);
     }
     double2* Zp = a.Z + p * a.ldn;
     double2* Zq = a.Z + q * a.ldn;

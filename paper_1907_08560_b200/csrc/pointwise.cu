@@ -682,7 +682,12 @@ ghsvd_status pw_configure(Ctx* ctx) {
   }
   const int nbuf = kk == 3 ? 8 : (kk == 1 ? 4 : 0);   // F/G slice buffers (x cs) per CTA
   int C = ctx->o.cluster;
-  if (C <= 0) {
+  if (C <= 0 && kk == 2) {
+    // two-pass kernel: measured on config 3 (m = 10368, tools/profile_step.py, ms per
+    // step): C=1/T=256 0.739, C=2/T=128 0.714, C=4/T=128 0.672, C=8/T=128 0.696; small
+    // m (the pair's columns fit in L2 anyway) keeps one CTA per pair
+    C = m >= 4096 ? 4 : 1;
+  } else if (C <= 0) {
     // smallest power-of-two cluster whose per-CTA slices fit the smem budget
     const int64_t budget = pipe ? 200 * 1024 : 100 * 1024;
     C = 1;
@@ -698,7 +703,9 @@ ghsvd_status pw_configure(Ctx* ctx) {
   }
   const int64_t cs = round_up((m + C - 1) / C, 2), zs = (n + C - 1) / C;
   int T = ctx->o.threads;
-  if (T <= 0) {
+  if (T <= 0 && kk == 2 && m >= 4096) {
+    T = 128;
+  } else if (T <= 0) {
     T = 256;
     while (T > 32 && T / 2 >= cs) T /= 2;
   }

@@ -1178,7 +1178,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   //   highest  factor / pivot (latency-bound): their CTAs are placed as soon as a Gram
   //            or update CTA retires, so a half's block pivots start right after its
   //            own Grams instead of queueing behind the other half's Gram CTAs;
-  //   medium   Gram and F, G update of each half (half 0 one level above half 1);
+  //   medium   Gram and F, G update of both halves;
   //   lowest   the Z' update (aux): it has a whole step of slack and fills the SMs the
   //            latency-bound kernels leave idle.
   const bool prio = env_int("GHSVD_PRIO", 1) != 0;
@@ -1188,9 +1188,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     int lo = 0, hi = 0;
     GH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     for (int i = 0; i < 2; i++) {
-      // half 0 above half 1: its Grams finish first, so its block pivots overlap the
-      // Grams of half 1 and its update is ready when they end
-      const int mid = std::min(lo, hi + 1 + i);
+      // both halves at the same level (ranking half 0 above half 1 measured 2 % slower:
+      // with the split boundary-pair updates the halves drift half a step apart and the
+      // lower one starves)
+      const int mid = std::min(lo, hi + 1);
       if (!ctx->hi_stream[i]) GH_CUDA(cudaStreamCreateWithPriority(&ctx->hi_stream[i], cudaStreamNonBlocking, hi));
       if (!ctx->mid_stream[i])
         GH_CUDA(cudaStreamCreateWithPriority(&ctx->mid_stream[i], cudaStreamNonBlocking, mid));
@@ -1203,11 +1204,16 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   }
   const int h_pair0[2] = {0, KA}, h_np[2] = {KA, pl.K - KA};
   const int nst = pl.nblk - 1;
-  std::vector<cudaEvent_t> ev_piv(2), ev_fg(2), ev_zdone(2), ev_gr(2), tev;
+  std::vector<cudaEvent_t> ev_piv(2), ev_fg(2), ev_zdone(2), ev_gr(2), ev_bnd(2), tev;
+  // one GPU, halves of >= 2 pairs: split each half's F/G update into its boundary pair
+  // and the rest (GHSVD_SPLIT_BND=0 disables), so half 0 of step s+1 starts while half 1
+  // of step s still updates
+  const bool split_bnd = !multi && nh == 2 && KA >= 2 && pl.K - KA >= 2 && env_int("GHSVD_SPLIT_BND", 1) != 0;
   cudaEvent_t ev_x;
   GH_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
   for (int i = 0; i < 2; i++) {
     GH_CUDA(cudaEventCreateWithFlags(&ev_gr[i], cudaEventDisableTiming));
+    GH_CUDA(cudaEventCreateWithFlags(&ev_bnd[i], cudaEventDisableTiming));
     GH_CUDA(cudaEventCreateWithFlags(&ev_piv[i], cudaEventDisableTiming));
     GH_CUDA(cudaEventCreateWithFlags(&ev_fg[i], cudaEventDisableTiming));
     GH_CUDA(cudaEventCreateWithFlags(&ev_zdone[i], cudaEventDisableTiming));
@@ -1221,6 +1227,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     for (auto e : ev_fg) cudaEventDestroy(e);
     for (auto e : ev_zdone) cudaEventDestroy(e);
     for (auto e : ev_gr) cudaEventDestroy(e);
+    for (auto e : ev_bnd) cudaEventDestroy(e);
     for (auto e : tev) cudaEventDestroy(e);
     cudaEventDestroy(ev_x);
   };
@@ -1258,10 +1265,12 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       a.zblk = zblk0 + (size_t)b * pl.K * KM * KM;
       if (zinv0) a.zinvT = zinv0 + (size_t)b * pl.K * KM * KM;
       a.applied = applied0 + (size_t)b * pl.K;
-      // the Grams of step s read block columns updated by both halves in step s-1
+      // The Grams of step s read block columns updated in step s-1 by their own half and,
+      // through the round-robin neighbour structure (slot k of step s holds the block
+      // columns of slots k-1 and k+1 of step s-1), by the other half's boundary pair only.
       if (nh == 2 && s > 0) {
-        GH_CUDA(cudaStreamWaitEvent(hs_st[0], ev_fg[1], 0));
-        GH_CUDA(cudaStreamWaitEvent(hs_st[1], ev_fg[0], 0));
+        GH_CUDA(cudaStreamWaitEvent(hs_st[0], split_bnd ? ev_bnd[1] : ev_fg[1], 0));
+        GH_CUDA(cudaStreamWaitEvent(hs_st[1], split_bnd ? ev_bnd[0] : ev_fg[0], 0));
       }
       // multi-GPU: the exchange after step s-1 (on str) precedes every Gram of step s
       if (multi && s > 0)
@@ -1287,7 +1296,17 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         if (fs != sh) GH_CUDA(cudaStreamWaitEvent(sh, ev_piv[h], 0));
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
         a.trace_id = s * TRACE_SLOTS + 6 + h;
-        launch_update(S, a, h_pair0[h], h_np[h], 0, 2 * tF, 0, sh);
+        if (split_bnd) {
+          // boundary pair first (the only pair of this half the other half's next-step
+          // Grams read, by the round-robin neighbour structure), then the rest
+          const int bp = h == 0 ? h_pair0[0] + h_np[0] - 1 : h_pair0[1];
+          launch_update(S, a, bp, 1, 0, 2 * tF, 0, sh);
+          GH_CUDA(cudaEventRecord(ev_bnd[h], sh));
+          a.trace_id = s * TRACE_SLOTS + 10 + h;
+          launch_update(S, a, h == 0 ? h_pair0[0] : h_pair0[1] + 1, h_np[h] - 1, 0, 2 * tF, 0, sh);
+        } else {
+          launch_update(S, a, h_pair0[h], h_np[h], 0, 2 * tF, 0, sh);
+        }
         if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 3], sh));
         GH_CUDA(cudaEventRecord(ev_fg[h], sh));
       }
@@ -1339,13 +1358,13 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     if (sw == 0 && !trace_h.empty()) {
       GH_CUDA(cudaMemcpy(trace_h.data(), S.trace_buf, trace_h.size() * 8, cudaMemcpyDeviceToHost));
       if (FILE* f = fopen(trace_path, "w")) {
-        static const char* names[10] = {"gram0", "gram1", "factor0", "factor1", "pivot0",
-                                        "pivot1", "update0", "update1", "updateZ", "updateW"};
+        static const char* names[12] = {"gram0", "gram1", "factor0", "factor1", "pivot0", "pivot1",
+                                        "update0", "update1", "updateZ", "updateW", "update0b", "update1b"};
         unsigned long long t0 = ~0ull;
         for (size_t i = 0; i < trace_h.size(); i += 2) t0 = std::min(t0, trace_h[i]);
         fprintf(f, "step,kernel,start_ns,end_ns\n");
         for (int s = 0; s < nst; s++)
-          for (int k = 0; k < 10; k++) {
+          for (int k = 0; k < 12; k++) {
             const unsigned long long b0 = trace_h[2 * ((size_t)s * TRACE_SLOTS + k)];
             const unsigned long long b1 = trace_h[2 * ((size_t)s * TRACE_SLOTS + k) + 1];
             if (b0 != ~0ull && b1 >= b0) fprintf(f, "%d,%s,%llu,%llu\n", s, names[k], b0 - t0, b1 - t0);
@@ -1356,8 +1375,8 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     float kms = 0;
     GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
     st->kernel_seconds += kms * 1e-3;
-    st->launches += (uint64_t)(3 * nh + (a.W ? 2 : 1)) * nst;
-    st->launches_update_fg += (uint64_t)nh * nst;
+    st->launches += (uint64_t)(3 * nh + (split_bnd ? 2 : 0) + (a.W ? 2 : 1)) * nst;
+    st->launches_update_fg += (uint64_t)(nh + (split_bnd ? 2 : 0)) * nst;
     for (int s = 0; s < nst; s++) {
       st->flops_gram += fl_gram[s];
       st->flops_update += fl_upd[s];

@@ -307,14 +307,37 @@ def run_ours(args):
     pairs = stats[-1]["pairs_visited"]
     peaks = _peaks()
     if blocked:
-        # dominant kernel: k_blk_update over the F and G row tiles (one launch per half
-        # of the block pairs per block step, medium-priority stream); its CUDA-event time
-        # on that stream.  The Z' row-tile launch (low priority, fills idle SMs) and the
-        # Gram launches (which end with the fused block-pivot factorizations) are listed
-        # under "others" with their event spans.
+        # dominant kernel: k_blk_update over the F and G row tiles; "achieved" uses its
+        # CUDA-event spans on its launching stream over the timed region.  In the timed
+        # schedule the two halves' kernels overlap (that is the point of the schedule), so
+        # a span also contains other kernels' work: the value is a lower bound.  The
+        # "isolated" entry times the same kernels live in this run on a one-sweep probe
+        # with GHSVD_SERIAL=1 (every kernel alone on the stream, one launch per kind and
+        # step), and "whole_step_tflops" is all algorithmic flops / the timed sweep time.
         t_upd = sum(s["t_update_fg"] for s in stats)
         f_upd = sum(s["flops_update_fg"] for s in stats)
         n_upd = sum(s["launches_update_fg"] for s in stats)
+        iso = None
+        if ws == 1:
+            os.environ["GHSVD_SERIAL"] = "1"
+            try:
+                cp = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=1,
+                                   nblocks=args.nblocks, detail_timing=True)
+                with torch.cuda.stream(stream):
+                    cp.set_factors(Fh, Jh, Gh)
+                    sp = cp.sweep()
+                stream.synchronize()
+                cp.close()
+            finally:
+                del os.environ["GHSVD_SERIAL"]
+            ia = sp["flops_update_fg"] / sp["t_update_fg"] / 1e12 if sp["t_update_fg"] > 0 else 0.0
+            ig = sp["flops_gram"] / sp["t_gram"] / 1e12 if sp["t_gram"] > 0 else 0.0
+            iso = {"achieved": ia, "frac": ia / zgemm_peak, "launches": int(sp["launches_update_fg"]),
+                   "alg_flops_per_launch": sp["flops_update_fg"] / max(sp["launches_update_fg"], 1),
+                   "avg_launch_us": sp["t_update_fg"] / max(sp["launches_update_fg"], 1) * 1e6,
+                   "k_blk_gram_achieved": ig, "k_blk_gram_frac": ig / zgemm_peak,
+                   "k_blk_gram_note": "span includes the fused HEBPJ / Cholesky tail of the last pairs",
+                   "probe": "1 sweep, GHSVD_SERIAL=1, same factors, CUDA events on the context stream"}
         t_gr = sum(s["t_gram"] for s in stats)
         f_gr = sum(s["flops_gram"] for s in stats)
         t_pv = sum(s["t_pivot"] for s in stats)
@@ -334,7 +357,9 @@ def run_ours(args):
                                                   "and the concurrent Grams of the other half"},
                            "k_blk_pivot": {"seconds": t_pv, "bound": "latency (inner one-sided sweep in shared "
                                                                       "memory)"}},
+                "isolated": iso,
                 "whole_step_tflops": sum(s["alg_flops"] for s in stats) / sum(s["kernel_seconds"] for s in stats) / 1e12}
+        roof["whole_step_frac"] = roof["whole_step_tflops"] / zgemm_peak
     else:
         kern_s = sum(s["kernel_seconds"] for s in stats)
         alg = sum(s["alg_bytes"] for s in stats)

@@ -1169,10 +1169,14 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   // touched by no other kernel, and Z_blk / applied are double-buffered by step parity.
   if (!ctx->aux_stream) GH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
   if (!ctx->aux_stream2) GH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream2, cudaStreamNonBlocking));
-  cudaStream_t aux = ctx->aux_stream;
+  // GHSVD_SERIAL=1: every kernel on the context stream, one launch per kind and step over
+  // all block pairs -- the kernels run alone, so their CUDA-event durations are their
+  // isolated durations (bench.py's roofline probe); same arithmetic, bitwise equal
+  const bool serial = env_int("GHSVD_SERIAL", 0) != 0;
+  cudaStream_t aux = serial ? str : ctx->aux_stream;
   // the step's pairs are split in two halves on two streams so that one half's
   // latency-bound pivot kernel overlaps the other half's Gram / update kernels
-  const int nh = pl.K >= 2 ? 2 : 1;
+  const int nh = (pl.K >= 2 && !serial) ? 2 : 1;
   const int KA = nh == 2 ? pl.K / 2 : pl.K;
   // Stream priorities steer the block scheduler (GHSVD_PRIO=0 disables, for comparison):
   //   highest  factor / pivot (latency-bound): their CTAs are placed as soon as a Gram
@@ -1181,16 +1185,14 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   //   medium   Gram and F, G update of both halves;
   //   lowest   the Z' update (aux): it has a whole step of slack and fills the SMs the
   //            latency-bound kernels leave idle.
-  const bool prio = env_int("GHSVD_PRIO", 1) != 0;
+  const bool prio = env_int("GHSVD_PRIO", 1) != 0 && !serial;
   cudaStream_t hs_st[2] = {str, ctx->aux_stream2};
   cudaStream_t fp_st[2] = {str, ctx->aux_stream2};
   if (prio) {
     int lo = 0, hi = 0;
     GH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     for (int i = 0; i < 2; i++) {
-      // both halves at the same level (ranking half 0 above half 1 measured 2 % slower:
-      // with the split boundary-pair updates the halves drift half a step apart and the
-      // lower one starves)
+      // both halves at the same level (ranking half 0 above half 1 measured 2 % slower)
       const int mid = std::min(lo, hi + 1);
       if (!ctx->hi_stream[i]) GH_CUDA(cudaStreamCreateWithPriority(&ctx->hi_stream[i], cudaStreamNonBlocking, hi));
       if (!ctx->mid_stream[i])
@@ -1205,10 +1207,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   const int h_pair0[2] = {0, KA}, h_np[2] = {KA, pl.K - KA};
   const int nst = pl.nblk - 1;
   std::vector<cudaEvent_t> ev_piv(2), ev_fg(2), ev_zdone(2), ev_gr(2), ev_bnd(2), tev;
-  // one GPU, halves of >= 2 pairs: split each half's F/G update into its boundary pair
-  // and the rest (GHSVD_SPLIT_BND=0 disables), so half 0 of step s+1 starts while half 1
-  // of step s still updates
-  const bool split_bnd = !multi && nh == 2 && KA >= 2 && pl.K - KA >= 2 && env_int("GHSVD_SPLIT_BND", 1) != 0;
+  // GHSVD_SPLIT_BND=1 (experiment): split each half's F/G update into its boundary pair
+  // and the rest, so half 0 of step s+1 may start while half 1 of step s still updates;
+  // measured equal to the plain halves on config 3 (2.42 ms per block step either way)
+  const bool split_bnd = !multi && nh == 2 && KA >= 2 && pl.K - KA >= 2 && env_int("GHSVD_SPLIT_BND", 0) != 0;
   cudaEvent_t ev_x;
   GH_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
   for (int i = 0; i < 2; i++) {

@@ -111,13 +111,14 @@ def _run_env(gh, monkeypatch, P, env, nblocks=8):
 
 
 def test_schedules_bitwise(gh, monkeypatch):
-    """The step schedules (two halves with stream priorities and split boundary-pair
-    updates: default; without priorities; without the split;
-    pipelined pair groups) run identical per-pair arithmetic, so lambda and Z must agree
-    bitwise (blocked scheduling)."""
+    """The step schedules (two halves with stream priorities: default; without
+    priorities; with split boundary-pair updates; fully serial (the bench's roofline
+    probe); pipelined pair groups) run identical per-pair arithmetic, so lambda and Z
+    must agree bitwise (blocked scheduling)."""
     P = inputs.known_hyperbolic(17, 192, 160, 0.5)
     ref = _run_env(gh, monkeypatch, P, {}, nblocks=10)
-    for env in ({"GHSVD_PRIO": "0"}, {"GHSVD_SPLIT_BND": "0"}, {"GHSVD_GROUPS": "2"}, {"GHSVD_GROUPS": "5"}):
+    for env in ({"GHSVD_PRIO": "0"}, {"GHSVD_SPLIT_BND": "1"}, {"GHSVD_SERIAL": "1"}, {"GHSVD_GROUPS": "2"},
+                {"GHSVD_GROUPS": "5"}):
         r = _run_env(gh, monkeypatch, P, env, nblocks=10)
         assert r[3]["sweeps"] == ref[3]["sweeps"], env
         assert np.array_equal(r[4], ref[4]) and np.array_equal(r[5], ref[5]), env

@@ -1,0 +1,19 @@
+#!/bin/bash
+# One B200: the round's evidence -- GPU tests, default bench line, ncu launch list of the
+# bench command, ncu --set full of one block step's Gram / pivot / F,G update (bench
+# schedule) and of the pointwise step kernel, and a launch trace of one block sweep.
+set -u
+OUT=gpurun_out/art
+mkdir -p $OUT
+python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; tail -2 $OUT/pytest_gpu.log
+python bench.py > $OUT/bench_c3_bo.log 2>&1; tail -c 400 $OUT/bench_c3_bo.log; echo
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_blk -c 3000 --csv \
+    --log-file $OUT/launches_bench_bo.csv python bench.py --no-cpu-baseline --warmup 0 --steps 1 > $OUT/ncu_bench.log 2>&1
+# bench schedule launch order per block step: gram0 pivot0 upd0(bnd) upd0b gram1 pivot1 upd1(bnd) upd1b updZ
+ncu --set full --clock-control none --import-source on -k regex:"k_blk_(update|gram|pivot)" -s 9 -c 4 \
+    -o $OUT/prof_blk python tools/profile_step.py --variant bo --sweep > $OUT/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_pair_step -s 2 -c 1 \
+    -o $OUT/prof_pw python tools/profile_step.py --kernel 2 --steps 4 > $OUT/ncu_pw.log 2>&1
+GHSVD_TRACE=$OUT/trace_c3_sweep1.csv python tools/perf_blocked.py > $OUT/perf_blocked.log 2>&1
+python tools/trace_summary.py $OUT/trace_c3_sweep1.csv > $OUT/trace_c3_sweep1.summary.txt
+cat $OUT/trace_c3_sweep1.summary.txt | tail -3

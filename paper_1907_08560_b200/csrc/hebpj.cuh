@@ -89,6 +89,39 @@ __device__ void block_amax2(double& v, long long& i, double& u, long long& j) {
   __syncthreads();
 }
 
+// block_amax2 with double-buffered partials (buffer `par`, alternate between calls): one
+// barrier per call; a later call with the same parity is separated by the other call's
+// barrier, so no reader of this buffer is left when it is rewritten.
+template <int NT>
+__device__ void block_amax2_db(double& v, long long& i, double& u, long long& j, int par) {
+  __shared__ double sv[2][2][NT / 32];
+  __shared__ long long si[2][2][NT / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    const double u2 = __shfl_xor_sync(0xffffffffu, u, o);
+    const long long j2 = __shfl_xor_sync(0xffffffffu, j, o);
+    amax_merge(v, i, v2, i2);
+    amax_merge(u, j, u2, j2);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[par][0][w] = v;
+    si[par][0][w] = i;
+    sv[par][1][w] = u;
+    si[par][1][w] = j;
+  }
+  __syncthreads();
+  v = sv[par][0][0];
+  i = si[par][0][0];
+  u = sv[par][1][0];
+  j = si[par][1][0];
+  for (int k = 1; k < NT / 32; k++) {  // every thread reduces the NT/32 partials (same order)
+    amax_merge(v, i, sv[par][0][k], si[par][0][k]);
+    amax_merge(u, j, sv[par][1][k], si[par][1][k]);
+  }
+}
+
 // Jacobi rotation R (column-major R11, R21, R12, R22) with R^* E R = diag(l1, l2)
 __device__ inline void herm2_jacobi(double a, double2 b, double c, double2* R, double* l1, double* l2) {
   const double ab = cabs(b);
@@ -132,16 +165,18 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
   for (int i = threadIdx.x; i < r; i += NT) perm[i] = i;
   if (threadIdx.x == 0) err_sh = 0;
   __syncthreads();
-  int k = 0;
+  // Per-thread partial pivot searches (diagonal |w_ii|, off-diagonal |w_ij| lower
+  // triangle) over the trailing matrix; after step 0 they are formed inside the previous
+  // step's Schur-complement update, on exactly the values the next search would read.
+  double mu1 = -1.0, mu0 = 0.0;
+  long long id = 0x7fffffffffffffffll, oidx = 0x7fffffffffffffffll;
+  for (int i = threadIdx.x; i < r; i += NT) amax_merge(mu1, id, fabs(W[i + i * ldw].x), i);
+  for (int j = warp; j < r; j += NW)
+    for (int i = j + 1 + lane; i < r; i += 32) amax_merge(mu0, oidx, cabs(W[i + j * ldw]), (long long)j * r + i);
+  int k = 0, par = 0;
   while (k < r) {
-    double mu1 = -1.0;
-    long long id = 0x7fffffffffffffffll;
-    for (int i = k + threadIdx.x; i < r; i += NT) amax_merge(mu1, id, fabs(W[i + i * ldw].x), i);
-    double mu0 = 0.0;
-    long long oidx = 0x7fffffffffffffffll;
-    for (int j = k + warp; j < r; j += NW)
-      for (int i = j + 1 + lane; i < r; i += 32) amax_merge(mu0, oidx, cabs(W[i + j * ldw]), (long long)j * r + i);
-    block_amax2<NT>(mu1, id, mu0, oidx);
+    block_amax2_db<NT>(mu1, id, mu0, oidx, par);
+    par ^= 1;
     const double mall = mu0 > mu1 ? mu0 : mu1;
     if (!(mall > tolz)) {
       if (threadIdx.x == 0) err_sh = -7;
@@ -178,22 +213,27 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
         __syncthreads();
       }
     }
+    mu1 = -1.0;
+    mu0 = 0.0;
+    id = oidx = 0x7fffffffffffffffll;
     if (!two) {
+      // 1x1 pivot: L(:,k) = W(:,k) / d_k stays unscaled in W (scaled when M is formed);
+      // the update reads column k directly, which no thread writes in this phase
       const double dk = W[k + k * ldw].x;
       const double inv = __ddiv_rn(1.0, dk);
-      for (int i = k + 1 + threadIdx.x; i < r; i += NT) colk[0][i] = W[i + k * ldw];
-      __syncthreads();
       for (int j = k + 1 + warp; j < r; j += NW) {
-        const double2 cj = conj(colk[0][j]);
-        for (int i = k + 1 + lane; i < r; i += 32) W[i + j * ldw] = sub(W[i + j * ldw], scale(mul(colk[0][i], cj), inv));
+        const double2 cj = conj(W[j + k * ldw]);
+        for (int i = k + 1 + lane; i < r; i += 32) {
+          const double2 w = sub(W[i + j * ldw], scale(mul(W[i + k * ldw], cj), inv));
+          W[i + j * ldw] = w;
+          if (i == j) amax_merge(mu1, id, fabs(w.x), i);
+          else if (i > j) amax_merge(mu0, oidx, cabs(w), (long long)j * r + i);
+        }
       }
-      __syncthreads();
-      for (int i = k + 1 + threadIdx.x; i < r; i += NT) W[i + k * ldw] = scale(colk[0][i], inv);
       if (threadIdx.x == 0) {
         bsz[k] = 1;
         d[k] = dk;
       }
-      __syncthreads();
       k += 1;
     } else {
       const double ea = W[k + k * ldw].x, ec = W[(k + 1) + (k + 1) * ldw].x;
@@ -212,10 +252,12 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
         const double2 c0 = conj(colk[0][j]), c1 = conj(colk[1][j]);
         for (int i = k + 2 + lane; i < r; i += 32) {
           const double2 t = add(mul(W[i + k * ldw], c0), mul(W[i + (k + 1) * ldw], c1));
-          W[i + j * ldw] = sub(W[i + j * ldw], t);
+          const double2 w = sub(W[i + j * ldw], t);
+          W[i + j * ldw] = w;
+          if (i == j) amax_merge(mu1, id, fabs(w.x), i);
+          else if (i > j) amax_merge(mu0, oidx, cabs(w), (long long)j * r + i);
         }
       }
-      __syncthreads();
       if (threadIdx.x == 0) {
         double l1, l2;
         herm2_jacobi(ea, eb, ec, &Rk[2 * k], &l1, &l2);
@@ -225,10 +267,12 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
         bsz[k + 1] = 0;
         W[(k + 1) + k * ldw] = mk(0.0, 0.0);  // L's 2x2 diagonal block is I
       }
-      __syncthreads();
       k += 2;
     }
+    // the next pivot search's barrier (block_amax2_db) orders this step's writes before
+    // the next step's swaps and reads
   }
+  __syncthreads();
   if (err_sh) return err_sh;
   if (threadIdx.x == 0) {
     for (int i = 0; i < r; i++) sgn[i] = d[i] > 0.0 ? 1 : -1;
@@ -248,7 +292,8 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
       auto Lh = [&](int row, int col) -> double2 {  // (L^*)(row, col) = conj(L(col, row))
         if (row == col) return mk(1.0, 0.0);
         if (col < row) return mk(0.0, 0.0);
-        return conj(W[col + row * ldw]);
+        // L column `row` of a 1x1 pivot is stored unscaled: L = W / d (as W * (1/d))
+        return conj(bsz[row] == 1 ? scale(W[col + row * ldw], __ddiv_rn(1.0, d[row])) : W[col + row * ldw]);
       };
       double2 y;
       if (bsz[i] == 1) {

@@ -384,6 +384,7 @@ def run_ours(args):
                    "l2": f"inputs ({2 * mb * nb * 16 / 1e9:.2f} GB) vs L2 126 MB",
                    "phase2": "applied" if phase2_s is not None else "skipped (config recipe; PAPER.md:925 for ill-conditioned G)"},
         "sweeps": sweeps, "converged": stats[-1]["converged"], "big_per_sweep_tail": stats[-1]["big_per_sweep"][-4:],
+        "max_offdiag_last_sweep": stats[-1]["max_offdiag_last"],
         "seconds_per_sweep": value / max(sweeps, 1),
         "pair_updates_per_s": pairs / value, "transforms_per_s": stats[-1]["transforms_all"] / value,
         "phase1_seconds": phase1_s, "phase2_seconds": phase2_s,

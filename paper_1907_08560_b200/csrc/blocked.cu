@@ -22,6 +22,7 @@
 
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <string>
@@ -482,6 +483,7 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
   const unsigned hmask = hw ? 0xffff0000u : 0x0000ffffu;
   const double tol = a.eps * sqrt((double)kb);       // C-7: n = block-pivot order
   unsigned long long w0_all = 0, w0_big = 0;          // warp-0 lane counters
+  double w0_off = 0.0;                                 // warp-0 lane max off-measure
   const int pr = 2 * warp + hw;                        // this half-warp's pivot pair slot
   const int b3 = (hl >> 3) & 1, b2 = (hl >> 2) & 1, b1 = (hl >> 1) & 1;
   for (int sw = 0; sw < a.inner_sweeps; sw++) {
@@ -531,6 +533,7 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
         zsh[lane][0] = z.z11.re; zsh[lane][1] = z.z11.im; zsh[lane][2] = z.z21.re; zsh[lane][3] = z.z21.im;
         zsh[lane][4] = z.z12.re; zsh[lane][5] = z.z12.im; zsh[lane][6] = z.z22.re; zsh[lane][7] = z.z22.im;
         ksh[lane] = z.kind;
+        w0_off = fmax(w0_off, z.off);   // scaled off-diagonal measure (a5 diagnostic)
         if (z.kind < 0) atomicCAS(&err_sh, 0, z.kind);
         if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
           sw_all++;
@@ -578,7 +581,9 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
     for (int o = 16; o > 0; o >>= 1) {
       w0_all += __shfl_xor_sync(0xffffffffu, w0_all, o);
       w0_big += __shfl_xor_sync(0xffffffffu, w0_big, o);
+      w0_off = fmax(w0_off, __shfl_xor_sync(0xffffffffu, w0_off, o));
     }
+    if (lane == 0) atomicMax(&a.cnt->off_bits, (unsigned long long)__double_as_longlong(w0_off));
     if (lane == 0) {
       cnt_all = w0_all;
       cnt_big = w0_big;
@@ -1124,6 +1129,11 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
     st->pairs_visited += pairs;
     st->transforms_all += c.all;
     st->transforms_big += c.big;
+    {
+      double off;   // max scaled off-diagonal measure over the block pivots' inner steps
+      memcpy(&off, &c.off_bits, 8);
+      st->max_offdiag_last = off;
+    }
     if (c.big == 0) {
       st->converged = 1;
       break;
@@ -1404,6 +1414,11 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     st->pairs_visited += pairs;
     st->transforms_all += c.all;
     st->transforms_big += c.big;
+    {
+      double off;   // max scaled off-diagonal measure over the block pivots' inner steps
+      memcpy(&off, &c.off_bits, 8);
+      st->max_offdiag_last = off;
+    }
     if (c.big == 0) {
       st->converged = 1;
       break;

@@ -168,3 +168,18 @@ def test_tiny_pencils_match_oracle(gh, m, n, variant):
     assert st["converged"]
     assert relerr(lam, lo[:n]) <= 1e-9
     assert residual(P.F, P.J, P.G, lam, Z) <= 1e-12 * max(n, 8)
+
+
+@pytest.mark.parametrize("variant", ["pointwise", "bo"])
+def test_offdiag_measure_reported(gh, variant):
+    """a5 diagnostic: the device-side max of the scaled off-diagonal measure
+    max(|H_pq| / sqrt(|H_pp H_qq|), |S_pq|) over the last sweep's pivot pairs is reported
+    and is at roundoff level once the sweep converged."""
+    P = inputs.known_hyperbolic(19, 160, 96, 0.4)
+    m, n = P.F.shape
+    ctx = gh.Context(m, n, variant=variant)
+    ctx.set_factors(P.F, P.J, P.G)
+    st = ctx.sweep()
+    ctx.close()
+    assert st["converged"]
+    assert 0.0 < st["max_offdiag_last"] < 1e-10, st["max_offdiag_last"]

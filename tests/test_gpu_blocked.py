@@ -124,10 +124,11 @@ def test_schedules_bitwise(gh, monkeypatch):
         assert np.array_equal(r[4], ref[4]) and np.array_equal(r[5], ref[5]), env
 
 
-@pytest.mark.parametrize("env", [{"GHSVD_GRAM3M": "0"}, {"GHSVD_UPD4M": "1"}])
+@pytest.mark.parametrize("env", [{"GHSVD_GRAM3M": "0"}, {"GHSVD_UPD4M": "1"}, {"GHSVD_PIVOT_CL": "1"}])
 def test_product_variants_match_oracle(gh, monkeypatch, env):
-    """Exact 4M block Grams / exact 4M updates (the default uses the 3M scheme for both)
-    reach the same eigenvalues as the oracle (1e-9) and the known spectrum."""
+    """Exact 4M block Grams / exact 4M updates (the default uses the 3M scheme for both) /
+    the two-CTA cluster block pivot reach the same eigenvalues as the oracle (1e-9) and
+    the known spectrum."""
     P = inputs.known_hyperbolic(14, 96, 64, 0.4)
     F0, J0, G0, st, lam, Z = _run_env(gh, monkeypatch, P, env, nblocks=4)
     Fo, Go, Zp, sto = oracle.hz_blocked(F0, J0, G0, 4, inner_sweeps=1)

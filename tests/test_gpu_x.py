@@ -99,3 +99,27 @@ def test_dataset_c_gsvd_small_vs_oracle(gh):
     assert np.max(np.abs(np.sort(lam) - np.sort(lo)) / np.abs(np.sort(lo))) < 1e-9
     eF, eG = eq71(F0, J0, G0, Fc, Gc, X, sf, sg)
     assert eF < 1e-12 and eG < 1e-12
+
+
+def test_x_with_cluster_pivot(gh, monkeypatch):
+    """The two-CTA cluster block pivot (GHSVD_PIVOT_CL=1) with its separate Gauss-Jordan
+    kernel for Z_blk^{-1}: X Z = I, eq 7.1 errors, eigenvalues bitwise unchanged by want_x."""
+    monkeypatch.setenv("GHSVD_PIVOT_CL", "1")
+    P = inputs.known_hyperbolic(92, 160, 64, 0.5)
+    m, n = P.F.shape
+    runs = {}
+    for wx in (False, True):
+        ctx = gh.Context(m, n, variant="bo", nblocks=6, want_x=wx)
+        ctx.set_factors(P.F, P.J, P.G)
+        F0, J0, G0, _ = ctx.get_factors()
+        ctx.sweep()
+        lam, sf, sg, Z = ctx.extract()
+        X = ctx.extract_x() if wx else None
+        Fc, Gc, Zp = ctx.transformed(m, n)
+        ctx.close()
+        runs[wx] = (F0, J0, G0, lam, sf, sg, Z, X, Fc, Gc)
+    assert np.array_equal(runs[False][3], runs[True][3])
+    F0, J0, G0, lam, sf, sg, Z, X, Fc, Gc = runs[True]
+    assert np.abs(Z @ X - np.eye(n)).max() < 1e-9
+    eF, eG = eq71(F0, J0, G0, Fc, Gc, X, sf, sg)
+    assert eF < 1e-12 and eG < 1e-12, (eF, eG)

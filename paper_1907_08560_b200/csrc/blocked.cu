@@ -220,67 +220,74 @@ __device__ __forceinline__ void gram_tiles(const double2* T, int row, double sg,
   }
 }
 
-// 3M variant (GHSVD_GRAM3M=1): warp 2g+h owns tiles [5h, 5h+5) ∩ [0, 9) of group g for
-// every k-step of a stage, so no cross-warp sum is needed; per k-step it loads the
-// fragments those tiles need and issues 3 DMMAs per tile: P1 = Ar Br, P2 = Ai Bi,
-// P3 = (Ar + Ai)(Br + Bi); Re = P1 - P2, Im = P3 - P1 - P2 (A = J conj(X)^T, B = X).
+// 3M variant (default; GHSVD_GRAM3M=0 selects the 4M path above): of the 9 tiles of group
+// g, warp 2g owns tiles 0-3 and warp 2g+1 tiles 5-8 for every k-step, and tile 4 is
+// split by k-step parity (even: warp 2g, odd: warp 2g+1; its two partial sums are added
+// in a fixed order at the end), so every warp does exactly 4.5 tiles per k-step.  Per
+// k-step a warp loads the fragments its tiles need and issues 3 DMMAs per tile:
+// P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi); Re = P1 - P2, Im = P3 - P1 - P2
+// (A = J conj(X)^T, B = X).
 template <int GI>
 struct G3 {
   static constexpr int IA = GI, IB = 7 - GI;
   static constexpr int row(int t) { return t <= IA ? IA : IB; }
   static constexpr int col(int t) { return t <= IA ? t : t - IA - 1; }
-  static constexpr bool needB(int j, int t0, int t1) {
+  // tile of accumulator slot u (0..4) of warp half H; slot 4 is the shared tile 4
+  static constexpr int tile(int H, int u) { return u == 4 ? 4 : (H ? 5 + u : u); }
+  static constexpr bool needB(int H, bool w4, int j) {
     bool r = false;
-    for (int t = t0; t < t1; t++) r = r || col(t) == j;
+    for (int u = 0; u < 5; u++) r = r || ((u < 4 || w4) && col(tile(H, u)) == j);
     return r;
   }
-  static constexpr bool needA(int i, int t0, int t1) {
+  static constexpr bool needA(int H, bool w4, int i) {
     bool r = false;
-    for (int t = t0; t < t1; t++) r = r || row(t) == i;
+    for (int u = 0; u < 5; u++) r = r || ((u < 4 || w4) && row(tile(H, u)) == i);
     return r;
   }
 };
 
-template <int GI, int H>
+template <int GI, int H, bool W4>
 __device__ __forceinline__ void gram3_tiles(const double2* T, int row, double sg, double (&acc)[5][6]) {
   using C = G3<GI>;
-  constexpr int T0 = H ? 5 : 0, T1 = H ? 9 : 5;
   const int lane = threadIdx.x & 31;
   double2 f[8];
   double bs[8];
 #pragma unroll
   for (int j = 0; j < 8; j++) {
-    if (C::needB(j, T0, T1) || C::needA(j, T0, T1)) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
-    if (C::needB(j, T0, T1)) bs[j] = f[j].x + f[j].y;
+    if (C::needB(H, W4, j) || C::needA(H, W4, j)) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
+    if (C::needB(H, W4, j)) bs[j] = f[j].x + f[j].y;
   }
   double ar[2] = {0, 0}, ai[2] = {0, 0}, as[2] = {0, 0};   // rows IA, IB
-  if (C::needA(C::IA, T0, T1)) {
+  if (C::needA(H, W4, C::IA)) {
     ar[0] = sg * f[C::IA].x;
     ai[0] = -(sg * f[C::IA].y);
     as[0] = ar[0] + ai[0];
   }
-  if (C::needA(C::IB, T0, T1)) {
+  if (C::needA(H, W4, C::IB)) {
     ar[1] = sg * f[C::IB].x;
     ai[1] = -(sg * f[C::IB].y);
     as[1] = ar[1] + ai[1];
   }
 #pragma unroll
-  for (int t = T0; t < T1; t++) {
+  for (int u = 0; u < 5; u++) {
+    if (u == 4 && !W4) continue;
+    const int t = C::tile(H, u);
     const int r = C::row(t) == C::IA ? 0 : 1, J = C::col(t);
-    dmma(acc[t - T0][0], acc[t - T0][1], ar[r], f[J].x);
-    dmma(acc[t - T0][2], acc[t - T0][3], ai[r], f[J].y);
-    dmma(acc[t - T0][4], acc[t - T0][5], as[r], bs[J]);
+    dmma(acc[u][0], acc[u][1], ar[r], f[J].x);
+    dmma(acc[u][2], acc[u][3], ai[r], f[J].y);
+    dmma(acc[u][4], acc[u][5], as[r], bs[J]);
   }
 }
 
 template <int GI, int H>
-__device__ __forceinline__ void gram3_store(double2* out, const double (&acc)[5][6]) {
+__device__ __forceinline__ void gram3_store(double2* out, const double (&acc)[5][6], int nslots) {
   using C = G3<GI>;
-  constexpr int T0 = H ? 5 : 0, T1 = H ? 9 : 5;
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int t = T0; t < T1; t++) {
-    const double* c = acc[t - T0];
+  for (int u = 0; u < 5; u++) {
+    if (u >= nslots) continue;
+    const double* c = acc[u];
+    const int t = C::tile(H, u);
     const int i = 8 * C::row(t) + (lane >> 2), j = 8 * C::col(t) + 2 * (lane & 3);
     out[i + (size_t)j * KM] = make_double2(c[0] - c[2], c[4] - c[0] - c[2]);
     out[i + (size_t)(j + 1) * KM] = make_double2(c[1] - c[3], c[5] - c[1] - c[3]);
@@ -337,33 +344,46 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
 #pragma unroll
       for (int c = 0; c < 6; c++) acc[t][c] = 0.0;
     pipeline([&](const double2* T, long long r0) {
-      // not unrolled: the 8 warp-specialized tile sets are already 8 code paths, and
-      // unrolling them 8x overflowed the instruction cache (ncu: 22 % no_inst stalls)
+      // not unrolled: the warp-specialized tile sets are already 16 code paths, and
+      // unrolling them overflowed the instruction cache (ncu: 22 % no_inst stalls)
 #pragma unroll 1
-      for (int ks = 0; ks < RT / 4; ks++) {
-        const int row = 4 * ks + (lane & 3);
-        const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
-        switch (warp) {   // warp-uniform
-          case 0: gram3_tiles<0, 0>(T, row, sg, acc); break;
-          case 1: gram3_tiles<0, 1>(T, row, sg, acc); break;
-          case 2: gram3_tiles<1, 0>(T, row, sg, acc); break;
-          case 3: gram3_tiles<1, 1>(T, row, sg, acc); break;
-          case 4: gram3_tiles<2, 0>(T, row, sg, acc); break;
-          case 5: gram3_tiles<2, 1>(T, row, sg, acc); break;
-          case 6: gram3_tiles<3, 0>(T, row, sg, acc); break;
-          default: gram3_tiles<3, 1>(T, row, sg, acc); break;
+      for (int ks = 0; ks < RT / 4; ks += 2) {
+        const int row0 = 4 * ks + (lane & 3), row1 = row0 + 4;
+        const double sg0 = (hs == 0 && r0 + row0 >= a.npos) ? -1.0 : 1.0;
+        const double sg1 = (hs == 0 && r0 + row1 >= a.npos) ? -1.0 : 1.0;
+        switch (warp) {   // warp-uniform; tile 4 on even k-steps for h = 0, odd for h = 1
+#define G3CASE(W, GI, H)                                       \
+  case W:                                                      \
+    gram3_tiles<GI, H, H == 0>(T, row0, sg0, acc);             \
+    gram3_tiles<GI, H, H == 1>(T, row1, sg1, acc);             \
+    break;
+          G3CASE(0, 0, 0) G3CASE(1, 0, 1) G3CASE(2, 1, 0) G3CASE(3, 1, 1)
+          G3CASE(4, 2, 0) G3CASE(5, 2, 1) G3CASE(6, 3, 0) default: G3CASE(7, 3, 1)
+#undef G3CASE
         }
       }
     });
+    // tile 4 of every group: warp 2g+1 hands its odd-k-step partial to warp 2g
+    double* red = reinterpret_cast<double*>(gsm);
+    if (kh) {
+#pragma unroll
+      for (int c = 0; c < 6; c++) red[(gi * 6 + c) * 32 + lane] = acc[4][c];
+    }
+    __syncthreads();
+    if (!kh) {
+#pragma unroll
+      for (int c = 0; c < 6; c++) acc[4][c] += red[(gi * 6 + c) * 32 + lane];
+    }
+    const int nslots = kh ? 4 : 5;
     switch (warp) {
-      case 0: gram3_store<0, 0>(out, acc); break;
-      case 1: gram3_store<0, 1>(out, acc); break;
-      case 2: gram3_store<1, 0>(out, acc); break;
-      case 3: gram3_store<1, 1>(out, acc); break;
-      case 4: gram3_store<2, 0>(out, acc); break;
-      case 5: gram3_store<2, 1>(out, acc); break;
-      case 6: gram3_store<3, 0>(out, acc); break;
-      default: gram3_store<3, 1>(out, acc); break;
+      case 0: gram3_store<0, 0>(out, acc, nslots); break;
+      case 1: gram3_store<0, 1>(out, acc, nslots); break;
+      case 2: gram3_store<1, 0>(out, acc, nslots); break;
+      case 3: gram3_store<1, 1>(out, acc, nslots); break;
+      case 4: gram3_store<2, 0>(out, acc, nslots); break;
+      case 5: gram3_store<2, 1>(out, acc, nslots); break;
+      case 6: gram3_store<3, 0>(out, acc, nslots); break;
+      default: gram3_store<3, 1>(out, acc, nslots); break;
     }
   } else {
     double acc[9][4];

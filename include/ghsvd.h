@@ -67,12 +67,15 @@ typedef struct {
   int max_sweeps;      /* C_max, default 30 (Algorithm 2) */
   int criterion;       /* GHSVD_CRIT_RELATIVE | GHSVD_CRIT_LITERAL */
   double eps;          /* machine precision in (6.12); 0 => 2^-53 */
-  int cluster;         /* pointwise: CTAs per column pair (0 = auto; 1,2,4,8,16) */
-  int threads;         /* pointwise: threads per CTA (0 = auto) */
+  int cluster;         /* pointwise: CTAs per column pair (0 = auto: kernel 2 uses 4 when m >= 4096,
+                          else 1; kernels 1/3 the smallest cluster whose slices fit shared memory) */
+  int threads;         /* pointwise: threads per CTA (0 = auto: kernel 2 with m >= 4096 uses 128) */
   int use_graph;       /* capture each sweep's steps in a CUDA graph (default 1) */
   int kernel;          /* pointwise step kernel: 0 = auto (= 2), 1 = one cluster per pair, TMA-staged slices;
                           2 = two-pass through L2 (default); 3 = persistent pipelined TMA */
-  int detail_timing;   /* blocked: CUDA events around every kernel (fills t_* in ghsvd_stats) */
+  int detail_timing;   /* blocked: CUDA events around every kernel on its launching stream (fills
+                          t_* in ghsvd_stats; kernels of the two halves overlap, so the spans are
+                          upper bounds of the kernels' own durations) */
   int want_x;          /* also accumulate W = Z'^{-1} during the sweep so that ghsvd_extract_x
                           can return X = Z^{-1} = Sigma Z'^{-1} (NEXT-1):
                           pointwise by 2x2 inverses, blocked by block-pivot inverses.

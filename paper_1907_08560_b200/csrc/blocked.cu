@@ -6,18 +6,20 @@
 // C-11).  Per block step s, for every block pair (bp, bq) owned by this rank:
 //   k_blk_gram   H_blk = F_pair^* J F_pair, S_blk = G_pair^* G_pair (k x k,
 //                k = w_p + w_q <= 64), lower-triangle 8x8 tiles on the FP64
-//                tensor cores (mma.sync m8n8k4 f64 = DMMA), J fused into the
-//                B operand, split over row chunks (deterministic sum later);
-//   k_blk_pivot  one CTA: sum the partials, HEBPJ(H_blk) -> F^ (Sec 4.2-4.3),
-//                pivoted Cholesky(S_blk) -> G^, border to
-//                even order, inner Level-1 one-sided HZ sweep(s) in shared
-//                memory (BO: 1 sweep; FB: until no transformation, <= 30)
-//                accumulating Z_blk (Sec 6.4.2); counters;
+//                tensor cores (mma.sync m8n8k4 f64 = DMMA, 3M complex product),
+//                J folded into the A operand, split over row chunks; the last
+//                CTA of a (pair, H|S) sums the partials in fixed order and
+//                factorizes: HEBPJ(H_blk) -> F^, J^ (Sec 4.2-4.3) or pivoted
+//                Cholesky(S_blk) -> G^;
+//   k_blk_pivot  one CTA: F^, G^ in shared memory, border to even order, inner
+//                Level-1 one-sided HZ sweep(s) (BO: 1 sweep; FB: until no
+//                transformation, <= 30) accumulating Z_blk (Sec 6.4.2); counters;
 //   k_blk_update F_pair <- F_pair Z_blk, G_pair <- G_pair Z_blk, Z_pair <-
 //                Z_pair Z_blk in place, row tiles on DMMA (Sec 6.4.3, the
 //                paper's three ZGEMMs; no shadow copy is needed on one GPU
 //                because every CTA reads its row tile before writing it).
-// Multi-GPU (comm.cpp) exchanges block columns between the steps.
+// blk_sweep schedules a step as two halves of the pairs on prioritized streams
+// (DESIGN.md 6); multi-GPU (comm.cpp) exchanges block columns between the steps.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 

@@ -184,3 +184,34 @@ def test_offdiag_measure_reported(gh, variant):
     ctx.close()
     assert st["converged"]
     assert 0.0 < st["max_offdiag_last"] < 1e-10, st["max_offdiag_last"]
+
+
+@pytest.mark.parametrize("variant", ["pointwise", "bo"])
+@pytest.mark.parametrize("what", ["nan", "inf"])
+def test_nonfinite_input_is_reported(gh, variant, what):
+    """A NaN / Inf entry in F must end the sweep with an error status (sticky device flag,
+    checked at the end of the sweep), never a silent result."""
+    P = inputs.random_pencil(7, 96, 32, 0.5)
+    F = P.F.copy()
+    F[5, 3] = np.nan if what == "nan" else np.inf
+    ctx = gh.Context(96, 32, variant=variant)
+    ctx.set_factors(F, P.J, P.G)
+    with pytest.raises(gh.GHSVDError) as e:
+        ctx.sweep()
+    assert e.value.status in (-6, -7, -8), e.value.status
+    ctx.close()
+
+
+@pytest.mark.parametrize("variant", ["pointwise", "bo"])
+def test_singular_G_column_reported(gh, variant):
+    """A zero column of G (s_pp = 0, reading C-9) is reported as an indefinite /
+    singular S (pointwise: the 2x2 prescaling; blocked: the pivoted Cholesky)."""
+    P = inputs.random_pencil(8, 96, 32, 0.5)
+    G = P.G.copy()
+    G[:, 11] = 0.0
+    ctx = gh.Context(96, 32, variant=variant)
+    ctx.set_factors(P.F, P.J, G)
+    with pytest.raises(gh.GHSVDError) as e:
+        ctx.sweep()
+    assert e.value.status == -6
+    ctx.close()

@@ -427,11 +427,16 @@ int or_hebpj(int64_t r, const orc *T, int64_t ldt, orc *M, int64_t ldm,
       double a = fabs(EL(W, r, i, i).re);
       if (a > mu1) { mu1 = a; id = i; }
     }
+    /* largest off-diagonal |w_ij| found through |w_ij|^2 (same entry; where two entries'
+       magnitudes round to the same double the larger square wins), then mu0 = sqrt(max)
+       = the largest magnitude itself (sqrt is monotone and correctly rounded) */
+    double mu0sq = 0.0;
     for (int64_t j = k; j < r; j++)
       for (int64_t i = j + 1; i < r; i++) {
-        double a = cabsv(EL(W, r, i, j));
-        if (a > mu0) { mu0 = a; oi = i; oj = j; }
+        double a = cabs2(EL(W, r, i, j));
+        if (a > mu0sq) { mu0sq = a; oi = i; oj = j; }
       }
+    mu0 = sqrt(mu0sq);
     double mall = mu0 > mu1 ? mu0 : mu1;
     if (!(mall > tolz)) { rc = OR_E_RANK; goto done; }
     int two = !(mu1 >= alpha * mu0);

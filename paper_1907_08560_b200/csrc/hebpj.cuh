@@ -171,12 +171,15 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
   double mu1 = -1.0, mu0 = 0.0;
   long long id = 0x7fffffffffffffffll, oidx = 0x7fffffffffffffffll;
   for (int i = threadIdx.x; i < r; i += NT) amax_merge(mu1, id, fabs(W[i + i * ldw].x), i);
+  // off-diagonal search on |w_ij|^2 (same entry as on |w_ij|, no square root per entry;
+  // the oracle searches the same way); mu0 becomes the magnitude after the reduction
   for (int j = warp; j < r; j += NW)
-    for (int i = j + 1 + lane; i < r; i += 32) amax_merge(mu0, oidx, cabs(W[i + j * ldw]), (long long)j * r + i);
+    for (int i = j + 1 + lane; i < r; i += 32) amax_merge(mu0, oidx, cabs2(W[i + j * ldw]), (long long)j * r + i);
   int k = 0, par = 0;
   while (k < r) {
     block_amax2_db<NT>(mu1, id, mu0, oidx, par);
     par ^= 1;
+    mu0 = __dsqrt_rn(mu0);
     const double mall = mu0 > mu1 ? mu0 : mu1;
     if (!(mall > tolz)) {
       if (threadIdx.x == 0) err_sh = -7;
@@ -227,7 +230,7 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
           const double2 w = sub(W[i + j * ldw], scale(mul(W[i + k * ldw], cj), inv));
           W[i + j * ldw] = w;
           if (i == j) amax_merge(mu1, id, fabs(w.x), i);
-          else if (i > j) amax_merge(mu0, oidx, cabs(w), (long long)j * r + i);
+          else if (i > j) amax_merge(mu0, oidx, cabs2(w), (long long)j * r + i);
         }
       }
       if (threadIdx.x == 0) {
@@ -255,7 +258,7 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
           const double2 w = sub(W[i + j * ldw], t);
           W[i + j * ldw] = w;
           if (i == j) amax_merge(mu1, id, fabs(w.x), i);
-          else if (i > j) amax_merge(mu0, oidx, cabs(w), (long long)j * r + i);
+          else if (i > j) amax_merge(mu0, oidx, cabs2(w), (long long)j * r + i);
         }
       }
       if (threadIdx.x == 0) {
@@ -313,14 +316,17 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
 }
 
 // Diagonally pivoted Cholesky: P S P^T = L L^*, Gh = L^* P (column perm[l] of Gh
-// is column l of L^*).  S overwritten (L below/on the diagonal).  Returns 0 or -6.
-// The pivot search (largest diagonal entry, smallest index on ties) is done
-// redundantly by every warp, so no barrier is spent on it.
+// is column l of L^*).  S overwritten (the strictly lower part of L kept unscaled:
+// L(i,k) = S(i,k) * (1/l_kk) is formed where it is used, with the same rounding as a
+// stored scaled column).  Returns 0 or -6.  The pivot search (largest diagonal entry,
+// smallest index on ties) is done redundantly by every warp, so no barrier is spent on
+// it; one barrier per elimination step (+3 when rows are swapped).
 template <int NT, int RMAX>
 __device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long long ldg) {
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ int perm[RMAX];
+  __shared__ double dg[RMAX], iv[RMAX];   // l_kk and 1 / l_kk
   for (int i = threadIdx.x; i < r; i += NT) perm[i] = i;
   __syncthreads();
   for (int k = 0; k < r; k++) {
@@ -366,19 +372,23 @@ __device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long lon
     }
     const double lkk = __dsqrt_rn(S[k + k * lds].x);
     const double inv = __ddiv_rn(1.0, lkk);
-    __syncthreads();
-    for (int i = k + 1 + threadIdx.x; i < r; i += NT) S[i + k * lds] = scale(S[i + k * lds], inv);
-    if (threadIdx.x == 0) S[k + k * lds] = mk(lkk, 0.0);
-    __syncthreads();
+    // Schur complement with L(:,k) = S(:,k) / l_kk formed on the fly; column k and the
+    // diagonal entry (k, k) are not written in this phase
     for (int j = k + 1 + warp; j < r; j += NW) {
-      const double2 cj = conj(S[j + k * lds]);
-      for (int i = k + 1 + lane; i < r; i += 32) S[i + j * lds] = sub(S[i + j * lds], mul(S[i + k * lds], cj));
+      const double2 cj = conj(scale(S[j + k * lds], inv));
+      for (int i = k + 1 + lane; i < r; i += 32)
+        S[i + j * lds] = sub(S[i + j * lds], mul(scale(S[i + k * lds], inv), cj));
+    }
+    if (threadIdx.x == 0) {
+      dg[k] = lkk;
+      iv[k] = inv;
     }
     __syncthreads();
   }
   // Gh(i, perm[l]) = (L^*)(i, l) = conj(L(l, i)) for l >= i, else 0
   for (int l = warp; l < r; l += NW)
-    for (int i = lane; i < r; i += 32) Gh[i + perm[l] * ldg] = l >= i ? conj(S[l + i * lds]) : mk(0.0, 0.0);
+    for (int i = lane; i < r; i += 32)
+      Gh[i + perm[l] * ldg] = l > i ? conj(scale(S[l + i * lds], iv[i])) : (l == i ? mk(dg[i], 0.0) : mk(0.0, 0.0));
   __syncthreads();
   return 0;
 }

@@ -1,0 +1,57 @@
+"""The bench.py JSON contract, checked on the committed round log (CPU-only): every key
+the driver and the judge read is present with the right type, and the roofline /
+cpu_baseline / e2e objects are complete (a regression in bench.py's line shows here)."""
+import json
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LOG = os.path.join(ROOT, "profiles", "r01", "bench_c3_bo.log")
+
+
+@pytest.fixture(scope="module")
+def line():
+    if not os.path.exists(LOG):
+        pytest.skip("no committed bench log")
+    return json.loads(open(LOG).read().strip().splitlines()[-1])
+
+
+def test_top_level_keys(line):
+    for k, t in [("metric", str), ("value", float), ("unit", str), ("n_gpus", int), ("steps", int),
+                 ("warmup", int), ("ms_per_step", float), ("higher_is_better", bool), ("scaling", str),
+                 ("dtype", str), ("data", str), ("config", dict), ("gpu_launches", int), ("clocks", dict)]:
+        assert isinstance(line[k], t), k
+    assert "vs_baseline" in line
+    assert line["metric"].startswith("GHSVD time-to-converge") and line["unit"] == "s"
+    assert line["higher_is_better"] is False
+    assert line["warmup"] >= 3
+    assert line["config"]["workload"] == "c3_illcond_4096"
+    assert abs(line["ms_per_step"] - 1e3 * line["value"]) < 1e-6 * line["ms_per_step"]
+
+
+def test_roofline_object(line):
+    r = line["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["bound"] in ("hbm", "tensor", "alu")
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert 0.0 < r["frac"] <= 1.5
+    assert r["traffic"] is None or r["traffic"] > 0
+
+
+def test_cpu_baseline_and_e2e(line):
+    cb = line["cpu_baseline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in cb, k
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1
+    e = line["e2e"]
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in e, k
+    assert e["value"] >= line["value"] and e["h2d_bytes_per_step"] > 0
+
+
+def test_clocks_sampled_without_throttle(line):
+    c = line["clocks"]
+    assert c["samples"] > 0 and c["sm_mhz"] is not None
+    assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(c["reasons"])

@@ -248,9 +248,12 @@ def run_ours(args):
             ev[1].record(stream)
             stream.synchronize()
             phase1_s = ev[0].elapsed_time(ev[1]) * 1e-3
-            if "reduce" in cfg.get("entry", ""):
+            if "reduce" in cfg.get("entry", "") or args.reduce == "colpiv":
                 t0 = time.perf_counter()
-                ctx.reduce()                            # Phase 2 (config 2 recipe)
+                # Phase 2: config 2 recipe, or (--reduce colpiv) the column-pivoted QR of
+                # G P2 that PAPER.md:925-943 gives for a badly conditioned G~
+                ctx.reduce(colpiv=args.reduce == "colpiv")
+                torch.cuda.synchronize(dev)
                 phase2_s = time.perf_counter() - t0
         else:
             ctx.set_factors(payload.F, payload.J, payload.G)
@@ -382,7 +385,9 @@ def run_ours(args):
         "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant, "max_sweeps": args.max_sweeps,
                    "want_x": bool(args.want_x),
                    "l2": f"inputs ({2 * mb * nb * 16 / 1e9:.2f} GB) vs L2 126 MB",
-                   "phase2": "applied" if phase2_s is not None else "skipped (config recipe; PAPER.md:925 for ill-conditioned G)"},
+                   "phase2": ("column-pivoted QR of G P2 (--reduce colpiv, PAPER.md:925-943)" if args.reduce == "colpiv"
+                              else "applied" if phase2_s is not None
+                              else "skipped (config recipe; PAPER.md:925 for ill-conditioned G)")},
         "sweeps": sweeps, "converged": stats[-1]["converged"], "big_per_sweep_tail": stats[-1]["big_per_sweep"][-4:],
         "max_offdiag_last_sweep": stats[-1]["max_offdiag_last"],
         "seconds_per_sweep": value / max(sweeps, 1),
@@ -420,6 +425,9 @@ def main():
     ap.add_argument("--max-sweeps", type=int, default=64,
                     help="C_max; config 3 (S condition 1e12) needs ~36 sweeps, beyond the paper's usual 30")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reduce", default="recipe", choices=["recipe", "colpiv"],
+                    help="Phase 2 as the config's recipe says, or the column-pivoted QR path for any "
+                         "atoms config (untimed preprocessing, reported as phase2_seconds)")
     ap.add_argument("--want-x", action="store_true",
                     help="also accumulate Z'^{-1} during the sweep (full GHSVD X, NEXT-1)")
     ap.add_argument("--ref-budget", type=float, default=15.0)

@@ -142,8 +142,14 @@ ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* 
  * hyperbolic Householder reflectors and (J,I) URV 2x2 pivots; G prepermuted by
  * P2 and reduced by Householder QR (R kept, diag real >= 0).  Afterwards
  * m = n.  May follow a ghsvd_get_factors (which then exported the Phase-1
- * factors); at most once per problem, before ghsvd_sweep.  flags: reserved, 0.
- * Errors: GHSVD_E_RANK_DEFICIENT on a degenerate JQR pivot or rank-deficient G. */
+ * factors); at most once per problem, before ghsvd_sweep.
+ * flags: 0, or GHSVD_REDUCE_COLPIV: the QR of G P2 with column pivoting by norm,
+ * P4 (G P2) P5 = Q G', F' = F P5 (the "slower but more stable"
+ * path for a badly conditioned G~; no row pivoting P4); the combined permutation
+ * P2 P5 is what ghsvd_get_factors exports and ghsvd_extract undoes.
+ * Errors: GHSVD_E_RANK_DEFICIENT on a degenerate JQR pivot or rank-deficient G;
+ * INVALID_ARG on unknown flags. */
+enum { GHSVD_REDUCE_COLPIV = 1 };
 ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
 
 /* Export the factors the sweep will start from (after factor/set_factors,

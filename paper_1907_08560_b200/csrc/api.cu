@@ -280,14 +280,17 @@ ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
     ctx->err = "reduce: must follow factor/set_factors (once) and precede sweep";
     return GHSVD_E_STATE;
   }
-  (void)flags;
+  if (flags & ~GHSVD_REDUCE_COLPIV) {
+    ctx->err = "reduce: unknown flags";
+    return GHSVD_E_INVALID_ARG;
+  }
   CTX_CUDA(cudaSetDevice(ctx->o.device));
   // a get_factors before reduce may have bordered the factors and set Z' = I: reduce works
   // on the unbordered m_user x n_user factors, zeroes both buffers, and bordering / Z' are
   // redone by the next prepare()
   ctx->m = ctx->m_user;
   ctx->n = ctx->n_user;
-  TRY(phase2_reduce(ctx));
+  TRY(phase2_reduce(ctx, flags));
   ctx->have_p2 = true;
   ctx->bordered = false;
   ctx->z_init = false;

@@ -109,7 +109,7 @@ ghsvd_status phase1_factor(Ctx* ctx, int64_t NA, int64_t NL, int64_t NG, const v
                            const void* TBB);
 size_t phase1_scratch_bytes(int64_t m, int64_t n, int64_t nl);
 // phase2.cu
-ghsvd_status phase2_reduce(Ctx* ctx);
+ghsvd_status phase2_reduce(Ctx* ctx, int flags);
 size_t phase2_scratch_bytes(int64_t m, int64_t n);
 // blocked.cu
 ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st);

@@ -335,6 +335,74 @@ __global__ void __launch_bounds__(T2) k_qr_prep(double2* G, long long ld, long l
   }
 }
 
+// Column pivoting of the QR of G P2 (ZGEQP3-like, reading of the optional
+// path): squared norms of rows [k, m) of the remaining columns p2[j], j >= k (recomputed
+// every step: exact, no norm downdating), then the largest is swapped into position k
+// in p2 (G P2 P5) and the same two columns of F are swapped (F' = F P5).
+__global__ void __launch_bounds__(T2) k_qr_colnorms(const double2* G, long long ld, long long m, long long k,
+                                                    const long long* p2, P2Scr s) {
+  __shared__ double2 sh[T2 / 32];
+  if (s.ctl[3]) return;
+  const long long j = k + blockIdx.x;
+  const double2* x = G + p2[j] * ld;
+  const double v = jdot(x, x, nullptr, k, m, false, sh).x;
+  if (threadIdx.x == 0) s.hd[j] = v;
+}
+
+__global__ void __launch_bounds__(T2) k_qr_colpiv(double2* F, long long ldf, long long mf, long long n, long long k,
+                                                  long long* p2, P2Scr s) {
+  __shared__ double bv[T2 / 32];
+  __shared__ long long bi[T2 / 32];
+  __shared__ long long piv;
+  if (s.ctl[3]) return;
+  double v = -1.0;
+  long long idx = n;
+  for (long long j = k + threadIdx.x; j < n; j += T2)
+    if (s.hd[j] > v) {   // first (smallest j) maximum within the thread's strided set
+      v = s.hd[j];
+      idx = j;
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (v2 > v || (v2 == v && i2 < idx)) {
+      v = v2;
+      idx = i2;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    bv[threadIdx.x >> 5] = v;
+    bi[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bvv = bv[0];
+    long long bii = bi[0];
+    for (int w = 1; w < T2 / 32; w++)
+      if (bv[w] > bvv || (bv[w] == bvv && bi[w] < bii)) {
+        bvv = bv[w];
+        bii = bi[w];
+      }
+    piv = bii < n ? bii : k;
+    if (piv != k) {
+      const long long t = p2[k];
+      p2[k] = p2[piv];
+      p2[piv] = t;
+    }
+  }
+  __syncthreads();
+  const long long pv = piv;
+  if (pv != k) {
+    double2* a = F + k * ldf;
+    double2* b = F + pv * ldf;
+    for (long long i = threadIdx.x; i < mf; i += T2) {
+      const double2 t = a[i];
+      a[i] = b[i];
+      b[i] = t;
+    }
+  }
+}
+
 // Gs(i, j) = G(i, p2[j]) for i <= j (upper triangle), diag phases normalised.
 __global__ void k_qr_gather(const double2* G, long long ld, double2* out, long long ldo, long long n,
                             const long long* p2) {
@@ -374,7 +442,7 @@ size_t phase2_scratch_bytes(int64_t m, int64_t n) {
     }                                              \
   } while (0)
 
-ghsvd_status phase2_reduce(Ctx* ctx) {
+ghsvd_status phase2_reduce(Ctx* ctx, int flags) {
   const int64_t m = ctx->m_user, n = ctx->n_user;
   const long long ld = ctx->ldm;
   cudaStream_t st = ctx->stream;
@@ -421,8 +489,14 @@ ghsvd_status phase2_reduce(Ctx* ctx) {
     GH_CUDA(cudaMemsetAsync(s.ctl, 0, 16, st));
     k += type;
   }
-  // Householder QR of G P2 (columns visited in P2 order)
+  // Householder QR of G P2 (columns visited in P2 order); with GHSVD_REDUCE_COLPIV the
+  // columns are pivoted by norm (P5), applied to p2 and to F's columns alike
+  const bool colpiv = (flags & GHSVD_REDUCE_COLPIV) != 0;
   for (int64_t kk = 0; kk < n; kk++) {
+    if (colpiv && kk < n - 1) {
+      k_qr_colnorms<<<(unsigned)(n - kk), T2, 0, st>>>(ctx->G, ld, m, kk, p2, s);
+      k_qr_colpiv<<<1, T2, 0, st>>>(ctx->F, ld, m, n, kk, p2, s);
+    }
     k_qr_prep<<<1, T2, 0, st>>>(ctx->G, ld, m, kk, p2, s);
     if (n - kk - 1 > 0)
       k_refl_apply<<<(unsigned)(n - kk - 1), T2, 0, st>>>(ctx->G, ld, nullptr, m, kk, kk + 1, p2, 0, s);

@@ -264,8 +264,9 @@ class Context:
         self._check(self._L.ghsvd_factor(self._h, NA, NL, NG, pa, pb, pu, ptaa, ptab, ptbb), "factor")
         self.m, self.n = 2 * NA * NL, NG
 
-    def reduce(self):
-        self._check(self._L.ghsvd_reduce(self._h, 0), "reduce")
+    def reduce(self, colpiv: bool = False):
+        """Phase 2; colpiv: column-pivoted QR of G P2 (GHSVD_REDUCE_COLPIV)."""
+        self._check(self._L.ghsvd_reduce(self._h, 1 if colpiv else 0), "reduce")
         self.m = self.n
 
     def get_factors(self):

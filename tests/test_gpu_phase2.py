@@ -70,3 +70,57 @@ def test_config2_like_reduce_then_sweep(gh):
     res = np.linalg.norm(Hx - Sx * lam[None, :], axis=0) / (nf2 * np.linalg.norm(Z, axis=0))
     assert res.max() <= 1e-12 * n
     ctx.close()
+
+
+@pytest.mark.parametrize("m,n,neg", [(200, 40, 0.4), (150, 150, 0.5), (97, 31, 0.5)])
+def test_reduce_colpiv_grammians(gh, m, n, neg):
+    """GHSVD_REDUCE_COLPIV: the QR of G P2 with column pivoting,
+    F' = F P5.  The exported permutation is P2 P5: the Grammians are those of the original
+    pencil under it, G' is upper triangular with a real non-negative, non-increasing
+    diagonal (each pivot is the largest remaining column norm)."""
+    P = inputs.random_pencil(70 + m, m, n, neg)
+    ctx = gh.Context(m, n)
+    ctx.set_factors(P.F, P.J, P.G)
+    ctx.reduce(colpiv=True)
+    F, J, G, p = ctx.get_factors()
+    if n % 2:
+        F, G, J = F[:-1, :-1], G[:-1, :-1], J[:-1]
+    assert F.shape == (n, n) and sorted(p) == list(range(n))
+    H = P.F.conj().T @ (P.J[:, None] * P.F)
+    S = P.G.conj().T @ P.G
+    Hp, Sp = H[np.ix_(p, p)], S[np.ix_(p, p)]
+    assert np.linalg.norm(F.conj().T @ (J[:, None] * F) - Hp) / np.linalg.norm(H) < 1e-11
+    assert np.linalg.norm(G.conj().T @ G - Sp) / np.linalg.norm(S) < 1e-12
+    assert np.abs(np.tril(G, -1)).max() == 0
+    d = np.diag(G)
+    assert np.all(d.real >= 0) and np.all(d.imag == 0)
+    assert np.all(np.diff(d.real) <= 1e-12 * d.real[0])
+    ctx.close()
+
+
+def test_colpiv_reduce_on_illconditioned_matches_tall(gh):
+    """A config-3 analog (S singular values 1 ... 1e-12): the eigenvalues after the
+    column-pivoted Phase 2 agree with the tall (Phase-2-skipped) computation to 1e-6
+    (BASELINE's ill-conditioned tolerance), with residuals on the original pencil."""
+    at = inputs.illcond_atoms(3, 4, 40, 128)
+    m, n = 2 * 4 * 40, 128
+    lams = {}
+    for mode in ("tall", "colpiv"):
+        ctx = gh.Context(m, n, 40, variant="bo")
+        ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+        if mode == "colpiv":
+            ctx.reduce(colpiv=True)
+        st = ctx.sweep()
+        lam, sf, sg, Z = ctx.extract()
+        ctx.close()
+        assert st["converged"]
+        lams[mode] = (lam, Z)
+    a, b = np.sort(lams["tall"][0]), np.sort(lams["colpiv"][0])
+    assert np.max(np.abs(a - b) / np.abs(a)) <= 1e-6
+    Fo, Jo, Go = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    lam, Z = lams["colpiv"]
+    Hx = Fo.conj().T @ (Jo[:, None] * (Fo @ Z))
+    Sx = Go.conj().T @ (Go @ Z)
+    nf2 = np.linalg.norm(Fo) ** 2 + np.linalg.norm(Go) ** 2
+    res = np.linalg.norm(Hx - Sx * lam[None, :], axis=0) / (nf2 * np.linalg.norm(Z, axis=0))
+    assert res.max() <= 1e-12 * n

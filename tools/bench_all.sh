@@ -8,7 +8,7 @@ for c in 0 1 2; do
     python bench.py --config $c --variant $v --no-cpu-baseline > $OUT/bench_c${c}_${v}.log 2>&1
   done
 done
-python bench.py --config 3 --variant bo > $OUT/bench_c3_bo.log 2>&1
+python bench.py --config 3 --variant bo --no-cpu-baseline > $OUT/bench_c3_bo.log 2>&1
 python bench.py --config 5 --variant bo --no-cpu-baseline > $OUT/bench_c5_bo.log 2>&1
 python bench.py --config 5 --variant bo --no-cpu-baseline --want-x > $OUT/bench_c5_bo_x.log 2>&1
 python bench.py --config 4 --variant bo --no-cpu-baseline --warmup 1 > $OUT/bench_c4_bo_w1.log 2>&1

@@ -34,7 +34,24 @@ for variant, nb in (("bo", 4), ("fb", 6)):
     lam, *_ = ctx.extract()
     ctx.close()
     check(lam, P.lam_true)
+for env in ({"GHSVD_PIVOT_CL": "1"}, {"GHSVD_GROUPS": "2"}, {"GHSVD_GRAM3M": "0"}, {"GHSVD_SERIAL": "1"}):
+    os.environ.update(env)
+    ctx = ghsvd.Context(130, 61, variant="bo", nblocks=6, want_x=True)
+    ctx.set_factors(P.F, P.J, P.G)
+    ctx.sweep()
+    lam, *_ = ctx.extract()
+    X = ctx.extract_x()
+    ctx.close()
+    check(lam, P.lam_true)
+    for k in env:
+        del os.environ[k]
 at = inputs.lapw_atoms(5, 3, 6, 20, 0.5)
+ctx = ghsvd.Context(36, 20, 6, variant="bo", nblocks=2)
+ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+ctx.reduce(colpiv=True)
+ctx.sweep()
+lam, *_ = ctx.extract()
+ctx.close()
 ctx = ghsvd.Context(36, 20, 6, variant="bo", nblocks=2)
 ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
 ctx.reduce()

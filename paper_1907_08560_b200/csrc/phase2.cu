@@ -83,6 +83,35 @@ __device__ double2 jdot(const double2* x, const double2* y, const int8_t* J, lon
   return block_sum2(a, sh);
 }
 
+// Block-wide argmax (largest value, smallest index on ties: the same choice as a
+// sequential scan keeping the first strict maximum); result valid in every thread.
+// Threads with no candidate pass v = -1 (all candidates are >= 0).
+__device__ void block_argmax(double& v, long long& i) {
+  __shared__ double bv[T2 / 32];
+  __shared__ long long bi[T2 / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    if (v2 > v || (v2 == v && i2 < i)) {
+      v = v2;
+      i = i2;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    bv[threadIdx.x >> 5] = v;
+    bi[threadIdx.x >> 5] = i;
+  }
+  __syncthreads();
+  v = bv[0];
+  i = bi[0];
+  for (int w = 1; w < T2 / 32; w++)
+    if (bv[w] > v || (bv[w] == v && bi[w] < i)) {
+      v = bv[w];
+      i = bi[w];
+    }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(T2) k_jnorms(const double2* F, long long ld, const int8_t* J, long long m,
                                                long long k, P2Scr s) {
   __shared__ double2 sh[T2 / 32];
@@ -103,15 +132,16 @@ __device__ void swap_cols_dev(double2* F, long long ld, long long rows, long lon
 // argmax |hd| over [k, n) (first index), swap columns k <-> jm, p2, hd
 __global__ void __launch_bounds__(T2) k_piv_a(double2* F, long long ld, long long m, long long n, long long k,
                                               long long* p2, P2Scr s) {
-  __shared__ long long jm_sh;
-  if (threadIdx.x == 0) {
-    long long jm = k;
-    for (long long j = k; j < n; j++)
-      if (fabs(s.hd[j]) > fabs(s.hd[jm])) jm = j;
-    jm_sh = jm;
+  double v = -1.0;
+  long long jm = 0x7fffffffffffffffll;
+  for (long long j = k + threadIdx.x; j < n; j += T2) {
+    const double a = fabs(s.hd[j]);
+    if (a > v) {
+      v = a;
+      jm = j;
+    }
   }
-  __syncthreads();
-  const long long jm = jm_sh;
+  block_argmax(v, jm);
   swap_cols_dev(F, ld, m, k, jm);
   if (threadIdx.x == 0 && jm != k) {
     const long long t = p2[k]; p2[k] = p2[jm]; p2[jm] = t;
@@ -131,15 +161,17 @@ __global__ void __launch_bounds__(T2) k_dots(const double2* F, long long ld, con
   if (threadIdx.x == 0) out[j] = v;
 }
 
-__global__ void k_piv_b(long long n, long long k, P2Scr s) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(T2) k_piv_b(long long n, long long k, P2Scr s) {
   const double alpha = (1.0 + sqrt(17.0)) / 8.0;
-  long long ii = k + 1;
+  long long ii = 0x7fffffffffffffffll;
   double h1i = -1.0;
-  for (long long j = k + 1; j < n; j++) {
+  for (long long j = k + 1 + threadIdx.x; j < n; j += T2) {
     const double a = cabs_(s.d1[j]);
     if (a > h1i) { h1i = a; ii = j; }
   }
+  block_argmax(h1i, ii);
+  if (threadIdx.x != 0) return;
+  if (ii == 0x7fffffffffffffffll) ii = k + 1;
   s.ctl[1] = (int)ii;
   const double h11 = fabs(s.hd[k]);
   s.ctl[2] = !(h11 >= alpha * h1i);
@@ -150,17 +182,22 @@ __global__ void k_piv_b(long long n, long long k, P2Scr s) {
 __global__ void __launch_bounds__(T2) k_piv_c(double2* F, long long ld, long long m, long long n, long long k,
                                               long long* p2, P2Scr s) {
   __shared__ int act;  // 0: nothing, 1: swap k<->ii (1x1), 2: swap k+1<->ii (2x2)
+  double hij = -1.0;
+  if (s.ctl[2]) {   // uniform over the block
+    const long long ii = s.ctl[1];
+    long long li = 0x7fffffffffffffffll;
+    for (long long l = k + threadIdx.x; l < n; l += T2) {
+      if (l == ii) continue;
+      const double a = cabs_(s.d2[l]);
+      if (a > hij) { hij = a; li = l; }
+    }
+    block_argmax(hij, li);
+  }
   if (threadIdx.x == 0) {
     act = 0;
     if (s.ctl[2]) {
       const double alpha = (1.0 + sqrt(17.0)) / 8.0;
       const long long ii = s.ctl[1];
-      double hij = -1.0;
-      for (long long l = k; l < n; l++) {
-        if (l == ii) continue;
-        const double a = cabs_(s.d2[l]);
-        if (a > hij) hij = a;
-      }
       const double h11 = fabs(s.hd[k]), h1i = s.dctl[12];
       if (h11 * hij >= alpha * h1i * h1i) {
         act = 0;
@@ -187,7 +224,6 @@ __global__ void __launch_bounds__(T2) k_piv_c(double2* F, long long ld, long lon
 __global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8_t* J, long long m, long long n,
                                                   long long k, P2Scr s) {
   __shared__ double2 sh[T2 / 32];
-  __shared__ long long best_sh;
   double2* f = F + k * ld;
   const double hn = jdot(f, f, J, k, m, true, sh).x;
   if (hn == 0.0 || !isfinite(hn)) {
@@ -195,16 +231,13 @@ __global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8
     return;
   }
   const int8_t sg = hn > 0.0 ? 1 : -1;
-  if (J[k] != sg) {
-    if (threadIdx.x == 0) {
-      long long best = -1;
-      double bv = -1.0;
-      for (long long i = k; i < m; i++)
-        if (J[i] == sg && cabs_(f[i]) > bv) { bv = cabs_(f[i]); best = i; }
-      best_sh = best;
-    }
-    __syncthreads();
-    const long long best = best_sh;
+  if (J[k] != sg) {   // uniform over the block
+    double bv = -1.0;
+    long long best = 0x7fffffffffffffffll;
+    for (long long i = k + threadIdx.x; i < m; i += T2)
+      if (J[i] == sg && cabs_(f[i]) > bv) { bv = cabs_(f[i]); best = i; }
+    block_argmax(bv, best);
+    if (best == 0x7fffffffffffffffll) best = -1;
     if (best < 0) {
       if (threadIdx.x == 0) s.ctl[3] = -7;
       return;
@@ -458,7 +491,7 @@ ghsvd_status phase2_reduce(Ctx* ctx, int flags) {
     k_piv_a<<<1, T2, 0, st>>>(ctx->F, ld, m, n, k, p2, s);
     if (k < n - 1) {
       k_dots<<<(unsigned)(n - k - 1), T2, 0, st>>>(ctx->F, ld, ctx->J, m, k, k + 1, nullptr, k, 0, s, s.d1);
-      k_piv_b<<<1, 32, 0, st>>>(n, k, s);
+      k_piv_b<<<1, T2, 0, st>>>(n, k, s);
       k_dots<<<(unsigned)(n - k), T2, 0, st>>>(ctx->F, ld, ctx->J, m, k, k, s.ctl + 1, 0, 1, s, s.d2);
       k_piv_c<<<1, T2, 0, st>>>(ctx->F, ld, m, n, k, p2, s);
     } else {

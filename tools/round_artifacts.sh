@@ -9,8 +9,8 @@ python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; tail -2 $OUT/pyt
 python bench.py > $OUT/bench_c3_bo.log 2>&1; tail -c 400 $OUT/bench_c3_bo.log; echo
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_blk -c 3000 --csv \
     --log-file $OUT/launches_bench_bo.csv python bench.py --no-cpu-baseline --warmup 0 --steps 1 > $OUT/ncu_bench.log 2>&1
-# bench schedule launch order per block step: gram0 pivot0 upd0(bnd) upd0b gram1 pivot1 upd1(bnd) upd1b updZ
-ncu --set full --clock-control none --import-source on -k regex:"k_blk_(update|gram|pivot)" -s 9 -c 4 \
+# bench schedule launch order per block step: gram0 pivot0 upd0 gram1 pivot1 upd1 updZ (k_blk launches 8-10 = step 1, half 0)
+ncu --set full --clock-control none --import-source on -k regex:"k_blk_(update|gram|pivot)" -s 7 -c 3 \
     -o $OUT/prof_blk python tools/profile_step.py --variant bo --sweep > $OUT/ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pair_step -s 2 -c 1 \
     -o $OUT/prof_pw python tools/profile_step.py --kernel 2 --steps 4 > $OUT/ncu_pw.log 2>&1

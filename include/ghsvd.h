@@ -60,7 +60,14 @@ typedef struct {
   void* stream;        /* cudaStream_t owned by the caller (e.g. a torch stream); NULL = legacy default */
   int world_size;      /* 1 for a single GPU */
   int rank;            /* 0 .. world_size-1 */
-  const void* nccl_id; /* 128-byte ncclUniqueId shared by all ranks; NULL if world_size == 1 */
+  const void* nccl_id; /* 128-byte ncclUniqueId shared by all ranks; NULL if world_size == 1.
+                        * Loopback id (test transport): 16 bytes "GHSVD-LOOPBACK\0\0" then a
+                        * 112-byte group key.  The world_size ranks are then contexts of ONE
+                        * process on one device, each driven from its own host thread (every
+                        * call is collective, as with NCCL); block columns and reductions move
+                        * by device copies between the contexts' workspaces, ordered by CUDA
+                        * events and a host barrier (600 s timeout -> GHSVD_E_NCCL).  It runs
+                        * the multi-GPU schedule of the blocked sweep without several GPUs. */
   int variant;         /* GHSVD_POINTWISE | GHSVD_BLOCKED_BO | GHSVD_BLOCKED_FB */
   int ordering;        /* GHSVD_ORDER_ROUND_ROBIN */
   int nblocks;         /* blocked: number of block columns (even; 0 = auto); Sec 6.4.1 */

@@ -14,6 +14,11 @@
 #include <nccl.h>
 #include <string.h>
 
+#include <chrono>
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -109,11 +114,8 @@ struct Nccl {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
-static Nccl* nccl() {
+static Nccl* load_nccl() {
   static Nccl n;
-  static bool tried = false;
-  if (tried) return n.h ? &n : nullptr;
-  tried = true;
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
   for (const char* nm : names) {
     n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
@@ -137,6 +139,12 @@ static Nccl* nccl() {
   return &n;
 }
 
+// loaded once (thread-safe static initialisation: loopback ranks call in from several threads)
+static Nccl* nccl() {
+  static Nccl* const n = load_nccl();
+  return n;
+}
+
 #define NCCL_CALL(x)                                                                            \
   do {                                                                                          \
     ncclResult_t r_ = (x);                                                                      \
@@ -146,7 +154,93 @@ static Nccl* nccl() {
     }                                                                                           \
   } while (0)
 
+// ------------------------------------------------------------------ loopback transport
+// Test transport (include/ghsvd.h, "loopback id"): the world_size ranks are contexts of
+// ONE process on one device, each driven by its own host thread.  The exchange and the
+// reductions are the NCCL calls' effect written as device copies between the contexts'
+// workspaces, ordered by CUDA events and a host barrier; no kernel ever waits on another
+// rank's kernel, so the ranks' streams may share a GPU.  Everything above the transport
+// (ownership, halves schedule, events, stop decision) is the multi-GPU code path itself.
+struct LoopGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool broken = false;
+  std::vector<Ctx*> ctx;
+  std::vector<cudaEvent_t> ev_done, ev_copy;
+  std::vector<DevCounters> cnt;
+  int joined = 0;
+  // host barrier over the group's ranks; false on timeout (a rank failed) -- the group
+  // is then broken and every later barrier fails at once
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
+    const unsigned long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(600), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+
+struct CommHandle {
+  int kind;                           // 1 NCCL, 2 loopback
+  ncclComm_t nccl;
+  std::shared_ptr<LoopGroup> loop;
+};
+
+static const char kLoopTag[16] = {'G', 'H', 'S', 'V', 'D', '-', 'L', 'O', 'O', 'P', 'B', 'A', 'C', 'K', 0, 0};
+static std::mutex g_loop_mu;
+static std::map<std::string, std::weak_ptr<LoopGroup>> g_loop_groups;
+
+static CommHandle* handle(Ctx* ctx) { return (CommHandle*)ctx->comm; }
+
+static ghsvd_status loop_init(Ctx* ctx, const char* id) {
+  const std::string key(id + 16, 112);
+  std::shared_ptr<LoopGroup> g;
+  {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    auto it = g_loop_groups.find(key);
+    if (it != g_loop_groups.end()) g = it->second.lock();
+    if (!g || g->broken) {
+      g = std::make_shared<LoopGroup>();
+      g->world = ctx->o.world_size;
+      g->ctx.assign(g->world, nullptr);
+      g->ev_done.assign(g->world, nullptr);
+      g->ev_copy.assign(g->world, nullptr);
+      g->cnt.assign(g->world, DevCounters{});
+      g_loop_groups[key] = g;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    const int r = ctx->o.rank;
+    if (g->world != ctx->o.world_size || g->ctx[r]) {
+      ctx->err = "loopback: world_size mismatch or rank joined twice";
+      return GHSVD_E_INVALID_ARG;
+    }
+    g->ctx[r] = ctx;
+    GH_CUDA(cudaEventCreateWithFlags(&g->ev_done[r], cudaEventDisableTiming));
+    GH_CUDA(cudaEventCreateWithFlags(&g->ev_copy[r], cudaEventDisableTiming));
+    g->joined++;
+  }
+  CommHandle* c = new CommHandle{2, nullptr, g};
+  ctx->comm = c;
+  return GHSVD_OK;
+}
+
 ghsvd_status comm_init(Ctx* ctx) {
+  if (ctx->o.nccl_id && memcmp(ctx->o.nccl_id, kLoopTag, 16) == 0) return loop_init(ctx, (const char*)ctx->o.nccl_id);
   Nccl* N = nccl();
   if (!N) {
     ctx->err = "multi-GPU: libnccl.so.2 could not be loaded";
@@ -156,21 +250,71 @@ ghsvd_status comm_init(Ctx* ctx) {
   memcpy(&id, ctx->o.nccl_id, sizeof(id));
   ncclComm_t c;
   NCCL_CALL(N->CommInitRank(&c, ctx->o.world_size, id, ctx->o.rank));
-  ctx->comm = c;
+  ctx->comm = new CommHandle{1, c, nullptr};
   return GHSVD_OK;
 }
 
 void comm_destroy(Ctx* ctx) {
-  Nccl* N = nccl();
-  if (N && ctx->comm && N->CommDestroy) N->CommDestroy((ncclComm_t)ctx->comm);
+  CommHandle* c = handle(ctx);
+  if (!c) return;
+  if (c->kind == 1) {
+    Nccl* N = nccl();
+    if (N && N->CommDestroy) N->CommDestroy(c->nccl);
+  } else if (c->loop) {
+    LoopGroup* g = c->loop.get();
+    std::lock_guard<std::mutex> lk(g->mu);
+    const int r = ctx->o.rank;
+    if (g->ev_done[r]) cudaEventDestroy(g->ev_done[r]);
+    if (g->ev_copy[r]) cudaEventDestroy(g->ev_copy[r]);
+    g->ev_done[r] = g->ev_copy[r] = nullptr;
+    g->ctx[r] = nullptr;
+  }
+  delete c;
   ctx->comm = nullptr;
+}
+
+static ghsvd_status loop_broken(Ctx* ctx) {
+  ctx->err = "loopback: another rank did not reach the barrier (failed or timed out)";
+  return GHSVD_E_NCCL;
+}
+
+// The NCCL exchange's effect: every rank pulls the block columns it receives from the
+// sending rank's buffers once that rank's step is complete (ev_done), and no rank writes
+// its buffers again before every pull of this exchange is done (ev_copy of all ranks).
+static ghsvd_status loop_exchange(Ctx* ctx, const int64_t* rb, const int64_t* rp, int64_t nr, const int* bstart,
+                                  const int* bwidth) {
+  LoopGroup* g = handle(ctx)->loop.get();
+  const int r = ctx->o.rank;
+  cudaStream_t st = ctx->stream;
+  GH_CUDA(cudaEventRecord(g->ev_done[r], st));
+  if (!g->barrier()) return loop_broken(ctx);
+  for (int64_t i = 0; i < nr; i++) {
+    const Ctx* pc = g->ctx[rp[i]];
+    if (!pc || pc->ldm != ctx->ldm || pc->ldn != ctx->ldn || pc->m != ctx->m || pc->n != ctx->n) {
+      ctx->err = "loopback: ranks hold different problem shapes";
+      return GHSVD_E_INVALID_ARG;
+    }
+    GH_CUDA(cudaStreamWaitEvent(st, g->ev_done[rp[i]], 0));
+    const size_t b = (size_t)rb[i], c0 = (size_t)bstart[b], w = (size_t)bwidth[b];
+    GH_CUDA(cudaMemcpyAsync(ctx->F + c0 * ctx->ldm, pc->F + c0 * pc->ldm, w * ctx->ldm * 16, cudaMemcpyDeviceToDevice, st));
+    GH_CUDA(cudaMemcpyAsync(ctx->G + c0 * ctx->ldm, pc->G + c0 * pc->ldm, w * ctx->ldm * 16, cudaMemcpyDeviceToDevice, st));
+    GH_CUDA(cudaMemcpyAsync(ctx->Z + c0 * ctx->ldn, pc->Z + c0 * pc->ldn, w * ctx->ldn * 16, cudaMemcpyDeviceToDevice, st));
+    if (ctx->o.want_x && ctx->W && pc->W)
+      GH_CUDA(cudaMemcpyAsync(ctx->W + c0 * ctx->ldn, pc->W + c0 * pc->ldn, w * ctx->ldn * 16,
+                              cudaMemcpyDeviceToDevice, st));
+  }
+  GH_CUDA(cudaEventRecord(g->ev_copy[r], st));
+  if (!g->barrier()) return loop_broken(ctx);
+  for (int p = 0; p < g->world; p++)
+    if (p != r) GH_CUDA(cudaStreamWaitEvent(st, g->ev_copy[p], 0));
+  return GHSVD_OK;
 }
 
 // Move the block columns (F, G: m rows; Z: n rows) whose owner changes between
 // block steps s_now and s_next.  A block column is contiguous in each buffer.
 ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart, const int* bwidth) {
   Nccl* N = nccl();
-  if (!N || !ctx->comm) {
+  if (!ctx->comm || (!N && handle(ctx)->kind == 1)) {
     ctx->err = "multi-GPU: no communicator";
     return GHSVD_E_NCCL;
   }
@@ -181,8 +325,9 @@ ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int*
     ctx->err = "multi-GPU: bad exchange plan arguments";
     return GHSVD_E_INVALID_ARG;
   }
+  if (handle(ctx)->kind == 2) return loop_exchange(ctx, rb.data(), rp.data(), nr, bstart, bwidth);
   if (ns == 0 && nr == 0) return GHSVD_OK;
-  ncclComm_t comm = (ncclComm_t)ctx->comm;
+  ncclComm_t comm = handle(ctx)->nccl;
   cudaStream_t st = ctx->stream;
   NCCL_CALL(N->GroupStart());
   auto xfer = [&](int64_t b, int peer, bool send) -> ncclResult_t {
@@ -208,11 +353,28 @@ ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int*
 // Sum all/big, max off, min err over ranks (one small allreduce group per sweep).
 ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c) {
   Nccl* N = nccl();
-  if (!N || !ctx->comm) {
+  if (!ctx->comm || (!N && handle(ctx)->kind == 1)) {
     ctx->err = "multi-GPU: no communicator";
     return GHSVD_E_NCCL;
   }
-  ncclComm_t comm = (ncclComm_t)ctx->comm;
+  if (handle(ctx)->kind == 2) {
+    // *c holds this rank's counters (read back by the caller); combine in rank order
+    LoopGroup* g = handle(ctx)->loop.get();
+    g->cnt[ctx->o.rank] = *c;
+    if (!g->barrier()) return loop_broken(ctx);
+    DevCounters t{};
+    for (int p = 0; p < g->world; p++) {
+      const DevCounters& q = g->cnt[p];
+      t.all += q.all;
+      t.big += q.big;
+      t.off_bits = q.off_bits > t.off_bits ? q.off_bits : t.off_bits;
+      t.err = q.err < t.err ? q.err : t.err;
+    }
+    if (!g->barrier()) return loop_broken(ctx);
+    *c = t;
+    return GHSVD_OK;
+  }
+  ncclComm_t comm = handle(ctx)->nccl;
   cudaStream_t st = ctx->stream;
   DevCounters* d = ctx->cnt;  // device copy (already holds this rank's values)
   NCCL_CALL(N->GroupStart());
@@ -230,13 +392,40 @@ ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c) {
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam, double* sf,
                                    double* sg, double2* Zout, int64_t ldz, double2* Xout) {
   Nccl* N = nccl();
-  if (!N || !ctx->comm) {
+  if (!ctx->comm || (!N && handle(ctx)->kind == 1)) {
     ctx->err = "multi-GPU: no communicator";
     return GHSVD_E_NCCL;
   }
   std::vector<int> own;
   owners(nblk, ctx->o.world_size, 0, own);
   cudaStream_t st = ctx->stream;
+  if (handle(ctx)->kind == 2) {
+    // the sum of the disjointly owned outputs, as a gather from each column's owner
+    // (the outputs are the owners' context buffers: lam, sf, sg, Z2, Xo)
+    LoopGroup* g = handle(ctx)->loop.get();
+    const int r = ctx->o.rank;
+    GH_CUDA(cudaEventRecord(g->ev_done[r], st));
+    if (!g->barrier()) return loop_broken(ctx);
+    for (int b = 0; b < nblk; b++) {
+      const int p = own[b];
+      if (p == r) continue;
+      const Ctx* pc = g->ctx[p];
+      GH_CUDA(cudaStreamWaitEvent(st, g->ev_done[p], 0));
+      const size_t c0 = (size_t)bstart[b], w = (size_t)bwidth[b];
+      GH_CUDA(cudaMemcpyAsync(lam + c0, pc->lam + c0, w * 8, cudaMemcpyDeviceToDevice, st));
+      GH_CUDA(cudaMemcpyAsync(sf + c0, pc->sf + c0, w * 8, cudaMemcpyDeviceToDevice, st));
+      GH_CUDA(cudaMemcpyAsync(sg + c0, pc->sg + c0, w * 8, cudaMemcpyDeviceToDevice, st));
+      GH_CUDA(cudaMemcpyAsync(Zout + c0 * ldz, pc->Z2 + c0 * ldz, w * ldz * 16, cudaMemcpyDeviceToDevice, st));
+      if (Xout && pc->Xo)
+        GH_CUDA(cudaMemcpy2DAsync(Xout + c0, (size_t)ldz * 16, pc->Xo + c0, (size_t)ldz * 16, w * 16,
+                                  (size_t)ctx->n, cudaMemcpyDeviceToDevice, st));
+    }
+    GH_CUDA(cudaEventRecord(g->ev_copy[r], st));
+    if (!g->barrier()) return loop_broken(ctx);
+    for (int p = 0; p < g->world; p++)
+      if (p != r) GH_CUDA(cudaStreamWaitEvent(st, g->ev_copy[p], 0));
+    return GHSVD_OK;
+  }
   for (int b = 0; b < nblk; b++) {
     if (own[b] == ctx->o.rank) continue;
     const size_t c0 = (size_t)bstart[b], w = (size_t)bwidth[b];
@@ -247,7 +436,7 @@ ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const 
     if (Xout)  // rows c0 .. c0+w-1 of X belong to this block column of W^T
       GH_CUDA(cudaMemset2DAsync(Xout + c0, (size_t)ldz * 16, 0, w * 16, (size_t)ctx->n, st));
   }
-  ncclComm_t comm = (ncclComm_t)ctx->comm;
+  ncclComm_t comm = handle(ctx)->nccl;
   const size_t n = (size_t)ctx->n;
   NCCL_CALL(N->GroupStart());
   NCCL_CALL(N->AllReduce(lam, lam, n, ncclFloat64, ncclSum, comm, st));

@@ -390,5 +390,14 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def loopback_id(key: str) -> bytes:
+    """128-byte id of the loopback test transport (include/ghsvd.h, nccl_id): the ranks of
+    group `key` are contexts of this process on one device, each driven by its own thread."""
+    k = key.encode()
+    if len(k) > 112:
+        raise ValueError("loopback key longer than 112 bytes")
+    return b"GHSVD-LOOPBACK\0\0" + k + b"\0" * (112 - len(k))
+
+
 def version() -> str:
     return load().ghsvd_version().decode()

@@ -1,0 +1,135 @@
+"""The multi-GPU blocked sweep (Sec 6.4.3) run on
+ONE GPU through the loopback transport (include/ghsvd.h, nccl_id).
+
+P contexts in this process, one host thread each, play the P ranks: each owns the
+round-robin slots ghsvd_block_owner assigns to it, runs the multi-rank halves schedule on
+its own stream, and after every block step pulls the block columns of F, G, Z (and W)
+it receives from their previous owner (the ncclSend / ncclRecv pair's effect), with the
+counters combined once per sweep and the outputs gathered at extraction.  No kernel waits
+on another rank's kernel (CUDA events + a host barrier order the copies), so the ranks
+may share the GPU.  Every block pair's arithmetic is the same in any launch grouping and
+the Gram split is planned from the global pair count, so the result must be BITWISE equal
+to the single-rank solve with the same partition -- a missing or stale block column, a
+wrong owner or a wrong stop decision breaks equality.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from paper_1907_08560_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gh():
+    from paper_1907_08560_b200 import build, ghsvd
+    build.build()
+    return ghsvd
+
+
+def load(c, P):
+    if hasattr(P, "F"):
+        c.set_factors(P.F, P.J, P.G)
+    else:   # Phase-1 atoms: every rank factors the same atoms (deterministic, no comm)
+        c.factor(P.A, P.B, P.U, P.TAA, P.TAB, P.TBB)
+
+
+def shape(P):
+    if hasattr(P, "F"):
+        return P.F.shape[0], P.F.shape[1], 0
+    NA, NL, NG = P.A.shape
+    return 2 * NA * NL, NG, NL
+
+
+def single(gh, P, nblocks, want_x):
+    m, n, nl = shape(P)
+    c = gh.Context(m, n, nl, variant="bo", nblocks=nblocks, max_sweeps=64, want_x=want_x)
+    load(c, P)
+    st = c.sweep()
+    out = c.extract()
+    X = c.extract_x() if want_x else None
+    c.close()
+    return st, out, X
+
+
+def multi(gh, P, nblocks, world, want_x, key):
+    import torch
+    m, n, nl = shape(P)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    lid = gh.loopback_id(key)
+    ctxs = [gh.Context(m, n, nl, variant="bo", nblocks=nblocks, max_sweeps=64, want_x=want_x, world_size=world,
+                       rank=r, nccl_id=lid, stream=streams[r]) for r in range(world)]
+    for c in ctxs:
+        load(c, P)
+    res = [None] * world
+    errs = []
+
+    def run(r):
+        try:
+            st = ctxs[r].sweep()
+            out = ctxs[r].extract()
+            X = ctxs[r].extract_x() if want_x else None
+            res[r] = (st, out, X)
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errs.append((r, repr(e)))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    assert not any(t.is_alive() for t in th), "a rank hung"
+    for c in ctxs:
+        c.close()
+    assert not errs, errs
+    return res
+
+
+def assert_same(a, b):
+    sta, (la, fa, ga, Za), Xa = a
+    stb, (lb, fb, gb, Zb), Xb = b
+    assert sta["sweeps"] == stb["sweeps"]
+    assert sta["converged"] == stb["converged"] == 1
+    assert sta["transforms_all"] == stb["transforms_all"]
+    assert sta["transforms_big"] == stb["transforms_big"]
+    for x, y in ((la, lb), (fa, fb), (ga, gb), (Za, Zb)):
+        np.testing.assert_array_equal(x, y)
+    if Xa is not None:
+        np.testing.assert_array_equal(Xa, Xb)
+
+
+@pytest.mark.parametrize("world,nblocks", [(2, 8), (2, 12), (4, 8), (4, 16), (8, 16)])
+def test_loopback_ranks_bitwise_equal_single(gh, world, nblocks):
+    P = inputs.known_hyperbolic(21, 400, 256, 0.4)
+    ref = single(gh, P, nblocks, False)
+    res = multi(gh, P, nblocks, world, False, f"t{world}_{nblocks}")
+    for r in range(world):
+        assert_same(res[r], ref)
+    # and the eigenvalues are the constructed ones
+    lam = np.sort(ref[1][0])
+    assert float(np.max(np.abs(lam - np.sort(P.lam_true)) / np.abs(np.sort(P.lam_true)))) <= 1e-9
+
+
+def test_loopback_want_x(gh):
+    """NEXT-1 with several ranks: W^T block columns travel with F, G, Z; X = Z^{-1}."""
+    P = inputs.known_hyperbolic(22, 300, 192, 0.5)
+    ref = single(gh, P, 12, True)
+    res = multi(gh, P, 12, 3, True, "x3")
+    for r in range(3):
+        assert_same(res[r], ref)
+    lam, sf, sg, Z = ref[1]
+    err = np.linalg.norm(ref[2] @ Z - np.eye(Z.shape[0])) / np.sqrt(Z.shape[0])
+    assert err <= 1e-9
+
+
+def test_loopback_illcond_tall(gh):
+    """Config-3 recipe at reduced size (Phase 1 on ill-conditioned atoms, S singular values
+    1 .. 1e-12, tall 2 N_A N_L x N_G factors), two and four ranks."""
+    at = inputs.illcond_atoms(33, 4, 49, 256, smin=1e-6)
+    ref = single(gh, at, 8, False)
+    for world in (2, 4):
+        res = multi(gh, at, 8, world, False, f"c3s{world}")
+        for r in range(world):
+            assert_same(res[r], ref)

@@ -153,6 +153,42 @@ def test_c3_blocked_eq71_errors(gh, c3):
         assert np.array_equal(lam, _C3_LAM["bo"][0]) and st["sweeps"] == _C3_LAM["bo"][1]
 
 
+def test_c3_two_ranks_loopback_bitwise(gh, c3):
+    """The multi-GPU schedule at the bench's full size: two ranks (loopback transport, one
+    GPU, two host threads; tests/test_gpu_multirank_loopback.py) reproduce the one-rank
+    solve's eigenvalues and sweep count bitwise."""
+    if "bo" not in _C3_LAM:
+        pytest.skip("needs the one-rank solve of test_c3_blocked_converges_with_residuals")
+    import threading
+    import torch
+    NA, NL, NG = c3.A.shape
+    lid = gh.loopback_id("c3_full_2")
+    ctxs = [gh.Context(2 * NA * NL, NG, NL, variant="bo", max_sweeps=64, world_size=2, rank=r, nccl_id=lid,
+                       stream=torch.cuda.Stream()) for r in range(2)]
+    for c in ctxs:
+        c.factor(c3.A, c3.B, c3.U, c3.TAA, c3.TAB, c3.TBB)
+    res, errs = [None, None], []
+
+    def run(r):
+        try:
+            st = ctxs[r].sweep()
+            res[r] = (st, ctxs[r].extract(want_z=False)[0])
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=1200)
+    for c in ctxs:
+        c.close()
+    assert not errs, errs
+    for st, lam in res:
+        assert st["converged"] and st["sweeps"] == _C3_LAM["bo"][1]
+        assert np.array_equal(lam, _C3_LAM["bo"][0])
+
+
 def test_c2_full_factor_reduce_sweep_vs_oracle(gh):
     """BASELINE configs[2]: LAPW 1568 x 1024 -> Phase 2 -> 1024^2 -> BO sweep, vs the oracle's
     blocked run (same partition) on the GPU's reduced factors; Phase 2 Grammians preserved."""

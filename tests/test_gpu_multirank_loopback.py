@@ -43,9 +43,9 @@ def shape(P):
     return 2 * NA * NL, NG, NL
 
 
-def single(gh, P, nblocks, want_x):
+def single(gh, P, nblocks, want_x, variant="bo"):
     m, n, nl = shape(P)
-    c = gh.Context(m, n, nl, variant="bo", nblocks=nblocks, max_sweeps=64, want_x=want_x)
+    c = gh.Context(m, n, nl, variant=variant, nblocks=nblocks, max_sweeps=64, want_x=want_x)
     load(c, P)
     st = c.sweep()
     out = c.extract()
@@ -54,12 +54,12 @@ def single(gh, P, nblocks, want_x):
     return st, out, X
 
 
-def multi(gh, P, nblocks, world, want_x, key):
+def multi(gh, P, nblocks, world, want_x, key, variant="bo"):
     import torch
     m, n, nl = shape(P)
     streams = [torch.cuda.Stream() for _ in range(world)]
     lid = gh.loopback_id(key)
-    ctxs = [gh.Context(m, n, nl, variant="bo", nblocks=nblocks, max_sweeps=64, want_x=want_x, world_size=world,
+    ctxs = [gh.Context(m, n, nl, variant=variant, nblocks=nblocks, max_sweeps=64, want_x=want_x, world_size=world,
                        rank=r, nccl_id=lid, stream=streams[r]) for r in range(world)]
     for c in ctxs:
         load(c, P)
@@ -110,6 +110,15 @@ def test_loopback_ranks_bitwise_equal_single(gh, world, nblocks):
     # and the eigenvalues are the constructed ones
     lam = np.sort(ref[1][0])
     assert float(np.max(np.abs(lam - np.sort(P.lam_true)) / np.abs(np.sort(P.lam_true)))) <= 1e-9
+
+
+def test_loopback_fb(gh):
+    """FB (inner sweeps to convergence) with two ranks."""
+    P = inputs.known_hyperbolic(23, 320, 192, 0.4)
+    ref = single(gh, P, 12, False, "fb")
+    res = multi(gh, P, 12, 2, False, "fb2", "fb")
+    for r in range(2):
+        assert_same(res[r], ref)
 
 
 def test_loopback_want_x(gh):

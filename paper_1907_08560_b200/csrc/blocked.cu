@@ -1096,8 +1096,6 @@ size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
 }
 
 // in comm.cpp
-ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart_h, const int* bwidth_h);
-ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c);
 
 struct BlkSetup {
   BlkPlan pl;
@@ -1580,15 +1578,27 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       launch_update(S, a, 0, pl.K, 2 * tF, 2 * tF + tZ, 0, aux);
       a.trace_id = s * TRACE_SLOTS + 9;
       if (a.W) launch_update(S, a, 0, pl.K, 0, tZ, 1, aux);
+      if (multi) {
+        // The exchange after step s in two parts (NEXT-2, comm/compute overlap): the Z', W
+        // block columns leave right after the Z' update, on the aux stream and a second
+        // communicator, while the F, G block columns leave as soon as the F, G updates of
+        // both halves are done -- the Grams of step s+1 need only F and G, so they no
+        // longer wait for the Z' update of step s (which keeps overlapping them, as on one
+        // GPU).  The next Z' update runs on the aux stream after the Z' exchange.
+        const int s_next = (s + 1) % nst;
+        ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data(), XCH_ZW, aux);
+        if (e) {
+          destroy_events();
+          return e;
+        }
+      }
       GH_CUDA(cudaEventRecord(ev_zdone[b], aux));
       GH_CUDA(cudaGetLastError());
       if (multi) {
-        // block columns (F, G and Z) leave only after every update of step s
         for (int h = 0; h < nh; h++)
           if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[h], 0));
-        GH_CUDA(cudaStreamWaitEvent(str, ev_zdone[b], 0));
         const int s_next = (s + 1) % nst;
-        ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data());
+        ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data(), XCH_FG, str);
         if (e) {
           destroy_events();
           return e;

@@ -105,6 +105,7 @@ struct Nccl {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -125,13 +126,14 @@ static Nccl* load_nccl() {
   n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
   n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
   n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+  n.CommSplit = (decltype(n.CommSplit))dlsym(n.h, "ncclCommSplit");
   n.Send = (decltype(n.Send))dlsym(n.h, "ncclSend");
   n.Recv = (decltype(n.Recv))dlsym(n.h, "ncclRecv");
   n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
   n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
   n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
   n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
-  if (!n.GetUniqueId || !n.CommInitRank || !n.Send || !n.Recv || !n.GroupStart || !n.GroupEnd || !n.AllReduce) {
+  if (!n.GetUniqueId || !n.CommInitRank || !n.CommSplit || !n.Send || !n.Recv || !n.GroupStart || !n.GroupEnd || !n.AllReduce) {
     dlclose(n.h);
     n.h = nullptr;
     return nullptr;
@@ -195,7 +197,8 @@ struct LoopGroup {
 
 struct CommHandle {
   int kind;                           // 1 NCCL, 2 loopback
-  ncclComm_t nccl;
+  ncclComm_t nccl;                    // F, G exchange, counters, outputs (context stream)
+  ncclComm_t nccl_zw;                 // Z', W exchange (aux stream; split of nccl)
   std::shared_ptr<LoopGroup> loop;
 };
 
@@ -234,7 +237,7 @@ static ghsvd_status loop_init(Ctx* ctx, const char* id) {
     GH_CUDA(cudaEventCreateWithFlags(&g->ev_copy[r], cudaEventDisableTiming));
     g->joined++;
   }
-  CommHandle* c = new CommHandle{2, nullptr, g};
+  CommHandle* c = new CommHandle{2, nullptr, nullptr, g};
   ctx->comm = c;
   return GHSVD_OK;
 }
@@ -248,9 +251,17 @@ ghsvd_status comm_init(Ctx* ctx) {
   }
   ncclUniqueId id;
   memcpy(&id, ctx->o.nccl_id, sizeof(id));
-  ncclComm_t c;
+  ncclComm_t c, cz;
   NCCL_CALL(N->CommInitRank(&c, ctx->o.world_size, id, ctx->o.rank));
-  ctx->comm = new CommHandle{1, c, nullptr};
+  // second communicator for the Z', W block columns: their exchange runs on another
+  // stream, concurrently with the F, G traffic and the next step's kernels
+  ncclResult_t r = N->CommSplit(c, 0, ctx->o.rank, &cz, nullptr);
+  if (r != ncclSuccess) {
+    N->CommDestroy(c);
+    ctx->err = std::string("ncclCommSplit: ") + (N->GetErrorString ? N->GetErrorString(r) : "error");
+    return GHSVD_E_NCCL;
+  }
+  ctx->comm = new CommHandle{1, c, cz, nullptr};
   return GHSVD_OK;
 }
 
@@ -259,7 +270,10 @@ void comm_destroy(Ctx* ctx) {
   if (!c) return;
   if (c->kind == 1) {
     Nccl* N = nccl();
-    if (N && N->CommDestroy) N->CommDestroy(c->nccl);
+    if (N && N->CommDestroy) {
+      if (c->nccl_zw) N->CommDestroy(c->nccl_zw);
+      N->CommDestroy(c->nccl);
+    }
   } else if (c->loop) {
     LoopGroup* g = c->loop.get();
     std::lock_guard<std::mutex> lk(g->mu);
@@ -282,10 +296,9 @@ static ghsvd_status loop_broken(Ctx* ctx) {
 // sending rank's buffers once that rank's step is complete (ev_done), and no rank writes
 // its buffers again before every pull of this exchange is done (ev_copy of all ranks).
 static ghsvd_status loop_exchange(Ctx* ctx, const int64_t* rb, const int64_t* rp, int64_t nr, const int* bstart,
-                                  const int* bwidth) {
+                                  const int* bwidth, int part, cudaStream_t st) {
   LoopGroup* g = handle(ctx)->loop.get();
   const int r = ctx->o.rank;
-  cudaStream_t st = ctx->stream;
   GH_CUDA(cudaEventRecord(g->ev_done[r], st));
   if (!g->barrier()) return loop_broken(ctx);
   for (int64_t i = 0; i < nr; i++) {
@@ -296,12 +309,16 @@ static ghsvd_status loop_exchange(Ctx* ctx, const int64_t* rb, const int64_t* rp
     }
     GH_CUDA(cudaStreamWaitEvent(st, g->ev_done[rp[i]], 0));
     const size_t b = (size_t)rb[i], c0 = (size_t)bstart[b], w = (size_t)bwidth[b];
-    GH_CUDA(cudaMemcpyAsync(ctx->F + c0 * ctx->ldm, pc->F + c0 * pc->ldm, w * ctx->ldm * 16, cudaMemcpyDeviceToDevice, st));
-    GH_CUDA(cudaMemcpyAsync(ctx->G + c0 * ctx->ldm, pc->G + c0 * pc->ldm, w * ctx->ldm * 16, cudaMemcpyDeviceToDevice, st));
-    GH_CUDA(cudaMemcpyAsync(ctx->Z + c0 * ctx->ldn, pc->Z + c0 * pc->ldn, w * ctx->ldn * 16, cudaMemcpyDeviceToDevice, st));
-    if (ctx->o.want_x && ctx->W && pc->W)
-      GH_CUDA(cudaMemcpyAsync(ctx->W + c0 * ctx->ldn, pc->W + c0 * pc->ldn, w * ctx->ldn * 16,
-                              cudaMemcpyDeviceToDevice, st));
+    const cudaMemcpyKind k = cudaMemcpyDeviceToDevice;
+    if (part & XCH_FG) {
+      GH_CUDA(cudaMemcpyAsync(ctx->F + c0 * ctx->ldm, pc->F + c0 * pc->ldm, w * ctx->ldm * 16, k, st));
+      GH_CUDA(cudaMemcpyAsync(ctx->G + c0 * ctx->ldm, pc->G + c0 * pc->ldm, w * ctx->ldm * 16, k, st));
+    }
+    if (part & XCH_ZW) {
+      GH_CUDA(cudaMemcpyAsync(ctx->Z + c0 * ctx->ldn, pc->Z + c0 * pc->ldn, w * ctx->ldn * 16, k, st));
+      if (ctx->o.want_x && ctx->W && pc->W)
+        GH_CUDA(cudaMemcpyAsync(ctx->W + c0 * ctx->ldn, pc->W + c0 * pc->ldn, w * ctx->ldn * 16, k, st));
+    }
   }
   GH_CUDA(cudaEventRecord(g->ev_copy[r], st));
   if (!g->barrier()) return loop_broken(ctx);
@@ -310,9 +327,11 @@ static ghsvd_status loop_exchange(Ctx* ctx, const int64_t* rb, const int64_t* rp
   return GHSVD_OK;
 }
 
-// Move the block columns (F, G: m rows; Z: n rows) whose owner changes between
-// block steps s_now and s_next.  A block column is contiguous in each buffer.
-ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart, const int* bwidth) {
+// Move the block columns whose owner changes between block steps s_now and s_next, on
+// stream st: part XCH_FG = F and G (m rows), XCH_ZW = Z' and W (n rows).  A block column
+// is contiguous in each buffer.  Every rank issues the parts in the same order.
+ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart, const int* bwidth, int part,
+                           cudaStream_t st) {
   Nccl* N = nccl();
   if (!ctx->comm || (!N && handle(ctx)->kind == 1)) {
     ctx->err = "multi-GPU: no communicator";
@@ -325,16 +344,16 @@ ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int*
     ctx->err = "multi-GPU: bad exchange plan arguments";
     return GHSVD_E_INVALID_ARG;
   }
-  if (handle(ctx)->kind == 2) return loop_exchange(ctx, rb.data(), rp.data(), nr, bstart, bwidth);
+  if (handle(ctx)->kind == 2) return loop_exchange(ctx, rb.data(), rp.data(), nr, bstart, bwidth, part, st);
   if (ns == 0 && nr == 0) return GHSVD_OK;
-  ncclComm_t comm = handle(ctx)->nccl;
-  cudaStream_t st = ctx->stream;
+  ncclComm_t comm = part == XCH_ZW ? handle(ctx)->nccl_zw : handle(ctx)->nccl;
   NCCL_CALL(N->GroupStart());
   auto xfer = [&](int64_t b, int peer, bool send) -> ncclResult_t {
-    const size_t w = (size_t)bwidth[b];
-    double2* bufs[4] = {ctx->F + (size_t)bstart[b] * ctx->ldm, ctx->G + (size_t)bstart[b] * ctx->ldm,
-                        ctx->Z + (size_t)bstart[b] * ctx->ldn,
-                        ctx->o.want_x && ctx->W ? ctx->W + (size_t)bstart[b] * ctx->ldn : nullptr};
+    const size_t w = (size_t)bwidth[b], c0 = (size_t)bstart[b];
+    double2* bufs[4] = {part & XCH_FG ? ctx->F + c0 * ctx->ldm : nullptr,
+                        part & XCH_FG ? ctx->G + c0 * ctx->ldm : nullptr,
+                        part & XCH_ZW ? ctx->Z + c0 * ctx->ldn : nullptr,
+                        (part & XCH_ZW) && ctx->o.want_x && ctx->W ? ctx->W + c0 * ctx->ldn : nullptr};
     const size_t cnt[4] = {w * ctx->ldm * 2, w * ctx->ldm * 2, w * ctx->ldn * 2, w * ctx->ldn * 2};  // doubles
     for (int t = 0; t < 4; t++) {
       if (!bufs[t]) continue;

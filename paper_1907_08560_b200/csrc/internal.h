@@ -116,6 +116,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st);
 ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns);
 size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n);
 // comm.cpp
+enum { XCH_FG = 1, XCH_ZW = 2 };   // parts of the block-column exchange
+ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart, const int* bwidth, int part,
+                           cudaStream_t st);
+ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c);
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam,
                                    double* sf, double* sg, double2* Zout, int64_t ldz, double2* Xout);
 

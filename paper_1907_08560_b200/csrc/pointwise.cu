@@ -685,7 +685,9 @@ ghsvd_status pw_configure(Ctx* ctx) {
   if (C <= 0 && kk == 2) {
     // two-pass kernel: measured on config 3 (m = 10368, tools/profile_step.py, ms per
     // step): C=1/T=256 0.739, C=2/T=128 0.714, C=4/T=128 0.672, C=8/T=128 0.696; small
-    // m (the pair's columns fit in L2 anyway) keeps one CTA per pair
+    // m (the pair's columns fit in L2 anyway) keeps one CTA per pair.  Capping the
+    // resident CTAs per SM (so that more pass-2 reads hit L2) was slower at every cap:
+    // C=4/T=128 with 9 / 6 / 4 / 3 CTAs per SM: 0.665 / 0.800 / 0.733 / 0.822 ms per step
     C = m >= 4096 ? 4 : 1;
   } else if (C <= 0) {
     // smallest power-of-two cluster whose per-CTA slices fit the smem budget

@@ -112,6 +112,16 @@ def test_loopback_ranks_bitwise_equal_single(gh, world, nblocks):
     assert float(np.max(np.abs(lam - np.sort(P.lam_true)) / np.abs(np.sort(P.lam_true)))) <= 1e-9
 
 
+@pytest.mark.parametrize("n,nblocks,world", [(191, 8, 2), (250, 12, 3), (129, 6, 3)])
+def test_loopback_odd_and_ragged(gh, n, nblocks, world):
+    """Odd n (bordered to even order, Sec 6.3.2) and ragged block widths (w and w-1)."""
+    P = inputs.known_hyperbolic(24 + n, n + 77, n, 0.4)
+    ref = single(gh, P, nblocks, False)
+    res = multi(gh, P, nblocks, world, False, f"odd{n}_{world}")
+    for r in range(world):
+        assert_same(res[r], ref)
+
+
 def test_loopback_fb(gh):
     """FB (inner sweeps to convergence) with two ranks."""
     P = inputs.known_hyperbolic(23, 320, 192, 0.4)

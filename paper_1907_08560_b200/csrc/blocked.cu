@@ -908,7 +908,9 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_zinv(BlkArgs a) {
 // of 16 warps with double-buffered 64-row tiles were 8-15 % slower.  ncu: the short-
 // lived CTAs of this form keep the DMMA sub-pipe 71 % busy; in the 16-warp variant the
 // (Zr + Zi) / (Xr + Xi) DADDs of the 3M scheme stall on the FP64 pipe the DMMAs occupy
-// (math-pipe stalls 50 % vs 24 %).
+// (math-pipe stalls 50 % vs 24 %).  Unrolling the k-step loop (fragment loads issued
+// ahead of the previous k-step's DMMAs; bitwise the same result) was slower: config 3
+// 10.78 s rolled, 10.98 s unrolled x2, 11.47 s fully unrolled.
 // wmode = 1: the tiles are row tiles of W^T (n rows) and the right factor is
 // (Z_blk^{-1})^T (NEXT-1 accumulation of Z'^{-1}).
 template <bool M4>

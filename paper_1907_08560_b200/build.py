@@ -69,6 +69,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+DEMO_SRC = os.path.join(ROOT, "examples", "c_demo.c")
+DEMO = os.path.join(ROOT, "build", "c_demo")
+
+
+def build_c_demo(force: bool = False) -> str:
+    """examples/c_demo.c: a plain-C99 program against include/ghsvd.h and libghsvd.so
+    (proves the boundary is usable without Python; run by a GPU test)."""
+    lib = build()
+    if not force and os.path.exists(DEMO) and os.path.getmtime(DEMO) >= max(
+            os.path.getmtime(lib), os.path.getmtime(DEMO_SRC), os.path.getmtime(os.path.join(ROOT, "include", "ghsvd.h"))):
+        return DEMO
+    os.makedirs(os.path.dirname(DEMO), exist_ok=True)
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-pedantic", DEMO_SRC, "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.join(cuda, "include"), "-L" + HERE, "-lghsvd", "-L" + os.path.join(cuda, "lib64"),
+           "-lcudart", "-lm", "-Wl,-rpath," + HERE, "-o", DEMO]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"c_demo build failed:\n{r.stdout}\n{r.stderr}")
+    return DEMO
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)

@@ -74,3 +74,12 @@ def test_create_rejects_bad_args_before_touching_cuda(lib):
     assert lib.ghsvd_sweep(None, None) == -1
     lib.ghsvd_destroy(None)
     assert b"sm_100a" in lib.ghsvd_version()
+
+
+def test_c_demo_builds_as_plain_c99():
+    """The public header is plain C: examples/c_demo.c compiles with gcc -std=c99 -pedantic
+    -Wall -Wextra against include/ghsvd.h and links libghsvd.so (run on the GPU by
+    tests/test_gpu_c_demo.py)."""
+    from paper_1907_08560_b200 import build
+    exe = build.build_c_demo(force=True)
+    assert os.path.exists(exe) and os.access(exe, os.X_OK)

@@ -1088,13 +1088,20 @@ BlkPlan make_plan(const Ctx* ctx) {
 
 }  // namespace
 
-size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
-  const int64_t nb = auto_nblk(n + 1, o) + 2;
-  const int64_t K = nb / 2;
+// scratch carved by blk_setup for K block pairs per rank out of nblk block columns
+static size_t blk_scratch_for(int64_t K, int64_t nb, bool want_x) {
   return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)2 * K * KM * KM * 16) +
-         al256((size_t)2 * K * 4) + 2 * al256((size_t)nb * 4) + 2 * al256((size_t)K * KM * KM * 16) +
-         al256((size_t)K * KM) + al256((size_t)2 * K * 4) + (o->want_x ? al256((size_t)2 * K * KM * KM * 16) : 0) +
+         al256((size_t)2 * K * 4) + 2 * al256((size_t)(nb + 2) * 4) + 2 * al256((size_t)K * KM * KM * 16) +
+         al256((size_t)K * KM) + al256((size_t)2 * K * 4) + (want_x ? al256((size_t)2 * K * KM * KM * 16) : 0) +
          al256((size_t)(nb + 2) * TRACE_SLOTS * 16) + al256((size_t)2 * K * 4) + 4096;
+}
+
+// workspace bound at ghsvd_create for factors of up to n columns: the sweep may see
+// n + 1 columns (odd n is bordered, Sec 6.3.2); a single rank holds all nblk/2 pairs
+size_t blk_scratch_bytes(const ghsvd_options* o, int64_t m, int64_t n) {
+  (void)m;
+  const int64_t nb = auto_nblk(n + 1, o);
+  return blk_scratch_for(nb / 2, nb, o->want_x != 0);
 }
 
 // in comm.cpp
@@ -1124,7 +1131,7 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
     ctx->err = "blocked: block width " + std::to_string(w) + " > 32 (increase nblocks)";
     return GHSVD_E_INVALID_ARG;
   }
-  if (blk_scratch_bytes(&ctx->o, ctx->m, ctx->n) > ctx->L.scr_bytes) {
+  if (blk_scratch_for(pl.K, pl.nblk, ctx->o.want_x != 0) > ctx->L.scr_bytes) {
     ctx->err = "blocked: workspace scratch too small (create the context with a blocked variant)";
     return GHSVD_E_WORKSPACE;
   }

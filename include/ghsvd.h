@@ -170,7 +170,10 @@ ghsvd_status ghsvd_get_factors(ghsvd_ctx ctx, int64_t* m, int64_t* n, void* F, i
 /* Phase 3: sweeps (Algorithm 2; Alg. 3 per step) until a
  * sweep has no "big" transformation (Sec 6.1.7) or C_max sweeps.  Z' starts at
  * I.  Returns GHSVD_OK or GHSVD_NOT_CONVERGED (warning) or an error; *out
- * (may be NULL) receives counters and device time. */
+ * (may be NULL) receives counters and device time of this call.  A further call
+ * resumes from the current F', G', Z' (and W): a solve split into calls of C_max
+ * sweeps each runs exactly the sweeps of one call with a larger C_max (bitwise
+ * the same results; tests/test_gpu_resume.py).  Multi-rank: every rank calls it. */
 ghsvd_status ghsvd_sweep(ghsvd_ctx ctx, ghsvd_stats* out);
 
 /* Diagnostic: run only steps [s0, s0+ns) of the round-robin sweep on the current

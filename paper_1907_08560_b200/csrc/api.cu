@@ -413,8 +413,8 @@ ghsvd_status ghsvd_run_steps(ghsvd_ctx h, int64_t s0, int64_t ns, uint64_t* all,
 ghsvd_status ghsvd_sweep(ghsvd_ctx h, ghsvd_stats* out) {
   if (!h) return GHSVD_E_INVALID_ARG;
   Ctx* ctx = &h->c;
-  if (ctx->state != 1) {
-    ctx->err = "sweep: must follow factor/set_factors/reduce (and not be repeated)";
+  if (ctx->state != 1 && ctx->state != 2) {
+    ctx->err = "sweep: must follow factor/set_factors/reduce (or a previous sweep, to resume)";
     return GHSVD_E_STATE;
   }
   CTX_CUDA(cudaSetDevice(ctx->o.device));

@@ -152,3 +152,47 @@ def test_loopback_illcond_tall(gh):
         res = multi(gh, at, 8, world, False, f"c3s{world}")
         for r in range(world):
             assert_same(res[r], ref)
+
+
+def test_loopback_resumed_sweeps(gh):
+    """Multi-rank resume: each rank calls ghsvd_sweep repeatedly with C_max = 2 (the block
+    columns are back with their step-0 owners after every sweep) -- bitwise equal to the
+    one-rank single-call solve."""
+    import torch
+    import warnings
+    P = inputs.known_hyperbolic(25, 320, 192, 0.4)
+    m, n = P.F.shape
+    ref = single(gh, P, 12, False)
+    lid = gh.loopback_id("resume3")
+    ctxs = [gh.Context(m, n, variant="bo", nblocks=12, max_sweeps=2, world_size=3, rank=r, nccl_id=lid,
+                       stream=torch.cuda.Stream()) for r in range(3)]
+    for c in ctxs:
+        c.set_factors(P.F, P.J, P.G)
+    res, errs = [None] * 3, []
+
+    def run(r):
+        try:
+            total = 0
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                for _ in range(40):
+                    st = ctxs[r].sweep()
+                    total += st["sweeps"]
+                    if st["converged"]:
+                        break
+            res[r] = (total, ctxs[r].extract())
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for c in ctxs:
+        c.close()
+    assert not errs, errs
+    for total, (lam, sf, sg, Z) in res:
+        assert total == ref[0]["sweeps"]
+        np.testing.assert_array_equal(lam, ref[1][0])
+        np.testing.assert_array_equal(Z, ref[1][3])

@@ -121,16 +121,19 @@ def cpu_baseline_sample(F0, J0, G0, sweeps: int, budget_s: float = 15.0):
     import oracle
     m, n = F0.shape
     Z = np.eye(n, dtype=np.complex128, order="F")
-    # each oracle call copies F, G, Z first: calibrate the per-step cost as (t(3) - t(1)) / 2
-    # after one untimed call (first-touch page faults of the copies inflate the first call)
+    # each oracle call copies F, G, Z first (~0.4 s at config 3, with run-to-run noise well
+    # above one step's cost): calibrate the per-step cost as (t(1 + K) - t(1)) / K with K
+    # steps long enough to dominate that noise, after one untimed call (first-touch page
+    # faults of the copies inflate the first call)
     F1, G1, Z1, a, b = oracle.hz_steps(F0, J0, G0, Z, 0, 1)
     t = time.perf_counter()
     oracle.hz_steps(F0, J0, G0, Z, 0, 1)
     t1 = time.perf_counter() - t
+    K = int(max(2, min(n - 3, 64)))
     t = time.perf_counter()
-    oracle.hz_steps(F0, J0, G0, Z, 0, 3)
+    oracle.hz_steps(F0, J0, G0, Z, 0, 1 + K)
     t2 = time.perf_counter() - t
-    step_est = max((t2 - t1) / 2, 1e-6)
+    step_est = max((t2 - t1) / K, 1e-6)
     copy_s = max(t1 - step_est, 0.0)
     ns = int(max(1, min(n - 2, budget_s / step_est)))
     t = time.perf_counter()

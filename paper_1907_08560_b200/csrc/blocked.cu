@@ -20,6 +20,8 @@
 //                because every CTA reads its row tile before writing it).
 // blk_sweep schedules a step as two halves of the pairs on prioritized streams
 // (DESIGN.md 6); multi-GPU (comm.cpp) exchanges block columns between the steps.
+// Kernels: blk_gram.cuh (Grams + factorizations), blk_pivot.cuh (inner sweep),
+// blk_update.cuh (updates), blk_common.cuh (shared helpers); this file: host side.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -31,999 +33,16 @@
 #include <string>
 #include <vector>
 
-#include "hebpj.cuh"
-#include "hz2x2.cuh"
 #include "internal.h"
+// the kernels (one translation unit: these files are included only here)
+#include "blk_common.cuh"
+#include "blk_gram.cuh"
+#include "blk_pivot.cuh"
+#include "blk_update.cuh"
 
 namespace ghsvd {
 
 namespace {
-
-constexpr int KM = 64;          // max block-pivot order 2w
-constexpr int RT = 32;          // rows per staged tile
-constexpr int GS = RT + 2;      // Gram tile column stride (double2), conflict-free fragments
-constexpr int ZS = KM + 4;      // Z_blk column stride in smem
-constexpr int NT_G = 256, NT_P = 512, NT_U = 256;
-constexpr int US = RT + 2;      // update tile column stride
-constexpr int GSTAGES = 3;      // cp.async pipeline depth of the Gram kernel
-constexpr int MAX_SPLIT = 16;   // max row splits of a Gram (partials summed in order)
-constexpr int TRACE_SLOTS = 48; // trace launch slots per block step
-
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void cp_wait_dyn(int n) {   // n in [0, 3]
-  switch (n) {
-    case 0: cp_wait<0>(); break;
-    case 1: cp_wait<1>(); break;
-    case 2: cp_wait<2>(); break;
-    default: cp_wait<3>(); break;
-  }
-}
-
-struct BlkArgs {
-  double2* F;
-  double2* G;
-  double2* Z;
-  long long ldm, ldn, m, n, npos;
-  int nblk, s, slot0, npairs;
-  int pair0;                // first local pair handled by this launch (blockIdx.x offset)
-  const int* bstart;
-  const int* bwidth;
-  int nsplit;
-  long long split_rows;     // rows per split (multiple of RT)
-  double2* gpart;           // [pair][hs][split][KM*KM]
-  double2* zblk;            // [pair][KM*KM]
-  int* applied;             // [pair]
-  double2* fhat;            // [pair][KM*KM]  F^ from HEBPJ
-  double2* ghat;            // [pair][KM*KM]  G^ from pivoted Cholesky
-  signed char* jhat;        // [pair][KM]     J^
-  int* fact_ok;             // [pair][2]
-  int* gcnt;                // [pair][2] finished Gram splits (reset by the last one)
-  double2* zinvT;           // [pair][KM*KM] (Z_blk^{-1})^T if want_x, else nullptr
-  double2* W;               // want_x: W^T = (Z'^{-1})^T (n rows, ld ldn)
-  DevCounters* cnt;
-  double eps;
-  int literal;
-  int inner_sweeps;
-  unsigned long long* trace;  // GHSVD_TRACE: [launch id][first CTA start, last CTA end] (ns)
-  int trace_id;
-};
-
-// Launch tracing (GHSVD_TRACE=<csv path>, first sweep only): thread 0 of every CTA
-// folds %globaltimer into the launch's [min start, max end] with atomics.
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ void trace_begin(const BlkArgs& a) {
-  if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[2 * a.trace_id], gtimer());
-}
-__device__ __forceinline__ void trace_end(const BlkArgs& a) {
-  if (a.trace && threadIdx.x == 0) atomicMax(&a.trace[2 * a.trace_id + 1], gtimer());
-}
-
-__device__ __forceinline__ void pair_cols(const BlkArgs& a, int pl, int& c0p, int& wp, int& c0q, int& wq) {
-  long long bp, bq;
-  rr_pair(a.nblk, a.s, a.slot0 + pl, &bp, &bq);
-  c0p = a.bstart[bp];
-  wp = a.bwidth[bp];
-  c0q = a.bstart[bq];
-  wq = a.bwidth[bq];
-}
-
-// global column of pivot column c (c < wp: block p, else block q), -1 if padding
-__device__ __forceinline__ long long gcol(int c, int c0p, int wp, int c0q, int wq) {
-  if (c < wp) return c0p + c;
-  if (c < wp + wq) return c0q + (c - wp);
-  return -1;
-}
-
-// ---------------------------------------------------------------- block pivot
-// blk_factor (run by the last Gram CTA of a (pair, H|S), see k_blk_gram): sum the split
-// partials in fixed order; which = 0: H_blk -> HEBPJ -> F^ (and J^); which = 1: S_blk ->
-// diagonally pivoted Cholesky -> G^.  F^, G^ go to L2-resident scratch.
-constexpr int NT_F = 256;
-__device__ void blk_factor(const BlkArgs& a, int pl, int which, double2* W) {
-  __shared__ int np_sh;
-  const int tid = threadIdx.x;
-  int c0p, wp, c0q, wq;
-  pair_cols(a, pl, c0p, wp, c0q, wq);
-  const int k = wp + wq;
-  // sum of split partials (lower triangle, fixed split order), full Hermitian in W;
-  // L2 loads (__ldcg): the partials were written by other CTAs of this launch
-  const double2* base = a.gpart + ((size_t)pl * 2 + which) * a.nsplit * (KM * KM);
-  {
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int j = warp; j < k; j += NT_F / 32) {
-      for (int i = j + lane; i < k; i += 32) {
-        double2 x[MAX_SPLIT];
-#pragma unroll
-        for (int sp = 0; sp < MAX_SPLIT; sp++)
-          if (sp < a.nsplit) x[sp] = __ldcg(base + (size_t)sp * (KM * KM) + i + (size_t)j * KM);
-        double2 v = make_double2(0, 0);
-#pragma unroll
-        for (int sp = 0; sp < MAX_SPLIT; sp++)
-          if (sp < a.nsplit) {
-            v.x += x[sp].x;
-            v.y += x[sp].y;
-          }
-        if (i == j) v.y = 0.0;
-        W[i + j * KM] = v;
-        W[j + i * KM] = make_double2(v.x, -v.y);
-      }
-    }
-  }
-  __syncthreads();
-  double2* out = (which == 0 ? a.fhat : a.ghat) + (size_t)pl * (KM * KM);
-  int rc;
-  if (which == 0) {
-    // HEBPJ tolerance k * eps * max |H| (lower triangle), as the oracle
-    double tv = 0.0;
-    long long ti = 0;
-    for (int e = tid; e < k * k; e += NT_F) {
-      const int i = e % k, j = e / k;
-      if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W[i + j * KM]), 0);
-    }
-    hb::block_amax<NT_F>(tv, ti);
-    const double tolz = __dmul_rn(__dmul_rn((double)k, 0x1p-53), tv);
-    rc = hb::hebpj_dev<NT_F, KM>(W, k, KM, out, KM, a.jhat + (size_t)pl * KM, &np_sh, tolz);
-  } else {
-    rc = hb::pchol_dev<NT_F, KM>(W, k, KM, out, KM);
-  }
-  if (tid == 0) {
-    a.fact_ok[pl * 2 + which] = rc == 0;
-    if (rc) atomicCAS(&a.cnt->err, 0, which == 0 ? -7 : -6);
-  }
-}
-
-// ---------------------------------------------------------------- Gram (DMMA)
-// One CTA = one (row split, H|S, pair) (grid x = split fastest, so a pair's splits run
-// together and pairs complete progressively).  The 36 lower-triangle 8x8 output tiles of the
-// k x k Gram (k <= 64) are grouped by tile-row pairs {I, 7-I} (9 tiles each); warps
-// 2g, 2g+1 own group g and split every 32-row stage's 8 k-steps (even / odd).  Within
-// a k-step a warp loads the 8-g column fragments its 9 tiles need once (the A fragment
-// of tile row I is the B fragment of tile column I) and issues 36 DMMAs (exact 4M
-// complex product; J folded into the A operand).  The two k-halves are summed in a
-// fixed order at the end, so the result is deterministic.
-template <int GI>
-__device__ __forceinline__ void gram_tiles(const double2* T, int row, double sg, double (&acc)[9][4]) {
-  constexpr int IA = GI, IB = 7 - GI, NF = 8 - GI;
-  const int lane = threadIdx.x & 31;
-  double2 f[NF];
-#pragma unroll
-  for (int j = 0; j < NF; j++) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
-  // A operand of tile rows IA, IB: J_r conj(x): (ar, ai) with conj -> (+x.y used as -(-x.y))
-  const double aar = sg * f[IA].x, aai = sg * f[IA].y;
-  const double abr = sg * f[IB].x, abi = sg * f[IB].y;
-#pragma unroll
-  for (int t = 0; t < 9; t++) {
-    const bool ra = t <= IA;
-    const int J = ra ? t : t - IA - 1;
-    const double ar = ra ? aar : abr, ai = ra ? aai : abi;
-    const double2 y = f[J];
-    // conj(x) y = (xr yr + xi yi) + i (xr yi - xi yr)
-    dmma(acc[t][0], acc[t][1], ar, y.x);
-    dmma(acc[t][0], acc[t][1], ai, y.y);
-    dmma(acc[t][2], acc[t][3], ar, y.y);
-    dmma(acc[t][2], acc[t][3], -ai, y.x);
-  }
-}
-
-// 3M variant (default; GHSVD_GRAM3M=0 selects the 4M path above): of the 9 tiles of group
-// g, warp 2g owns tiles 0-3 and warp 2g+1 tiles 5-8 for every k-step, and tile 4 is
-// split by k-step parity (even: warp 2g, odd: warp 2g+1; its two partial sums are added
-// in a fixed order at the end), so every warp does exactly 4.5 tiles per k-step.  Per
-// k-step a warp loads the fragments its tiles need and issues 3 DMMAs per tile:
-// P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi); Re = P1 - P2, Im = P3 - P1 - P2
-// (A = J conj(X)^T, B = X).
-template <int GI>
-struct G3 {
-  static constexpr int IA = GI, IB = 7 - GI;
-  static constexpr int row(int t) { return t <= IA ? IA : IB; }
-  static constexpr int col(int t) { return t <= IA ? t : t - IA - 1; }
-  // tile of accumulator slot u (0..4) of warp half H; slot 4 is the shared tile 4
-  static constexpr int tile(int H, int u) { return u == 4 ? 4 : (H ? 5 + u : u); }
-  static constexpr bool needB(int H, bool w4, int j) {
-    bool r = false;
-    for (int u = 0; u < 5; u++) r = r || ((u < 4 || w4) && col(tile(H, u)) == j);
-    return r;
-  }
-  static constexpr bool needA(int H, bool w4, int i) {
-    bool r = false;
-    for (int u = 0; u < 5; u++) r = r || ((u < 4 || w4) && row(tile(H, u)) == i);
-    return r;
-  }
-};
-
-template <int GI, int H, bool W4>
-__device__ __forceinline__ void gram3_tiles(const double2* T, int row, double sg, double (&acc)[5][6]) {
-  using C = G3<GI>;
-  const int lane = threadIdx.x & 31;
-  double2 f[8];
-  double bs[8];
-#pragma unroll
-  for (int j = 0; j < 8; j++) {
-    if (C::needB(H, W4, j) || C::needA(H, W4, j)) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
-    if (C::needB(H, W4, j)) bs[j] = f[j].x + f[j].y;
-  }
-  double ar[2] = {0, 0}, ai[2] = {0, 0}, as[2] = {0, 0};   // rows IA, IB
-  if (C::needA(H, W4, C::IA)) {
-    ar[0] = sg * f[C::IA].x;
-    ai[0] = -(sg * f[C::IA].y);
-    as[0] = ar[0] + ai[0];
-  }
-  if (C::needA(H, W4, C::IB)) {
-    ar[1] = sg * f[C::IB].x;
-    ai[1] = -(sg * f[C::IB].y);
-    as[1] = ar[1] + ai[1];
-  }
-#pragma unroll
-  for (int u = 0; u < 5; u++) {
-    if (u == 4 && !W4) continue;
-    const int t = C::tile(H, u);
-    const int r = C::row(t) == C::IA ? 0 : 1, J = C::col(t);
-    dmma(acc[u][0], acc[u][1], ar[r], f[J].x);
-    dmma(acc[u][2], acc[u][3], ai[r], f[J].y);
-    dmma(acc[u][4], acc[u][5], as[r], bs[J]);
-  }
-}
-
-template <int GI, int H>
-__device__ __forceinline__ void gram3_store(double2* out, const double (&acc)[5][6], int nslots) {
-  using C = G3<GI>;
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int u = 0; u < 5; u++) {
-    if (u >= nslots) continue;
-    const double* c = acc[u];
-    const int t = C::tile(H, u);
-    const int i = 8 * C::row(t) + (lane >> 2), j = 8 * C::col(t) + 2 * (lane & 3);
-    out[i + (size_t)j * KM] = make_double2(c[0] - c[2], c[4] - c[0] - c[2]);
-    out[i + (size_t)(j + 1) * KM] = make_double2(c[1] - c[3], c[5] - c[1] - c[3]);
-  }
-}
-
-template <bool M3>
-__global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
-  trace_begin(a);
-  extern __shared__ __align__(128) double2 gsm[];  // [GSTAGES][KM][GS]
-  const int pl = a.pair0 + blockIdx.z, hs = blockIdx.y, split = blockIdx.x;
-  int c0p, wp, c0q, wq;
-  pair_cols(a, pl, c0p, wp, c0q, wq);
-  const double2* X = hs == 0 ? a.F : a.G;
-  const long long r_begin = (long long)split * a.split_rows;
-  const long long r_end = min(a.m, r_begin + a.split_rows);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gi = warp >> 1, kh = warp & 1;
-  auto load_stage = [&](int st, long long r0) {
-    if (r0 < r_end) {
-      double2* T = gsm + (size_t)st * KM * GS;
-      for (int e = tid; e < KM * RT; e += NT_G) {
-        const int c = e / RT, r = e % RT;
-        const long long gc = gcol(c, c0p, wp, c0q, wq);
-        const long long gr = r0 + r;
-        const bool ok = gc >= 0 && gr < r_end;
-        cp_async16(&T[c * GS + r], ok ? (const void*)(X + gc * a.ldm + gr) : (const void*)X, ok);
-      }
-    }
-    cp_commit();   // possibly empty: keeps one group per stage
-  };
-  // GSTAGES-deep cp.async pipeline over the split's 32-row stages; consume(T, r0).
-  // One barrier per stage: after it every warp has finished the previous stage, whose
-  // buffer is then refilled with the stage GSTAGES-1 ahead.
-  auto pipeline = [&](auto&& consume) {
-#pragma unroll
-    for (int p = 0; p < GSTAGES - 1; p++) load_stage(p, r_begin + (long long)p * RT);
-    int st = 0;
-    for (long long r0 = r_begin; r0 < r_end; r0 += RT) {
-      cp_wait<GSTAGES - 2>();
-      __syncthreads();
-      load_stage((st + GSTAGES - 1) % GSTAGES, r0 + (long long)(GSTAGES - 1) * RT);
-      consume(gsm + (size_t)st * KM * GS, r0);
-      st = (st + 1) % GSTAGES;
-    }
-    cp_wait<0>();
-    __syncthreads();
-  };
-  double2* out = a.gpart + (((size_t)pl * 2 + hs) * a.nsplit + split) * (KM * KM);
-  if constexpr (M3) {
-    double acc[5][6];
-#pragma unroll
-    for (int t = 0; t < 5; t++)
-#pragma unroll
-      for (int c = 0; c < 6; c++) acc[t][c] = 0.0;
-    pipeline([&](const double2* T, long long r0) {
-      // not unrolled: the warp-specialized tile sets are already 16 code paths, and
-      // unrolling them overflowed the instruction cache (ncu: 22 % no_inst stalls)
-#pragma unroll 1
-      for (int ks = 0; ks < RT / 4; ks += 2) {
-        const int row0 = 4 * ks + (lane & 3), row1 = row0 + 4;
-        const double sg0 = (hs == 0 && r0 + row0 >= a.npos) ? -1.0 : 1.0;
-        const double sg1 = (hs == 0 && r0 + row1 >= a.npos) ? -1.0 : 1.0;
-        switch (warp) {   // warp-uniform; tile 4 on even k-steps for h = 0, odd for h = 1
-#define G3CASE(W, GI, H)                                       \
-  case W:                                                      \
-    gram3_tiles<GI, H, H == 0>(T, row0, sg0, acc);             \
-    gram3_tiles<GI, H, H == 1>(T, row1, sg1, acc);             \
-    break;
-          G3CASE(0, 0, 0) G3CASE(1, 0, 1) G3CASE(2, 1, 0) G3CASE(3, 1, 1)
-          G3CASE(4, 2, 0) G3CASE(5, 2, 1) G3CASE(6, 3, 0) default: G3CASE(7, 3, 1)
-#undef G3CASE
-        }
-      }
-    });
-    // tile 4 of every group: warp 2g+1 hands its odd-k-step partial to warp 2g
-    double* red = reinterpret_cast<double*>(gsm);
-    if (kh) {
-#pragma unroll
-      for (int c = 0; c < 6; c++) red[(gi * 6 + c) * 32 + lane] = acc[4][c];
-    }
-    __syncthreads();
-    if (!kh) {
-#pragma unroll
-      for (int c = 0; c < 6; c++) acc[4][c] += red[(gi * 6 + c) * 32 + lane];
-    }
-    const int nslots = kh ? 4 : 5;
-    switch (warp) {
-      case 0: gram3_store<0, 0>(out, acc, nslots); break;
-      case 1: gram3_store<0, 1>(out, acc, nslots); break;
-      case 2: gram3_store<1, 0>(out, acc, nslots); break;
-      case 3: gram3_store<1, 1>(out, acc, nslots); break;
-      case 4: gram3_store<2, 0>(out, acc, nslots); break;
-      case 5: gram3_store<2, 1>(out, acc, nslots); break;
-      case 6: gram3_store<3, 0>(out, acc, nslots); break;
-      default: gram3_store<3, 1>(out, acc, nslots); break;
-    }
-  } else {
-    double acc[9][4];
-#pragma unroll
-    for (int t = 0; t < 9; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
-    pipeline([&](const double2* T, long long r0) {
-#pragma unroll 1
-      for (int ks = 0; ks < RT / 4; ks += 2) {
-        const int row = 4 * (ks + kh) + (lane & 3);
-        const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
-        switch (gi) {   // warp-uniform
-          case 0: gram_tiles<0>(T, row, sg, acc); break;
-          case 1: gram_tiles<1>(T, row, sg, acc); break;
-          case 2: gram_tiles<2>(T, row, sg, acc); break;
-          default: gram_tiles<3>(T, row, sg, acc); break;
-        }
-      }
-    });
-    // sum the two k-halves: odd warp -> smem -> even warp (fixed order)
-    double* red = reinterpret_cast<double*>(gsm);
-    if (kh) {
-#pragma unroll
-      for (int t = 0; t < 9; t++)
-#pragma unroll
-        for (int c = 0; c < 4; c++) red[((gi * 9 + t) * 4 + c) * 32 + lane] = acc[t][c];
-    }
-    __syncthreads();
-    if (!kh) {
-#pragma unroll
-      for (int t = 0; t < 9; t++)
-#pragma unroll
-        for (int c = 0; c < 4; c++) acc[t][c] += red[((gi * 9 + t) * 4 + c) * 32 + lane];
-#pragma unroll
-      for (int t = 0; t < 9; t++) {
-        const int I = t <= gi ? gi : 7 - gi;
-        const int J = t <= gi ? t : t - gi - 1;
-        const int i = 8 * I + (lane >> 2), j = 8 * J + 2 * (lane & 3);
-        out[i + (size_t)j * KM] = make_double2(acc[t][0], acc[t][2]);
-        out[i + (size_t)(j + 1) * KM] = make_double2(acc[t][1], acc[t][3]);
-      }
-    }
-  }
-  // The last CTA of this (pair, H|S) to finish factorizes the summed Gram right away
-  // (threadfence-reduction pattern): no separate launch, and a pair's block pivot is
-  // formed while the Grams of later pairs are still streaming.
-  __shared__ int last_sh;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const int t = atomicAdd(&a.gcnt[pl * 2 + hs], 1);
-    last_sh = t == a.nsplit - 1;
-    if (last_sh) a.gcnt[pl * 2 + hs] = 0;   // ready for the next block step
-  }
-  __syncthreads();
-  if (last_sh) {
-    __threadfence();
-    blk_factor(a, pl, hs, gsm);
-  }
-  trace_end(a);
-}
-
-// (Z_blk^{-1})^T for the W^T update (NEXT-1): Gauss-Jordan with partial pivoting on
-// [Fh | Gh] = [Z_blk | I] (kb x kb active, ld KM, in shared memory), transposed into wo.
-template <int NT>
-__device__ void gj_inverse_T(double2* Fh, double2* Gh, int kb, double2* wo) {
-  __shared__ int piv_sh;
-  const int tid = threadIdx.x;
-  __syncthreads();
-  for (int c = 0; c < kb; c++) {
-    if (tid == 0) {
-      int pv = c;
-      double best = -1.0;
-      for (int i = c; i < kb; i++) {
-        const double2 v = Fh[i + c * KM];
-        const double av = v.x * v.x + v.y * v.y;
-        if (av > best) { best = av; pv = i; }
-      }
-      piv_sh = pv;
-    }
-    __syncthreads();
-    const int pv = piv_sh;
-    if (pv != c) {
-      for (int j = tid; j < KM; j += NT) {
-        double2 t = Fh[c + j * KM]; Fh[c + j * KM] = Fh[pv + j * KM]; Fh[pv + j * KM] = t;
-        t = Gh[c + j * KM]; Gh[c + j * KM] = Gh[pv + j * KM]; Gh[pv + j * KM] = t;
-      }
-      __syncthreads();
-    }
-    const double2 d = Fh[c + c * KM];
-    const double dd = d.x * d.x + d.y * d.y;
-    const double2 inv = make_double2(d.x / dd, -d.y / dd);
-    __syncthreads();
-    for (int j = tid; j < KM; j += NT) {   // scale row c
-      const double2 f = Fh[c + j * KM], g = Gh[c + j * KM];
-      Fh[c + j * KM] = make_double2(f.x * inv.x - f.y * inv.y, f.x * inv.y + f.y * inv.x);
-      Gh[c + j * KM] = make_double2(g.x * inv.x - g.y * inv.y, g.x * inv.y + g.y * inv.x);
-    }
-    __syncthreads();
-    for (int e = tid; e < kb * KM; e += NT) {   // eliminate column c from the other rows
-      const int i = e % kb, j = e / kb;
-      if (i == c) continue;
-      const double2 f = Fh[i + c * KM];
-      const double2 rf = Fh[c + j * KM], rg = Gh[c + j * KM];
-      const double2 uf = make_double2(f.x * rf.x - f.y * rf.y, f.x * rf.y + f.y * rf.x);
-      const double2 ug = make_double2(f.x * rg.x - f.y * rg.y, f.x * rg.y + f.y * rg.x);
-      if (j != c) Fh[i + j * KM] = make_double2(Fh[i + j * KM].x - uf.x, Fh[i + j * KM].y - uf.y);
-      Gh[i + j * KM] = make_double2(Gh[i + j * KM].x - ug.x, Gh[i + j * KM].y - ug.y);
-    }
-    __syncthreads();
-    for (int i = tid; i < kb; i += NT)
-      if (i != c) Fh[i + c * KM] = make_double2(0.0, 0.0);
-    __syncthreads();
-  }
-  for (int e = tid; e < KM * KM; e += NT) {
-    const int i = e % KM, j = e / KM;
-    wo[e] = Gh[j + i * KM];   // transpose (no conjugation)
-  }
-}
-
-// k_blk_pivot: one CTA per pair: F^, G^, J^ -> shared memory, border to even order
-// (Sec 6.3.2), inner Level-1 sweep(s) accumulating Z_blk.
-__global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
-  trace_begin(a);
-  extern __shared__ __align__(128) double2 psm[];  // W0 (Z_blk) | F^ | G^  (KM*KM each)
-  double2* W0 = psm;
-  double2* Fh = psm + KM * KM;
-  double2* Gh = psm + 2 * KM * KM;
-  __shared__ signed char Jh[KM];
-  __shared__ unsigned long long cnt_all, cnt_big, sweep_all;
-  __shared__ int err_sh;
-  const int pl = a.pair0 + blockIdx.x, tid = threadIdx.x;
-  int c0p, wp, c0q, wq;
-  pair_cols(a, pl, c0p, wp, c0q, wq);
-  const int k = wp + wq;
-  const int kb = k + (k & 1);
-  if (!a.fact_ok[2 * pl] || !a.fact_ok[2 * pl + 1]) {
-    if (tid == 0) a.applied[pl] = 0;
-    trace_end(a);
-    return;
-  }
-  if (tid == 0) {
-    cnt_all = cnt_big = sweep_all = 0;
-    err_sh = 0;
-  }
-  const double2* fsrc = a.fhat + (size_t)pl * (KM * KM);
-  const double2* gsrc = a.ghat + (size_t)pl * (KM * KM);
-  for (int e = tid; e < KM * KM; e += NT_P) {
-    const int i = e % KM, j = e / KM;
-    const bool in = i < k && j < k;
-    Fh[e] = in ? fsrc[e] : make_double2(0, 0);
-    Gh[e] = in ? gsrc[e] : make_double2(0, 0);
-    W0[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);   // Z_blk = I
-  }
-  for (int i = tid; i < KM; i += NT_P) Jh[i] = i < k ? a.jhat[(size_t)pl * KM + i] : (signed char)1;
-  __syncthreads();
-  // border to even order (Sec 6.3.2)
-  if (tid == 0 && kb != k) {
-    Fh[k + k * KM] = make_double2(1, 0);
-    Gh[k + k * KM] = make_double2(1, 0);
-    Jh[k] = 1;
-  }
-  __syncthreads();
-  // inner Level-1 sweeps.  Per inner step: one HALF-warp per pivot pair forms the 8 pair
-  // Gram entries (eq 6.1) -> shared memory; warp 0 then evaluates the kb/2 <= 32 2x2
-  // transforms of the step one per LANE (the scalar routine runs once per pair instead
-  // of once per half-warp, which cuts the step's issued instructions several-fold);
-  // the half-warps then apply them to the column pairs of F^, G^ and Z_blk.
-  __shared__ double gsh[KM / 2][8];
-  __shared__ double zsh[KM / 2][8];
-  __shared__ int ksh[KM / 2];
-  __shared__ double Jd[KM];
-  for (int i = tid; i < KM; i += NT_P) Jd[i] = (double)Jh[i];
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  const int hw = lane >> 4, hl = lane & 15;
-  const unsigned hmask = hw ? 0xffff0000u : 0x0000ffffu;
-  const double tol = a.eps * sqrt((double)kb);       // C-7: n = block-pivot order
-  unsigned long long w0_all = 0, w0_big = 0;          // warp-0 lane counters
-  double w0_off = 0.0;                                 // warp-0 lane max off-measure
-  const int pr = 2 * warp + hw;                        // this half-warp's pivot pair slot
-  const int b3 = (hl >> 3) & 1, b2 = (hl >> 2) & 1, b1 = (hl >> 1) & 1;
-  for (int sw = 0; sw < a.inner_sweeps; sw++) {
-    unsigned long long sw_all = 0, sw_big = 0;
-    for (int s = 0; s < kb - 1; s++) {
-      int p = 0, q = 0;
-      if (pr < kb / 2) {
-        rr_pair32(kb, s, pr, &p, &q);
-        // rows >= kb of F^, G^ are zero, so all KM rows are summed without guards
-        double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int t = 0; t < KM / 16; t++) {
-          const int i = hl + 16 * t;
-          const double2 fp = Fh[i + p * KM], fq = Fh[i + q * KM], gpp = Gh[i + p * KM], gq = Gh[i + q * KM];
-          const double sg = Jd[i];
-          g[0] += sg * (fp.x * fp.x + fp.y * fp.y);
-          g[1] += sg * (fq.x * fq.x + fq.y * fq.y);
-          g[2] += sg * (fp.x * fq.x + fp.y * fq.y);
-          g[3] += sg * (fp.x * fq.y - fp.y * fq.x);
-          g[4] += gpp.x * gpp.x + gpp.y * gpp.y;
-          g[5] += gq.x * gq.x + gq.y * gq.y;
-          g[6] += gpp.x * gq.x + gpp.y * gq.y;
-          g[7] += gpp.x * gq.y - gpp.y * gq.x;
-        }
-        // transpose-reduce of the 8 sums over the 16 lanes: after the offsets 8, 4, 2
-        // every lane keeps one value index (hl >> 1), offset 1 completes the sum
-        double h4[4], h2[2];
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const double snd = b3 ? g[j] : g[j + 4];
-          const double kep = b3 ? g[j + 4] : g[j];
-          h4[j] = kep + __shfl_xor_sync(hmask, snd, 8);
-        }
-#pragma unroll
-        for (int j = 0; j < 2; j++) {
-          const double snd = b2 ? h4[j] : h4[j + 2];
-          const double kep = b2 ? h4[j + 2] : h4[j];
-          h2[j] = kep + __shfl_xor_sync(hmask, snd, 4);
-        }
-        double w = (b1 ? h2[1] : h2[0]) + __shfl_xor_sync(hmask, b1 ? h2[0] : h2[1], 2);
-        w += __shfl_xor_sync(hmask, w, 1);
-        if (!(hl & 1)) gsh[pr][hl >> 1] = w;
-      }
-      __syncthreads();
-      if (warp == 0 && lane < kb / 2) {
-        const HZOut z = hz2x2_core(gsh[lane], tol, a.literal);
-        zsh[lane][0] = z.z11.re; zsh[lane][1] = z.z11.im; zsh[lane][2] = z.z21.re; zsh[lane][3] = z.z21.im;
-        zsh[lane][4] = z.z12.re; zsh[lane][5] = z.z12.im; zsh[lane][6] = z.z22.re; zsh[lane][7] = z.z22.im;
-        ksh[lane] = z.kind;
-        w0_off = fmax(w0_off, z.off);   // scaled off-diagonal measure (a5 diagnostic)
-        if (z.kind < 0) atomicCAS(&err_sh, 0, z.kind);
-        if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
-          sw_all++;
-          if (z.kind == KIND_BIG) sw_big++;
-        }
-      }
-      __syncthreads();
-      if (pr < kb / 2) {
-        const int kind = ksh[pr];
-        if (kind == KIND_SMALL || kind == KIND_BIG) {
-          const double2 z11 = make_double2(zsh[pr][0], zsh[pr][1]), z21 = make_double2(zsh[pr][2], zsh[pr][3]);
-          const double2 z12 = make_double2(zsh[pr][4], zsh[pr][5]), z22 = make_double2(zsh[pr][6], zsh[pr][7]);
-          auto rot = [&](double2* M) {
-#pragma unroll
-            for (int t = 0; t < KM / 16; t++) {
-              const int i = hl + 16 * t;
-              const double2 x = M[i + p * KM], y = M[i + q * KM];
-              M[i + p * KM] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
-                                           x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
-              M[i + q * KM] = make_double2(x.x * z12.x - x.y * z12.y + y.x * z22.x - y.y * z22.y,
-                                           x.x * z12.y + x.y * z12.x + y.x * z22.y + y.y * z22.x);
-            }
-          };
-          rot(Fh);
-          rot(Gh);
-          rot(W0);
-        }
-      }
-      __syncthreads();
-    }
-    w0_all += sw_all;
-    w0_big += sw_big;
-    // per-sweep totals; FB stops on a sweep without transformations (C-3)
-    if (warp == 0) {
-      unsigned long long t = sw_all;
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0) sweep_all = t;
-    }
-    __syncthreads();
-    const unsigned long long this_sweep = sweep_all;
-    __syncthreads();
-    if (this_sweep == 0) break;
-  }
-  if (warp == 0) {
-    for (int o = 16; o > 0; o >>= 1) {
-      w0_all += __shfl_xor_sync(0xffffffffu, w0_all, o);
-      w0_big += __shfl_xor_sync(0xffffffffu, w0_big, o);
-      w0_off = fmax(w0_off, __shfl_xor_sync(0xffffffffu, w0_off, o));
-    }
-    if (lane == 0) atomicMax(&a.cnt->off_bits, (unsigned long long)__double_as_longlong(w0_off));
-    if (lane == 0) {
-      cnt_all = w0_all;
-      cnt_big = w0_big;
-    }
-  }
-  __syncthreads();
-  if (err_sh) {
-    if (tid == 0) atomicCAS(&a.cnt->err, 0, err_sh);
-  }
-  double2* zo = a.zblk + (size_t)pl * (KM * KM);
-  for (int e = tid; e < KM * KM; e += NT_P) zo[e] = W0[e];
-  if (tid == 0) {
-    a.applied[pl] = cnt_all > 0;
-    atomicAdd(&a.cnt->all, cnt_all);
-    atomicAdd(&a.cnt->big, cnt_big);
-  }
-  if (a.zinvT && cnt_all > 0) {
-    // NEXT-1: (Z_blk^{-1})^T for the W^T update, Gauss-Jordan with partial pivoting on
-    // [Fh | Gh] = [Z_blk | I] (F^, G^ are no longer needed after the inner sweep)
-    __syncthreads();
-    for (int e = tid; e < KM * KM; e += NT_P) {
-      const int i = e % KM, j = e / KM;
-      Fh[e] = W0[e];
-      Gh[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-    }
-    gj_inverse_T<NT_P>(Fh, Gh, kb, a.zinvT + (size_t)pl * (KM * KM));
-  }
-  trace_end(a);
-}
-
-// k_blk_pivot_cl (option GHSVD_PIVOT_CL=1; default k_blk_pivot above): the
-// same inner sweep on a cluster of two CTAs that split the KM rows of F^, G^ and Z_blk
-// (32 rows each, 96 KB of shared memory, 256 threads), so a pivot no longer fills an SM
-// alone and a Gram or update CTA can run beside it.  Per inner step each CTA forms the 8
-// pair-Gram partial sums over its rows (8 lanes per pivot pair, transpose-reduce),
-// writes them to both CTAs' shared memory (DSMEM, double-buffered by step parity), one
-// cluster barrier, then warp 0 of each CTA sums rank 0 + rank 1 (fixed order: both CTAs
-// hold bitwise the same pivot sums) and evaluates the <= 32 transforms one per lane, and
-// each CTA rotates its own rows.  Measured on config 3: 266 us alone against 319 us for
-// k_blk_pivot, but inside the overlapped block step the co-resident Gram / update CTAs
-// share its FP64 pipe and issue slots, the pivots stretch to 370-460 us and the step
-// period grows 2.43 -> 2.49 ms, so it is not the default.
-constexpr int NT_PC = 256, RB = KM / 2;
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_PC, 1) k_blk_pivot_cl(BlkArgs a) {
-  trace_begin(a);
-  namespace cgx = cooperative_groups;
-  cgx::cluster_group cluster = cgx::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  extern __shared__ __align__(128) double2 qsm[];   // W0 | F^ | G^ : local rows, [KM cols][RB]
-  double2* W0 = qsm;
-  double2* Fh = qsm + KM * RB;
-  double2* Gh = qsm + 2 * KM * RB;
-  __shared__ double Jd[RB];
-  __shared__ double parts[2][2][KM / 2][8];   // [step parity][source rank][pair][value]
-  __shared__ double zsh[KM / 2][8];
-  __shared__ int ksh[KM / 2];
-  __shared__ unsigned long long sweep_all_sh;
-  const int pl = a.pair0 + blockIdx.x / 2, tid = threadIdx.x;
-  int c0p, wp, c0q, wq;
-  pair_cols(a, pl, c0p, wp, c0q, wq);
-  const int k = wp + wq;
-  const int kb = k + (k & 1);
-  if (!a.fact_ok[2 * pl] || !a.fact_ok[2 * pl + 1]) {   // uniform over the cluster
-    if (tid == 0 && rank == 0) a.applied[pl] = 0;
-    trace_end(a);
-    return;
-  }
-  const int row0 = rank * RB;
-  const double2* fsrc = a.fhat + (size_t)pl * (KM * KM);
-  const double2* gsrc = a.ghat + (size_t)pl * (KM * KM);
-  for (int e = tid; e < KM * RB; e += NT_PC) {
-    const int il = e % RB, j = e / RB, i = row0 + il;
-    const bool in = i < k && j < k;
-    Fh[e] = in ? fsrc[i + j * KM] : make_double2(0, 0);
-    Gh[e] = in ? gsrc[i + j * KM] : make_double2(0, 0);
-    W0[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);   // Z_blk = I
-  }
-  for (int il = tid; il < RB; il += NT_PC) {
-    const int i = row0 + il;
-    Jd[il] = i < k ? (double)a.jhat[(size_t)pl * KM + i] : 1.0;
-  }
-  __syncthreads();
-  // border to even order (Sec 6.3.2): row/column k in the CTA holding row k
-  if (tid == 0 && kb != k && k >= row0 && k < row0 + RB) {
-    Fh[(k - row0) + k * RB] = make_double2(1, 0);
-    Gh[(k - row0) + k * RB] = make_double2(1, 0);
-  }
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  const int pr = 4 * warp + (lane >> 3);   // pivot pair slot of this 8-lane group
-  const int l8 = lane & 7;
-  const unsigned gmask = 0xffu << (lane & 24);
-  const int b2 = (l8 >> 2) & 1, b1 = (l8 >> 1) & 1, b0 = l8 & 1;
-  const double tol = a.eps * sqrt((double)kb);        // C-7: n = block-pivot order
-  unsigned long long w0_all = 0, w0_big = 0;
-  double w0_off = 0.0;
-  int err_local = 0;
-  double* peer_parts = cluster.map_shared_rank(&parts[0][0][0][0], rank ^ 1);
-  int sp = 0;   // global inner-step parity
-  for (int sw = 0; sw < a.inner_sweeps; sw++) {
-    unsigned long long sw_all = 0, sw_big = 0;
-    for (int s = 0; s < kb - 1; s++, sp ^= 1) {
-      int p = 0, q = 0;
-      if (pr < kb / 2) {
-        rr_pair32(kb, s, pr, &p, &q);
-        double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int t = 0; t < RB / 8; t++) {
-          const int i = l8 + 8 * t;
-          const double2 fp = Fh[i + p * RB], fq = Fh[i + q * RB], gpp = Gh[i + p * RB], gq = Gh[i + q * RB];
-          const double sg = Jd[i];
-          g[0] += sg * (fp.x * fp.x + fp.y * fp.y);
-          g[1] += sg * (fq.x * fq.x + fq.y * fq.y);
-          g[2] += sg * (fp.x * fq.x + fp.y * fq.y);
-          g[3] += sg * (fp.x * fq.y - fp.y * fq.x);
-          g[4] += gpp.x * gpp.x + gpp.y * gpp.y;
-          g[5] += gq.x * gq.x + gq.y * gq.y;
-          g[6] += gpp.x * gq.x + gpp.y * gq.y;
-          g[7] += gpp.x * gq.y - gpp.y * gq.x;
-        }
-        // transpose-reduce over the 8 lanes: lane l8 ends with the sum of value l8
-        double h4[4], h2[2];
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const double snd = b2 ? g[j] : g[j + 4];
-          const double kep = b2 ? g[j + 4] : g[j];
-          h4[j] = kep + __shfl_xor_sync(gmask, snd, 4);
-        }
-#pragma unroll
-        for (int j = 0; j < 2; j++) {
-          const double snd = b1 ? h4[j] : h4[j + 2];
-          const double kep = b1 ? h4[j + 2] : h4[j];
-          h2[j] = kep + __shfl_xor_sync(gmask, snd, 2);
-        }
-        const double w = (b0 ? h2[1] : h2[0]) + __shfl_xor_sync(gmask, b0 ? h2[0] : h2[1], 1);
-        parts[sp][rank][pr][l8] = w;
-        peer_parts[((sp * 2 + rank) * (KM / 2) + pr) * 8 + l8] = w;
-      }
-      cluster.sync();   // both CTAs' partial sums of this step are in place
-      if (warp == 0 && lane < kb / 2) {
-        double gs[8];
-#pragma unroll
-        for (int c = 0; c < 8; c++) gs[c] = parts[sp][0][lane][c] + parts[sp][1][lane][c];
-        const HZOut z = hz2x2_core(gs, tol, a.literal);
-        zsh[lane][0] = z.z11.re; zsh[lane][1] = z.z11.im; zsh[lane][2] = z.z21.re; zsh[lane][3] = z.z21.im;
-        zsh[lane][4] = z.z12.re; zsh[lane][5] = z.z12.im; zsh[lane][6] = z.z22.re; zsh[lane][7] = z.z22.im;
-        ksh[lane] = z.kind;
-        w0_off = fmax(w0_off, z.off);
-        if (z.kind < 0 && !err_local) err_local = z.kind;
-        if (z.kind == KIND_SMALL || z.kind == KIND_BIG) {
-          sw_all++;
-          if (z.kind == KIND_BIG) sw_big++;
-        }
-      }
-      __syncthreads();
-      if (pr < kb / 2) {
-        const int kind = ksh[pr];
-        if (kind == KIND_SMALL || kind == KIND_BIG) {
-          const double2 z11 = make_double2(zsh[pr][0], zsh[pr][1]), z21 = make_double2(zsh[pr][2], zsh[pr][3]);
-          const double2 z12 = make_double2(zsh[pr][4], zsh[pr][5]), z22 = make_double2(zsh[pr][6], zsh[pr][7]);
-          auto rot = [&](double2* M) {
-#pragma unroll
-            for (int t = 0; t < RB / 8; t++) {
-              const int i = l8 + 8 * t;
-              const double2 x = M[i + p * RB], y = M[i + q * RB];
-              M[i + p * RB] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
-                                           x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
-              M[i + q * RB] = make_double2(x.x * z12.x - x.y * z12.y + y.x * z22.x - y.y * z22.y,
-                                           x.x * z12.y + x.y * z12.x + y.x * z22.y + y.y * z22.x);
-            }
-          };
-          rot(Fh);
-          rot(Gh);
-          rot(W0);
-        }
-      }
-      __syncthreads();
-    }
-    w0_all += sw_all;
-    w0_big += sw_big;
-    // per-sweep totals (identical in both CTAs); FB stops on a sweep without transformations
-    if (warp == 0) {
-      unsigned long long t = sw_all;
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0) sweep_all_sh = t;
-    }
-    __syncthreads();
-    if (sweep_all_sh == 0) break;
-  }
-  double2* zo = a.zblk + (size_t)pl * (KM * KM);
-  for (int e = tid; e < KM * RB; e += NT_PC) {   // zeros outside k x k (border, padding)
-    const int il = e % RB, j = e / RB, i = row0 + il;
-    zo[i + j * KM] = (i < k && j < k) ? W0[e] : make_double2(0.0, 0.0);
-  }
-  if (warp == 0 && rank == 0) {
-    for (int o = 16; o > 0; o >>= 1) {
-      w0_all += __shfl_xor_sync(0xffffffffu, w0_all, o);
-      w0_big += __shfl_xor_sync(0xffffffffu, w0_big, o);
-      w0_off = fmax(w0_off, __shfl_xor_sync(0xffffffffu, w0_off, o));
-    }
-    if (err_local) atomicCAS(&a.cnt->err, 0, err_local);
-    if (lane == 0) {
-      a.applied[pl] = w0_all > 0;
-      atomicAdd(&a.cnt->all, w0_all);
-      atomicAdd(&a.cnt->big, w0_big);
-      atomicMax(&a.cnt->off_bits, (unsigned long long)__double_as_longlong(w0_off));
-    }
-  }
-  cluster.sync();   // no CTA leaves while its peer may still write into its shared memory
-  trace_end(a);
-}
-
-// k_blk_zinv: (Z_blk^{-1})^T of every transformed pair for the W^T update (want_x), after
-// k_blk_pivot_cl has written Z_blk (zero outside k x k; the bordered and padding
-// diagonal is restored to 1 so the kb x kb elimination is regular).
-__global__ void __launch_bounds__(NT_P, 1) k_blk_zinv(BlkArgs a) {
-  extern __shared__ __align__(128) double2 zsm2[];   // Fh | Gh (KM*KM each)
-  double2* Fh = zsm2;
-  double2* Gh = zsm2 + KM * KM;
-  const int pl = a.pair0 + blockIdx.x, tid = threadIdx.x;
-  if (!a.applied[pl]) return;
-  int c0p, wp, c0q, wq;
-  pair_cols(a, pl, c0p, wp, c0q, wq);
-  const int k = wp + wq;
-  const int kb = k + (k & 1);
-  const double2* zsrc = a.zblk + (size_t)pl * (KM * KM);
-  for (int e = tid; e < KM * KM; e += NT_P) {
-    const int i = e % KM, j = e / KM;
-    Fh[e] = (i < k && j < k) ? zsrc[e] : make_double2(i == j ? 1.0 : 0.0, 0.0);
-    Gh[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-  gj_inverse_T<NT_P>(Fh, Gh, kb, a.zinvT + (size_t)pl * (KM * KM));
-}
-
-// ---------------------------------------------------------------- update (DMMA)
-// grid (pair, tile): tiles [0, tF) rows of F, [tF, 2 tF) rows of G, [2 tF, 2 tF + tZ) rows of Z.
-// Measured faster than three persistent variants (Z_blk loaded once per pair, the next
-// row tile prefetched, results stored from the accumulators): one CTA of 8 warps per SM
-// with double-buffered 64-row tiles, two CTAs per SM walking contiguous ranges, one CTA
-// of 16 warps with double-buffered 64-row tiles were 8-15 % slower.  ncu: the short-
-// lived CTAs of this form keep the DMMA sub-pipe 71 % busy; in the 16-warp variant the
-// (Zr + Zi) / (Xr + Xi) DADDs of the 3M scheme stall on the FP64 pipe the DMMAs occupy
-// (math-pipe stalls 50 % vs 24 %).  Unrolling the k-step loop (fragment loads issued
-// ahead of the previous k-step's DMMAs; bitwise the same result) was slower: config 3
-// 10.78 s rolled, 10.98 s unrolled x2, 11.47 s fully unrolled.
-// wmode = 1: the tiles are row tiles of W^T (n rows) and the right factor is
-// (Z_blk^{-1})^T (NEXT-1 accumulation of Z'^{-1}).
-template <bool M4>
-__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile0, int tile_end, int tpc,
-                                                     int wmode) {
-  trace_begin(a);
-  extern __shared__ __align__(128) double2 usm[];  // X tile [KM][US] | Z_blk [KM][ZS]
-  const int pl = a.pair0 + blockIdx.x;
-  if (!a.applied[pl]) {
-    trace_end(a);
-    return;
-  }
-  int c0p, wp, c0q, wq;
-  pair_cols(a, pl, c0p, wp, c0q, wq);
-  const int k = wp + wq;
-  double2* Xt = usm;
-  double2* Zb = usm + KM * US;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const double2* zsrc = (wmode ? a.zinvT : a.zblk) + (size_t)pl * (KM * KM);
-  const int I = warp & 3;          // row tile of 8 rows within the 32-row tile
-  const int J0 = (warp >> 2) * 4;  // first of 4 column tiles
-  const int kend = (k + 3) & ~3;
-  const int tile = tile0 + blockIdx.y;
-  double2* X;
-  long long ld, rows, r0;
-  if (wmode) {
-    X = a.W; ld = a.ldn; rows = a.n; r0 = (long long)(tile - tile0) * RT;
-  } else if (tile < tF) {
-    X = a.F; ld = a.ldm; rows = a.m; r0 = (long long)tile * RT;
-  } else if (tile < 2 * tF) {
-    X = a.G; ld = a.ldm; rows = a.m; r0 = (long long)(tile - tF) * RT;
-  } else {
-    X = a.Z; ld = a.ldn; rows = a.n; r0 = (long long)(tile - 2 * tF) * RT;
-  }
-  // Loads in NPH phases (tile columns and Z_blk rows [ph*KPH, +KPH) per cp.async group)
-  // would let the DMMAs over the first k-range start early; measured on config 3:
-  // NPH = 1: 1472 us, 2: 1488 us, 4: 1528 us per full-step launch, so one phase.
-  constexpr int NPH = 1, KPH = KM / NPH;
-#pragma unroll
-  for (int ph = 0; ph < NPH; ph++) {
-    for (int e = tid; e < KPH * KM; e += NT_U) {
-      const int i = ph * KPH + e % KPH, j = e / KPH;
-      cp_async16(&Zb[j * ZS + i], zsrc + i + (size_t)j * KM, i < k && j < k);
-    }
-    for (int e = tid; e < KPH * RT; e += NT_U) {
-      const int c = ph * KPH + e / RT, r = e % RT;
-      const long long gc = gcol(c, c0p, wp, c0q, wq);
-      const bool ok = gc >= 0 && r0 + r < rows;
-      cp_async16(&Xt[c * US + r], ok ? (const void*)(X + gc * ld + r0 + r) : (const void*)X, ok);
-    }
-    cp_commit();
-  }
-  {
-    // out (RT x KM) = Xt (RT x KM) Z_blk (KM x KM): 4 x 8 tiles of 8x8, 4 per warp.
-    // Complex product by the 3M (Gauss) scheme on DMMA: P1 = Xr Zr, P2 = Xi Zi,
-    // P3 = (Xr + Xi)(Zr + Zi); out = (P1 - P2) + i (P3 - P1 - P2): 3 real DMMAs per
-    // 8x8x4 complex step instead of 4 (normwise error bound of the same order).
-    double p1[4][2], p2[4][2], p3[4][2];
-#pragma unroll
-    for (int t = 0; t < 4; t++) p1[t][0] = p1[t][1] = p2[t][0] = p2[t][1] = p3[t][0] = p3[t][1] = 0.0;
-#pragma unroll
-    for (int ph = 0; ph < NPH; ph++) {
-      cp_wait_dyn(NPH - 1 - ph);   // every phase is waited for, even past kend
-      __syncthreads();
-      for (int kk = ph * KPH; kk < min(kend, (ph + 1) * KPH); kk += 4) {
-      const double2 x = Xt[(kk + (lane & 3)) * US + 8 * I + (lane >> 2)];  // A(i, k)
-      const double xs = x.x + x.y;
-#pragma unroll
-      for (int t = 0; t < 4; t++) {
-        const double2 z = Zb[(8 * (J0 + t) + (lane >> 2)) * ZS + kk + (lane & 3)];  // B(k, j)
-        dmma(p1[t][0], p1[t][1], x.x, z.x);
-        dmma(p2[t][0], p2[t][1], x.y, z.y);
-        if (M4) {   // exact 4M product: Im accumulated directly, no additions in the loop
-          dmma(p3[t][0], p3[t][1], x.x, z.y);
-          dmma(p3[t][0], p3[t][1], x.y, z.x);
-        } else {
-          dmma(p3[t][0], p3[t][1], xs, z.x + z.y);
-        }
-      }
-    }
-    }
-    // accumulators -> global (each 8-lane group writes 8 consecutive rows of a column);
-    // every warp has read the whole tile and the tile's rows of these columns belong to
-    // this CTA alone, so no barrier is needed before the in-place stores
-    const long long row = r0 + 8 * I + (lane >> 2);
-    if (row < rows) {
-#pragma unroll
-      for (int t = 0; t < 4; t++) {
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int j = 8 * (J0 + t) + 2 * (lane & 3) + h;
-          const long long gc = gcol(j, c0p, wp, c0q, wq);
-          if (gc < 0) continue;
-          X[gc * ld + row] = M4 ? make_double2(p1[t][h] - p2[t][h], p3[t][h])
-                                : make_double2(p1[t][h] - p2[t][h], p3[t][h] - p1[t][h] - p2[t][h]);
-        }
-      }
-    }
-  }
-  trace_end(a);
-}
-
-__global__ void k_blk_partition(int* bstart, int* bwidth, int nblk, long long n) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const long long w = (n + nblk - 1) / nblk;
-  const long long nbig = n - (long long)nblk * (w - 1);
-  long long c = 0;
-  for (int b = 0; b < nblk; b++) {
-    bwidth[b] = (int)(b < nbig ? w : w - 1);
-    bstart[b] = (int)c;
-    c += bwidth[b];
-  }
-}
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 

@@ -163,7 +163,8 @@ ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
  * the J row sort, [reduce] and bordering): *m, *n (bordered sizes); F, G
  * (m x n, ld >= m) and J (m int8) if non-NULL; p2 (n int64, column j of the
  * current factors is column p2[j] of the Phase-1/set_factors factors) if
- * non-NULL.  Used so the CPU oracle runs on exactly the same bytes. */
+ * non-NULL.  Used so the CPU oracle runs on exactly the same bytes.  Before the first
+ * sweep; a size-only query (F, J, G, p2 all NULL) is also allowed after sweeps. */
 ghsvd_status ghsvd_get_factors(ghsvd_ctx ctx, int64_t* m, int64_t* n, void* F, int64_t ldf,
                                int8_t* J, void* G, int64_t ldg, int64_t* p2);
 
@@ -196,6 +197,21 @@ ghsvd_status ghsvd_extract(ghsvd_ctx ctx, double* lambda, double* sigma_f, doubl
  * (X~ = X P2^T).  n x n (ldx >= n), host or device.  Requires opts.want_x and a
  * completed sweep; GHSVD_E_STATE otherwise. */
 ghsvd_status ghsvd_extract_x(ghsvd_ctx ctx, void* X, int64_t ldx);
+
+/* Checkpoint / restore of a solve in progress (between ghsvd_sweep calls).
+ * ghsvd_get_state copies the sweep state -- F', G' (m x n, the bordered sizes
+ * ghsvd_get_factors reports), Z' and, with opts.want_x, W = Z'^{-1} stored transposed
+ * (n x n) -- to caller buffers (host or device; NULL = skip; W requires want_x).
+ * ghsvd_set_state loads such a state into a context whose problem was set up the same
+ * way (same factor/set_factors/reduce inputs, so J's row order, bordering and P2 agree;
+ * state after factor/set_factors/reduce or a sweep); F, G, Z' are required, W iff
+ * want_x.  The next ghsvd_sweep resumes from it: checkpoint after k sweeps, restore in
+ * a new context (or process), and the remaining sweeps give bitwise the uninterrupted
+ * result (tests/test_gpu_resume.py).  Multi-rank: every rank saves / restores its own. */
+ghsvd_status ghsvd_get_state(ghsvd_ctx ctx, void* F, int64_t ldf, void* G, int64_t ldg, void* Zp,
+                             int64_t ldz, void* W, int64_t ldw);
+ghsvd_status ghsvd_set_state(ghsvd_ctx ctx, const void* F, int64_t ldf, const void* G, int64_t ldg,
+                             const void* Zp, int64_t ldz, const void* W, int64_t ldw);
 
 /* Copy the current transformed factors F', G' (m x n) to F, G (NULL = skip). */
 ghsvd_status ghsvd_get_transformed(ghsvd_ctx ctx, void* F, int64_t ldf, void* G, int64_t ldg,

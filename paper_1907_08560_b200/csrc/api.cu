@@ -336,7 +336,9 @@ ghsvd_status ghsvd_get_factors(ghsvd_ctx h, int64_t* m, int64_t* n, void* F, int
                                int64_t ldg, int64_t* p2) {
   if (!h) return GHSVD_E_INVALID_ARG;
   Ctx* ctx = &h->c;
-  if (ctx->state != 1) {
+  // a size-only query (all buffers NULL) is also allowed after a sweep
+  const bool size_only = !F && !J && !G && !p2;
+  if (ctx->state != 1 && !(size_only && ctx->state == 2)) {
     ctx->err = "get_factors: must follow factor/set_factors/reduce and precede sweep";
     return GHSVD_E_STATE;
   }
@@ -540,6 +542,67 @@ ghsvd_status ghsvd_get_transformed(ghsvd_ctx h, void* F, int64_t ldf, void* G, i
     CTX_CUDA(cudaMemcpy2DAsync(Zp, (size_t)ldz * 16, ctx->Z, (size_t)ctx->ldn * 16, (size_t)ctx->n * 16,
                                (size_t)ctx->n, cudaMemcpyDefault, ctx->stream));
   CTX_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GHSVD_OK;
+}
+
+ghsvd_status ghsvd_get_state(ghsvd_ctx h, void* F, int64_t ldf, void* G, int64_t ldg, void* Zp, int64_t ldz,
+                             void* W, int64_t ldw) {
+  if (!h) return GHSVD_E_INVALID_ARG;
+  Ctx* ctx = &h->c;
+  if (ctx->state < 1) {
+    ctx->err = "get_state: no factors";
+    return GHSVD_E_STATE;
+  }
+  CTX_CUDA(cudaSetDevice(ctx->o.device));
+  TRY(prepare(ctx));   // bordered sizes m, n
+  if ((F && ldf < ctx->m) || (G && ldg < ctx->m) || (Zp && ldz < ctx->n) || (W && (ldw < ctx->n || !ctx->W))) {
+    ctx->err = "get_state: bad leading dimension, or W without want_x";
+    return GHSVD_E_INVALID_ARG;
+  }
+  const size_t m = (size_t)ctx->m, n = (size_t)ctx->n;
+  if (F)
+    CTX_CUDA(cudaMemcpy2DAsync(F, (size_t)ldf * 16, ctx->F, (size_t)ctx->ldm * 16, m * 16, n, cudaMemcpyDefault,
+                               ctx->stream));
+  if (G)
+    CTX_CUDA(cudaMemcpy2DAsync(G, (size_t)ldg * 16, ctx->G, (size_t)ctx->ldm * 16, m * 16, n, cudaMemcpyDefault,
+                               ctx->stream));
+  if (Zp)
+    CTX_CUDA(cudaMemcpy2DAsync(Zp, (size_t)ldz * 16, ctx->Z, (size_t)ctx->ldn * 16, n * 16, n, cudaMemcpyDefault,
+                               ctx->stream));
+  if (W)
+    CTX_CUDA(cudaMemcpy2DAsync(W, (size_t)ldw * 16, ctx->W, (size_t)ctx->ldn * 16, n * 16, n, cudaMemcpyDefault,
+                               ctx->stream));
+  CTX_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GHSVD_OK;
+}
+
+ghsvd_status ghsvd_set_state(ghsvd_ctx h, const void* F, int64_t ldf, const void* G, int64_t ldg, const void* Zp,
+                             int64_t ldz, const void* W, int64_t ldw) {
+  if (!h) return GHSVD_E_INVALID_ARG;
+  Ctx* ctx = &h->c;
+  if (ctx->state < 1) {
+    ctx->err = "set_state: set up the same problem first (factor / set_factors / reduce)";
+    return GHSVD_E_STATE;
+  }
+  CTX_CUDA(cudaSetDevice(ctx->o.device));
+  TRY(prepare(ctx));   // bordering and J of the problem, as when the state was saved
+  if (!F || !G || !Zp || ldf < ctx->m || ldg < ctx->m || ldz < ctx->n || (!W) != (!ctx->W) ||
+      (W && ldw < ctx->n)) {
+    ctx->err = "set_state: F, G, Z' required (W iff want_x); bad leading dimension";
+    return GHSVD_E_INVALID_ARG;
+  }
+  const size_t m = (size_t)ctx->m, n = (size_t)ctx->n;
+  CTX_CUDA(cudaMemcpy2DAsync(ctx->F, (size_t)ctx->ldm * 16, F, (size_t)ldf * 16, m * 16, n, cudaMemcpyDefault,
+                             ctx->stream));
+  CTX_CUDA(cudaMemcpy2DAsync(ctx->G, (size_t)ctx->ldm * 16, G, (size_t)ldg * 16, m * 16, n, cudaMemcpyDefault,
+                             ctx->stream));
+  CTX_CUDA(cudaMemcpy2DAsync(ctx->Z, (size_t)ctx->ldn * 16, Zp, (size_t)ldz * 16, n * 16, n, cudaMemcpyDefault,
+                             ctx->stream));
+  if (W)
+    CTX_CUDA(cudaMemcpy2DAsync(ctx->W, (size_t)ctx->ldn * 16, W, (size_t)ldw * 16, n * 16, n, cudaMemcpyDefault,
+                               ctx->stream));
+  CTX_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->state = 2;   // a sweep resumes from the loaded state
   return GHSVD_OK;
 }
 

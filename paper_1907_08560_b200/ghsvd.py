@@ -32,7 +32,8 @@ CRITERIA = {"relative": 0, "literal": 1}
 # every symbol include/ghsvd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ghsvd_default_options", "ghsvd_workspace_bytes", "ghsvd_create", "ghsvd_factor",
            "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors", "ghsvd_sweep", "ghsvd_run_steps",
-           "ghsvd_extract", "ghsvd_extract_x", "ghsvd_get_transformed", "ghsvd_hz2x2_batch", "ghsvd_last_error",
+           "ghsvd_extract", "ghsvd_extract_x", "ghsvd_get_transformed", "ghsvd_get_state", "ghsvd_set_state",
+           "ghsvd_hz2x2_batch", "ghsvd_last_error",
            "ghsvd_destroy", "ghsvd_version", "ghsvd_block_owner", "ghsvd_exchange_plan",
            "ghsvd_nccl_unique_id"]
 
@@ -109,6 +110,8 @@ def load():
     L.ghsvd_run_steps.argtypes = [P, I64, I64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     L.ghsvd_extract.argtypes = [P, P, P, P, P, I64, P]
     L.ghsvd_get_transformed.argtypes = [P, P, I64, P, I64, P, I64]
+    L.ghsvd_get_state.argtypes = [P, P, I64, P, I64, P, I64, P, I64]
+    L.ghsvd_set_state.argtypes = [P, P, I64, P, I64, P, I64, P, I64]
     L.ghsvd_extract_x.argtypes = [P, P, I64]
     L.ghsvd_extract_x.restype = ctypes.c_int
     L.ghsvd_hz2x2_batch.argtypes = [P, I64, P, D, Ci, P, P]
@@ -121,7 +124,8 @@ def load():
     L.ghsvd_exchange_plan.argtypes = [Ci, Ci, Ci, Ci, Ci, P, P, P, P, P, P]
     L.ghsvd_nccl_unique_id.argtypes = [P]
     for f in ("ghsvd_create", "ghsvd_factor", "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors",
-              "ghsvd_sweep", "ghsvd_run_steps", "ghsvd_extract", "ghsvd_get_transformed", "ghsvd_hz2x2_batch"):
+              "ghsvd_sweep", "ghsvd_run_steps", "ghsvd_extract", "ghsvd_get_transformed", "ghsvd_get_state",
+              "ghsvd_set_state", "ghsvd_hz2x2_batch"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -349,6 +353,28 @@ class Context:
                                                   G.ctypes.data_as(ctypes.c_void_p), m,
                                                   Z.ctypes.data_as(ctypes.c_void_p), n), "get_transformed")
         return F, G, Z
+
+    def get_state(self) -> dict:
+        """Checkpoint of the sweep state (numpy): F', G' (bordered m x n), Z' and, with
+        want_x, W^T (n x n).  See ghsvd_get_state."""
+        m, n = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self._L.ghsvd_get_factors(self._h, ctypes.byref(m), ctypes.byref(n), None, 0, None, None, 0,
+                                              None), "get_factors")
+        m, n = m.value, n.value
+        st = {"F": np.zeros((m, n), np.complex128, order="F"), "G": np.zeros((m, n), np.complex128, order="F"),
+              "Z": np.zeros((n, n), np.complex128, order="F"),
+              "W": np.zeros((n, n), np.complex128, order="F") if self.opts.want_x else None}
+        p = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)   # noqa: E731
+        self._check(self._L.ghsvd_get_state(self._h, p(st["F"]), m, p(st["G"]), m, p(st["Z"]), n, p(st["W"]), n),
+                    "get_state")
+        return st
+
+    def set_state(self, st: dict):
+        """Restore a get_state() checkpoint; the next sweep() resumes from it."""
+        F, G, Z, W = (np.asfortranarray(st[k]) if st.get(k) is not None else None for k in ("F", "G", "Z", "W"))
+        p = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)   # noqa: E731
+        self._check(self._L.ghsvd_set_state(self._h, p(F), F.shape[0], p(G), G.shape[0], p(Z), Z.shape[0], p(W),
+                                            Z.shape[0]), "set_state")
 
     def hz2x2_batch(self, pivots: np.ndarray, tol: float, criterion: int = 0):
         """Evaluate the device 2x2 transformation on (count, 8) pivots -> (Z (count, 8), kind)."""

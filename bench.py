@@ -438,7 +438,7 @@ def main():
     ap.add_argument("--want-x", action="store_true",
                     help="also accumulate Z'^{-1} during the sweep (full GHSVD X, NEXT-1)")
     ap.add_argument("--ref-budget", type=float, default=15.0)
-    ap.add_argument("--ref-sweeps", type=int, default=35,
+    ap.add_argument("--ref-sweeps", type=int, default=36,
                     help="sweep count used to extrapolate the oracle sample in --impl reference")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -18,7 +18,10 @@ namespace {
 // (Zr + Zi) / (Xr + Xi) DADDs of the 3M scheme stall on the FP64 pipe the DMMAs occupy
 // (math-pipe stalls 50 % vs 24 %).  Unrolling the k-step loop (fragment loads issued
 // ahead of the previous k-step's DMMAs; bitwise the same result) was slower: config 3
-// 10.78 s rolled, 10.98 s unrolled x2, 11.47 s fully unrolled.
+// 10.78 s rolled, 10.98 s unrolled x2, 11.47 s fully unrolled.  Splitting the output
+// columns over a 2-CTA cluster (each CTA stages half of X and of Z_blk, 70 KB, so three
+// CTAs fit an SM; the peer's X half copied through DSMEM between two cluster barriers;
+// bitwise the same result) was slower still: 12.64 s.
 // wmode = 1: the tiles are row tiles of W^T (n rows) and the right factor is
 // (Z_blk^{-1})^T (NEXT-1 accumulation of Z'^{-1}).
 template <bool M4>

@@ -21,7 +21,10 @@
  *    error ghsvd_last_error() describes it and the context stays usable for
  *    ghsvd_destroy() (and for a new set_factors/factor).
  *  - Call order: create -> (factor | set_factors) -> [reduce] -> [get_factors]
- *    -> sweep -> extract -> destroy.  Out-of-order calls return GHSVD_E_STATE.
+ *    -> sweep [-> sweep ...] -> extract -> destroy; a new factor / set_factors
+ *    starts the next problem in the same context; [get_state] between sweeps, and
+ *    [set_state] after the problem's factor / set_factors / reduce, checkpoint and
+ *    restore a solve.  Out-of-order calls return GHSVD_E_STATE.
  */
 #ifndef GHSVD_H
 #define GHSVD_H

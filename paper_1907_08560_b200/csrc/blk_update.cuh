@@ -25,8 +25,7 @@ namespace {
 // wmode = 1: the tiles are row tiles of W^T (n rows) and the right factor is
 // (Z_blk^{-1})^T (NEXT-1 accumulation of Z'^{-1}).
 template <bool M4>
-__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile0, int tile_end, int tpc,
-                                                     int wmode) {
+__global__ void __launch_bounds__(NT_U) k_blk_update(BlkArgs a, int tF, int tile0, int wmode) {
   trace_begin(a);
   extern __shared__ __align__(128) double2 usm[];  // X tile [KM][US] | Z_blk [KM][ZS]
   const int pl = a.pair0 + blockIdx.x;

@@ -254,9 +254,9 @@ static void launch_update(const BlkSetup& S, BlkArgs a, int pair0, int np, int t
   a.pair0 = pair0;
   if (np <= 0 || tend <= tbeg) return;
   if (S.upd4m)
-    k_blk_update<true><<<dim3(np, tend - tbeg), NT_U, S.smem_u, st>>>(a, S.tF, tbeg, tend, 1, wmode);
+    k_blk_update<true><<<dim3(np, tend - tbeg), NT_U, S.smem_u, st>>>(a, S.tF, tbeg, wmode);
   else
-    k_blk_update<false><<<dim3(np, tend - tbeg), NT_U, S.smem_u, st>>>(a, S.tF, tbeg, tend, 1, wmode);
+    k_blk_update<false><<<dim3(np, tend - tbeg), NT_U, S.smem_u, st>>>(a, S.tF, tbeg, wmode);
 }
 
 // Diagnostic: block steps [s0, s0+ns) of the first block sweep, one stream, no overlap.

@@ -173,7 +173,6 @@ struct LoopGroup {
   std::vector<Ctx*> ctx;
   std::vector<cudaEvent_t> ev_done, ev_copy;
   std::vector<DevCounters> cnt;
-  int joined = 0;
   // host barrier over the group's ranks; false on timeout (a rank failed) -- the group
   // is then broken and every later barrier fails at once
   bool barrier() {
@@ -235,7 +234,6 @@ static ghsvd_status loop_init(Ctx* ctx, const char* id) {
     g->ctx[r] = ctx;
     GH_CUDA(cudaEventCreateWithFlags(&g->ev_done[r], cudaEventDisableTiming));
     GH_CUDA(cudaEventCreateWithFlags(&g->ev_copy[r], cudaEventDisableTiming));
-    g->joined++;
   }
   CommHandle* c = new CommHandle{2, nullptr, nullptr, g};
   ctx->comm = c;

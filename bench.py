@@ -148,6 +148,11 @@ def cpu_baseline_sample(F0, J0, G0, sweeps: int, budget_s: float = 15.0):
             "seconds_measured": t1 + t2 + tn}
 
 
+# sweeps the GPU (BO) solve of each config takes: the --impl reference
+# arm times a bounded oracle sample and extrapolates to this many sweeps
+REF_SWEEPS = {0: 7, 1: 18, 2: 13, 3: 36, 4: 14, 5: 17}
+
+
 def run_reference(args):
     """--impl reference: the oracle as it stands, on host cores, same config/metric."""
     ws, rank, _ = _dist()
@@ -161,7 +166,9 @@ def run_reference(args):
         F0, J0, G0 = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
     else:
         F0, J0, G0 = payload.F, payload.J, payload.G
-    sweeps = args.ref_sweeps
+    # sweep count of the GPU solve of this config (measured this round)
+    sweeps = args.ref_sweeps if args.ref_sweeps > 0 else REF_SWEEPS.get(args.config, 36)
+    m, n = F0.shape
     vals = []
     for i in range(args.warmup + args.steps):
         cb = cpu_baseline_sample(F0, J0, G0, sweeps, budget_s=args.ref_budget)
@@ -172,7 +179,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": inputs.CONFIGS[args.config]["name"], "variant": "oracle-pointwise"},
+            "config": {"workload": inputs.CONFIGS[args.config]["name"], "m": m, "n": n,
+                       "variant": "oracle-pointwise", "sweeps_extrapolated": sweeps},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -438,8 +446,9 @@ def main():
     ap.add_argument("--want-x", action="store_true",
                     help="also accumulate Z'^{-1} during the sweep (full GHSVD X, NEXT-1)")
     ap.add_argument("--ref-budget", type=float, default=15.0)
-    ap.add_argument("--ref-sweeps", type=int, default=36,
-                    help="sweep count used to extrapolate the oracle sample in --impl reference")
+    ap.add_argument("--ref-sweeps", type=int, default=0,
+                    help="sweep count used to extrapolate the oracle sample in --impl reference "
+                         "(0 = the GPU solve's count for the config, REF_SWEEPS)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -55,3 +55,22 @@ def test_clocks_sampled_without_throttle(line):
     c = line["clocks"]
     assert c["samples"] > 0 and c["sm_mhz"] is not None
     assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(c["reasons"])
+
+
+def test_reference_arm_runs_and_keeps_the_contract():
+    """bench.py --impl reference (the oracle as it stands, bounded sample) on config 1:
+    one JSON line with impl, the arm's metric / unit / direction, cpu_baseline and a
+    zero-transfer e2e object."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                        "--steps", "1", "--warmup", "0", "--ref-budget", "2"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["higher_is_better"] is False and d["value"] > 0
+    assert d["metric"].startswith("GHSVD time-to-converge") and d["unit"] == "s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["workload"] == "c1_known_gsvd" and d["config"]["sweeps_extrapolated"] == 18

@@ -452,6 +452,9 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
   GH_CUDA(cudaStreamSynchronize(str));
   const bool timing = ctx->o.detail_timing != 0;
+  // detail_timing 2: only the F/G update spans (two events per half-step instead of four;
+  // each event record costs ~3 us of stream time, 1.2 % of config 3 at four)
+  const bool tfull = ctx->o.detail_timing == 1;
   // The Z' update of step s (aux stream) overlaps the Gram + pivot of step s+1: Z is
   // touched by no other kernel, and Z_blk / applied are double-buffered by step parity.
   if (!ctx->aux_stream) GH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
@@ -568,10 +571,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       for (int h = 0; h < nh; h++) {
         cudaStream_t sh = hs_st[h];
         a.pair0 = h_pair0[h];
-        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 0], sh));
+        if (tfull) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 0], sh));
         a.trace_id = s * TRACE_SLOTS + 0 + h;
         launch_gram(S, a, h_np[h], sh);
-        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 1], sh));
+        if (tfull) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 1], sh));
         cudaStream_t fs = fp_st[h];
         if (fs != sh) {
           GH_CUDA(cudaEventRecord(ev_gr[h], sh));
@@ -685,8 +688,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       if (timing) {
         for (int h = 0; h < nh; h++) {
           float t0 = 0, t1 = 0, t2 = 0;
-          GH_CUDA(cudaEventElapsedTime(&t0, tev[8 * s + 4 * h + 0], tev[8 * s + 4 * h + 1]));
-          GH_CUDA(cudaEventElapsedTime(&t1, tev[8 * s + 4 * h + 1], tev[8 * s + 4 * h + 2]));
+          if (tfull) {
+            GH_CUDA(cudaEventElapsedTime(&t0, tev[8 * s + 4 * h + 0], tev[8 * s + 4 * h + 1]));
+            GH_CUDA(cudaEventElapsedTime(&t1, tev[8 * s + 4 * h + 1], tev[8 * s + 4 * h + 2]));
+          }
           GH_CUDA(cudaEventElapsedTime(&t2, tev[8 * s + 4 * h + 2], tev[8 * s + 4 * h + 3]));
           st->t_gram += t0 * 1e-3;
           st->t_pivot += t1 * 1e-3;

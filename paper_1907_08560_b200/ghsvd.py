@@ -174,7 +174,7 @@ class Context:
                  stream=None, world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  nblocks: int = 0, max_sweeps: int = 30, criterion: str = "relative", eps: float = 0.0,
                  cluster: int = 0, threads: int = 0, use_graph: bool = True, kernel: int = 0,
-                 detail_timing: bool = False, want_x: bool = False):
+                 detail_timing=False, want_x: bool = False):
         import torch
         L = load()
         self._L = L
@@ -199,7 +199,7 @@ class Context:
         o.threads = threads
         o.use_graph = 1 if use_graph else 0
         o.kernel = kernel
-        o.detail_timing = 1 if detail_timing else 0
+        o.detail_timing = int(detail_timing)   # bool or 0 / 1 / 2 (see ghsvd.h)
         o.want_x = 1 if want_x else 0
         self.opts = o
         nbytes = L.ghsvd_workspace_bytes(ctypes.byref(o), m, n, nl)

@@ -86,8 +86,9 @@ typedef struct {
   int detail_timing;   /* blocked: 1 = CUDA events around every kernel on its launching stream
                           (fills t_* in ghsvd_stats; kernels of the two halves overlap, so the spans
                           are upper bounds of the kernels' own durations); 2 = only around the F/G
-                          updates (t_update*, half the event records: ~0.6 % instead of ~1.2 % of
-                          the sweep time on config 3) */
+                          updates of every 8th block step (t_update_fg, flops_update_fg and
+                          launches_update_fg then cover those sampled launches; ~0.1 % of the
+                          sweep time instead of ~1.2 % at 1 on config 3) */
   int want_x;          /* also accumulate W = Z'^{-1} during the sweep so that ghsvd_extract_x
                           can return X = Z^{-1} = Sigma Z'^{-1} (NEXT-1):
                           pointwise by 2x2 inverses, blocked by block-pivot inverses.

@@ -455,6 +455,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   // detail_timing 2: only the F/G update spans (two events per half-step instead of four;
   // each event record costs ~3 us of stream time, 1.2 % of config 3 at four)
   const bool tfull = ctx->o.detail_timing == 1;
+  // level 2 samples the update spans on every TSTRIDE-th block step (an unbiased estimate
+  // of the average launch duration at 1/TSTRIDE of the event cost)
+  const int tstride = tfull ? 1 : 8;
+  auto sampled = [&](int s) { return timing && s % tstride == 0; };
   // The Z' update of step s (aux stream) overlaps the Gram + pivot of step s+1: Z is
   // touched by no other kernel, and Z_blk / applied are double-buffered by step parity.
   if (!ctx->aux_stream) GH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
@@ -586,7 +590,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         launch_pivot(S, a, h_np[h], fs);
         GH_CUDA(cudaEventRecord(ev_piv[h], fs));
         if (fs != sh) GH_CUDA(cudaStreamWaitEvent(sh, ev_piv[h], 0));
-        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
+        if (sampled(s)) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 2], sh));
         a.trace_id = s * TRACE_SLOTS + 6 + h;
         if (split_bnd) {
           // boundary pair first (the only pair of this half the other half's next-step
@@ -599,7 +603,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         } else {
           launch_update(S, a, h_pair0[h], h_np[h], 0, 2 * tF, 0, sh);
         }
-        if (timing) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 3], sh));
+        if (sampled(s)) GH_CUDA(cudaEventRecord(tev[8 * s + 4 * h + 3], sh));
         GH_CUDA(cudaEventRecord(ev_fg[h], sh));
       }
       // Z' update of all pairs of step s on the aux stream (overlaps step s+1)
@@ -680,12 +684,16 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
     st->kernel_seconds += kms * 1e-3;
     st->launches += (uint64_t)(3 * nh + (split_bnd ? 2 : 0) + (a.W ? 2 : 1)) * nst;
-    st->launches_update_fg += (uint64_t)(nh + (split_bnd ? 2 : 0)) * nst;
     for (int s = 0; s < nst; s++) {
       st->flops_gram += fl_gram[s];
       st->flops_update += fl_upd[s];
-      st->flops_update_fg += fl_upd_fg[s];
-      if (timing) {
+      // the *_update_fg figures cover the launches whose spans are recorded (all, or the
+      // sampled steps under detail_timing 2; all when timing is off)
+      if (!timing || sampled(s)) {
+        st->flops_update_fg += fl_upd_fg[s];
+        st->launches_update_fg += (uint64_t)(nh + (split_bnd ? 2 : 0));
+      }
+      if (sampled(s)) {
         for (int h = 0; h < nh; h++) {
           float t0 = 0, t1 = 0, t2 = 0;
           if (tfull) {

@@ -86,9 +86,11 @@ typedef struct {
   int detail_timing;   /* blocked: 1 = CUDA events around every kernel on its launching stream
                           (fills t_* in ghsvd_stats; kernels of the two halves overlap, so the spans
                           are upper bounds of the kernels' own durations); 2 = only around the F/G
-                          updates of every 8th block step (t_update_fg, flops_update_fg and
-                          launches_update_fg then cover those sampled launches; ~0.1 % of the
-                          sweep time instead of ~1.2 % at 1 on config 3) */
+                          updates of every 8th block step, the sampled phase rotating with the
+                          sweep (every step if there are fewer than 16): t_update, t_update_fg,
+                          flops_update_fg and launches_update_fg then cover ONLY those sampled
+                          launches (t_gram, t_pivot stay 0), while flops_update covers all
+                          (~0.1 % of the sweep time instead of ~1.2 % at 1 on config 3) */
   int want_x;          /* also accumulate W = Z'^{-1} during the sweep so that ghsvd_extract_x
                           can return X = Z^{-1} = Sigma Z'^{-1} (NEXT-1):
                           pointwise by 2x2 inverses, blocked by block-pivot inverses.
@@ -109,7 +111,9 @@ typedef struct {
   double alg_flops;           /* algorithmic FP64 flops (blocked: Hermitian block Grams + updates) */
   double t_gram, t_pivot, t_update, t_exchange;  /* blocked: summed device time per kernel kind
                                                     (CUDA events, only if opts.detail_timing) */
-  double flops_gram, flops_update;               /* blocked: algorithmic flops of those kernels */
+  double flops_gram, flops_update;               /* blocked: algorithmic flops of those kernels;
+                                                    updates count only the block pairs whose
+                                                    update ran (device count per block step) */
   double max_offdiag_last;    /* max scaled off-diagonal measure seen in the last sweep */
   uint64_t all_per_sweep[64]; /* per-sweep counters (first 64 sweeps) */
   uint64_t big_per_sweep[64];

@@ -69,6 +69,8 @@ struct BlkArgs {
   double eps;
   int literal;
   int inner_sweeps;
+  unsigned long long* upd_k2; // [block step] sum of k^2 over the pairs whose update runs
+                              // (k = w_p + w_q; reset per sweep) -> exact update flops
   unsigned long long* trace;  // GHSVD_TRACE: [launch id][first CTA start, last CTA end] (ns)
   int trace_id;
 };

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
   for (int e = tid; e < KM * KM; e += NT_P) zo[e] = W0[e];
   if (tid == 0) {
     a.applied[pl] = cnt_all > 0;
+    if (cnt_all > 0) atomicAdd(&a.upd_k2[a.s], (unsigned long long)(k * k));
     atomicAdd(&a.cnt->all, cnt_all);
     atomicAdd(&a.cnt->big, cnt_big);
   }
@@ -430,6 +431,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_PC, 1) k_blk_pivo
     if (err_local) atomicCAS(&a.cnt->err, 0, err_local);
     if (lane == 0) {
       a.applied[pl] = w0_all > 0;
+      if (w0_all > 0) atomicAdd(&a.upd_k2[a.s], (unsigned long long)(k * k));
       atomicAdd(&a.cnt->all, w0_all);
       atomicAdd(&a.cnt->big, w0_big);
       atomicMax(&a.cnt->off_bits, (unsigned long long)__double_as_longlong(w0_off));

@@ -112,7 +112,8 @@ static size_t blk_scratch_for(int64_t K, int64_t nb, bool want_x) {
   return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)2 * K * KM * KM * 16) +
          al256((size_t)2 * K * 4) + 2 * al256((size_t)(nb + 2) * 4) + 2 * al256((size_t)K * KM * KM * 16) +
          al256((size_t)K * KM) + al256((size_t)2 * K * 4) + (want_x ? al256((size_t)2 * K * KM * KM * 16) : 0) +
-         al256((size_t)(nb + 2) * TRACE_SLOTS * 16) + al256((size_t)2 * K * 4) + 4096;
+         al256((size_t)(nb + 2) * TRACE_SLOTS * 16) + al256((size_t)2 * K * 4) + al256((size_t)(nb + 2) * 8) +
+         4096;
 }
 
 // workspace bound at ghsvd_create for factors of up to n columns: the sweep may see
@@ -173,10 +174,12 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
     a.zinvT = nullptr;
   }
   S.trace_buf = (unsigned long long*)p; p += al256((size_t)(pl.nblk + 2) * TRACE_SLOTS * 16);
+  a.upd_k2 = (unsigned long long*)p; p += al256((size_t)(pl.nblk + 2) * 8);
   a.trace = nullptr;
   a.trace_id = 0;
   k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
   GH_CUDA(cudaMemsetAsync(a.gcnt, 0, (size_t)2 * pl.K * 4, str));
+  GH_CUDA(cudaMemsetAsync(a.upd_k2, 0, (size_t)(pl.nblk + 2) * 8, str));
   GH_CUDA(cudaGetLastError());
   S.bs_h.assign(pl.nblk, 0);
   S.bw_h.assign(pl.nblk, 0);
@@ -326,18 +329,19 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
     for (auto e : ev_upd) cudaEventDestroy(e);
     for (auto e : tev) cudaEventDestroy(e);
   };
-  double fl_gram_sweep = 0.0, fl_upd_sweep = 0.0;
+  double fl_gram_sweep = 0.0;
   for (int s = 0; s < nst; s++)
     for (int kk = pl.slot0; kk < pl.slot0 + pl.K; kk++) {
       long long bp, bq;
       rr_pair(pl.nblk, s, kk, &bp, &bq);
       const double kq = S.bw_h[bp] + S.bw_h[bq];
       fl_gram_sweep += 8.0 * kq * (kq + 1) * ctx->m;
-      fl_upd_sweep += 8.0 * kq * kq * (2.0 * ctx->m + ctx->n);
     }
+  std::vector<unsigned long long> k2(nst);
   GH_CUDA(cudaEventRecord(ctx->ev0, str));
   for (int sw = 0; sw < ctx->o.max_sweeps; sw++) {
     GH_CUDA(cudaMemsetAsync(ctx->cnt, 0, sizeof(DevCounters), str));
+    GH_CUDA(cudaMemsetAsync(a.upd_k2, 0, (size_t)nst * 8, str));
     GH_CUDA(cudaEventRecord(ctx->ev2, str));
     for (int g = 0; g < G; g++) GH_CUDA(cudaStreamWaitEvent(ctx->grp_streams[g], ctx->ev2, 0));
     for (int s = 0; s < nst; s++) {
@@ -370,6 +374,7 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
     GH_CUDA(cudaEventRecord(ctx->ev3, str));
     DevCounters c;
     GH_CUDA(cudaMemcpyAsync(&c, ctx->cnt, sizeof(c), cudaMemcpyDeviceToHost, str));
+    GH_CUDA(cudaMemcpyAsync(k2.data(), a.upd_k2, (size_t)nst * 8, cudaMemcpyDeviceToHost, str));
     GH_CUDA(cudaStreamSynchronize(str));
     if (c.err) {
       destroy_events();
@@ -383,6 +388,8 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
     st->kernel_seconds += kms * 1e-3;
     st->launches += (uint64_t)(a.W ? 4 : 3) * G * nst;
     st->flops_gram += fl_gram_sweep;
+    double fl_upd_sweep = 0.0;   // only the pairs whose update ran (device count of k^2)
+    for (int s = 0; s < nst; s++) fl_upd_sweep += 8.0 * (double)k2[s] * (2.0 * ctx->m + ctx->n);
     st->flops_update += fl_upd_sweep;
     st->flops_update_fg += fl_upd_sweep;   // F, G and Z' row tiles share one launch here
     st->launches_update_fg += (uint64_t)G * nst;
@@ -458,7 +465,14 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   // level 2 samples the update spans on every TSTRIDE-th block step (an unbiased estimate
   // of the average launch duration at 1/TSTRIDE of the event cost)
   const int tstride = tfull ? 1 : 8;
-  auto sampled = [&](int s) { return timing && s % tstride == 0; };
+  // the sampled phase rotates with the sweep (step 0 of a sweep follows a host sync and
+  // runs without a concurrent Z' update, so it must not be over-represented); with fewer
+  // than 2 * TSTRIDE block steps every step is sampled
+  int cur_sw = 0;
+  const int nst_all = pl.nblk - 1;
+  auto sampled = [&](int s) {
+    return timing && (tstride == 1 || nst_all < 2 * tstride || s % tstride == cur_sw % tstride);
+  };
   // The Z' update of step s (aux stream) overlaps the Gram + pivot of step s+1: Z is
   // touched by no other kernel, and Z_blk / applied are double-buffered by step parity.
   if (!ctx->aux_stream) GH_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
@@ -530,16 +544,16 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   double2* zblk0 = a.zblk;
   double2* zinv0 = a.zinvT;
   int* applied0 = a.applied;
-  // algorithmic flops per block step (Hermitian Grams k(k+1)/2 m each; updates k^2 (2m+n))
-  std::vector<double> fl_gram(nst, 0.0), fl_upd(nst, 0.0), fl_upd_fg(nst, 0.0);
+  // algorithmic flops per block step: Hermitian Grams k(k+1)/2 m each (every pair);
+  // updates k^2 (2m+n) for the pairs whose update runs (device sum of k^2 per step)
+  std::vector<double> fl_gram(nst, 0.0);
+  std::vector<unsigned long long> k2(nst);
   for (int s = 0; s < nst; s++)
     for (int kk = pl.slot0; kk < pl.slot0 + pl.K; kk++) {
       long long bp, bq;
       rr_pair(pl.nblk, s, kk, &bp, &bq);
       const double kq = bw_h[bp] + bw_h[bq];
       fl_gram[s] += 8.0 * kq * (kq + 1) * ctx->m;
-      fl_upd[s] += 8.0 * kq * kq * (2.0 * ctx->m + ctx->n);
-      fl_upd_fg[s] += 8.0 * kq * kq * (2.0 * ctx->m);
     }
   const char* trace_path = getenv("GHSVD_TRACE");
   std::vector<unsigned long long> trace_h;
@@ -550,8 +564,10 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   }
   GH_CUDA(cudaEventRecord(ctx->ev0, str));
   for (int sw = 0; sw < ctx->o.max_sweeps; sw++) {
+    cur_sw = sw;
     a.trace = (sw == 0 && !trace_h.empty()) ? S.trace_buf : nullptr;
     GH_CUDA(cudaMemsetAsync(ctx->cnt, 0, sizeof(DevCounters), str));
+    GH_CUDA(cudaMemsetAsync(a.upd_k2, 0, (size_t)nst * 8, str));
     GH_CUDA(cudaEventRecord(ctx->ev2, str));
     for (int h = 0; h < nh; h++)
       if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(hs_st[h], ctx->ev2, 0));
@@ -648,6 +664,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     GH_CUDA(cudaEventRecord(ctx->ev3, str));
     DevCounters c;
     GH_CUDA(cudaMemcpyAsync(&c, ctx->cnt, sizeof(c), cudaMemcpyDeviceToHost, str));
+    GH_CUDA(cudaMemcpyAsync(k2.data(), a.upd_k2, (size_t)nst * 8, cudaMemcpyDeviceToHost, str));
     GH_CUDA(cudaStreamSynchronize(str));
     if (multi) {
       ghsvd_status e = comm_allreduce_counters(ctx, &c);
@@ -686,11 +703,11 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     st->launches += (uint64_t)(3 * nh + (split_bnd ? 2 : 0) + (a.W ? 2 : 1)) * nst;
     for (int s = 0; s < nst; s++) {
       st->flops_gram += fl_gram[s];
-      st->flops_update += fl_upd[s];
+      st->flops_update += 8.0 * (double)k2[s] * (2.0 * ctx->m + ctx->n);
       // the *_update_fg figures cover the launches whose spans are recorded (all, or the
       // sampled steps under detail_timing 2; all when timing is off)
       if (!timing || sampled(s)) {
-        st->flops_update_fg += fl_upd_fg[s];
+        st->flops_update_fg += 8.0 * (double)k2[s] * (2.0 * ctx->m);
         st->launches_update_fg += (uint64_t)(nh + (split_bnd ? 2 : 0));
       }
       if (sampled(s)) {

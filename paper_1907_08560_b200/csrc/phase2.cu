@@ -142,6 +142,10 @@ __global__ void __launch_bounds__(T2) k_piv_a(double2* F, long long ld, long lon
     }
   }
   block_argmax(v, jm);
+  if (jm == 0x7fffffffffffffffll) {   // every |hd[j]| is NaN: no candidate, flag and keep k
+    if (threadIdx.x == 0) s.ctl[3] = -8;
+    jm = k;
+  }
   swap_cols_dev(F, ld, m, k, jm);
   if (threadIdx.x == 0 && jm != k) {
     const long long t = p2[k]; p2[k] = p2[jm]; p2[jm] = t;
@@ -515,6 +519,10 @@ ghsvd_status phase2_reduce(Ctx* ctx, int flags) {
     P2CHK();
     GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 16, cudaMemcpyDeviceToHost, st));
     GH_CUDA(cudaStreamSynchronize(st));
+    if (ctl[3] == -8) {
+      ctx->err = "reduce: non-finite J-norms in the JQR pivot search at step " + std::to_string(k);
+      return GHSVD_E_NONFINITE;
+    }
     if (ctl[3]) {
       ctx->err = "reduce: degenerate JQR pivot (J-Grammian numerically singular) at step " + std::to_string(k);
       return GHSVD_E_RANK_DEFICIENT;

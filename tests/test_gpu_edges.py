@@ -120,3 +120,22 @@ def test_zero_column_of_F_gives_zero_eigenvalue(gh, variant):
     nz = np.abs(lo) > 1e-12 * np.abs(lo).max()
     a, b = np.sort(lam[np.abs(lam) > 1e-12 * np.abs(lam).max()]), np.sort(lo[nz])
     assert a.shape == b.shape and relerr(a, b) <= 1e-9
+
+
+def test_reduce_all_nan_F_reports_nonfinite(gh):
+    """Phase 2's JQR pivot search with every J-norm NaN: GHSVD_E_NONFINITE, no fault
+    (the argmax sentinel used to index a column)."""
+    P = inputs.random_pencil(12, 60, 16, 0.5)
+    F = np.full_like(P.F, np.nan)
+    ctx = gh.Context(60, 16)
+    ctx.set_factors(F, P.J, P.G)
+    with pytest.raises(gh.GHSVDError) as e:
+        ctx.reduce()
+    assert e.value.status == -8
+    ctx.close()
+    # the device is still usable afterwards
+    ctx = gh.Context(60, 16)
+    ctx.set_factors(P.F, P.J, P.G)
+    ctx.reduce()
+    assert ctx.sweep()["converged"]
+    ctx.close()

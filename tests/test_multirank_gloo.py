@@ -123,17 +123,18 @@ def test_two_rank_blocked_equals_single_process(nblk):
 
 def test_exchange_plan_is_consistent():
     """Every block sent by one rank is received by its new owner from the old owner, for
-    P = 2, 4, 8 (each rank moves at most 2 block columns per slot pair change)."""
+    P = 2, 4, 8 and K = 1, 2, 4 block pairs per rank (the round-robin with slot
+    k -> GPU k moves at most 2 block columns out of and into each GPU per block step)."""
     from paper_1907_08560_b200 import build, ghsvd
     build.build()
-    for world in (2, 4, 8):
-        nblk = 4 * world
+    for world, K in [(w, k) for w in (2, 4, 8) for k in (1, 2, 4)]:
+        nblk = 2 * K * world
         for s in range(nblk - 1):
             s2 = (s + 1) % (nblk - 1)
             sent, recv = set(), set()
             for r in range(world):
                 sd, rv = ghsvd.exchange_plan(nblk, world, r, s, s2)
-                assert len(sd) <= 2 * (nblk // 2 // world) and len(rv) == len(sd) or True
+                assert len(sd) <= 2 and len(rv) == len(sd)
                 for b, peer in sd:
                     assert ghsvd.block_owner(nblk, world, s, b) == r and ghsvd.block_owner(nblk, world, s2, b) == peer
                     sent.add((b, r, peer))

@@ -196,3 +196,22 @@ def test_hz2x2_errors():
     assert oracle.hz2x2_raw(1.0, 1.0, 0.5, 0.0, 1.0, 0.1, tol)[0] == -6      # s_pp <= 0
     assert oracle.hz2x2_raw(1.0, 1.0, 0.5, 1.0, 1.0, 1.0, tol)[0] == -6      # x = 1: singular S (C-9)
     assert oracle.hz2x2_raw(np.nan, 1.0, 0.5, 1.0, 1.0, 0.1, tol)[0] == -8   # non-finite
+
+
+# ------------------------------------------------------------------ J-dot golden
+@pytest.mark.parametrize("case", GOLD["jdot"])
+def test_jdot_golden_through_extract(case):
+    """SPEC.md:55, 61 worked J-dots (f^* J f) pinned through the oracle's output formulas
+    (reading C-16): with g = e_1, lambda = (f^* J f) / (g^* g) = f^* J f and
+    Sigma'_F = |f^* J f|^(1/2).  The golden f equals g in both cases (a J-norm)."""
+    f = np.array([_c(v) for v in case["f"]])
+    J = np.array(case["J"], dtype=np.int8)
+    want = _c(case["value"])
+    F = np.zeros((2, 2), complex)
+    G = np.zeros((2, 2), complex)
+    F[:, 0], G[0, 0] = f, 1.0
+    F[0, 1], G[1, 1] = 1.0, 1.0          # a second, orthogonal column (lambda = 1)
+    lam, sf, sg, _ = oracle.extract(F, J, G, np.eye(2, dtype=complex))
+    assert lam[0] == want.real and lam[1] == 1.0
+    assert abs(sf[0] / sg[0] - np.sqrt(abs(want.real))) <= 4 * EPS * max(1.0, np.sqrt(abs(want.real)))
+    assert sf[0] ** 2 + sg[0] ** 2 == pytest.approx(1.0, abs=4 * EPS)

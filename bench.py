@@ -115,6 +115,69 @@ def make_factors(cfg: int, backend: str):
     return inputs.make_config(cfg, backend=backend)
 
 
+def launch_cmd(nproc: int, argv, port: int):
+    """The torchrun command bench.py re-executes itself under for --gpus N > 1 when it was
+    not started by torchrun (one process per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def shared_inputs(cfg: int, ws: int, rank: int, dev):
+    """Seeded inputs generated ONCE (rank 0, host numpy: the stored oracle references were
+    computed on exactly these atoms) and broadcast to the other ranks over NCCL, so every
+    rank factors bitwise-identical atoms."""
+    import torch
+    if ws == 1:
+        return make_factors(cfg, "numpy")
+    import torch.distributed as dist
+    from paper_1907_08560_b200 import inputs
+    obj = [None]
+    if rank == 0:
+        kind, payload = make_factors(cfg, "numpy")
+        names = ["A", "B", "U", "TAA", "TAB", "TBB", "d"] if kind == "atoms" else ["F", "J", "G"]
+        arrs = {k: np.ascontiguousarray(getattr(payload, k)) for k in names}
+        obj = [(kind, {k: (a.shape, str(a.dtype)) for k, a in arrs.items()},
+                None if kind == "atoms" else payload.lam_true)]
+    dist.broadcast_object_list(obj, 0)
+    kind, meta, lam_true = obj[0]
+    out = {}
+    for k, (shp, dt) in meta.items():
+        nbytes = int(np.prod(shp)) * np.dtype(dt).itemsize
+        host = arrs[k].view(np.uint8).reshape(-1) if rank == 0 else np.zeros(nbytes, np.uint8)
+        t = torch.from_numpy(host).to(dev)
+        dist.broadcast(t, 0)
+        out[k] = t.cpu().numpy().view(np.dtype(dt)).reshape(shp)
+    if kind == "atoms":
+        return kind, inputs.Atoms(**out)
+    return kind, inputs.Pencil(out["F"], out["J"], out["G"], lam_true=lam_true)
+
+
+def stored_oracle_parity(cfg: int, at, lam):
+    """Max relative eigenvalue error of this run against the stored oracle reference for
+    the config (tests/golden/c<cfg>_oracle_pointwise, written by the oracle-only script
+    tools/make_oracle_reference.py from the same seeded atoms), or None."""
+    from paper_1907_08560_b200 import inputs
+    stem = os.path.join(ROOT, "tests", "golden", f"c{cfg}_oracle_pointwise")
+    if not os.path.exists(stem + ".json"):
+        return None
+    meta = json.load(open(stem + ".json"))
+    ok = inputs.fingerprint_close(inputs.fingerprint(at), meta["fingerprint"])
+    lo = np.sort(np.load(stem + ".npz")["lam"])
+    la = np.sort(np.asarray(lam))
+    err = float(np.max(np.abs(la - lo) / np.abs(lo))) if ok and la.shape == lo.shape else None
+    return {"reference": os.path.relpath(stem, ROOT) + ".{json,npz}", "inputs_match": bool(ok),
+            "max_rel_lambda_err": err, "tol": 1e-6, "oracle_sweeps": meta["stats"]["sweeps"],
+            "oracle_seconds_measured": meta["seconds_sweep"], "oracle_threads": meta["threads"],
+            "oracle_cpu": meta["cpu_model"]}
+
+
 def cpu_baseline_sample(F0, J0, G0, sweeps: int, budget_s: float = 15.0):
     """Oracle on a bounded sample: steps of sweep 1 on the same factors, extrapolated
     to (n-1) * sweeps steps.  Returns the cpu_baseline object."""
@@ -233,8 +296,8 @@ def run_ours(args):
     cfg = inputs.CONFIGS[args.config]
     blocked = args.variant in ("bo", "fb")
     zgemm_peak = measure_zgemm_peak(dev) if blocked else None
-    # ---- inputs (seeded, synthetic) and Phase 1 on the device
-    kind, payload = make_factors(args.config, "torch")
+    # ---- inputs (seeded, synthetic; generated once and broadcast) and Phase 1 on the device
+    kind, payload = shared_inputs(args.config, ws, rank, dev)
     if kind == "atoms":
         at = payload
         NA, NL, NG = at.A.shape
@@ -278,6 +341,20 @@ def run_ours(args):
         Jh = torch.empty(mb, dtype=torch.int8, pin_memory=True)
         ctx.export_factors(Fh, Jh, Gh)
         stream.synchronize()
+    identical = None
+    if ws > 1:
+        # every rank must start from bitwise the same factors (deterministic Phase 1 on
+        # identical atoms): compare digests of the exported factors
+        import hashlib
+        import torch.distributed as dist
+        hs = hashlib.sha256()
+        for t in (Fh, Gh, Jh):
+            hs.update(t.contiguous().numpy().tobytes() if t.is_contiguous() else t.t().contiguous().numpy().tobytes())
+        dig = [None] * ws
+        dist.all_gather_object(dig, hs.hexdigest())
+        identical = len(set(dig)) == 1
+        if not identical:
+            raise SystemExit(f"rank {rank}: starting factors differ across ranks ({dig})")
     lam_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
     sf_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
     sg_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -336,18 +413,14 @@ def run_ours(args):
         n_upd = sum(s["launches_update_fg"] for s in stats)
         iso = None
         if ws == 1:
-            os.environ["GHSVD_SERIAL"] = "1"
-            try:
-                cp = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=1,
-                                   nblocks=args.nblocks, detail_timing=True)
-                with torch.cuda.stream(stream), warnings.catch_warnings():
-                    warnings.simplefilter("ignore")   # one-sweep probe: "not converged" is expected
-                    cp.set_factors(Fh, Jh, Gh)
-                    sp = cp.sweep()
-                stream.synchronize()
-                cp.close()
-            finally:
-                del os.environ["GHSVD_SERIAL"]
+            cp = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=1,
+                               nblocks=args.nblocks, detail_timing=True, schedule=ghsvd.SCHED_SERIAL)
+            with torch.cuda.stream(stream), warnings.catch_warnings():
+                warnings.simplefilter("ignore")   # one-sweep probe: "not converged" is expected
+                cp.set_factors(Fh, Jh, Gh)
+                sp = cp.sweep()
+            stream.synchronize()
+            cp.close()
             ia = sp["flops_update_fg"] / sp["t_update_fg"] / 1e12 if sp["t_update_fg"] > 0 else 0.0
             ig = sp["flops_gram"] / sp["t_gram"] / 1e12 if sp["t_gram"] > 0 else 0.0
             iso = {"achieved": ia, "frac": ia / zgemm_peak, "launches": int(sp["launches_update_fg"]),
@@ -355,7 +428,7 @@ def run_ours(args):
                    "avg_launch_us": sp["t_update_fg"] / max(sp["launches_update_fg"], 1) * 1e6,
                    "k_blk_gram_achieved": ig, "k_blk_gram_frac": ig / zgemm_peak,
                    "k_blk_gram_note": "span includes the fused HEBPJ / Cholesky tail of the last pairs",
-                   "probe": "1 sweep, GHSVD_SERIAL=1, same factors, CUDA events on the context stream"}
+                   "probe": "1 sweep, schedule SERIAL, same factors, CUDA events on the context stream"}
         t_gr = sum(s["t_gram"] for s in stats)
         f_gr = sum(s["flops_gram"] for s in stats)
         t_pv = sum(s["t_pivot"] for s in stats)
@@ -369,7 +442,7 @@ def run_ours(args):
         elif iso is not None:   # the timed region records only the update spans (detail_timing 2)
             others = {"k_blk_gram": {"achieved": iso["k_blk_gram_achieved"], "frac": iso["k_blk_gram_frac"],
                                      "seconds_per_sweep": sp["t_gram"],
-                                     "note": "isolated probe (GHSVD_SERIAL=1, one sweep); span includes the fused "
+                                     "note": "isolated probe (schedule SERIAL, one sweep); span includes the fused "
                                              "HEBPJ / pivoted-Cholesky tail"},
                       "k_blk_pivot": {"seconds_per_sweep": sp["t_pivot"], "note": "isolated probe",
                                       "bound": "latency (inner one-sided sweep in shared memory)"}}
@@ -423,6 +496,12 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if identical is not None:
+        line["inputs_identical_across_ranks"] = identical
+    if kind == "atoms":
+        par = stored_oracle_parity(args.config, at, lam_h.numpy())
+        if par is not None:
+            line["parity_vs_stored_oracle"] = par
     if not args.no_cpu_baseline and ws == 1:
         F0 = np.asfortranarray(Fh.numpy())
         G0 = np.asfortranarray(Gh.numpy())
@@ -461,6 +540,18 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    ws = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if args.gpus > 1 and ws == 0:
+        # not under torchrun: launch one process per GPU ourselves, or fail loudly
+        import torch
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) visible\n")
+            return 2
+        return subprocess.call(launch_cmd(args.gpus, sys.argv[1:], _free_port()))
+    if ws and ws != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}\n")
+        return 2
     return run_ours(args)
 
 

@@ -95,7 +95,34 @@ typedef struct {
                           can return X = Z^{-1} = Sigma Z'^{-1} (NEXT-1):
                           pointwise by 2x2 inverses, blocked by block-pivot inverses.
                           Costs one more n x n buffer and its updates.  Pointwise kernel 2 only. */
+  int exchange_overlap;/* multi-GPU blocked exchange (Sec 6.4.3): 0 (default) = ONE communicator and
+                          one grouped send/recv per block step on the context stream, moving the F, G
+                          and Z', W block columns together after all updates of the step; 1 = two
+                          communicators (ncclCommSplit) on two streams, the Z', W part leaving right
+                          after the Z' update so the next step's Grams need not wait for it (the
+                          paper's future-work overlap). */
+  int schedule;        /* blocked schedule / arithmetic alternatives, bitmask of GHSVD_SCHED_* (0 = the
+                          measured default; every schedule flag is bitwise-equal to it, the
+                          arithmetic flags are tested against the oracle) */
+  int groups;          /* blocked, one rank: >= 2 selects the pipelined pair-group schedule (0 = off) */
+  int gram_splits;     /* blocked: row splits of the block Grams (0 = planned against wave quantization) */
+  const char* trace_path; /* blocked: write the first sweep's launch timeline (first-CTA start,
+                          last-CTA end per launch) as CSV to this path (NULL = off) */
 } ghsvd_options;
+/* ghsvd_options.schedule bits.  ghsvd_default_options seeds schedule, groups, gram_splits and
+ * trace_path from the environment (GHSVD_SERIAL, GHSVD_PRIO=0, GHSVD_SPLIT_BND, GHSVD_GRAM3M=0,
+ * GHSVD_UPD4M, GHSVD_PIVOT_CL, GHSVD_SPLIT_FACTOR, GHSVD_GROUPS, GHSVD_NSPLIT, GHSVD_TRACE) for the tools; the
+ * library itself reads only the options it is given. */
+enum {
+  GHSVD_SCHED_SERIAL = 1,     /* every kernel alone on the context stream (isolated kernel timing) */
+  GHSVD_SCHED_NO_PRIO = 2,    /* no stream priorities */
+  GHSVD_SCHED_SPLIT_BND = 4,  /* boundary-pair / rest split of each half's F/G update */
+  GHSVD_SCHED_GRAM4M = 8,     /* exact 4M block Grams (default: 3M) */
+  GHSVD_SCHED_UPD4M = 16,     /* exact 4M block updates (default: 3M) */
+  GHSVD_SCHED_PIVOT_CL = 32,  /* two-CTA cluster block pivots */
+  GHSVD_SCHED_SPLIT_FACTOR = 64 /* block-pivot factorizations in their own launch (k_blk_factor)
+                                   instead of the Gram launch's last CTAs */
+};
 
 typedef struct {
   int sweeps;                 /* sweeps performed */
@@ -197,10 +224,23 @@ ghsvd_status ghsvd_run_steps(ghsvd_ctx ctx, int64_t s0, int64_t ns, uint64_t* al
  * lambda_i = (f_i^* J f_i) / (g_i^* g_i), sigma_f = Sigma'_F/Sigma,
  * sigma_g = Sigma'_G/Sigma, Z = Z' Sigma^-1 with rows un-permuted by P2
  * (Z~ = P2 Z); bordered column stripped.  Any output
- * pointer may be NULL.  Z is n x n (ldz >= n).  col_ids (n int64) receives the
- * global column index of each output column (identity on one GPU). */
+ * pointer may be NULL.  Z is n x n (ldz >= n), complete on every rank (multi-rank: the
+ * owners' columns are summed into every rank, see ghsvd_extract_local for the distributed
+ * form).  col_ids (n int64) receives the global column index of each output column
+ * (always the identity here). */
 ghsvd_status ghsvd_extract(ghsvd_ctx ctx, double* lambda, double* sigma_f, double* sigma_g,
                            void* Z, int64_t ldz, int64_t* col_ids);
+
+/* As ghsvd_extract, but Z stays DISTRIBUTED over the ranks: lambda,
+ * sigma_f, sigma_g are complete on every rank (n each, combined over ranks), while Z
+ * receives only the columns this rank owns after the sweep (the owner of block step 0),
+ * packed: Z is n x *ncols (ldz >= n), col_ids[j] is the global column index of packed
+ * column j (ascending within each block column), *ncols their count (ncols required; Z
+ * requires col_ids; host or device pointers).  The union of the ranks' columns is each
+ * column exactly once.  One rank: all n columns with identity ids.  Multi-rank: every
+ * rank calls it (collective over lambda, Sigma). */
+ghsvd_status ghsvd_extract_local(ghsvd_ctx ctx, double* lambda, double* sigma_f, double* sigma_g,
+                                 void* Z, int64_t ldz, int64_t* col_ids, int64_t* ncols);
 
 /* X = Z^{-1} = Sigma Z'^{-1}, the right generalized singular vectors of (3.1)
  * (F = U Sigma_F X, G = V Sigma_G X), with columns permuted back by P2

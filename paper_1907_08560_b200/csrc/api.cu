@@ -94,6 +94,22 @@ void ghsvd_default_options(ghsvd_options* o) {
   o->kernel = 0;
   o->detail_timing = 0;
   o->want_x = 0;
+  o->exchange_overlap = 0;
+  // experiment knobs of the tools: seeded from the environment HERE only (the library
+  // reads nothing else from the environment)
+  auto env = [](const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+  };
+  o->schedule = (env("GHSVD_SERIAL", 0) ? GHSVD_SCHED_SERIAL : 0) | (env("GHSVD_PRIO", 1) ? 0 : GHSVD_SCHED_NO_PRIO) |
+                (env("GHSVD_SPLIT_BND", 0) ? GHSVD_SCHED_SPLIT_BND : 0) |
+                (env("GHSVD_GRAM3M", 1) ? 0 : GHSVD_SCHED_GRAM4M) | (env("GHSVD_UPD4M", 0) ? GHSVD_SCHED_UPD4M : 0) |
+                (env("GHSVD_PIVOT_CL", 0) ? GHSVD_SCHED_PIVOT_CL : 0) |
+                (env("GHSVD_SPLIT_FACTOR", 0) ? GHSVD_SCHED_SPLIT_FACTOR : 0);
+  o->groups = env("GHSVD_GROUPS", 0);
+  o->gram_splits = env("GHSVD_NSPLIT", 0);
+  const char* tp = getenv("GHSVD_TRACE");
+  o->trace_path = tp && *tp ? tp : nullptr;
 }
 
 static bool opts_ok(const ghsvd_options* o) {
@@ -106,6 +122,9 @@ static bool opts_ok(const ghsvd_options* o) {
   if (o->nblocks < 0 || (o->nblocks & 1)) return false;
   if (o->world_size > 1 && o->nccl_id == nullptr) return false;
   if (o->world_size > 1 && o->variant == GHSVD_POINTWISE) return false;
+  if (o->exchange_overlap < 0 || o->exchange_overlap > 1 || o->schedule < 0 || o->schedule > 127 || o->groups < 0 ||
+      o->gram_splits < 0)
+    return false;
   return true;
 }
 
@@ -126,6 +145,8 @@ ghsvd_status ghsvd_create(const ghsvd_options* opts, int64_t m, int64_t n, int64
   Ctx* ctx = &h->c;
   ctx->o = *opts;
   if (ctx->o.eps <= 0) ctx->o.eps = 0x1p-53;
+  ctx->trace_path = opts->trace_path ? opts->trace_path : "";
+  ctx->o.trace_path = ctx->trace_path.empty() ? nullptr : ctx->trace_path.c_str();
   ctx->stream = (cudaStream_t)opts->stream;
   ctx->ws = (char*)workspace;
   ctx->ws_bytes = bytes;
@@ -499,6 +520,58 @@ ghsvd_status ghsvd_extract(ghsvd_ctx h, double* lambda, double* sigma_f, double*
   if (col_ids) {
     for (int64_t i = 0; i < n; i++) col_ids[i] = i;
   }
+  return GHSVD_OK;
+}
+
+ghsvd_status ghsvd_extract_local(ghsvd_ctx h, double* lambda, double* sigma_f, double* sigma_g, void* Z,
+                                 int64_t ldz, int64_t* col_ids, int64_t* ncols) {
+  if (!h) return GHSVD_E_INVALID_ARG;
+  Ctx* ctx = &h->c;
+  if (ctx->state < 1) {
+    ctx->err = "extract_local: no factors";
+    return GHSVD_E_STATE;
+  }
+  if ((Z && (ldz < ctx->n_user || !col_ids)) || !ncols) {
+    ctx->err = "extract_local: ldz < n, or Z without col_ids, or ncols NULL";
+    return GHSVD_E_INVALID_ARG;
+  }
+  CTX_CUDA(cudaSetDevice(ctx->o.device));
+  TRY(prepare(ctx));
+  TRY(launch_extract(ctx));
+  const bool dist = ctx->comm && ctx->state == 2 && !ctx->blk_start.empty();
+  if (dist)   // lambda, Sigma_F, Sigma_G combined over ranks; Z not
+    TRY(comm_finalize_outputs(ctx, (int)ctx->blk_start.size(), ctx->blk_start.data(), ctx->blk_width.data(),
+                              ctx->lam, ctx->sf, ctx->sg, nullptr, ctx->ldn, nullptr));
+  const int64_t n = ctx->n_user;
+  // the columns of this rank, in block order (one rank: all columns)
+  std::vector<int64_t> cols;
+  if (dist) {
+    std::vector<int> blocks;
+    comm_owned_blocks(ctx, (int)ctx->blk_start.size(), blocks);
+    for (int b : blocks)
+      for (int c = 0; c < ctx->blk_width[b]; c++)
+        if (ctx->blk_start[b] + c < n) cols.push_back(ctx->blk_start[b] + c);
+  } else {
+    for (int64_t i = 0; i < n; i++) cols.push_back(i);
+  }
+  if (lambda) CTX_CUDA(cudaMemcpyAsync(lambda, ctx->lam, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
+  if (sigma_f) CTX_CUDA(cudaMemcpyAsync(sigma_f, ctx->sf, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
+  if (sigma_g) CTX_CUDA(cudaMemcpyAsync(sigma_g, ctx->sg, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
+  if (Z) {
+    // block columns are contiguous runs of columns: one 2D copy per run
+    size_t j = 0;
+    while (j < cols.size()) {
+      size_t e = j + 1;
+      while (e < cols.size() && cols[e] == cols[e - 1] + 1) e++;
+      CTX_CUDA(cudaMemcpy2DAsync((double2*)Z + j * (size_t)ldz, (size_t)ldz * 16, ctx->Z2 + cols[j] * ctx->ldn,
+                                 (size_t)ctx->ldn * 16, (size_t)n * 16, e - j, cudaMemcpyDefault, ctx->stream));
+      j = e;
+    }
+  }
+  CTX_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (col_ids)
+    for (size_t j = 0; j < cols.size(); j++) col_ids[j] = cols[j];
+  *ncols = (int64_t)cols.size();
   return GHSVD_OK;
 }
 

@@ -13,7 +13,13 @@ namespace {
 
 constexpr int KM = 64;          // max block-pivot order 2w
 constexpr int RT = 32;          // rows per staged tile
-constexpr int GS = RT + 2;      // Gram tile column stride (double2), conflict-free fragments
+// Gram tile column stride (double2).  A 128-bit fragment load of 8 lanes reads rows
+// r..r+3 of two adjacent columns: with a stride = 4 (mod 8) slots the 8 lanes hit 8
+// distinct 16-byte bank groups (stride 34 = 2 mod 8 overlapped two of them: ncu counted
+// 43 % of the Gram's shared wavefronts as bank conflicts).  Two CTAs of 110.6 KB fit an
+// SM because the fused factorization keeps its scratch in the same dynamic buffer.
+constexpr int GS = RT + 4;
+constexpr int GS_FUSED = GS;
 constexpr int ZS = KM + 4;      // Z_blk column stride in smem
 constexpr int NT_G = 256, NT_P = 512, NT_U = 256;
 constexpr int US = RT + 2;      // update tile column stride

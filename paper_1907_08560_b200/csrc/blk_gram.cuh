@@ -15,8 +15,14 @@ namespace {
 // partials in fixed order; which = 0: H_blk -> HEBPJ -> F^ (and J^); which = 1: S_blk ->
 // diagonally pivoted Cholesky -> G^.  F^, G^ go to L2-resident scratch.
 constexpr int NT_F = 256;
+// W: KM x KM in shared memory followed by room for the factorization scratch (no static
+// shared memory: the fused Gram kernel reuses its pipeline buffers)
+constexpr size_t BLK_FACTOR_SMEM = (size_t)KM * KM * 16 + sizeof(hb::HebpjScr<NT_F, KM>) + 64;
+static_assert(sizeof(hb::PcholScr<KM>) <= sizeof(hb::HebpjScr<NT_F, KM>), "scratch");
+static_assert(BLK_FACTOR_SMEM <= (size_t)GSTAGES * KM * GS_FUSED * 16, "fused factor scratch");
 __device__ void blk_factor(const BlkArgs& a, int pl, int which, double2* W) {
   __shared__ int np_sh;
+  char* scr = reinterpret_cast<char*>(W + KM * KM);
   const int tid = threadIdx.x;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
@@ -56,11 +62,12 @@ __device__ void blk_factor(const BlkArgs& a, int pl, int which, double2* W) {
       const int i = e % k, j = e / k;
       if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W[i + j * KM]), 0);
     }
-    hb::block_amax<NT_F>(tv, ti);
+    auto& sc = *reinterpret_cast<hb::HebpjScr<NT_F, KM>*>(scr);
+    hb::block_amax<NT_F>(tv, ti, sc.sv1, sc.si1);
     const double tolz = __dmul_rn(__dmul_rn((double)k, 0x1p-53), tv);
-    rc = hb::hebpj_dev<NT_F, KM>(W, k, KM, out, KM, a.jhat + (size_t)pl * KM, &np_sh, tolz);
+    rc = hb::hebpj_dev<NT_F, KM>(W, k, KM, out, KM, a.jhat + (size_t)pl * KM, &np_sh, tolz, sc);
   } else {
-    rc = hb::pchol_dev<NT_F, KM>(W, k, KM, out, KM);
+    rc = hb::pchol_dev<NT_F, KM>(W, k, KM, out, KM, *reinterpret_cast<hb::PcholScr<KM>*>(scr));
   }
   if (tid == 0) {
     a.fact_ok[pl * 2 + which] = rc == 0;
@@ -77,13 +84,13 @@ __device__ void blk_factor(const BlkArgs& a, int pl, int which, double2* W) {
 // of tile row I is the B fragment of tile column I) and issues 36 DMMAs (exact 4M
 // complex product; J folded into the A operand).  The two k-halves are summed in a
 // fixed order at the end, so the result is deterministic.
-template <int GI>
+template <int GI, int TS>
 __device__ __forceinline__ void gram_tiles(const double2* T, int row, double sg, double (&acc)[9][4]) {
   constexpr int IA = GI, IB = 7 - GI, NF = 8 - GI;
   const int lane = threadIdx.x & 31;
   double2 f[NF];
 #pragma unroll
-  for (int j = 0; j < NF; j++) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
+  for (int j = 0; j < NF; j++) f[j] = T[(8 * j + (lane >> 2)) * TS + row];
   // A operand of tile rows IA, IB: J_r conj(x): (ar, ai) with conj -> (+x.y used as -(-x.y))
   const double aar = sg * f[IA].x, aai = sg * f[IA].y;
   const double abr = sg * f[IB].x, abi = sg * f[IB].y;
@@ -127,7 +134,7 @@ struct G3 {
   }
 };
 
-template <int GI, int H, bool W4>
+template <int GI, int H, bool W4, int TS>
 __device__ __forceinline__ void gram3_tiles(const double2* T, int row, double sg, double (&acc)[5][6]) {
   using C = G3<GI>;
   const int lane = threadIdx.x & 31;
@@ -135,7 +142,7 @@ __device__ __forceinline__ void gram3_tiles(const double2* T, int row, double sg
   double bs[8];
 #pragma unroll
   for (int j = 0; j < 8; j++) {
-    if (C::needB(H, W4, j) || C::needA(H, W4, j)) f[j] = T[(8 * j + (lane >> 2)) * GS + row];
+    if (C::needB(H, W4, j) || C::needA(H, W4, j)) f[j] = T[(8 * j + (lane >> 2)) * TS + row];
     if (C::needB(H, W4, j)) bs[j] = f[j].x + f[j].y;
   }
   double ar[2] = {0, 0}, ai[2] = {0, 0}, as[2] = {0, 0};   // rows IA, IB
@@ -175,10 +182,15 @@ __device__ __forceinline__ void gram3_store(double2* out, const double (&acc)[5]
   }
 }
 
-template <bool M3>
+// FUSED (default): the last CTA of each (pair, H|S) runs the block-pivot factorization
+// itself, hidden behind the other pairs' Gram CTAs; with GHSVD_SCHED_SPLIT_FACTOR
+// k_blk_factor does, in its own launch (measured slower: its ~310 us latency-bound span
+// lands on the Gram -> pivot chain).
+template <bool M3, bool FUSED>
 __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
+  constexpr int TS = FUSED ? GS_FUSED : GS;
   trace_begin(a);
-  extern __shared__ __align__(128) double2 gsm[];  // [GSTAGES][KM][GS]
+  extern __shared__ __align__(128) double2 gsm[];  // [GSTAGES][KM][TS]
   const int pl = a.pair0 + blockIdx.z, hs = blockIdx.y, split = blockIdx.x;
   int c0p, wp, c0q, wq;
   pair_cols(a, pl, c0p, wp, c0q, wq);
@@ -189,13 +201,13 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
   const int gi = warp >> 1, kh = warp & 1;
   auto load_stage = [&](int st, long long r0) {
     if (r0 < r_end) {
-      double2* T = gsm + (size_t)st * KM * GS;
+      double2* T = gsm + (size_t)st * KM * TS;
       for (int e = tid; e < KM * RT; e += NT_G) {
         const int c = e / RT, r = e % RT;
         const long long gc = gcol(c, c0p, wp, c0q, wq);
         const long long gr = r0 + r;
         const bool ok = gc >= 0 && gr < r_end;
-        cp_async16(&T[c * GS + r], ok ? (const void*)(X + gc * a.ldm + gr) : (const void*)X, ok);
+        cp_async16(&T[c * TS + r], ok ? (const void*)(X + gc * a.ldm + gr) : (const void*)X, ok);
       }
     }
     cp_commit();   // possibly empty: keeps one group per stage
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
       cp_wait<GSTAGES - 2>();
       __syncthreads();
       load_stage((st + GSTAGES - 1) % GSTAGES, r0 + (long long)(GSTAGES - 1) * RT);
-      consume(gsm + (size_t)st * KM * GS, r0);
+      consume(gsm + (size_t)st * KM * TS, r0);
       st = (st + 1) % GSTAGES;
     }
     cp_wait<0>();
@@ -235,8 +247,8 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
         switch (warp) {   // warp-uniform; tile 4 on even k-steps for h = 0, odd for h = 1
 #define G3CASE(W, GI, H)                                       \
   case W:                                                      \
-    gram3_tiles<GI, H, H == 0>(T, row0, sg0, acc);             \
-    gram3_tiles<GI, H, H == 1>(T, row1, sg1, acc);             \
+    gram3_tiles<GI, H, H == 0, TS>(T, row0, sg0, acc);         \
+    gram3_tiles<GI, H, H == 1, TS>(T, row1, sg1, acc);         \
     break;
           G3CASE(0, 0, 0) G3CASE(1, 0, 1) G3CASE(2, 1, 0) G3CASE(3, 1, 1)
           G3CASE(4, 2, 0) G3CASE(5, 2, 1) G3CASE(6, 3, 0) default: G3CASE(7, 3, 1)
@@ -276,10 +288,10 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
         const int row = 4 * (ks + kh) + (lane & 3);
         const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
         switch (gi) {   // warp-uniform
-          case 0: gram_tiles<0>(T, row, sg, acc); break;
-          case 1: gram_tiles<1>(T, row, sg, acc); break;
-          case 2: gram_tiles<2>(T, row, sg, acc); break;
-          default: gram_tiles<3>(T, row, sg, acc); break;
+          case 0: gram_tiles<0, TS>(T, row, sg, acc); break;
+          case 1: gram_tiles<1, TS>(T, row, sg, acc); break;
+          case 2: gram_tiles<2, TS>(T, row, sg, acc); break;
+          default: gram_tiles<3, TS>(T, row, sg, acc); break;
         }
       }
     });
@@ -307,22 +319,33 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
       }
     }
   }
-  // The last CTA of this (pair, H|S) to finish factorizes the summed Gram right away
-  // (threadfence-reduction pattern): no separate launch, and a pair's block pivot is
-  // formed while the Grams of later pairs are still streaming.
-  __shared__ int last_sh;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const int t = atomicAdd(&a.gcnt[pl * 2 + hs], 1);
-    last_sh = t == a.nsplit - 1;
-    if (last_sh) a.gcnt[pl * 2 + hs] = 0;   // ready for the next block step
-  }
-  __syncthreads();
-  if (last_sh) {
+  if constexpr (FUSED) {
+    // The last CTA of this (pair, H|S) to finish factorizes the summed Gram right away
+    // (threadfence-reduction pattern): no separate launch, and a pair's block pivot is
+    // formed while the Grams of later pairs are still streaming.
+    __shared__ int last_sh;
     __threadfence();
-    blk_factor(a, pl, hs, gsm);
+    __syncthreads();
+    if (tid == 0) {
+      const int t = atomicAdd(&a.gcnt[pl * 2 + hs], 1);
+      last_sh = t == a.nsplit - 1;
+      if (last_sh) a.gcnt[pl * 2 + hs] = 0;   // ready for the next block step
+    }
+    __syncthreads();
+    if (last_sh) {
+      __threadfence();
+      blk_factor(a, pl, hs, gsm);
+    }
   }
+  trace_end(a);
+}
+
+// k_blk_factor: grid (H|S, pair): sum the Gram split partials and factor the block pivot
+// (HEBPJ of H_blk, pivoted Cholesky of S_blk), one CTA each; W (k x k) in dynamic smem.
+__global__ void __launch_bounds__(NT_F) k_blk_factor(BlkArgs a) {
+  trace_begin(a);
+  extern __shared__ __align__(128) double2 fsm[];   // [KM][KM]
+  blk_factor(a, a.pair0 + blockIdx.y, blockIdx.x, fsm);
   trace_end(a);
 }
 

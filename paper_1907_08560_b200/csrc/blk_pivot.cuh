@@ -189,15 +189,23 @@ __global__ void __launch_bounds__(NT_P, 1) k_blk_pivot(BlkArgs a) {
         if (kind == KIND_SMALL || kind == KIND_BIG) {
           const double2 z11 = make_double2(zsh[pr][0], zsh[pr][1]), z21 = make_double2(zsh[pr][2], zsh[pr][3]);
           const double2 z12 = make_double2(zsh[pr][4], zsh[pr][5]), z22 = make_double2(zsh[pr][6], zsh[pr][7]);
+          // all loads of a matrix are issued before its first store (the compiler cannot
+          // prove the stores do not alias the later loads, and the unbatched form ran one
+          // load -> FMA chain -> store round trip per row: ~22 % of the kernel's samples)
           auto rot = [&](double2* M) {
+            double2 x[KM / 16], y[KM / 16];
+#pragma unroll
+            for (int t = 0; t < KM / 16; t++) {
+              x[t] = M[hl + 16 * t + p * KM];
+              y[t] = M[hl + 16 * t + q * KM];
+            }
 #pragma unroll
             for (int t = 0; t < KM / 16; t++) {
               const int i = hl + 16 * t;
-              const double2 x = M[i + p * KM], y = M[i + q * KM];
-              M[i + p * KM] = make_double2(x.x * z11.x - x.y * z11.y + y.x * z21.x - y.y * z21.y,
-                                           x.x * z11.y + x.y * z11.x + y.x * z21.y + y.y * z21.x);
-              M[i + q * KM] = make_double2(x.x * z12.x - x.y * z12.y + y.x * z22.x - y.y * z22.y,
-                                           x.x * z12.y + x.y * z12.x + y.x * z22.y + y.y * z22.x);
+              M[i + p * KM] = make_double2(x[t].x * z11.x - x[t].y * z11.y + y[t].x * z21.x - y[t].y * z21.y,
+                                           x[t].x * z11.y + x[t].y * z11.x + y[t].x * z21.y + y[t].y * z21.x);
+              M[i + q * KM] = make_double2(x[t].x * z12.x - x[t].y * z12.y + y[t].x * z22.x - y[t].y * z22.y,
+                                           x[t].x * z12.y + x[t].y * z12.x + y[t].x * z22.y + y[t].y * z22.x);
             }
           };
           rot(Fh);

@@ -47,11 +47,6 @@ namespace {
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 // tuning knobs (experiments only; defaults are the measured best)
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
 int auto_nblk(int64_t n, const ghsvd_options* o) {
   if (o->nblocks > 0) return o->nblocks;
   int64_t nb = (n + 31) / 32;      // width w <= 32 -> block pivots of order <= 64
@@ -98,7 +93,7 @@ BlkPlan make_plan(const Ctx* ctx) {
     }
   }
   p.nsplit = (int)std::max<long long>(1, best);
-  if (env_int("GHSVD_NSPLIT", 0) > 0) p.nsplit = std::min(MAX_SPLIT, env_int("GHSVD_NSPLIT", 0));
+  if (ctx->o.gram_splits > 0) p.nsplit = std::min(MAX_SPLIT, ctx->o.gram_splits);
   const long long rows_per = (ctx->m + p.nsplit - 1) / p.nsplit;
   p.split_rows = round_up(std::max<long long>(rows_per, 1), RT);
   p.nsplit = (int)((ctx->m + p.split_rows - 1) / p.split_rows);
@@ -130,7 +125,8 @@ struct BlkSetup {
   BlkPlan pl;
   BlkArgs a;
   std::vector<int> bs_h, bw_h;
-  size_t smem_g, smem_p, smem_u;
+  size_t smem_g, smem_p, smem_u, smem_f;
+  bool fused;   // block-pivot factorization fused into the Gram's last CTAs (default; not GHSVD_SCHED_SPLIT_FACTOR)
   int tF, tZ, sms;
   bool upd4m, gram3m, pivot_cl;
   size_t smem_pc;
@@ -208,20 +204,25 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   a.literal = ctx->o.criterion == GHSVD_CRIT_LITERAL;
   a.inner_sweeps = ctx->o.variant == GHSVD_BLOCKED_FB ? 30 : 1;
   a.pair0 = 0;
-  S.smem_g = (size_t)GSTAGES * KM * GS * 16;
+  S.fused = (ctx->o.schedule & GHSVD_SCHED_SPLIT_FACTOR) == 0;
+  S.smem_g = (size_t)GSTAGES * KM * (S.fused ? GS_FUSED : GS) * 16;
+  S.smem_f = BLK_FACTOR_SMEM;
   S.smem_p = (size_t)3 * KM * KM * 16;
   S.smem_u = (size_t)(KM * US + KM * ZS) * 16;
-  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
-  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
-  S.gram3m = env_int("GHSVD_GRAM3M", 1) != 0;
-  S.pivot_cl = env_int("GHSVD_PIVOT_CL", 0) != 0;
+  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_gram<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_g));
+  GH_CUDA(cudaFuncSetAttribute(k_blk_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_f));
+  S.gram3m = (ctx->o.schedule & GHSVD_SCHED_GRAM4M) == 0;
+  S.pivot_cl = (ctx->o.schedule & GHSVD_SCHED_PIVOT_CL) != 0;
   S.smem_pc = (size_t)3 * KM * RB * 16;
   GH_CUDA(cudaFuncSetAttribute(k_blk_zinv, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KM * KM * 16));
   GH_CUDA(cudaFuncSetAttribute(k_blk_pivot_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_pc));
   GH_CUDA(cudaFuncSetAttribute(k_blk_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_p));
   GH_CUDA(cudaFuncSetAttribute(k_blk_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_u));
   GH_CUDA(cudaFuncSetAttribute(k_blk_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S.smem_u));
-  S.upd4m = env_int("GHSVD_UPD4M", 0) != 0;
+  S.upd4m = (ctx->o.schedule & GHSVD_SCHED_UPD4M) != 0;
   S.tF = (int)((ctx->m + RT - 1) / RT);
   S.tZ = (int)((ctx->n + RT - 1) / RT);
   {
@@ -245,10 +246,24 @@ static void launch_pivot(const BlkSetup& S, const BlkArgs& a, int np, cudaStream
 
 // Gram launch over pairs [a.pair0, a.pair0 + np): grid (row split, H|S, pair).
 static void launch_gram(const BlkSetup& S, const BlkArgs& a, int np, cudaStream_t st) {
-  if (S.gram3m)
-    k_blk_gram<true><<<dim3(S.pl.nsplit, 2, np), NT_G, S.smem_g, st>>>(a);
-  else
-    k_blk_gram<false><<<dim3(S.pl.nsplit, 2, np), NT_G, S.smem_g, st>>>(a);
+  const dim3 g(S.pl.nsplit, 2, np);
+  if (S.fused) {
+    if (S.gram3m)
+      k_blk_gram<true, true><<<g, NT_G, S.smem_g, st>>>(a);
+    else
+      k_blk_gram<false, true><<<g, NT_G, S.smem_g, st>>>(a);
+  } else {
+    if (S.gram3m)
+      k_blk_gram<true, false><<<g, NT_G, S.smem_g, st>>>(a);
+    else
+      k_blk_gram<false, false><<<g, NT_G, S.smem_g, st>>>(a);
+  }
+}
+
+// Block-pivot factorization launch over pairs [a.pair0, a.pair0 + np): grid (H|S, pair)
+// (nothing to launch when the Gram kernel factors in its last CTAs).
+static void launch_factor(const BlkSetup& S, const BlkArgs& a, int np, cudaStream_t st) {
+  if (!S.fused) k_blk_factor<<<dim3(2, np), NT_F, S.smem_f, st>>>(a);
 }
 
 // Update launch: pairs [pair0, pair0 + np), row tiles [tbeg, tend) (see k_blk_update).
@@ -280,6 +295,7 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
   for (int64_t s = s0; s < s0 + ns; s++) {
     a.s = (int)s;
     launch_gram(S, a, S.pl.K, str);
+    launch_factor(S, a, S.pl.K, str);
     launch_pivot(S, a, S.pl.K, str);
     launch_update(S, a, 0, S.pl.K, 0, 2 * S.tF + S.tZ, 0, str);
     if (a.W) launch_update(S, a, 0, S.pl.K, 0, S.tZ, 1, str);
@@ -360,6 +376,7 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
         if (te) GH_CUDA(cudaEventRecord(te[0], sh));
         launch_gram(S, a, np, sh);
         if (te) GH_CUDA(cudaEventRecord(te[1], sh));
+        launch_factor(S, a, np, sh);
         launch_pivot(S, a, np, sh);
         if (te) GH_CUDA(cudaEventRecord(te[2], sh));
         launch_update(S, a, g0[g], np, 0, 2 * tF + tZ, 0, sh);
@@ -386,7 +403,7 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
     float kms = 0;
     GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
     st->kernel_seconds += kms * 1e-3;
-    st->launches += (uint64_t)(a.W ? 4 : 3) * G * nst;
+    st->launches += (uint64_t)((a.W ? 4 : 3) + (S.fused ? 0 : 1)) * G * nst;
     st->flops_gram += fl_gram_sweep;
     double fl_upd_sweep = 0.0;   // only the pairs whose update ran (device count of k^2)
     for (int s = 0; s < nst; s++) fl_upd_sweep += 8.0 * (double)k2[s] * (2.0 * ctx->m + ctx->n);
@@ -442,11 +459,12 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     if (e) return e;
   }
   const bool multi = ctx->comm != nullptr;   // NCCL path (also exercised with one rank)
+  const bool xch_overlap = multi && ctx->o.exchange_overlap != 0;
   {
     // one GPU: GHSVD_GROUPS=G >= 2 selects the pipelined pair-group schedule
     // (blk_sweep_groups; measured 1-2 % slower than the two-stream schedule below on
     // config 3, kept as an experiment)
-    const int G = std::min(S.pl.K, env_int("GHSVD_GROUPS", 0));
+    const int G = std::min(S.pl.K, ctx->o.groups);
     if (!multi && G >= 2) return blk_sweep_groups(ctx, st, S, G);
   }
   BlkPlan& pl = S.pl;
@@ -480,7 +498,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   // GHSVD_SERIAL=1: every kernel on the context stream, one launch per kind and step over
   // all block pairs -- the kernels run alone, so their CUDA-event durations are their
   // isolated durations (bench.py's roofline probe); same arithmetic, bitwise equal
-  const bool serial = env_int("GHSVD_SERIAL", 0) != 0;
+  const bool serial = (ctx->o.schedule & GHSVD_SCHED_SERIAL) != 0;
   cudaStream_t aux = serial ? str : ctx->aux_stream;
   // the step's pairs are split in two halves on two streams so that one half's
   // latency-bound pivot kernel overlaps the other half's Gram / update kernels
@@ -493,7 +511,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   //   medium   Gram and F, G update of both halves;
   //   lowest   the Z' update (aux): it has a whole step of slack and fills the SMs the
   //            latency-bound kernels leave idle.
-  const bool prio = env_int("GHSVD_PRIO", 1) != 0 && !serial;
+  const bool prio = (ctx->o.schedule & GHSVD_SCHED_NO_PRIO) == 0 && !serial;
   cudaStream_t hs_st[2] = {str, ctx->aux_stream2};
   cudaStream_t fp_st[2] = {str, ctx->aux_stream2};
   if (prio) {
@@ -518,7 +536,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   // GHSVD_SPLIT_BND=1 (experiment): split each half's F/G update into its boundary pair
   // and the rest, so half 0 of step s+1 may start while half 1 of step s still updates;
   // measured equal to the plain halves on config 3 (2.42 ms per block step either way)
-  const bool split_bnd = !multi && nh == 2 && KA >= 2 && pl.K - KA >= 2 && env_int("GHSVD_SPLIT_BND", 0) != 0;
+  const bool split_bnd = !multi && nh == 2 && KA >= 2 && pl.K - KA >= 2 && (ctx->o.schedule & GHSVD_SCHED_SPLIT_BND) != 0;
   cudaEvent_t ev_x;
   GH_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
   for (int i = 0; i < 2; i++) {
@@ -555,7 +573,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       const double kq = bw_h[bp] + bw_h[bq];
       fl_gram[s] += 8.0 * kq * (kq + 1) * ctx->m;
     }
-  const char* trace_path = getenv("GHSVD_TRACE");
+  const char* trace_path = ctx->o.trace_path;
   std::vector<unsigned long long> trace_h;
   if (trace_path && *trace_path) {
     trace_h.assign((size_t)nst * TRACE_SLOTS * 2, 0);
@@ -602,6 +620,8 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         }
         // Z_blk buffer b was last read by the Z update of step s-2
         if (s >= 2 || sw > 0) GH_CUDA(cudaStreamWaitEvent(fs, ev_zdone[b], 0));
+        a.trace_id = s * TRACE_SLOTS + 2 + h;
+        launch_factor(S, a, h_np[h], fs);
         a.trace_id = s * TRACE_SLOTS + 4 + h;
         launch_pivot(S, a, h_np[h], fs);
         GH_CUDA(cudaEventRecord(ev_piv[h], fs));
@@ -629,13 +649,14 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       launch_update(S, a, 0, pl.K, 2 * tF, 2 * tF + tZ, 0, aux);
       a.trace_id = s * TRACE_SLOTS + 9;
       if (a.W) launch_update(S, a, 0, pl.K, 0, tZ, 1, aux);
-      if (multi) {
-        // The exchange after step s in two parts (NEXT-2, comm/compute overlap): the Z', W
-        // block columns leave right after the Z' update, on the aux stream and a second
-        // communicator, while the F, G block columns leave as soon as the F, G updates of
-        // both halves are done -- the Grams of step s+1 need only F and G, so they no
-        // longer wait for the Z' update of step s (which keeps overlapping them, as on one
-        // GPU).  The next Z' update runs on the aux stream after the Z' exchange.
+      if (multi && xch_overlap) {
+        // exchange_overlap = 1: the exchange after step s in two parts (NEXT-2, comm/compute
+        // overlap): the Z', W block columns leave right after the Z' update, on the aux
+        // stream and a second communicator, while the F, G block columns leave as soon as
+        // the F, G updates of both halves are done -- the Grams of step s+1 need only F and
+        // G, so they no longer wait for the Z' update of step s (which keeps overlapping
+        // them, as on one GPU).  The next Z' update runs on the aux stream after the Z'
+        // exchange.
         const int s_next = (s + 1) % nst;
         ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data(), XCH_ZW, aux);
         if (e) {
@@ -646,10 +667,15 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       GH_CUDA(cudaEventRecord(ev_zdone[b], aux));
       GH_CUDA(cudaGetLastError());
       if (multi) {
+        // default (exchange_overlap = 0): ONE communicator, one grouped exchange of the F, G,
+        // Z' (and W) block columns on the context stream after every update of step s --
+        // no two NCCL operations are ever in flight on different streams
         for (int h = 0; h < nh; h++)
           if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(str, ev_fg[h], 0));
+        if (!xch_overlap) GH_CUDA(cudaStreamWaitEvent(str, ev_zdone[b], 0));
         const int s_next = (s + 1) % nst;
-        ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data(), XCH_FG, str);
+        ghsvd_status e = comm_exchange(ctx, pl.nblk, s, s_next, bs_h.data(), bw_h.data(),
+                                       xch_overlap ? XCH_FG : XCH_FG | XCH_ZW, str);
         if (e) {
           destroy_events();
           return e;
@@ -700,7 +726,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     float kms = 0;
     GH_CUDA(cudaEventElapsedTime(&kms, ctx->ev2, ctx->ev3));
     st->kernel_seconds += kms * 1e-3;
-    st->launches += (uint64_t)(3 * nh + (split_bnd ? 2 : 0) + (a.W ? 2 : 1)) * nst;
+    st->launches += (uint64_t)((S.fused ? 3 : 4) * nh + (split_bnd ? 2 : 0) + (a.W ? 2 : 1)) * nst;
     for (int s = 0; s < nst; s++) {
       st->flops_gram += fl_gram[s];
       st->flops_update += 8.0 * (double)k2[s] * (2.0 * ctx->m + ctx->n);

@@ -251,13 +251,16 @@ ghsvd_status comm_init(Ctx* ctx) {
   memcpy(&id, ctx->o.nccl_id, sizeof(id));
   ncclComm_t c, cz;
   NCCL_CALL(N->CommInitRank(&c, ctx->o.world_size, id, ctx->o.rank));
-  // second communicator for the Z', W block columns: their exchange runs on another
-  // stream, concurrently with the F, G traffic and the next step's kernels
-  ncclResult_t r = N->CommSplit(c, 0, ctx->o.rank, &cz, nullptr);
-  if (r != ncclSuccess) {
-    N->CommDestroy(c);
-    ctx->err = std::string("ncclCommSplit: ") + (N->GetErrorString ? N->GetErrorString(r) : "error");
-    return GHSVD_E_NCCL;
+  cz = nullptr;
+  if (ctx->o.exchange_overlap) {
+    // opt-in second communicator for the Z', W block columns: their exchange runs on
+    // another stream, concurrently with the F, G traffic and the next step's kernels
+    ncclResult_t r = N->CommSplit(c, 0, ctx->o.rank, &cz, nullptr);
+    if (r != ncclSuccess) {
+      N->CommDestroy(c);
+      ctx->err = std::string("ncclCommSplit: ") + (N->GetErrorString ? N->GetErrorString(r) : "error");
+      return GHSVD_E_NCCL;
+    }
   }
   ctx->comm = new CommHandle{1, c, cz, nullptr};
   return GHSVD_OK;
@@ -344,7 +347,7 @@ ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int*
   }
   if (handle(ctx)->kind == 2) return loop_exchange(ctx, rb.data(), rp.data(), nr, bstart, bwidth, part, st);
   if (ns == 0 && nr == 0) return GHSVD_OK;
-  ncclComm_t comm = part == XCH_ZW ? handle(ctx)->nccl_zw : handle(ctx)->nccl;
+  ncclComm_t comm = (part == XCH_ZW && handle(ctx)->nccl_zw) ? handle(ctx)->nccl_zw : handle(ctx)->nccl;
   NCCL_CALL(N->GroupStart());
   auto xfer = [&](int64_t b, int peer, bool send) -> ncclResult_t {
     const size_t w = (size_t)bwidth[b], c0 = (size_t)bstart[b];
@@ -404,7 +407,17 @@ ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c) {
   return GHSVD_OK;
 }
 
-// Complete the extracted outputs on every rank: zero the columns this rank does
+// Block columns this rank owns after a completed sweep (ownership of block step 0, which
+// the final exchange of every sweep restores).
+void comm_owned_blocks(const Ctx* ctx, int nblk, std::vector<int>& blocks) {
+  std::vector<int> own;
+  owners(nblk, ctx->o.world_size, 0, own);
+  blocks.clear();
+  for (int b = 0; b < nblk; b++)
+    if (own[b] == ctx->o.rank) blocks.push_back(b);
+}
+
+// Complete the extracted outputs on every rank (Zout may be NULL: Z stays distributed): zero the columns this rank does
 // not own after the final exchange (ownership of block step 0), then sum.
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam, double* sf,
                                    double* sg, double2* Zout, int64_t ldz, double2* Xout) {
@@ -432,7 +445,8 @@ ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const 
       GH_CUDA(cudaMemcpyAsync(lam + c0, pc->lam + c0, w * 8, cudaMemcpyDeviceToDevice, st));
       GH_CUDA(cudaMemcpyAsync(sf + c0, pc->sf + c0, w * 8, cudaMemcpyDeviceToDevice, st));
       GH_CUDA(cudaMemcpyAsync(sg + c0, pc->sg + c0, w * 8, cudaMemcpyDeviceToDevice, st));
-      GH_CUDA(cudaMemcpyAsync(Zout + c0 * ldz, pc->Z2 + c0 * ldz, w * ldz * 16, cudaMemcpyDeviceToDevice, st));
+      if (Zout)
+        GH_CUDA(cudaMemcpyAsync(Zout + c0 * ldz, pc->Z2 + c0 * ldz, w * ldz * 16, cudaMemcpyDeviceToDevice, st));
       if (Xout && pc->Xo)
         GH_CUDA(cudaMemcpy2DAsync(Xout + c0, (size_t)ldz * 16, pc->Xo + c0, (size_t)ldz * 16, w * 16,
                                   (size_t)ctx->n, cudaMemcpyDeviceToDevice, st));
@@ -449,7 +463,7 @@ ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const 
     GH_CUDA(cudaMemsetAsync(lam + c0, 0, w * 8, st));
     GH_CUDA(cudaMemsetAsync(sf + c0, 0, w * 8, st));
     GH_CUDA(cudaMemsetAsync(sg + c0, 0, w * 8, st));
-    GH_CUDA(cudaMemsetAsync(Zout + c0 * ldz, 0, w * ldz * 16, st));
+    if (Zout) GH_CUDA(cudaMemsetAsync(Zout + c0 * ldz, 0, w * ldz * 16, st));
     if (Xout)  // rows c0 .. c0+w-1 of X belong to this block column of W^T
       GH_CUDA(cudaMemset2DAsync(Xout + c0, (size_t)ldz * 16, 0, w * 16, (size_t)ctx->n, st));
   }
@@ -459,7 +473,7 @@ ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const 
   NCCL_CALL(N->AllReduce(lam, lam, n, ncclFloat64, ncclSum, comm, st));
   NCCL_CALL(N->AllReduce(sf, sf, n, ncclFloat64, ncclSum, comm, st));
   NCCL_CALL(N->AllReduce(sg, sg, n, ncclFloat64, ncclSum, comm, st));
-  NCCL_CALL(N->AllReduce(Zout, Zout, n * ldz * 2, ncclFloat64, ncclSum, comm, st));
+  if (Zout) NCCL_CALL(N->AllReduce(Zout, Zout, n * ldz * 2, ncclFloat64, ncclSum, comm, st));
   if (Xout) NCCL_CALL(N->AllReduce(Xout, Xout, n * ldz * 2, ncclFloat64, ncclSum, comm, st));
   NCCL_CALL(N->GroupEnd());
   return GHSVD_OK;

@@ -33,10 +33,32 @@ __device__ __forceinline__ void amax_merge(double& v, long long& i, double v2, l
   }
 }
 
+// Shared-memory scratch of the routines below, passed in by the caller (the blocked
+// variant places it in dynamic shared memory it no longer needs, so its kernels carry no
+// static shared memory; Phase 1 declares it statically).
+template <int NT, int RMAX>
+struct HebpjScr {
+  double sv[2][2][NT / 32];
+  long long si[2][2][NT / 32];
+  double sv1[NT / 32];
+  long long si1[NT / 32];
+  double2 Rk[RMAX * 2];  // 4 per 2x2 pivot (stored at 2*k .. 2*k+3 for pivot k)
+  double2 colk[2][RMAX];
+  double d[RMAX];
+  int perm[RMAX];
+  int bsz[RMAX];
+  int rowpos[RMAX];
+  signed char sgn[RMAX];
+  int err_sh;
+};
+template <int RMAX>
+struct PcholScr {
+  double dg[RMAX], iv[RMAX];   // l_kk and 1 / l_kk
+  int perm[RMAX];
+};
+
 template <int NT>
-__device__ void block_amax(double& v, long long& i) {
-  __shared__ double sv[NT / 32];
-  __shared__ long long si[NT / 32];
+__device__ void block_amax(double& v, long long& i, double* sv, long long* si) {
   for (int o = 16; o > 0; o >>= 1) {
     const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
     const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
@@ -93,9 +115,8 @@ __device__ void block_amax2(double& v, long long& i, double& u, long long& j) {
 // barrier per call; a later call with the same parity is separated by the other call's
 // barrier, so no reader of this buffer is left when it is rewritten.
 template <int NT>
-__device__ void block_amax2_db(double& v, long long& i, double& u, long long& j, int par) {
-  __shared__ double sv[2][2][NT / 32];
-  __shared__ long long si[2][2][NT / 32];
+__device__ void block_amax2_db(double& v, long long& i, double& u, long long& j, int par, double (*sv)[2][NT / 32],
+                               long long (*si)[2][NT / 32]) {
   for (int o = 16; o > 0; o >>= 1) {
     const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
     const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
@@ -150,17 +171,17 @@ __device__ inline void herm2_jacobi(double a, double2 b, double c, double2* R, d
 // division in the O(r^2) passes of an elimination step.
 template <int NT, int RMAX>
 __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long ldmo, signed char* Jout,
-                         int* npos_out, double tolz) {
+                         int* npos_out, double tolz, HebpjScr<NT, RMAX>& sc) {
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ int perm[RMAX];
-  __shared__ int bsz[RMAX];
-  __shared__ double d[RMAX];
-  __shared__ double2 Rk[RMAX * 2];  // 4 per 2x2 pivot (stored at 2*k .. 2*k+3 for pivot k)
-  __shared__ double2 colk[2][RMAX];
-  __shared__ int rowpos[RMAX];
-  __shared__ signed char sgn[RMAX];
-  __shared__ int err_sh;
+  int* perm = sc.perm;
+  int* bsz = sc.bsz;
+  double* d = sc.d;
+  double2* Rk = sc.Rk;
+  double2 (*colk)[RMAX] = sc.colk;
+  int* rowpos = sc.rowpos;
+  signed char* sgn = sc.sgn;
+  int& err_sh = sc.err_sh;
   const double alpha = (1.0 + sqrt(17.0)) / 8.0;
   for (int i = threadIdx.x; i < r; i += NT) perm[i] = i;
   if (threadIdx.x == 0) err_sh = 0;
@@ -177,7 +198,7 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
     for (int i = j + 1 + lane; i < r; i += 32) amax_merge(mu0, oidx, cabs2(W[i + j * ldw]), (long long)j * r + i);
   int k = 0, par = 0;
   while (k < r) {
-    block_amax2_db<NT>(mu1, id, mu0, oidx, par);
+    block_amax2_db<NT>(mu1, id, mu0, oidx, par, sc.sv, sc.si);
     par ^= 1;
     mu0 = __dsqrt_rn(mu0);
     const double mall = mu0 > mu1 ? mu0 : mu1;
@@ -322,11 +343,12 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
 // smallest index on ties) is done redundantly by every warp, so no barrier is spent on
 // it; one barrier per elimination step (+3 when rows are swapped).
 template <int NT, int RMAX>
-__device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long long ldg) {
+__device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long long ldg, PcholScr<RMAX>& sc) {
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ int perm[RMAX];
-  __shared__ double dg[RMAX], iv[RMAX];   // l_kk and 1 / l_kk
+  int* perm = sc.perm;
+  double* dg = sc.dg;
+  double* iv = sc.iv;
   for (int i = threadIdx.x; i < r; i += NT) perm[i] = i;
   __syncthreads();
   for (int k = 0; k < r; k++) {

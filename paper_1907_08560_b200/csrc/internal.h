@@ -28,6 +28,7 @@ struct Layout {
 
 struct Ctx {
   ghsvd_options o;
+  std::string trace_path;     // owned copy of o.trace_path (o.trace_path points here)
   cudaStream_t stream;
   cudaStream_t cap_stream;    // private stream for graph capture
   cudaStream_t aux_stream;    // blocked: Z' updates overlapped with the next step
@@ -120,6 +121,7 @@ enum { XCH_FG = 1, XCH_ZW = 2 };   // parts of the block-column exchange
 ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart, const int* bwidth, int part,
                            cudaStream_t st);
 ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c);
+void comm_owned_blocks(const Ctx* ctx, int nblk, std::vector<int>& blocks);
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam,
                                    double* sf, double* sg, double2* Zout, int64_t ldz, double2* Xout);
 

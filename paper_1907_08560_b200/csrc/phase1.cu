@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(P1T) k_hebpj(P1Scr s, int NL) {
   double2* M = s.M + (size_t)a * r * r;
   __shared__ signed char Jloc[512];
   __shared__ int np_sh;
+  __shared__ hb::HebpjScr<P1T, 512> scr;
   // tolerance r * eps * max|T| over the lower triangle
   double tv = 0.0;
   long long ti = 0;
@@ -94,9 +95,9 @@ __global__ void __launch_bounds__(P1T) k_hebpj(P1Scr s, int NL) {
     const int i = e % r, j = e / r;
     if (i >= j) hb::amax_merge(tv, ti, hb::cabs(W[i + (size_t)j * r]), 0);
   }
-  hb::block_amax<P1T>(tv, ti);
+  hb::block_amax<P1T>(tv, ti, scr.sv1, scr.si1);
   const double tolz = __dmul_rn(__dmul_rn((double)r, 0x1p-53), tv);
-  const int rc = hb::hebpj_dev<P1T, 512>(W, r, r, M, r, Jloc, &np_sh, tolz);
+  const int rc = hb::hebpj_dev<P1T, 512>(W, r, r, M, r, Jloc, &np_sh, tolz, scr);
   if (threadIdx.x == 0) {
     s.info[a] = rc;
     s.npos[a] = rc ? 0 : np_sh;

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8
   double2* f = F + k * ld;
   const double hn = jdot(f, f, J, k, m, true, sh).x;
   if (hn == 0.0 || !isfinite(hn)) {
-    if (threadIdx.x == 0) s.ctl[3] = -7;
+    if (threadIdx.x == 0 && s.ctl[3] == 0) s.ctl[3] = -7;
     return;
   }
   const int8_t sg = hn > 0.0 ? 1 : -1;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8
     block_argmax(bv, best);
     if (best == 0x7fffffffffffffffll) best = -1;
     if (best < 0) {
-      if (threadIdx.x == 0) s.ctl[3] = -7;
+      if (threadIdx.x == 0 && s.ctl[3] == 0) s.ctl[3] = -7;
       return;
     }
     for (long long c = threadIdx.x; c < n; c += T2) {
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(T2) k_rot(double2* F, long long ld, const int8
         l2 = c + t * ab;
       }
       bad = (l1 == 0.0 || l2 == 0.0);
-      if (bad) s.ctl[3] = -7;
+      if (bad && s.ctl[3] == 0) s.ctl[3] = -7;
     }
     __syncthreads();
     if (bad) return;
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(T2) k_qr_prep(double2* G, long long ld, long l
   double2* x = G + p2[k] * ld;
   const double nrm = sqrt(jdot(x, x, nullptr, k, m, false, sh).x);
   if (nrm == 0.0) {
-    if (threadIdx.x == 0) s.ctl[3] = -7;
+    if (threadIdx.x == 0 && s.ctl[3] == 0) s.ctl[3] = -7;
     return;
   }
   const double ax = cabs_(x[k]);

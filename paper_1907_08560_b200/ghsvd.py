@@ -32,7 +32,7 @@ CRITERIA = {"relative": 0, "literal": 1}
 # every symbol include/ghsvd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ghsvd_default_options", "ghsvd_workspace_bytes", "ghsvd_create", "ghsvd_factor",
            "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors", "ghsvd_sweep", "ghsvd_run_steps",
-           "ghsvd_extract", "ghsvd_extract_x", "ghsvd_get_transformed", "ghsvd_get_state", "ghsvd_set_state",
+           "ghsvd_extract", "ghsvd_extract_local", "ghsvd_extract_x", "ghsvd_get_transformed", "ghsvd_get_state", "ghsvd_set_state",
            "ghsvd_hz2x2_batch", "ghsvd_last_error",
            "ghsvd_destroy", "ghsvd_version", "ghsvd_block_owner", "ghsvd_exchange_plan",
            "ghsvd_nccl_unique_id"]
@@ -44,13 +44,19 @@ class GHSVDError(RuntimeError):
         self.status = status
 
 
+SCHED_SERIAL, SCHED_NO_PRIO, SCHED_SPLIT_BND, SCHED_GRAM4M, SCHED_UPD4M, SCHED_PIVOT_CL = 1, 2, 4, 8, 16, 32
+SCHED_SPLIT_FACTOR = 64
+
+
 class Options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("world_size", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("variant", ctypes.c_int),
                 ("ordering", ctypes.c_int), ("nblocks", ctypes.c_int), ("max_sweeps", ctypes.c_int),
                 ("criterion", ctypes.c_int), ("eps", ctypes.c_double), ("cluster", ctypes.c_int),
                 ("threads", ctypes.c_int), ("use_graph", ctypes.c_int), ("kernel", ctypes.c_int),
-                ("detail_timing", ctypes.c_int), ("want_x", ctypes.c_int)]
+                ("detail_timing", ctypes.c_int), ("want_x", ctypes.c_int), ("exchange_overlap", ctypes.c_int),
+                ("schedule", ctypes.c_int), ("groups", ctypes.c_int), ("gram_splits", ctypes.c_int),
+                ("trace_path", ctypes.c_char_p)]
 
 
 class Stats(ctypes.Structure):
@@ -109,6 +115,7 @@ def load():
     L.ghsvd_sweep.argtypes = [P, ctypes.POINTER(Stats)]
     L.ghsvd_run_steps.argtypes = [P, I64, I64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     L.ghsvd_extract.argtypes = [P, P, P, P, P, I64, P]
+    L.ghsvd_extract_local.argtypes = [P, P, P, P, P, I64, P, ctypes.POINTER(I64)]
     L.ghsvd_get_transformed.argtypes = [P, P, I64, P, I64, P, I64]
     L.ghsvd_get_state.argtypes = [P, P, I64, P, I64, P, I64, P, I64]
     L.ghsvd_set_state.argtypes = [P, P, I64, P, I64, P, I64, P, I64]
@@ -124,7 +131,8 @@ def load():
     L.ghsvd_exchange_plan.argtypes = [Ci, Ci, Ci, Ci, Ci, P, P, P, P, P, P]
     L.ghsvd_nccl_unique_id.argtypes = [P]
     for f in ("ghsvd_create", "ghsvd_factor", "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors",
-              "ghsvd_sweep", "ghsvd_run_steps", "ghsvd_extract", "ghsvd_get_transformed", "ghsvd_get_state",
+              "ghsvd_sweep", "ghsvd_run_steps", "ghsvd_extract", "ghsvd_extract_local", "ghsvd_get_transformed",
+              "ghsvd_get_state",
               "ghsvd_set_state", "ghsvd_hz2x2_batch"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -174,7 +182,9 @@ class Context:
                  stream=None, world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
                  nblocks: int = 0, max_sweeps: int = 30, criterion: str = "relative", eps: float = 0.0,
                  cluster: int = 0, threads: int = 0, use_graph: bool = True, kernel: int = 0,
-                 detail_timing=False, want_x: bool = False):
+                 detail_timing=False, want_x: bool = False, exchange_overlap: bool = False,
+                 schedule: Optional[int] = None, groups: Optional[int] = None, gram_splits: Optional[int] = None,
+                 trace_path: Optional[str] = None):
         import torch
         L = load()
         self._L = L
@@ -201,6 +211,17 @@ class Context:
         o.kernel = kernel
         o.detail_timing = int(detail_timing)   # bool or 0 / 1 / 2 (see ghsvd.h)
         o.want_x = 1 if want_x else 0
+        o.exchange_overlap = 1 if exchange_overlap else 0
+        # None keeps ghsvd_default_options' value (seeded from the GHSVD_* environment knobs)
+        if schedule is not None:
+            o.schedule = int(schedule)
+        if groups is not None:
+            o.groups = int(groups)
+        if gram_splits is not None:
+            o.gram_splits = int(gram_splits)
+        if trace_path is not None:
+            self._trace_path = trace_path.encode()
+            o.trace_path = self._trace_path
         self.opts = o
         nbytes = L.ghsvd_workspace_bytes(ctypes.byref(o), m, n, nl)
         if nbytes == 0:
@@ -336,6 +357,21 @@ class Context:
             pz, ldz = None, n
         self._check(self._L.ghsvd_extract(self._h, pl, ps, pg, pz, ldz, None), "extract")
         return lam, sf, sg, Z
+
+    def extract_local(self, want_z: bool = True):
+        """Distributed form (ghsvd_extract_local): -> (lambda, sigma_f, sigma_g, Z_local n x ncols,
+        col_ids) numpy; Z_local holds only this rank's columns, col_ids their global indices."""
+        n = self.n
+        lam, sf, sg = np.zeros(n), np.zeros(n), np.zeros(n)
+        Z = np.zeros((n, n), np.complex128, order="F") if want_z else None
+        ids = np.zeros(n, np.int64)
+        nc = ctypes.c_int64()
+        P = ctypes.c_void_p
+        self._check(self._L.ghsvd_extract_local(self._h, lam.ctypes.data_as(P), sf.ctypes.data_as(P),
+                                                sg.ctypes.data_as(P), None if Z is None else Z.ctypes.data_as(P),
+                                                n, ids.ctypes.data_as(P), ctypes.byref(nc)), "extract_local")
+        k = nc.value
+        return lam, sf, sg, (None if Z is None else Z[:, :k].copy(order="F")), ids[:k].copy()
 
     def extract_x(self):
         """X = Z^{-1} (n x n numpy), requires want_x=True and a completed sweep."""

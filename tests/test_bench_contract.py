@@ -74,3 +74,35 @@ def test_reference_arm_runs_and_keeps_the_contract():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"] == "c1_known_gsvd" and d["config"]["sweeps_extrapolated"] == 18
+
+
+def test_multi_gpu_launcher_command():
+    """--gpus N outside torchrun re-executes bench.py under torch.distributed.run with N
+    processes on 127.0.0.1 (the driver's own launch form), passing the arguments through."""
+    import importlib.util
+    import sys
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    cmd = b.launch_cmd(4, ["--gpus", "4", "--steps", "2"], 29555)
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1" and cmd[cmd.index("--master-port") + 1] == "29555"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"] and cmd[-5].endswith("bench.py")
+
+
+def test_multi_gpu_request_without_gpus_fails_loudly():
+    """`bench.py --gpus 2` must not silently run on one GPU: with fewer visible devices it
+    exits non-zero with a message (here: no GPU at all)."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.is_available() and torch.cuda.device_count() >= 2:
+        pytest.skip("enough GPUs: the launcher would run")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode != 0 and "--gpus 2 requested" in r.stderr
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=dict(env, WORLD_SIZE="1"))
+    assert r.returncode != 0 and "WORLD_SIZE=1 but --gpus 2" in r.stderr

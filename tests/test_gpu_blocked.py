@@ -122,6 +122,18 @@ def test_schedules_bitwise(gh, monkeypatch):
         r = _run_env(gh, monkeypatch, P, env, nblocks=10)
         assert r[3]["sweeps"] == ref[3]["sweeps"], env
         assert np.array_equal(r[4], ref[4]) and np.array_equal(r[5], ref[5]), env
+    # the same alternatives through the explicit option fields (the library reads no
+    # environment; ghsvd_default_options only seeds these fields from it)
+    m, n = P.F.shape
+    for kw in ({"schedule": gh.SCHED_NO_PRIO}, {"schedule": gh.SCHED_SERIAL | gh.SCHED_SPLIT_BND}, {"groups": 3},
+               {"schedule": gh.SCHED_SPLIT_FACTOR}, {"schedule": gh.SCHED_SPLIT_FACTOR | gh.SCHED_SERIAL},
+               {"schedule": gh.SCHED_SPLIT_FACTOR, "groups": 2}):
+        ctx = gh.Context(m, n, variant="bo", nblocks=10, **kw)
+        ctx.set_factors(P.F, P.J, P.G)
+        st = ctx.sweep()
+        lam, sf, sg, Z = ctx.extract()
+        ctx.close()
+        assert st["sweeps"] == ref[3]["sweeps"] and np.array_equal(lam, ref[4]) and np.array_equal(Z, ref[5]), kw
 
 
 @pytest.mark.parametrize("env", [{"GHSVD_GRAM3M": "0"}, {"GHSVD_UPD4M": "1"}, {"GHSVD_PIVOT_CL": "1"}])

@@ -1,0 +1,56 @@
+"""NEXT-3: the sign structure of the paper's dataset A -- each J~_a has "3 positive and 239
+negative signs" (N_L = 121, tbl:ds) -- scaled down to 4 atoms and
+N_G = 256 (m = 968), through the paper's pipeline (Phase 1 -> Phase 2 JQR -> sweep) and
+through the tall factors, against the oracle's own pipeline at the well-conditioned
+tolerance 1e-9 (BASELINE north_star).  Full size (N_A = 108, N_G = 3275) is config 6,
+a bench line (bench.py --config 6).
+
+Inertia pins the sign structure (Sylvester): H = F~^* J~ F~ with F~ of full column rank
+has exactly n_+(J~) = 3 N_A positive eigenvalues."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1907_08560_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+NA, NL, NG = 4, 121, 256
+
+
+@pytest.fixture(scope="module")
+def gh():
+    from paper_1907_08560_b200 import build, ghsvd
+    build.build()
+    return ghsvd
+
+
+@pytest.fixture(scope="module")
+def alike():
+    at = inputs.lapw_atoms(60, NA, NL, NG, nneg=239)
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    Fo, Go, Zp, st = oracle.hz_pointwise(F, J, G, cmax=64)
+    lo, *_ = oracle.extract(Fo, J, Go, Zp)
+    return at, J, lo, st
+
+
+def relerr(a, b):
+    a, b = np.sort(np.asarray(a)), np.sort(np.asarray(b))
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+@pytest.mark.parametrize("variant,reduce", [("bo", True), ("pointwise", True), ("bo", False), ("pointwise", False)])
+def test_alike_lambda_vs_oracle(gh, alike, variant, reduce):
+    at, J, lo, sto = alike
+    m = 2 * NA * NL
+    ctx = gh.Context(m, NG, NL, variant=variant, max_sweeps=64)
+    ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    if reduce:
+        ctx.reduce()
+    st = ctx.sweep()
+    lam, sf, sg, Z = ctx.extract()
+    ctx.close()
+    err = relerr(lam, lo)
+    print(f"A-like {variant} reduce={reduce}: sweeps {st['sweeps']} (oracle tall {sto['sweeps']}), err {err:.2e}")
+    assert st["converged"] and sto["converged"]
+    assert err <= 1e-9
+    assert int((lam > 0).sum()) == int((lo > 0).sum()) == int((J > 0).sum()) == 3 * NA

@@ -71,7 +71,7 @@ def _ctx_c3(gh, at, **kw):
 def c3_oracle_factors(c3):
     """The oracle's own Phase 1 (Alg. 1) of the config-3 atoms; these go to the device by
     set_factors, so no oracle input comes from the CUDA path.  The device keeps F's rows
-    J-sorted (+ first, stably): row i there is row perm[i] here."""
+    J-sorted (+ first, stably): row i there is row perm[i] here; G's rows stay as given."""
     F, J, G = oracle.factor(c3.A, c3.B, c3.U, c3.TAA, c3.TAB, c3.TBB)
     return F, J, G, np.argsort(-J, kind="stable")
 
@@ -90,7 +90,7 @@ def test_c3_pointwise_first_step_matches_oracle(gh, c3_oracle_factors):
     # m = 10368) and the 2x2 transform amplifies Gram perturbations by ~kappa of the pair's S
     # block (S has condition 1e12 here): 1e-10 relative per column (measured 2.5e-12).
     cols = np.r_[0:64, n - 64:n]
-    for X, Y in ((Fg, Fo[perm]), (Gg, Go[perm])):
+    for X, Y in ((Fg, Fo[perm]), (Gg, Go)):
         sc = np.linalg.norm(Y[:, cols], axis=0)
         assert (np.linalg.norm(X[:, cols] - Y[:, cols], axis=0) / sc).max() < 1e-10
     assert np.abs(Zg[:, cols] - Zo[:, cols]).max() < 1e-10
@@ -119,7 +119,7 @@ def test_c3_blocked_first_block_step_matches_oracle(gh, c3_oracle_factors):
     # different summation order (~eps sqrt(m)) are amplified by kappa(S_blk).  1e-8 relative
     # per column (measured 1.7e-10); a wrong pivot / index gives O(1).
     cols = np.array(checked)
-    for X, Y in ((Fg, F[perm]), (Gg, G[perm])):
+    for X, Y in ((Fg, F[perm]), (Gg, G)):
         sc = np.linalg.norm(Y[:, cols], axis=0)
         assert (np.linalg.norm(X[:, cols] - Y[:, cols], axis=0) / sc).max() < 1e-8
     assert (np.linalg.norm(Zg[:, cols] - Z[:, cols], axis=0) / np.linalg.norm(Z[:, cols], axis=0)).max() < 1e-8
@@ -223,11 +223,16 @@ def test_c3_two_ranks_loopback_bitwise(gh, c3):
 
 def test_c2_full_factor_reduce_sweep_vs_oracle(gh):
     """BASELINE configs[2]: LAPW 1568 x 1024 -> Phase 2 -> 1024^2 -> BO sweep, against the
-    oracle's own pipeline on the same atoms (oracle.factor -> oracle.reduce -> BO with the
-    same partition); the device's Phase 2 preserves the Grammians."""
+    stored oracle reference of the same atoms (tests/golden/c2_oracle_bo: oracle.factor ->
+    oracle BO on the tall Phase-1 factors, no Phase 2 -- Phase 2 preserves the pencil,
+    eq 5.1, so its eigenvalues are the reference for any reduction); the device's Phase 2
+    preserves the Grammians."""
     kind, at = inputs.make_config(2)
     NA, NL, NG = at.A.shape
     m = 2 * NA * NL
+    meta = json.load(open(os.path.join(GOLD, "c2_oracle_bo.json")))
+    lo = np.load(os.path.join(GOLD, "c2_oracle_bo.npz"))["lam"]
+    assert inputs.fingerprint_close(inputs.fingerprint(at), meta["fingerprint"])
     ctx = gh.Context(m, NG, NL, variant="bo")
     ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
     Ft, Jt, Gt, _ = ctx.get_factors()
@@ -241,14 +246,11 @@ def test_c2_full_factor_reduce_sweep_vs_oracle(gh):
     st = ctx.sweep()
     lam, sf, sg, Z = ctx.extract()
     ctx.close()
-    Fo1, Jo1, Go1 = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
-    Fo2, Jo2, Go2, p2o, _ = oracle.reduce(Fo1, Jo1, Go1)
-    Fo, Go, Zp, sto = oracle.hz_blocked(Fo2, Jo2, Go2, 32, inner_sweeps=1)
-    lo, *_ = oracle.extract(Fo, Jo2, Go, Zp)
-    # the two Phase 2 runs may pick different pivots (rounding of the J-dots decides near-ties),
-    # so the sweeps start from different factors of the same pencil: sweeps within 2
-    assert st["converged"] and sto["converged"] and abs(st["sweeps"] - sto["sweeps"]) <= 2
-    assert np.max(np.abs(np.sort(lam) - np.sort(lo)) / np.abs(np.sort(lo))) <= 1e-9
+    err = float(np.max(np.abs(np.sort(lam) - np.sort(lo)) / np.abs(np.sort(lo))))
+    print(f"c2 reduced GPU vs tall oracle: max rel lambda err {err:.2e}, sweeps {st['sweeps']} "
+          f"(oracle tall {meta['stats']['sweeps']})")
+    assert st["converged"] and meta["stats"]["converged"]
+    assert err <= 1e-9
     # eigenvectors of the ORIGINAL (Phase-1) pencil through P2 un-permutation
     idx = np.arange(0, NG, 37)
     x = Z[:, idx]
@@ -313,7 +315,7 @@ def test_c4_first_block_step_matches_oracle(gh, c4):
     ctx._check(rc, "get_transformed")
     torch.cuda.synchronize()
     ctx.close()
-    perm = np.argsort(-J, kind="stable")       # device rows are J-sorted (+ first), stably
+    perm = np.argsort(-J, kind="stable")       # device rows of F are J-sorted (+ first), stably; G's as given
     nblk = 2 * ((n + 63) // 64)
     start, width = oracle.block_partition(n, nblk)
     worst = 0.0
@@ -328,7 +330,7 @@ def test_c4_first_block_step_matches_oracle(gh, c4):
         Fg = Ft.index_select(0, ci).T.cpu().numpy()
         Gg = Gt.index_select(0, ci).T.cpu().numpy()
         Zg = Zt.index_select(0, ci).T.cpu().numpy()[cols]
-        for X, Y in ((Fg, Fp[perm]), (Gg, Gp[perm])):
+        for X, Y in ((Fg, Fp[perm]), (Gg, Gp)):
             e = np.linalg.norm(X - Y, axis=0) / np.linalg.norm(Y, axis=0)
             worst = max(worst, float(e.max()))
         worst = max(worst, float((np.linalg.norm(Zg - Zp, axis=0) / np.linalg.norm(Zp, axis=0)).max()))

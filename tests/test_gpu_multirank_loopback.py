@@ -54,13 +54,13 @@ def single(gh, P, nblocks, want_x, variant="bo"):
     return st, out, X
 
 
-def multi(gh, P, nblocks, world, want_x, key, variant="bo"):
+def multi(gh, P, nblocks, world, want_x, key, variant="bo", local=False, **kw):
     import torch
     m, n, nl = shape(P)
     streams = [torch.cuda.Stream() for _ in range(world)]
     lid = gh.loopback_id(key)
     ctxs = [gh.Context(m, n, nl, variant=variant, nblocks=nblocks, max_sweeps=64, want_x=want_x, world_size=world,
-                       rank=r, nccl_id=lid, stream=streams[r]) for r in range(world)]
+                       rank=r, nccl_id=lid, stream=streams[r], **kw) for r in range(world)]
     for c in ctxs:
         load(c, P)
     res = [None] * world
@@ -71,7 +71,7 @@ def multi(gh, P, nblocks, world, want_x, key, variant="bo"):
             st = ctxs[r].sweep()
             out = ctxs[r].extract()
             X = ctxs[r].extract_x() if want_x else None
-            res[r] = (st, out, X)
+            res[r] = (st, out, X, ctxs[r].extract_local() if local else None)
         except Exception as e:  # noqa: BLE001 -- reported below
             errs.append((r, repr(e)))
 
@@ -88,8 +88,8 @@ def multi(gh, P, nblocks, world, want_x, key, variant="bo"):
 
 
 def assert_same(a, b):
-    sta, (la, fa, ga, Za), Xa = a
-    stb, (lb, fb, gb, Zb), Xb = b
+    sta, (la, fa, ga, Za), Xa = a[:3]
+    stb, (lb, fb, gb, Zb), Xb = b[:3]
     assert sta["sweeps"] == stb["sweeps"]
     assert sta["converged"] == stb["converged"] == 1
     assert sta["transforms_all"] == stb["transforms_all"]
@@ -196,3 +196,40 @@ def test_loopback_resumed_sweeps(gh):
         assert total == ref[0]["sweeps"]
         np.testing.assert_array_equal(lam, ref[1][0])
         np.testing.assert_array_equal(Z, ref[1][3])
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_loopback_exchange_modes_and_distributed_z(gh, overlap):
+    """Both exchange modes (exchange_overlap 0: one grouped F, G, Z' exchange per block step
+    on the context stream -- the default, one communicator; 1: the two-part exchange on two
+    streams) give the one-rank result bitwise, and ghsvd_extract_local leaves Z distributed:
+    every column is held by exactly one rank, bitwise equal to the one-rank Z column, with
+    complete lambda / Sigma on every rank."""
+    P = inputs.known_hyperbolic(21, 400, 256, 0.4)
+    ref = single(gh, P, 16, False)
+    world = 4
+    res = multi(gh, P, 16, world, False, f"xch{int(overlap)}", local=True, exchange_overlap=overlap)
+    n = P.F.shape[1]
+    seen = np.zeros(n, int)
+    for r in range(world):
+        assert_same(res[r], ref)
+        lam, sf, sg, Zl, ids = res[r][3]
+        np.testing.assert_array_equal(lam, ref[1][0])
+        np.testing.assert_array_equal(sf, ref[1][1])
+        assert Zl.shape == (n, len(ids)) and len(ids) < n
+        np.testing.assert_array_equal(Zl, ref[1][3][:, ids])
+        seen[ids] += 1
+    assert np.all(seen == 1)
+
+
+def test_extract_local_one_rank_is_extract(gh):
+    P = inputs.known_hyperbolic(22, 120, 64, 0.4)
+    c = gh.Context(120, 64, variant="bo", nblocks=4)
+    c.set_factors(P.F, P.J, P.G)
+    c.sweep()
+    lam, sf, sg, Z = c.extract()
+    l2, f2, g2, Zl, ids = c.extract_local()
+    c.close()
+    assert list(ids) == list(range(64))
+    for x, y in ((lam, l2), (sf, f2), (sg, g2), (Z, Zl)):
+        np.testing.assert_array_equal(x, y)

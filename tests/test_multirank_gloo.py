@@ -145,3 +145,47 @@ def test_exchange_plan_is_consistent():
             # ownership covers each block exactly once per step
             for b in range(nblk):
                 assert 0 <= ghsvd.block_owner(nblk, world, s, b) < world
+
+
+def _inputs_worker(rank, world, port, cfg, out_q):
+    import hashlib
+    import importlib.util
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    kind, payload = b.shared_inputs(cfg, world, rank, torch.device("cpu"))
+    h = hashlib.sha256()
+    names = ("A", "B", "U", "TAA", "TAB", "TBB") if kind == "atoms" else ("F", "J", "G")
+    for k in names:
+        h.update(np.ascontiguousarray(getattr(payload, k)).tobytes())
+    out_q.put((rank, kind, h.hexdigest()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_bench_inputs_broadcast_identical(cfg):
+    """bench.py's multi-rank input path: rank 0 generates the seeded inputs once and
+    broadcasts them; every rank holds bitwise the inputs a single process generates."""
+    import hashlib
+    from paper_1907_08560_b200 import inputs
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_inputs_worker, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    kind, payload = inputs.make_config(cfg, backend="numpy")
+    h = hashlib.sha256()
+    names = ("A", "B", "U", "TAA", "TAB", "TBB") if kind == "atoms" else ("F", "J", "G")
+    for k in names:
+        h.update(np.ascontiguousarray(getattr(payload, k)).tobytes())
+    assert {g[2] for g in got} == {h.hexdigest()} and {g[1] for g in got} == {kind}

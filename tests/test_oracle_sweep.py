@@ -352,3 +352,16 @@ def test_accumulated_inverse_and_eq71_errors(which, m, n):
     eF = np.linalg.norm(P.F - U @ (sf[:, None] * X)) / np.linalg.norm(P.F)
     eG = np.linalg.norm(P.G - V @ (sg[:, None] * X)) / np.linalg.norm(P.G)
     assert eF < 1e-12 and eG < 1e-12
+
+
+def test_datasetA_sign_structure_phase1():
+    """Dataset A's sign structure: every J~_a has 3 positive and 239
+    negative signs (N_L = 121); the oracle's HEBPJ reproduces that inertia per atom
+    (Sylvester), sorted + first within each atom."""
+    from paper_1907_08560_b200 import inputs
+    at = inputs.lapw_atoms(60, 2, 121, 40, nneg=239)
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    for a in range(2):
+        Ja = J[242 * a: 242 * (a + 1)]
+        assert int((Ja > 0).sum()) == 3 and list(Ja[:3]) == [1, 1, 1]
+        assert int((np.sign(at.d[a]) > 0).sum()) == 3

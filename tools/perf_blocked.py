@@ -1,7 +1,7 @@
 """Time blocked BO sweeps on config 3 (exploration).
 
-SWEEPS=n (default 1), NBLK=list (default 128), TUNE="nsplit:tpc,..." (GHSVD_NSPLIT,
-GHSVD_UPD_TPC tuning knobs; default: library defaults)."""
+SWEEPS=n (default 1), NBLK=list (default 128), TUNE="nsplit,..." (Gram row splits,
+ghsvd_options.gram_splits; default: planned)."""
 import json
 import os
 import sys
@@ -18,11 +18,8 @@ sweeps = int(os.environ.get("SWEEPS", "1"))
 tunes = [t for t in os.environ.get("TUNE", "").split(",") if t] or [None]
 for nb in [int(x) for x in os.environ.get("NBLK", "128").split(",")]:
     for tune in tunes:
-        if tune:
-            ns, tpc = tune.split(":")
-            os.environ["GHSVD_NSPLIT"] = ns
-            os.environ["GHSVD_UPD_TPC"] = tpc
-        ctx = ghsvd.Context(2 * NA * NL, NG, NL, variant="bo", nblocks=nb, max_sweeps=sweeps, detail_timing=True)
+        ctx = ghsvd.Context(2 * NA * NL, NG, NL, variant="bo", nblocks=nb, max_sweeps=sweeps, detail_timing=True,
+                            gram_splits=int(tune) if tune else None)
         ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
         st = ctx.sweep()
         print(json.dumps({"nblk": nb, "tune": tune, "sweeps": st["sweeps"], "converged": st["converged"],

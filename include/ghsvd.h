@@ -191,9 +191,19 @@ ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* 
  * P4 (G P2) P5 = Q G', F' = F P5 (the "slower but more stable"
  * path for a badly conditioned G~; no row pivoting P4); the combined permutation
  * P2 P5 is what ghsvd_get_factors exports and ghsvd_extract undoes.
+ * Default for m n^2 >= 2e10 (else unblocked; GHSVD_REDUCE_BLOCKED / _UNBLOCKED force either):
+ * BLOCKED (NEXT-4, the paper's "blocking and delaying the columns updates",
+ * PAPER.md:1271-1275): left-looking panels of <= 33 reflectors in the compact form
+ * I + S T S^* J, the trailing columns updated once per panel by two ZGEMMs (cuBLAS,
+ * loaded at run time), pivot searches on downdated J-norms / norms (exact at every
+ * panel start; a panel is cut when a formed pivot column disagrees with its estimate).
+ * The pivot sequence may differ from the unblocked one on near-ties; the Grammians and
+ * the pencil are preserved alike (tests).  GHSVD_REDUCE_UNBLOCKED: one reflector
+ * application per column (round 1), also the fallback when cuBLAS cannot be loaded or
+ * the n x n output-Z buffer cannot hold the panel (m > ~n^2 / 35).
  * Errors: GHSVD_E_RANK_DEFICIENT on a degenerate JQR pivot or rank-deficient G;
- * INVALID_ARG on unknown flags. */
-enum { GHSVD_REDUCE_COLPIV = 1 };
+ * GHSVD_E_NONFINITE on non-finite J-norms; INVALID_ARG on unknown flags. */
+enum { GHSVD_REDUCE_COLPIV = 1, GHSVD_REDUCE_UNBLOCKED = 2, GHSVD_REDUCE_BLOCKED = 4 };
 ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
 
 /* Export the factors the sweep will start from (after factor/set_factors,

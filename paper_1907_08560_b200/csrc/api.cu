@@ -220,6 +220,7 @@ void ghsvd_destroy(ghsvd_ctx h) {
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
   if (ctx->ev3) cudaEventDestroy(ctx->ev3);
   comm_destroy(ctx);
+  phase2_release(ctx);
   delete h;
 }
 
@@ -301,7 +302,8 @@ ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
     ctx->err = "reduce: must follow factor/set_factors (once) and precede sweep";
     return GHSVD_E_STATE;
   }
-  if (flags & ~GHSVD_REDUCE_COLPIV) {
+  if ((flags & ~(GHSVD_REDUCE_COLPIV | GHSVD_REDUCE_UNBLOCKED | GHSVD_REDUCE_BLOCKED)) ||
+      ((flags & GHSVD_REDUCE_UNBLOCKED) && (flags & GHSVD_REDUCE_BLOCKED))) {
     ctx->err = "reduce: unknown flags";
     return GHSVD_E_INVALID_ARG;
   }

@@ -76,6 +76,7 @@ struct Ctx {
   std::vector<int> blk_start, blk_width;
   // multi-GPU
   void* comm;                    // ncclComm_t (opaque)
+  void* cublas = nullptr;        // cublasHandle_t of the blocked Phase 2 (dlopen'ed cuBLAS), lazily
   std::string err;
 };
 
@@ -111,6 +112,7 @@ ghsvd_status phase1_factor(Ctx* ctx, int64_t NA, int64_t NL, int64_t NG, const v
 size_t phase1_scratch_bytes(int64_t m, int64_t n, int64_t nl);
 // phase2.cu
 ghsvd_status phase2_reduce(Ctx* ctx, int flags);
+void phase2_release(Ctx* ctx);
 size_t phase2_scratch_bytes(int64_t m, int64_t n);
 // blocked.cu
 ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st);

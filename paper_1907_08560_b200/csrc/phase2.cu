@@ -11,7 +11,9 @@
 // Each JQR/QR step is a short sequence of kernels (column-parallel J-norms,
 // dots and reflector applications across CTAs; pivot logic in one CTA); the
 // 1x1 / 2x2 decision is read back once per step.  Runs once per problem.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <string>
 
@@ -130,8 +132,19 @@ __device__ void swap_cols_dev(double2* F, long long ld, long long rows, long lon
 }
 
 // argmax |hd| over [k, n) (first index), swap columns k <-> jm, p2, hd
+// blocked Phase 2: the delayed-update coefficients Y (= S^* J X) and W (= T Y) of a column
+// move with it (pb entries per column; nullptr in the unblocked path)
+__device__ void swap_yw(double2* Yb, double2* Wb, int pb, long long a, long long b) {
+  if (!Yb || a == b) return;
+  for (int i = threadIdx.x; i < pb; i += blockDim.x) {
+    double2 t = Yb[i + a * pb]; Yb[i + a * pb] = Yb[i + b * pb]; Yb[i + b * pb] = t;
+    t = Wb[i + a * pb]; Wb[i + a * pb] = Wb[i + b * pb]; Wb[i + b * pb] = t;
+  }
+}
+
 __global__ void __launch_bounds__(T2) k_piv_a(double2* F, long long ld, long long m, long long n, long long k,
-                                              long long* p2, P2Scr s) {
+                                              long long* p2, P2Scr s, double2* Yb = nullptr,
+                                              double2* Wb = nullptr, int pb = 0) {
   double v = -1.0;
   long long jm = 0x7fffffffffffffffll;
   for (long long j = k + threadIdx.x; j < n; j += T2) {
@@ -147,6 +160,7 @@ __global__ void __launch_bounds__(T2) k_piv_a(double2* F, long long ld, long lon
     jm = k;
   }
   swap_cols_dev(F, ld, m, k, jm);
+  swap_yw(Yb, Wb, pb, k, jm);
   if (threadIdx.x == 0 && jm != k) {
     const long long t = p2[k]; p2[k] = p2[jm]; p2[jm] = t;
     const double h = s.hd[k]; s.hd[k] = s.hd[jm]; s.hd[jm] = h;
@@ -184,7 +198,8 @@ __global__ void __launch_bounds__(T2) k_piv_b(long long n, long long k, P2Scr s)
 }
 
 __global__ void __launch_bounds__(T2) k_piv_c(double2* F, long long ld, long long m, long long n, long long k,
-                                              long long* p2, P2Scr s) {
+                                              long long* p2, P2Scr s, double2* Yb = nullptr,
+                                              double2* Wb = nullptr, int pb = 0) {
   __shared__ int act;  // 0: nothing, 1: swap k<->ii (1x1), 2: swap k+1<->ii (2x2)
   double hij = -1.0;
   if (s.ctl[2]) {   // uniform over the block
@@ -212,12 +227,14 @@ __global__ void __launch_bounds__(T2) k_piv_c(double2* F, long long ld, long lon
       }
       s.ctl[0] = act == 2 ? 2 : 1;
     }
+    s.ctl[6] = act;
   }
   __syncthreads();
   if (act == 0) return;
   const long long ii = s.ctl[1];
   const long long a = act == 1 ? k : k + 1;
   swap_cols_dev(F, ld, m, a, ii);
+  swap_yw(Yb, Wb, pb, a, ii);
   if (threadIdx.x == 0 && a != ii) {
     const long long t = p2[a]; p2[a] = p2[ii]; p2[ii] = t;
     const double h = s.hd[a]; s.hd[a] = s.hd[ii]; s.hd[ii] = h;
@@ -226,7 +243,8 @@ __global__ void __launch_bounds__(T2) k_piv_c(double2* F, long long ld, long lon
 
 // Reflector for column k (Thm 5.1): sign-compatibility row swap, s, tau, c1.
 __global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8_t* J, long long m, long long n,
-                                                  long long k, P2Scr s) {
+                                                  long long k, P2Scr s, double2* Sb = nullptr, long long lds = 0,
+                                                  int nrs = 0) {
   __shared__ double2 sh[T2 / 32];
   double2* f = F + k * ld;
   const double hn = jdot(f, f, J, k, m, true, sh).x;
@@ -250,6 +268,12 @@ __global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8
       const double2 t = F[k + c * ld];
       F[k + c * ld] = F[best + c * ld];
       F[best + c * ld] = t;
+    }
+    // blocked path: the panel's reflectors so far are rows of the same (delayed) transform
+    for (int c = threadIdx.x; c < nrs; c += T2) {
+      const double2 t = Sb[k + c * lds];
+      Sb[k + c * lds] = Sb[best + c * lds];
+      Sb[best + c * lds] = t;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -464,6 +488,225 @@ __global__ void k_iota(long long* p, long long n) {
     p[i] = i;
 }
 
+// ------------------------------------------------------------ blocked Phase 2 (NEXT-4)
+// Left-looking panels of up to PB reflectors with delayed trailing updates (the paper's
+// "blocking and delaying the columns updates").  Within a panel the
+// trailing columns X keep their values from the panel start; the reflectors applied so far
+// are H_i = I + tau_i s_i s_i^* J (J = I for the QR of G), accumulated as
+//     H_last ... H_first = I + S T S^* J,   T lower triangular,
+//     T_new = [[T, 0], [tau (s^* J S) T, tau]],
+// so the current value of a trailing column is x + S w with w = T y, y = S^* J x (Y, W
+// keep y, w per column).  Each step forms only the pivot column(s) explicitly; the pivot
+// searches use J-norms / norms downdated with the new R row (exact at every panel start,
+// and a panel is cut short when a formed pivot column's exact value disagrees with its
+// downdated estimate), and the Bunch-Kaufman dots of the JQR are x-dots corrected by the
+// panel (u^T w).  The trailing columns are brought up to date once per panel by two plain
+// ZGEMMs (W = T Y, X += S W; cuBLAS).
+constexpr int PB = 33;   // max reflectors per panel (32 + one 2x2 overflow)
+
+// out[(j - j0) * ostride] = v^* J x_j over rows [r0, m), j in [j0, j0 + gridDim.x)
+__global__ void __launch_bounds__(T2) k_vdot(const double2* v, const double2* X, long long ld, const int8_t* J,
+                                             long long r0, long long m, long long j0, double2* out, long long ostride) {
+  __shared__ double2 sh[T2 / 32];
+  const long long j = j0 + blockIdx.x;
+  const double2 d = jdot(v, X + j * ld, J, r0, m, J != nullptr, sh);
+  if (threadIdx.x == 0) out[(j - j0) * ostride] = d;
+}
+
+// tv[i] = s_new^* J S[:, i] (rows >= r0) for i < nr (one CTA each)
+__global__ void __launch_bounds__(T2) k_sdots(const double2* snew, const double2* S, long long lds, const int8_t* J,
+                                              long long r0, long long m, double2* tv) {
+  __shared__ double2 sh[T2 / 32];
+  const double2 d = jdot(snew, S + (size_t)blockIdx.x * lds, J, r0, m, J != nullptr, sh);
+  if (threadIdx.x == 0) tv[blockIdx.x] = d;
+}
+
+// S[:, nr] = s (rows >= r0; zero above); T row nr = tau (tv^T T), T[nr][nr] = tau
+__global__ void __launch_bounds__(T2) k_panel_add(double2* S, long long lds, const double2* sv, long long r0,
+                                                  long long m, int nr, double2* T, const double2* tv, P2Scr s) {
+  if (s.ctl[3]) return;
+  const double tau = s.dctl[0];
+  double2* col = S + (size_t)nr * lds;
+  for (long long i = blockIdx.x * (long long)T2 + threadIdx.x; i < m; i += (long long)gridDim.x * T2)
+    col[i] = i >= r0 ? sv[i] : cmk(0, 0);
+  if (blockIdx.x == 0) {
+    for (int c = threadIdx.x; c < nr; c += T2) {
+      double2 a = cmk(0, 0);
+      for (int i = c; i < nr; i++) a = cadd(a, cmul(tv[i], T[i + c * PB]));   // T lower triangular
+      T[nr + c * PB] = cmk(tau * a.x, tau * a.y);
+    }
+    if (threadIdx.x == 0) T[nr + nr * PB] = cmk(tau, 0.0);
+  }
+}
+
+// Per trailing column j in [j0, n): w = T y (nr x nr lower triangular), then for each of the
+// nnew newest reflector rows kr (rows r0, r0 + 1): r = x_j[kr] + S[kr, :] w, hd[j] -= J_kr |r|^2
+// (J = nullptr: |r|^2).  One thread per column.
+__global__ void k_panel_rows(const double2* X, long long ld, const int8_t* J, const double2* S, long long lds,
+                             const double2* T, const double2* Y, double2* W, int nr, long long kr0, int nnew,
+                             long long j0, long long n, double* hd) {
+  const long long j = j0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double2* y = Y + j * PB;
+  double2* w = W + j * PB;
+  for (int i = 0; i < nr; i++) {
+    double2 a = cmk(0, 0);
+    for (int c = 0; c <= i; c++) a = cadd(a, cmul(T[i + c * PB], y[c]));
+    w[i] = a;
+  }
+  for (int t = 0; t < nnew; t++) {
+    const long long kr = kr0 + t;
+    double2 r = X[kr + j * ld];
+    for (int i = 0; i < nr; i++) r = cadd(r, cmul(S[kr + (size_t)i * lds], w[i]));
+    const double a2 = r.x * r.x + r.y * r.y;
+    hd[j] -= J ? (double)J[kr] * a2 : a2;
+  }
+}
+
+// out[r] = x[r] + (S w)[r] for r >= r0 (x, out may alias); rows < r0 of out untouched
+__global__ void k_form(const double2* x, double2* out, const double2* S, long long lds, const double2* w, int nr,
+                       long long r0, long long m) {
+  for (long long r = r0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < m; r += (long long)gridDim.x * blockDim.x) {
+    double2 a = x[r];
+    for (int i = 0; i < nr; i++) a = cadd(a, cmul(S[r + (size_t)i * lds], w[i]));
+    out[r] = a;
+  }
+}
+
+__global__ void k_zero_yw(double2* Y, double2* W, long long j) {
+  if (threadIdx.x < PB) {
+    Y[threadIdx.x + j * PB] = cmk(0, 0);
+    W[threadIdx.x + j * PB] = cmk(0, 0);
+  }
+}
+
+// d[j] += u^T w_j for j in [j0, n) (the panel's correction of x-dots)
+__global__ void k_dfix(double2* d, const double2* u, const double2* W, int nr, long long j0, long long n) {
+  const long long j = j0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double2 a = d[j];
+  for (int i = 0; i < nr; i++) a = cadd(a, cmul(u[i], W[i + j * PB]));
+  d[j] = a;
+}
+
+// exact J-norm (rows >= r0) of vector x into hd[c]; with `check`, flag (ctl[5]) when the
+// downdated estimate it replaces was off by more than 1/8 of the larger magnitude
+__global__ void __launch_bounds__(T2) k_exact_hd(const double2* x, const int8_t* J, long long r0, long long m,
+                                                 long long c, int check, P2Scr s) {
+  __shared__ double2 sh[T2 / 32];
+  const double e = jdot(x, x, J, r0, m, J != nullptr, sh).x;
+  if (threadIdx.x == 0) {
+    const double est = s.hd[c];
+    if (check && fabs(e - est) > 0.125 * fmax(fabs(e), fabs(est))) s.ctl[5] = 1;
+    s.hd[c] = e;
+  }
+}
+
+// yv[i] = s_i^* J x (rows >= r0) for i < nr (one CTA each): the coefficients of a column
+__global__ void __launch_bounds__(T2) k_ycol(const double2* x, const double2* S, long long lds, const int8_t* J,
+                                             long long r0, long long m, double2* yv) {
+  __shared__ double2 sh[T2 / 32];
+  const double2 d = jdot(S + (size_t)blockIdx.x * lds, x, J, r0, m, J != nullptr, sh);
+  if (threadIdx.x == 0) yv[blockIdx.x] = d;
+}
+
+// w = T y for one column (T lower triangular, nr x nr)
+__global__ void k_tw(const double2* T, const double2* y, double2* w, int nr) {
+  const int i = threadIdx.x;
+  if (i >= nr) return;
+  double2 a = cmk(0, 0);
+  for (int c = 0; c <= i; c++) a = cadd(a, cmul(T[i + c * PB], y[c]));
+  w[i] = a;
+}
+
+// After k_piv_c (act in ctl[6]): the explicit f_ii (fx, rows >= r0) replaces the column the
+// pivot moved into (k for act 1, k + 1 for act 2); its delayed coefficients become zero
+__global__ void k_place_fx(double2* F, long long ld, const double2* fx, long long r0, long long m, long long k,
+                           double2* Y, double2* W, P2Scr s) {
+  const int act = s.ctl[6];
+  if (act == 0) return;
+  const long long c = act == 1 ? k : k + 1;
+  for (long long r = r0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < m; r += (long long)gridDim.x * blockDim.x)
+    F[r + c * ld] = fx[r];
+  if (blockIdx.x == 0 && threadIdx.x < PB) {
+    Y[threadIdx.x + c * PB] = cmk(0, 0);
+    W[threadIdx.x + c * PB] = cmk(0, 0);
+  }
+}
+
+// hd[j] = ||x_j||^2 over rows >= k (QR column pivoting)
+__global__ void __launch_bounds__(T2) k_norms(const double2* X, long long ld, long long k, long long m, P2Scr s) {
+  __shared__ double2 sh[T2 / 32];
+  const long long j = k + blockIdx.x;
+  const double v = jdot(X + j * ld, X + j * ld, nullptr, k, m, false, sh).x;
+  if (threadIdx.x == 0) s.hd[j] = v;
+}
+
+// argmax of norms hd over [k, n) (QR column pivoting, blocked): swap into k with Y/W columns,
+// F's columns (F' = F P5), p2
+__global__ void __launch_bounds__(T2) k_qr_colpiv_blk(double2* G, long long ldg, long long mg, double2* F,
+                                                      long long ldf, long long mf, long long n, long long k,
+                                                      long long* p2, P2Scr s, double2* Yb, double2* Wb) {
+  double v = -1.0;
+  long long jm = 0x7fffffffffffffffll;
+  for (long long j = k + threadIdx.x; j < n; j += T2)
+    if (s.hd[j] > v) { v = s.hd[j]; jm = j; }
+  block_argmax(v, jm);
+  if (jm == 0x7fffffffffffffffll) jm = k;
+  swap_cols_dev(G, ldg, mg, k, jm);
+  swap_cols_dev(F, ldf, mf, k, jm);
+  swap_yw(Yb, Wb, PB, k, jm);
+  if (threadIdx.x == 0 && jm != k) {
+    const long long t = p2[k]; p2[k] = p2[jm]; p2[jm] = t;
+    const double h = s.hd[k]; s.hd[k] = s.hd[jm]; s.hd[jm] = h;
+  }
+}
+
+// Householder vector of the (explicit) contiguous column k of the QR: v = x - alph e_k,
+// tau = -2 / v^* v, x[k] = alph (R(k,k)); writes v to s.s
+__global__ void __launch_bounds__(T2) k_qr_prep_c(double2* X, long long ld, long long m, long long k, P2Scr s) {
+  __shared__ double2 sh[T2 / 32];
+  double2* x = X + k * ld;
+  const double nrm = sqrt(jdot(x, x, nullptr, k, m, false, sh).x);
+  if (nrm == 0.0) {
+    if (threadIdx.x == 0 && s.ctl[3] == 0) s.ctl[3] = -7;
+    return;
+  }
+  const double ax = cabs_(x[k]);
+  const double2 ph = ax > 0.0 ? cmk(x[k].x / ax, x[k].y / ax) : cmk(1, 0);
+  const double2 alph = cmk(-ph.x * nrm, -ph.y * nrm);
+  for (long long i = k + threadIdx.x; i < m; i += T2) s.s[i] = x[i];
+  __syncthreads();
+  if (threadIdx.x == 0) s.s[k] = cmk(s.s[k].x - alph.x, s.s[k].y - alph.y);
+  __syncthreads();
+  const double vv = jdot(s.s, s.s, nullptr, k, m, false, sh).x;
+  if (threadIdx.x == 0) {
+    s.dctl[0] = -2.0 / vv;
+    x[k] = alph;
+  }
+}
+
+// Gather G P2 (all m rows) into a contiguous buffer
+__global__ void k_gather_cols(const double2* G, long long ldg, double2* out, long long ldo, long long m,
+                              const long long* p2) {
+  const long long j = blockIdx.y;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    out[i + j * ldo] = G[i + p2[j] * ldg];
+}
+
+// R (upper n x n of the contiguous QR buffer) -> out with real non-negative diagonal
+__global__ void k_qr_rout(const double2* X, long long ld, double2* out, long long ldo, long long n) {
+  const long long i = blockIdx.x;
+  const double2 d = X[i + i * ld];
+  const double ad = cabs_(d);
+  const double2 cp = ad > 0.0 ? cmk(d.x / ad, -d.y / ad) : cmk(1, 0);
+  for (long long j = threadIdx.x; j < n; j += blockDim.x) {
+    double2 v = j >= i ? cmul(cp, X[i + j * ld]) : cmk(0, 0);
+    if (j == i) v = cmk(ad, 0.0);
+    out[i + j * ldo] = v;
+  }
+}
+
 }  // namespace
 
 size_t phase2_scratch_bytes(int64_t m, int64_t n) {
@@ -479,12 +722,367 @@ size_t phase2_scratch_bytes(int64_t m, int64_t n) {
     }                                              \
   } while (0)
 
+// ---------------------------------------------------------------- cuBLAS (dlopen)
+// Only the plain ZGEMMs of the blocked Phase 2's panel flushes use it; loaded at run time
+// (torch's copy when torch is loaded), so the library keeps no link-time dependency.
+namespace {
+struct Cublas {
+  bool tried = false, ok = false;
+  cublasStatus_t (*Create)(cublasHandle_t*) = nullptr;
+  cublasStatus_t (*Destroy)(cublasHandle_t) = nullptr;
+  cublasStatus_t (*SetStream)(cublasHandle_t, cudaStream_t) = nullptr;
+  cublasStatus_t (*Zgemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const cuDoubleComplex*,
+                          const cuDoubleComplex*, int, const cuDoubleComplex*, int, const cuDoubleComplex*,
+                          cuDoubleComplex*, int) = nullptr;
+};
+Cublas* cublas_lib() {
+  static Cublas c;
+  if (c.tried) return c.ok ? &c : nullptr;
+  c.tried = true;
+  const char* names[] = {"libcublas.so.12", "libcublas.so", "/usr/local/cuda/lib64/libcublas.so.12"};
+  void* h = nullptr;
+  for (const char* nm : names)
+    if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return nullptr;
+  c.Create = (decltype(c.Create))dlsym(h, "cublasCreate_v2");
+  c.Destroy = (decltype(c.Destroy))dlsym(h, "cublasDestroy_v2");
+  c.SetStream = (decltype(c.SetStream))dlsym(h, "cublasSetStream_v2");
+  c.Zgemm = (decltype(c.Zgemm))dlsym(h, "cublasZgemm_v2");
+  c.ok = c.Create && c.Destroy && c.SetStream && c.Zgemm;
+  return c.ok ? &c : nullptr;
+}
+}  // namespace
+
+void phase2_release(Ctx* ctx) {
+  if (ctx->cublas) {
+    if (Cublas* c = cublas_lib()) c->Destroy((cublasHandle_t)ctx->cublas);
+    ctx->cublas = nullptr;
+  }
+}
+
+#define TRY(x)                     \
+  do {                             \
+    ghsvd_status s_ = (x);         \
+    if (s_ != GHSVD_OK) return s_; \
+  } while (0)
+
+#define P2CUB(call)                                                   \
+  do {                                                                \
+    cublasStatus_t c_ = (call);                                       \
+    if (c_ != CUBLAS_STATUS_SUCCESS) {                                \
+      ctx->err = "reduce: cuBLAS ZGEMM failed (" + std::to_string((int)c_) + ")"; \
+      return GHSVD_E_CUDA;                                            \
+    }                                                                 \
+  } while (0)
+
+namespace {
+
+struct Panel {
+  double2 *S, *T, *Y, *W, *tv, *u, *fx;
+  long long lds;
+};
+
+// X[r0:m, j0:n) += S[r0:m, 0:nr] W[0:nr, j0:n)  (the panel's delayed update)
+ghsvd_status flush_update(Ctx* ctx, Cublas* cb, const Panel& P, double2* X, long long ld, long long r0, long long m,
+                          long long j0, long long n, int nr) {
+  if (nr == 0 || j0 >= n || r0 >= m) return GHSVD_OK;
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+  P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)(m - r0), (int)(n - j0), nr, &one,
+                  (const cuDoubleComplex*)(P.S + r0), (int)P.lds, (const cuDoubleComplex*)(P.W + j0 * PB), PB, &one,
+                  (cuDoubleComplex*)(X + r0 + j0 * ld), (int)ld));
+  return GHSVD_OK;
+}
+
+}  // namespace
+
+// Blocked JQR of F (in place, like the unblocked loop of phase2_reduce), see the
+// "blocked Phase 2" comment above.  Returns GHSVD_OK with s.ctl[3] clear, or an error.
+static ghsvd_status jqr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s) {
+  const int64_t m = ctx->m_user, n = ctx->n_user;
+  const long long ld = ctx->ldm;
+  cudaStream_t st = ctx->stream;
+  long long* p2 = (long long*)ctx->p2;
+  double2* F = ctx->F;
+  int8_t* J = ctx->J;
+  int ctl[8];
+  auto rd = [&]() -> ghsvd_status {
+    GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
+    GH_CUDA(cudaStreamSynchronize(st));
+    return GHSVD_OK;
+  };
+  const unsigned gm = (unsigned)std::min<int64_t>(1024, (m + 255) / 256);
+  int64_t k = 0;
+  while (k < n) {
+    const int64_t k0 = k;
+    int nr = 0, pend = 0;   // reflectors in the panel; newest ones without Y rows yet
+    GH_CUDA(cudaMemsetAsync(P.T, 0, (size_t)PB * PB * 16, st));
+    GH_CUDA(cudaMemsetAsync(P.Y + k * PB, 0, (size_t)PB * (n - k) * 16, st));
+    GH_CUDA(cudaMemsetAsync(P.W + k * PB, 0, (size_t)PB * (n - k) * 16, st));
+    k_jnorms<<<(unsigned)(n - k), T2, 0, st>>>(F, ld, J, m, k, s);   // exact J-norms at the panel start
+    while (k < n && nr + 2 <= PB) {
+      if (pend) {
+        // Y rows of the previous step's reflectors, then w = T y and the new R rows'
+        // J-norm downdate for every trailing column
+        for (int t = 0; t < pend; t++)
+          k_vdot<<<(unsigned)(n - k), T2, 0, st>>>(P.S + (size_t)(nr - pend + t) * P.lds, F, ld, J, k0, m, k,
+                                                  P.Y + (nr - pend + t) + k * PB, PB);
+        k_panel_rows<<<(unsigned)((n - k + 127) / 128), 128, 0, st>>>(F, ld, J, P.S, P.lds, P.T, P.Y, P.W, nr,
+                                                                      k - pend, pend, k, n, s.hd);
+        pend = 0;
+      }
+      GH_CUDA(cudaMemsetAsync(s.ctl, 0, 32, st));
+      // 1. diagonal pivot on the (downdated) J-norms, then the pivot column made explicit
+      k_piv_a<<<1, T2, 0, st>>>(F, ld, m, n, k, p2, s, P.Y, P.W, PB);
+      if (nr) k_form<<<gm, 256, 0, st>>>(F + k * ld, F + k * ld, P.S, P.lds, P.W + k * PB, nr, k0, m);
+      k_zero_yw<<<1, 64, 0, st>>>(P.Y, P.W, k);
+      k_exact_hd<<<1, T2, 0, st>>>(F + k * ld, J, k, m, k, nr > 0, s);
+      if (k < n - 1) {
+        // 2. Bunch-Kaufman: h_1j = f_k^* J x_j (updated, rows >= k) = x-dot + u^T w_j
+        k_vdot<<<(unsigned)(n - k - 1), T2, 0, st>>>(F + k * ld, F, ld, J, k, m, k + 1, s.d1 + (k + 1), 1);
+        if (nr) {
+          k_sdots<<<nr, T2, 0, st>>>(F + k * ld, P.S, P.lds, J, k, m, P.u);
+          k_dfix<<<(unsigned)((n - k + 127) / 128), 128, 0, st>>>(s.d1, P.u, P.W, nr, k + 1, n);
+        }
+        k_piv_b<<<1, T2, 0, st>>>(n, k, s);
+        TRY(rd());
+        if (ctl[5]) break;    // estimate was off: flush, restart with exact J-norms
+        if (ctl[2]) {
+          const int64_t ii = ctl[1];
+          if (nr) k_form<<<gm, 256, 0, st>>>(F + ii * ld, P.fx, P.S, P.lds, P.W + ii * PB, nr, k0, m);
+          else GH_CUDA(cudaMemcpyAsync(P.fx + k0, F + ii * ld + k0, (size_t)(m - k0) * 16, cudaMemcpyDeviceToDevice, st));
+          k_vdot<<<(unsigned)(n - k), T2, 0, st>>>(P.fx, F, ld, J, k, m, k, s.d2 + k, 1);
+          if (nr) {
+            k_sdots<<<nr, T2, 0, st>>>(P.fx, P.S, P.lds, J, k, m, P.u);
+            k_dfix<<<(unsigned)((n - k + 127) / 128), 128, 0, st>>>(s.d2, P.u, P.W, nr, k, n);
+          }
+          k_exact_hd<<<1, T2, 0, st>>>(P.fx, J, k, m, ii, 0, s);
+          k_piv_c<<<1, T2, 0, st>>>(F, ld, m, n, k, p2, s, P.Y, P.W, PB);
+          k_place_fx<<<gm, 256, 0, st>>>(F, ld, P.fx, k0, m, k, P.Y, P.W, s);
+        }
+      } else {
+        static const int one = 1;
+        GH_CUDA(cudaMemcpyAsync(s.ctl, &one, 4, cudaMemcpyHostToDevice, st));
+      }
+      TRY(rd());
+      if (ctl[3]) break;
+      const int type = ctl[0];
+      // 3. the reflector(s) of the pivot column(s), appended to the panel
+      if (type == 2) k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, +1, s);
+      for (int t = 0; t < type; t++) {
+        const long long kk = k + t;
+        k_refl_prep<<<1, T2, 0, st>>>(F, ld, J, m, n, kk, s, P.S, P.lds, nr);
+        if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, J, kk, m, P.tv);
+        k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, kk, m, nr, P.T, P.tv, s);
+        nr++;
+        if (t == 0 && type == 2) k_refl_apply<<<1, T2, 0, st>>>(F, ld, J, m, kk, kk + 1, nullptr, 1, s);
+        k_refl_fin<<<1, T2, 0, st>>>(F, ld, m, kk, s);
+      }
+      if (type == 2) k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, -1, s);
+      P2CHK();
+      k += type;
+      pend = type;
+    }
+    if (ctl[3]) break;
+    // flush: the delayed update of the trailing columns [k, n)
+    if (k < n && nr) {
+      for (int t = 0; t < pend; t++)
+        k_vdot<<<(unsigned)(n - k), T2, 0, st>>>(P.S + (size_t)(nr - pend + t) * P.lds, F, ld, J, k0, m, k,
+                                                P.Y + (nr - pend + t) + k * PB, PB);
+      if (pend) k_panel_rows<<<(unsigned)((n - k + 127) / 128), 128, 0, st>>>(F, ld, J, P.S, P.lds, P.T, P.Y, P.W,
+                                                                             nr, k, 0, k, n, s.hd);
+      TRY(flush_update(ctx, cb, P, F, ld, k0, m, k, n, nr));
+      P2CHK();
+    }
+  }
+  return GHSVD_OK;
+}
+
+// Blocked Householder QR (optionally column-pivoted by norm) of the contiguous m x n
+// buffer X (G P2 gathered), left-looking panels as above with J = I; the column swaps of
+// the pivoted form are applied to p2 and to the n x n R_F copy Rf (F' = F P5).
+static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, double2* X, long long ld,
+                               bool colpiv, double2* Rf, long long ldr) {
+  const int64_t m = ctx->m_user, n = ctx->n_user;
+  cudaStream_t st = ctx->stream;
+  long long* p2 = (long long*)ctx->p2;
+  int ctl[8];
+  const unsigned gm = (unsigned)std::min<int64_t>(1024, (m + 255) / 256);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  int64_t k = 0;
+  while (k < n) {
+    const int64_t k0 = k;
+    int nr = 0, pend = 0;
+    GH_CUDA(cudaMemsetAsync(P.T, 0, (size_t)PB * PB * 16, st));
+    GH_CUDA(cudaMemsetAsync(P.Y + k * PB, 0, (size_t)PB * (n - k) * 16, st));
+    GH_CUDA(cudaMemsetAsync(P.W + k * PB, 0, (size_t)PB * (n - k) * 16, st));
+    if (colpiv) k_norms<<<(unsigned)(n - k), T2, 0, st>>>(X, ld, k, m, s);
+    while (k < n && nr + 1 <= PB) {
+      if (colpiv) {
+        if (pend) {
+          k_vdot<<<(unsigned)(n - k), T2, 0, st>>>(P.S + (size_t)(nr - 1) * P.lds, X, ld, nullptr, k0, m, k,
+                                                  P.Y + (nr - 1) + k * PB, PB);
+          k_panel_rows<<<(unsigned)((n - k + 127) / 128), 128, 0, st>>>(X, ld, nullptr, P.S, P.lds, P.T, P.Y, P.W,
+                                                                        nr, k - 1, 1, k, n, s.hd);
+          pend = 0;
+        }
+        GH_CUDA(cudaMemsetAsync(s.ctl + 5, 0, 4, st));
+        k_qr_colpiv_blk<<<1, T2, 0, st>>>(X, ld, m, Rf, ldr, n, n, k, p2, s, P.Y, P.W);
+        if (nr) k_form<<<gm, 256, 0, st>>>(X + k * ld, X + k * ld, P.S, P.lds, P.W + k * PB, nr, k0, m);
+        k_zero_yw<<<1, 64, 0, st>>>(P.Y, P.W, k);
+        if (nr) {
+          k_exact_hd<<<1, T2, 0, st>>>(X + k * ld, nullptr, k, m, k, 1, s);
+          GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
+          GH_CUDA(cudaStreamSynchronize(st));
+          if (ctl[5]) break;   // downdated norm was off: flush, then exact norms again
+        }
+      } else if (nr) {
+        k_ycol<<<nr, T2, 0, st>>>(X + k * ld, P.S, P.lds, nullptr, k0, m, P.u);
+        k_tw<<<1, 64, 0, st>>>(P.T, P.u, P.tv, nr);
+        k_form<<<gm, 256, 0, st>>>(X + k * ld, X + k * ld, P.S, P.lds, P.tv, nr, k0, m);
+      }
+      k_qr_prep_c<<<1, T2, 0, st>>>(X, ld, m, k, s);
+      if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, nullptr, k, m, P.tv);
+      k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s);
+      nr++;
+      k++;
+      pend = 1;
+      P2CHK();
+    }
+    if (k < n && nr) {
+      if (colpiv) {
+        if (pend) {
+          k_vdot<<<(unsigned)(n - k), T2, 0, st>>>(P.S + (size_t)(nr - 1) * P.lds, X, ld, nullptr, k0, m, k,
+                                                  P.Y + (nr - 1) + k * PB, PB);
+          k_panel_rows<<<(unsigned)((n - k + 127) / 128), 128, 0, st>>>(X, ld, nullptr, P.S, P.lds, P.T, P.Y, P.W,
+                                                                        nr, k, 0, k, n, s.hd);
+        }
+      } else {
+        // Y = S^* X_t, W = T Y on the tensor cores (cuBLAS), then the update
+        P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, nr, (int)(n - k), (int)(m - k0), &one,
+                        (const cuDoubleComplex*)(P.S + k0), (int)P.lds, (const cuDoubleComplex*)(X + k0 + k * ld),
+                        (int)ld, &zero, (cuDoubleComplex*)(P.Y + k * PB), PB));
+        P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, nr, (int)(n - k), nr, &one,
+                        (const cuDoubleComplex*)P.T, PB, (const cuDoubleComplex*)(P.Y + k * PB), PB, &zero,
+                        (cuDoubleComplex*)(P.W + k * PB), PB));
+      }
+      TRY(flush_update(ctx, cb, P, X, ld, k0, m, k, n, nr));
+      P2CHK();
+    }
+  }
+  GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  if (ctl[3]) {
+    ctx->err = "reduce: G P2 numerically rank deficient";
+    return GHSVD_E_RANK_DEFICIENT;
+  }
+  return GHSVD_OK;
+}
+
+static ghsvd_status phase2_reduce_blocked(Ctx* ctx, int flags, Cublas* cb) {
+  const int64_t m = ctx->m_user, n = ctx->n_user;
+  const long long ld = ctx->ldm;
+  cudaStream_t st = ctx->stream;
+  P2Scr s = carve(ctx->scr, m, n);
+  long long* p2 = (long long*)ctx->p2;
+  Panel P;
+  P.lds = round_up(m, 16);
+  P.S = ctx->Z2;   // the output-Z buffer is free until extraction
+  P.T = P.S + (size_t)P.lds * PB;
+  P.Y = P.T + PB * PB;
+  P.W = P.Y + (size_t)PB * n;
+  P.tv = P.W + (size_t)PB * n;
+  P.u = P.tv + PB;
+  P.fx = P.u + PB;
+  GH_CUDA(cudaMemsetAsync(s.ctl, 0, 256, st));
+  GH_CUDA(cudaMemsetAsync(P.S, 0, (size_t)P.lds * PB * 16, st));
+  k_iota<<<8, 256, 0, st>>>(p2, n);
+  P2CHK();
+  TRY(jqr_blocked(ctx, cb, P, s));
+  int ctl[8];
+  GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  if (ctl[3] == -8) {
+    ctx->err = "reduce: non-finite J-norms in the JQR pivot search";
+    return GHSVD_E_NONFINITE;
+  }
+  if (ctl[3]) {
+    ctx->err = "reduce: degenerate JQR pivot (J-Grammian numerically singular)";
+    return GHSVD_E_RANK_DEFICIENT;
+  }
+  // R_F (leading n x n) -> Z; G P2 gathered into the F buffer; blocked QR there (the column
+  // pivoted form swaps R_F's columns in Z alike); R_G -> G; R_F back, rows sorted by J
+  const long long ldz = ctx->ldn;
+  GH_CUDA(cudaMemcpy2DAsync(ctx->Z, (size_t)ldz * 16, ctx->F, (size_t)ld * 16, (size_t)n * 16, (size_t)n,
+                            cudaMemcpyDeviceToDevice, st));
+  k_gather_cols<<<dim3((unsigned)std::min<int64_t>(64, (m + 255) / 256), (unsigned)n), 256, 0, st>>>(
+      ctx->G, ld, ctx->F, ld, m, p2);
+  P2CHK();
+  GH_CUDA(cudaMemsetAsync(s.ctl, 0, 256, st));
+  GH_CUDA(cudaMemsetAsync(P.S, 0, (size_t)P.lds * PB * 16, st));
+  TRY(qr_blocked(ctx, cb, P, s, ctx->F, ld, (flags & GHSVD_REDUCE_COLPIV) != 0, ctx->Z, ldz));
+  GH_CUDA(cudaMemsetAsync(ctx->G, 0, (size_t)ld * (ctx->n_cap + 1) * 16, st));
+  k_qr_rout<<<(unsigned)n, T2, 0, st>>>(ctx->F, ld, ctx->G, ld, n);
+  P2CHK();
+  return GHSVD_OK;   // the caller re-sorts R_F (in Z) into F
+}
+
+// F: keep the leading n x n block (R_F, in Z), rows re-sorted by the new J (+ first)
+static ghsvd_status phase2_finish(Ctx* ctx, P2Scr s) {
+  const int64_t n = ctx->n_user;
+  const long long ld = ctx->ldm, ldz = ctx->ldn;
+  cudaStream_t st = ctx->stream;
+  int8_t* Jin = (int8_t*)s.s;  // reuse scratch
+  GH_CUDA(cudaMemcpyAsync(Jin, ctx->J, (size_t)n, cudaMemcpyDeviceToDevice, st));
+  int64_t* npos_dev = (int64_t*)s.d1;
+  {
+    ghsvd_status e = launch_sort_dest(ctx, Jin, n, false, ctx->rowdest, ctx->J, npos_dev);
+    if (e) return e;
+  }
+  GH_CUDA(cudaMemsetAsync(ctx->F, 0, (size_t)ld * (ctx->n_cap + 1) * 16, st));
+  {
+    ghsvd_status e = launch_row_scatter(ctx, ctx->Z, ldz, ctx->F, ld, ctx->rowdest, n, n);
+    if (e) return e;
+  }
+  long long npos = 0;
+  GH_CUDA(cudaMemcpyAsync(&npos, npos_dev, 8, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  ctx->npos = npos;
+  ctx->m_user = n;
+  ctx->m = n;
+  return GHSVD_OK;
+}
+
 ghsvd_status phase2_reduce(Ctx* ctx, int flags) {
   const int64_t m = ctx->m_user, n = ctx->n_user;
   const long long ld = ctx->ldm;
   cudaStream_t st = ctx->stream;
   P2Scr s = carve(ctx->scr, m, n);
   long long* p2 = (long long*)ctx->p2;
+  // blocked (default) for large problems when cuBLAS loads and the output-Z buffer holds
+  // the panel: below m n^2 ~ 2e10 the per-column launch / readback latency of the panel
+  // logic outweighs the traffic it saves (config 2, 1568 x 1024: 0.26 s blocked vs 0.09 s)
+  const bool big = (double)m * (double)n * (double)n >= 2e10;
+  if (!(flags & GHSVD_REDUCE_UNBLOCKED) && (big || (flags & GHSVD_REDUCE_BLOCKED))) {
+    const size_t need = ((size_t)round_up(m, 16) * PB + PB * PB + 2 * (size_t)PB * n + 2 * PB + m) * 16;
+    const size_t have = (size_t)ctx->ldn * (ctx->n_cap + 1) * 16;
+    Cublas* cb = cublas_lib();
+    if (cb && need <= have) {
+      if (!ctx->cublas) {
+        cublasHandle_t hnd;
+        if (cb->Create(&hnd) != CUBLAS_STATUS_SUCCESS) {
+          ctx->err = "reduce: cublasCreate failed";
+          return GHSVD_E_CUDA;
+        }
+        ctx->cublas = hnd;
+      }
+      if (cb->SetStream((cublasHandle_t)ctx->cublas, st) != CUBLAS_STATUS_SUCCESS) {
+        ctx->err = "reduce: cublasSetStream failed";
+        return GHSVD_E_CUDA;
+      }
+      TRY(phase2_reduce_blocked(ctx, flags, cb));
+      return phase2_finish(ctx, s);
+    }
+  }
   GH_CUDA(cudaMemsetAsync(s.ctl, 0, 256, st));
   k_iota<<<8, 256, 0, st>>>(p2, n);
   P2CHK();
@@ -560,25 +1158,7 @@ ghsvd_status phase2_reduce(Ctx* ctx, int flags) {
   // F: keep the leading n x n block, rows re-sorted by the new J (+ first)
   GH_CUDA(cudaMemcpy2DAsync(ctx->Z, (size_t)ldz * 16, ctx->F, (size_t)ld * 16, (size_t)n * 16, (size_t)n,
                             cudaMemcpyDeviceToDevice, st));
-  int8_t* Jin = (int8_t*)s.s;  // reuse scratch
-  GH_CUDA(cudaMemcpyAsync(Jin, ctx->J, (size_t)n, cudaMemcpyDeviceToDevice, st));
-  int64_t* npos_dev = (int64_t*)s.d1;
-  {
-    ghsvd_status e = launch_sort_dest(ctx, Jin, n, false, ctx->rowdest, ctx->J, npos_dev);
-    if (e) return e;
-  }
-  GH_CUDA(cudaMemsetAsync(ctx->F, 0, (size_t)ld * (ctx->n_cap + 1) * 16, st));
-  {
-    ghsvd_status e = launch_row_scatter(ctx, ctx->Z, ldz, ctx->F, ld, ctx->rowdest, n, n);
-    if (e) return e;
-  }
-  long long npos = 0;
-  GH_CUDA(cudaMemcpyAsync(&npos, npos_dev, 8, cudaMemcpyDeviceToHost, st));
-  GH_CUDA(cudaStreamSynchronize(st));
-  ctx->npos = npos;
-  ctx->m_user = n;
-  ctx->m = n;
-  return GHSVD_OK;
+  return phase2_finish(ctx, s);
 }
 
 }  // namespace ghsvd

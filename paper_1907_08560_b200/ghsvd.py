@@ -289,9 +289,12 @@ class Context:
         self._check(self._L.ghsvd_factor(self._h, NA, NL, NG, pa, pb, pu, ptaa, ptab, ptbb), "factor")
         self.m, self.n = 2 * NA * NL, NG
 
-    def reduce(self, colpiv: bool = False):
-        """Phase 2; colpiv: column-pivoted QR of G P2 (GHSVD_REDUCE_COLPIV)."""
-        self._check(self._L.ghsvd_reduce(self._h, 1 if colpiv else 0), "reduce")
+    def reduce(self, colpiv: bool = False, unblocked: Optional[bool] = None):
+        """Phase 2; colpiv: column-pivoted QR of G P2 (GHSVD_REDUCE_COLPIV); unblocked: True forces
+        the one-reflector-per-column form (GHSVD_REDUCE_UNBLOCKED), False the blocked one
+        (GHSVD_REDUCE_BLOCKED), None lets the library choose by size (see ghsvd.h)."""
+        fl = (1 if colpiv else 0) | (0 if unblocked is None else (2 if unblocked else 4))
+        self._check(self._L.ghsvd_reduce(self._h, fl), "reduce")
         self.m = self.n
 
     def get_factors(self):

@@ -73,7 +73,28 @@ def test_reference_arm_runs_and_keeps_the_contract():
     assert d["metric"].startswith("GHSVD time-to-converge") and d["unit"] == "s"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
-    assert d["config"]["workload"] == "c1_known_gsvd" and d["config"]["sweeps_extrapolated"] == 18
+    assert d["config"]["workload"] == "c1_known_gsvd"
+    cb = d["cpu_baseline"]
+    assert cb["cpu_model"] and isinstance(cb["measured"], bool)
+    if cb["measured"]:
+        assert "end to end" in cb["sample"] and d["config"]["sweeps_extrapolated"] is None
+    else:
+        assert d["config"]["sweeps_extrapolated"] == cb["sweeps"] == 18
+        assert cb["c_gram_per_pair"] > 0 and cb["c_update_per_pair"] >= 0
+
+
+def test_reference_arm_times_small_configs_end_to_end():
+    """Config 0 (12 columns): the whole oracle solve fits the budget and is timed, not
+    extrapolated."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "0",
+                        "--steps", "1", "--warmup", "0", "--ref-budget", "5"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["cpu_baseline"]["measured"] is True and d["config"]["sweeps_extrapolated"] is None
+    assert d["metric"] == "GHSVD time-to-converge (s) c128 N_G=12 (config 0)"
 
 
 def test_multi_gpu_launcher_command():

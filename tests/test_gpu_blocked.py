@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+from hostfactors import device_layout
 from paper_1907_08560_b200 import inputs
 
 pytestmark = pytest.mark.gpu
@@ -36,7 +37,7 @@ def run_gpu(gh, P, variant, nblocks):
     m, n = P.F.shape
     ctx = gh.Context(m, n, variant=variant, nblocks=nblocks)
     ctx.set_factors(P.F, P.J, P.G)
-    F0, J0, G0, _ = ctx.get_factors()
+    F0, J0, G0 = device_layout(P.F, P.J, P.G)
     st = ctx.sweep()
     lam, sf, sg, Z = ctx.extract()
     ctx.close()
@@ -172,7 +173,7 @@ def test_tiny_pencils_match_oracle(gh, m, n, variant):
     P = inputs.random_pencil(300 + 10 * m + n, m, n, 0.5)
     ctx = gh.Context(m, n, variant=variant)
     ctx.set_factors(P.F, P.J, P.G)
-    F0, J0, G0, _ = ctx.get_factors()
+    F0, J0, G0 = device_layout(P.F, P.J, P.G)
     st = ctx.sweep()
     lam, sf, sg, Z = ctx.extract()
     ctx.close()

@@ -5,8 +5,9 @@ through the tall factors, against the oracle's own pipeline at the well-conditio
 tolerance 1e-9 (BASELINE north_star).  Full size (N_A = 108, N_G = 3275) is config 6,
 a bench line (bench.py --config 6).
 
-Inertia pins the sign structure (Sylvester): H = F~^* J~ F~ with F~ of full column rank
-has exactly n_+(J~) = 3 N_A positive eigenvalues."""
+Inertia bounds the sign structure: H = F~^* J~ F~ has at most n_+(J~) = 3 N_A positive
+eigenvalues (Sylvester's law on the m x m congruence, restricted to n columns); with
+m = 968 rows dominated by the 956 negative ones, the spectrum here is all negative."""
 import numpy as np
 import pytest
 
@@ -53,4 +54,5 @@ def test_alike_lambda_vs_oracle(gh, alike, variant, reduce):
     print(f"A-like {variant} reduce={reduce}: sweeps {st['sweeps']} (oracle tall {sto['sweeps']}), err {err:.2e}")
     assert st["converged"] and sto["converged"]
     assert err <= 1e-9
-    assert int((lam > 0).sum()) == int((lo > 0).sum()) == int((J > 0).sum()) == 3 * NA
+    assert int((J > 0).sum()) == 3 * NA
+    assert int((lam > 0).sum()) == int((lo > 0).sum()) <= 3 * NA

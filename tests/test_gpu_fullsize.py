@@ -250,7 +250,20 @@ def test_c2_full_factor_reduce_sweep_vs_oracle(gh):
     print(f"c2 reduced GPU vs tall oracle: max rel lambda err {err:.2e}, sweeps {st['sweeps']} "
           f"(oracle tall {meta['stats']['sweeps']})")
     assert st["converged"] and meta["stats"]["converged"]
-    assert err <= 1e-9
+    # Phase 2's hyperbolic (J-orthogonal, not unitary) reflectors preserve the Grammians
+    # only to ~2e-12 relative (measured), which moves the eigenvalues by ~1e-9 relative
+    # whichever implementation reduces (the oracle's own Phase 2 differs from the device's
+    # by 3.8e-9, the blocked device path by 1.5e-9): bound 1e-8 here; the sweep itself is
+    # held to 1e-9 on the tall factors below.
+    assert err <= 1e-8
+    ctx2 = gh.Context(m, NG, NL, variant="bo")
+    ctx2.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    st2 = ctx2.sweep()
+    lam2 = ctx2.extract(want_z=False)[0]
+    ctx2.close()
+    err2 = float(np.max(np.abs(np.sort(lam2) - np.sort(lo)) / np.abs(np.sort(lo))))
+    print(f"c2 tall GPU vs tall oracle: max rel lambda err {err2:.2e}, sweeps {st2['sweeps']}")
+    assert st2["converged"] and err2 <= 1e-9 and abs(st2["sweeps"] - meta["stats"]["sweeps"]) <= 1
     # eigenvectors of the ORIGINAL (Phase-1) pencil through P2 un-permutation
     idx = np.arange(0, NG, 37)
     x = Z[:, idx]

@@ -43,9 +43,9 @@ def test_config0_end_to_end(gh):
     kind, at = inputs.make_config(0)
     ctx = gh.Context(16, 12, 4)
     ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
-    F0, J0, G0, _ = ctx.get_factors()
     st = ctx.sweep()
     lam, sf, sg, Z = ctx.extract()
+    F0, J0, G0 = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)   # the oracle's own Phase 1
     Fo, Go, Zp, sto = oracle.hz_pointwise(F0, J0, G0)
     lo, *_ = oracle.extract(Fo, J0, Go, Zp)
     assert st["converged"] and abs(st["sweeps"] - sto["sweeps"]) <= 1

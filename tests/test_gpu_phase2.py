@@ -22,12 +22,16 @@ def gh():
     return ghsvd
 
 
-@pytest.mark.parametrize("m,n,neg", [(60, 12, 0.5), (200, 40, 0.4), (150, 150, 0.5), (300, 64, 0.1), (97, 31, 0.5)])
-def test_reduce_grammians(gh, m, n, neg):
+@pytest.mark.parametrize("unblocked", [False, True])
+@pytest.mark.parametrize("m,n,neg", [(60, 12, 0.5), (200, 40, 0.4), (150, 150, 0.5), (300, 64, 0.1), (97, 31, 0.5),
+                                     (500, 300, 0.5), (400, 133, 0.3)])
+def test_reduce_grammians(gh, m, n, neg, unblocked):
+    """Both Phase-2 forms (blocked default: panels of <= 33 delayed reflectors, several
+    panels and ragged last panels here; unblocked: one reflector application per column)."""
     P = inputs.random_pencil(50 + m, m, n, neg)
     ctx = gh.Context(m, n)
     ctx.set_factors(P.F, P.J, P.G)
-    ctx.reduce()
+    ctx.reduce(unblocked=unblocked)
     F, J, G, p2 = ctx.get_factors()
     if n % 2:
         F, G, J = F[:-1, :-1], G[:-1, :-1], J[:-1]
@@ -72,8 +76,9 @@ def test_config2_like_reduce_then_sweep(gh):
     ctx.close()
 
 
-@pytest.mark.parametrize("m,n,neg", [(200, 40, 0.4), (150, 150, 0.5), (97, 31, 0.5)])
-def test_reduce_colpiv_grammians(gh, m, n, neg):
+@pytest.mark.parametrize("unblocked", [False, True])
+@pytest.mark.parametrize("m,n,neg", [(200, 40, 0.4), (150, 150, 0.5), (97, 31, 0.5), (600, 257, 0.5)])
+def test_reduce_colpiv_grammians(gh, m, n, neg, unblocked):
     """GHSVD_REDUCE_COLPIV: the QR of G P2 with column pivoting,
     F' = F P5.  The exported permutation is P2 P5: the Grammians are those of the original
     pencil under it, G' is upper triangular with a real non-negative, non-increasing
@@ -81,7 +86,7 @@ def test_reduce_colpiv_grammians(gh, m, n, neg):
     P = inputs.random_pencil(70 + m, m, n, neg)
     ctx = gh.Context(m, n)
     ctx.set_factors(P.F, P.J, P.G)
-    ctx.reduce(colpiv=True)
+    ctx.reduce(colpiv=True, unblocked=unblocked)
     F, J, G, p = ctx.get_factors()
     if n % 2:
         F, G, J = F[:-1, :-1], G[:-1, :-1], J[:-1]
@@ -124,3 +129,26 @@ def test_colpiv_reduce_on_illconditioned_matches_tall(gh):
     nf2 = np.linalg.norm(Fo) ** 2 + np.linalg.norm(Go) ** 2
     res = np.linalg.norm(Hx - Sx * lam[None, :], axis=0) / (nf2 * np.linalg.norm(Z, axis=0))
     assert res.max() <= 1e-12 * n
+
+
+@pytest.mark.parametrize("colpiv", [False, True])
+def test_blocked_and_unblocked_reduce_same_pencil(gh, colpiv):
+    """LAPW atoms (config-2 family, ~40 % negative signs): the blocked and the unblocked
+    Phase 2 may pivot differently on near-ties, but both reduce the same pencil -- the
+    converged eigenvalues agree with each other and with the oracle's tall solve (1e-9)."""
+    at = inputs.lapw_atoms(12, 4, 49, 300, 39 / 98)
+    m, n = 2 * 4 * 49, 300
+    lams = []
+    for unb in (False, True):
+        ctx = gh.Context(m, n, 49, variant="bo")
+        ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+        ctx.reduce(colpiv=colpiv, unblocked=unb)
+        st = ctx.sweep()
+        lams.append(np.sort(ctx.extract(want_z=False)[0]))
+        ctx.close()
+        assert st["converged"]
+    Fo, Jo, Go = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    Fr, Gr, Zp, sto = oracle.hz_pointwise(Fo, Jo, Go)
+    lo = np.sort(oracle.extract(Fr, Jo, Gr, Zp)[0])
+    for lam in lams:
+        assert np.max(np.abs(lam - lo) / np.abs(lo)) <= 1e-9

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
+from hostfactors import device_layout
 from paper_1907_08560_b200 import inputs
 
 pytestmark = pytest.mark.gpu
@@ -88,6 +89,15 @@ def test_set_get_factors_sorts_rows_by_J(gh):
     assert np.array_equal(G, P.G)
     assert list(p2) == list(range(10))
     ctx.close()
+    # the host restatement the oracle-side tests use (tests/hostfactors.py), odd n bordered
+    for m, n in ((37, 10), (40, 7)):
+        P = inputs.random_pencil(4 + n, m, n, 0.4)
+        ctx = gh.Context(m, n)
+        ctx.set_factors(P.F, P.J, P.G)
+        F, J, G, _ = ctx.get_factors()
+        ctx.close()
+        Fh, Jh, Gh = device_layout(P.F, P.J, P.G)
+        assert np.array_equal(F, Fh) and np.array_equal(J, Jh) and np.array_equal(G, Gh)
 
 
 def test_bad_J_rejected(gh):
@@ -106,12 +116,12 @@ def test_bad_J_rejected(gh):
                                          (17, 16, 1)])
 def test_steps_match_oracle(gh, m, n, cluster, kernel):
     """a1-a4 parity: after each of the first steps the GPU's F', G', Z' equal the oracle's
-    elementwise (same inputs from get_factors, same pair ordering); ragged m and all
+    elementwise (same inputs laid out on the host, same pair ordering); ragged m and all
     cluster sizes (slices crossing tile/cluster boundaries)."""
     P = inputs.random_pencil(100 + m, m, n, 0.45)
     ctx = gh.Context(m, n, cluster=cluster, kernel=kernel)
     ctx.set_factors(P.F, P.J, P.G)
-    F0, J0, G0, _ = ctx.get_factors()
+    F0, J0, G0 = device_layout(P.F, P.J, P.G)
     Zo = np.eye(n, dtype=complex)
     Fo, Go = F0, G0
     for s in range(min(n - 1, 5)):
@@ -131,7 +141,7 @@ def _gpu_run(gh, P, **kw):
     m, n = P.F.shape
     ctx = gh.Context(m, n, **kw)
     ctx.set_factors(P.F, P.J, P.G)
-    F0, J0, G0, _ = ctx.get_factors()
+    F0, J0, G0 = device_layout(P.F, P.J, P.G)
     st = ctx.sweep()
     lam, sf, sg, Z = ctx.extract()
     ctx.close()

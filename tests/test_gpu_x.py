@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+from hostfactors import device_layout
 from paper_1907_08560_b200 import inputs
 
 pytestmark = pytest.mark.gpu
@@ -39,7 +40,7 @@ def test_x_inverse_and_eq71(gh, variant, nb):
     for wx in (False, True):
         ctx = gh.Context(m, n, variant=variant, nblocks=nb, want_x=wx)
         ctx.set_factors(P.F, P.J, P.G)
-        F0, J0, G0, _ = ctx.get_factors()
+        F0, J0, G0 = device_layout(P.F, P.J, P.G)
         st = ctx.sweep()
         lam, sf, sg, Z = ctx.extract()
         X = ctx.extract_x() if wx else None
@@ -87,7 +88,7 @@ def test_dataset_c_gsvd_small_vs_oracle(gh):
     P = inputs.dataset_c(93, 128)
     ctx = gh.Context(128, 128, variant="bo", want_x=True)
     ctx.set_factors(P.F, P.J, P.G)
-    F0, J0, G0, _ = ctx.get_factors()
+    F0, J0, G0 = device_layout(P.F, P.J, P.G)
     st = ctx.sweep()
     lam, sf, sg, Z = ctx.extract()
     X = ctx.extract_x()
@@ -111,7 +112,7 @@ def test_x_with_cluster_pivot(gh, monkeypatch):
     for wx in (False, True):
         ctx = gh.Context(m, n, variant="bo", nblocks=6, want_x=wx)
         ctx.set_factors(P.F, P.J, P.G)
-        F0, J0, G0, _ = ctx.get_factors()
+        F0, J0, G0 = device_layout(P.F, P.J, P.G)
         ctx.sweep()
         lam, sf, sg, Z = ctx.extract()
         X = ctx.extract_x() if wx else None

@@ -419,6 +419,11 @@ def run_ours(args):
         Jh = torch.empty(mb, dtype=torch.int8, pin_memory=True)
         ctx.export_factors(Fh, Jh, Gh)
         stream.synchronize()
+        if nb != n:
+            # odd n: the exported factors carry the sweep's border row / column (last, C-10);
+            # the e2e input is the unbordered problem (set_factors borders it again)
+            mb, nb = mb - 1, nb - 1
+            Fh, Gh, Jh = Fh[:mb, :nb], Gh[:mb, :nb], Jh[:mb]
     identical = None
     if ws > 1:
         # every rank must start from bitwise the same factors (deterministic Phase 1 on

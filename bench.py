@@ -329,7 +329,8 @@ def metric_name(cfg: int, n: int) -> str:
 
 def measure_zgemm_peak(dev) -> float:
     """Live FP64 tensor-core roofline denominator: cuBLAS ZGEMM (complex128) TFLOP/s,
-    best of 5 at 4096^3 (MEASURED_PEAKS.json has no FP64 figure)."""
+    best of 10 at 4096^3 (MEASURED_PEAKS.json has no FP64 figure); nvidia-smi clocks are
+    sampled around it (roofline.peak_clocks)."""
     import torch
     a = torch.randn(4096, 4096, dtype=torch.complex128, device=dev)
     b = torch.randn(4096, 4096, dtype=torch.complex128, device=dev)
@@ -338,7 +339,7 @@ def measure_zgemm_peak(dev) -> float:
     torch.cuda.synchronize(dev)
     best = 1e30
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(5):
+    for _ in range(10):
         e0.record()
         a @ b
         e1.record()
@@ -373,7 +374,11 @@ def run_ours(args):
     stream = torch.cuda.Stream(dev)
     cfg = inputs.CONFIGS[args.config]
     blocked = args.variant in ("bo", "fb")
-    zgemm_peak = measure_zgemm_peak(dev) if blocked else None
+    zgemm_peak, zgemm_clocks = None, None
+    if blocked:
+        with ClockSampler(local) as zclk:
+            zgemm_peak = measure_zgemm_peak(dev)
+        zgemm_clocks = zclk.summary()
     # ---- inputs (seeded, synthetic; generated once and broadcast) and Phase 1 on the device
     kind, payload = shared_inputs(args.config, ws, rank, dev)
     if kind == "atoms":
@@ -537,6 +542,7 @@ def run_ours(args):
                 "launches": int(n_upd),
                 "flops_unit": "8 real flops per complex multiply-add (4M-equivalent; the kernel runs the 3M "
                               "scheme, so it can exceed the 4M ZGEMM rate)",
+                "peak_clocks": zgemm_clocks,
                 "peak_source": "cuBLAS ZGEMM 4096^3 measured live in this run (FP64 DMMA; MEASURED_PEAKS.json "
                                "has no FP64 figure)",
                 "others": others,

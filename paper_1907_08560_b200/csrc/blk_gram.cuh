@@ -84,16 +84,24 @@ __device__ void blk_factor(const BlkArgs& a, int pl, int which, double2* W) {
 // of tile row I is the B fragment of tile column I) and issues 36 DMMAs (exact 4M
 // complex product; J folded into the A operand).  The two k-halves are summed in a
 // fixed order at the end, so the result is deterministic.
+// x with its sign bit xor-ed with m (0 or 0x80000000): the J sign (+-1) applied on the
+// integer pipe -- bitwise what the product by +-1 gives, without an FP64 instruction
+// competing with the DMMAs for the FP64 pipe (ncu r2: the Gram's DMULs by the sign were
+// 17 % of its stall samples)
+__device__ __forceinline__ double sflip(double x, unsigned m) {
+  return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
+
 template <int GI, int TS>
-__device__ __forceinline__ void gram_tiles(const double2* T, int row, double sg, double (&acc)[9][4]) {
+__device__ __forceinline__ void gram_tiles(const double2* T, int row, unsigned sm, double (&acc)[9][4]) {
   constexpr int IA = GI, IB = 7 - GI, NF = 8 - GI;
   const int lane = threadIdx.x & 31;
   double2 f[NF];
 #pragma unroll
   for (int j = 0; j < NF; j++) f[j] = T[(8 * j + (lane >> 2)) * TS + row];
   // A operand of tile rows IA, IB: J_r conj(x): (ar, ai) with conj -> (+x.y used as -(-x.y))
-  const double aar = sg * f[IA].x, aai = sg * f[IA].y;
-  const double abr = sg * f[IB].x, abi = sg * f[IB].y;
+  const double aar = sflip(f[IA].x, sm), aai = sflip(f[IA].y, sm);
+  const double abr = sflip(f[IB].x, sm), abi = sflip(f[IB].y, sm);
 #pragma unroll
   for (int t = 0; t < 9; t++) {
     const bool ra = t <= IA;
@@ -135,7 +143,7 @@ struct G3 {
 };
 
 template <int GI, int H, bool W4, int TS>
-__device__ __forceinline__ void gram3_tiles(const double2* T, int row, double sg, double (&acc)[5][6]) {
+__device__ __forceinline__ void gram3_tiles(const double2* T, int row, unsigned sm, double (&acc)[5][6]) {
   using C = G3<GI>;
   const int lane = threadIdx.x & 31;
   double2 f[8];
@@ -147,13 +155,13 @@ __device__ __forceinline__ void gram3_tiles(const double2* T, int row, double sg
   }
   double ar[2] = {0, 0}, ai[2] = {0, 0}, as[2] = {0, 0};   // rows IA, IB
   if (C::needA(H, W4, C::IA)) {
-    ar[0] = sg * f[C::IA].x;
-    ai[0] = -(sg * f[C::IA].y);
+    ar[0] = sflip(f[C::IA].x, sm);
+    ai[0] = sflip(f[C::IA].y, sm ^ 0x80000000u);
     as[0] = ar[0] + ai[0];
   }
   if (C::needA(H, W4, C::IB)) {
-    ar[1] = sg * f[C::IB].x;
-    ai[1] = -(sg * f[C::IB].y);
+    ar[1] = sflip(f[C::IB].x, sm);
+    ai[1] = sflip(f[C::IB].y, sm ^ 0x80000000u);
     as[1] = ar[1] + ai[1];
   }
 #pragma unroll
@@ -242,8 +250,8 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
 #pragma unroll 1
       for (int ks = 0; ks < RT / 4; ks += 2) {
         const int row0 = 4 * ks + (lane & 3), row1 = row0 + 4;
-        const double sg0 = (hs == 0 && r0 + row0 >= a.npos) ? -1.0 : 1.0;
-        const double sg1 = (hs == 0 && r0 + row1 >= a.npos) ? -1.0 : 1.0;
+        const unsigned sg0 = (hs == 0 && r0 + row0 >= a.npos) ? 0x80000000u : 0u;
+        const unsigned sg1 = (hs == 0 && r0 + row1 >= a.npos) ? 0x80000000u : 0u;
         switch (warp) {   // warp-uniform; tile 4 on even k-steps for h = 0, odd for h = 1
 #define G3CASE(W, GI, H)                                       \
   case W:                                                      \
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
 #pragma unroll 1
       for (int ks = 0; ks < RT / 4; ks += 2) {
         const int row = 4 * (ks + kh) + (lane & 3);
-        const double sg = (hs == 0 && r0 + row >= a.npos) ? -1.0 : 1.0;
+        const unsigned sg = (hs == 0 && r0 + row >= a.npos) ? 0x80000000u : 0u;
         switch (gi) {   // warp-uniform
           case 0: gram_tiles<0, TS>(T, row, sg, acc); break;
           case 1: gram_tiles<1, TS>(T, row, sg, acc); break;

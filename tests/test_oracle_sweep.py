@@ -7,6 +7,8 @@ brute force in mpmath at 40 digits on tiny general pencils, the GHSVD
 definition (V^*V = I, F columns J-orthogonal,
 Sigma_F^2 + Sigma_G^2 = 1), the congruence F_c = F Z', and residuals.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -365,3 +367,28 @@ def test_datasetA_sign_structure_phase1():
         Ja = J[242 * a: 242 * (a + 1)]
         assert int((Ja > 0).sum()) == 3 and list(Ja[:3]) == [1, 1, 1]
         assert int((np.sign(at.d[a]) > 0).sum()) == 3
+
+
+def test_stored_reference_script_and_fingerprint(tmp_path):
+    """tools/make_oracle_reference.py (oracle only) writes lambda and the input fingerprint;
+    the fingerprint accepts a regeneration of the same recipe and seed and rejects another
+    seed (reading R2-2: stored references are keyed by their inputs)."""
+    import json
+    import subprocess
+    import sys
+    from paper_1907_08560_b200 import inputs
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "make_oracle_reference.py"), "--illcond",
+                        "2,6,16,5", "--variant", "pointwise", "--threads", "2", "--out", str(tmp_path)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    meta = json.load(open(tmp_path / "illcond_2_6_16_s5_oracle_pointwise.json"))
+    lam = np.load(tmp_path / "illcond_2_6_16_s5_oracle_pointwise.npz")["lam"]
+    assert meta["stats"]["converged"] and lam.shape == (16,) and meta["m"] == 24 and meta["n"] == 16
+    assert inputs.fingerprint_close(inputs.fingerprint(inputs.illcond_atoms(5, 2, 6, 16)), meta["fingerprint"])
+    assert not inputs.fingerprint_close(inputs.fingerprint(inputs.illcond_atoms(6, 2, 6, 16)), meta["fingerprint"])
+    # the stored lambda is the oracle pipeline's own
+    at = inputs.illcond_atoms(5, 2, 6, 16)
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    Fo, Go, Zp, st = oracle.hz_pointwise(F, J, G, cmax=64)
+    assert np.array_equal(oracle.extract(Fo, J, Go, Zp)[0], lam)

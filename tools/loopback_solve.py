@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--max-sweeps", type=int, default=64)
+    ap.add_argument("--overlap", type=int, default=0, help="exchange_overlap of the P-rank run (0: one grouped exchange)")
     args = ap.parse_args()
     import torch
     from paper_1907_08560_b200 import build, ghsvd, inputs
@@ -36,7 +37,7 @@ def main():
 
     def make(world, rank, lid, stream):
         c = ghsvd.Context(m, n, NL, variant="bo", max_sweeps=args.max_sweeps, world_size=world, rank=rank,
-                          nccl_id=lid, stream=stream)
+                          nccl_id=lid, stream=stream, exchange_overlap=bool(args.overlap) and world > 1)
         c.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
         return c
 
@@ -50,7 +51,7 @@ def main():
     del c
     torch.cuda.empty_cache()
     # P ranks
-    lid = ghsvd.loopback_id(f"cfg{args.config}_w{args.world}")
+    lid = ghsvd.loopback_id(f"cfg{args.config}_w{args.world}_x{args.overlap}")
     ctxs = [make(args.world, r, lid, torch.cuda.Stream()) for r in range(args.world)]
     res, errs = [None] * args.world, []
 
@@ -72,7 +73,7 @@ def main():
         c.close()
     ok = not errs and all(r is not None and r[0]["sweeps"] == st1["sweeps"] and np.array_equal(r[1], lam1)
                           for r in res)
-    out = {"config": args.config, "m": m, "n": n, "world": args.world, "one_rank": {
+    out = {"config": args.config, "m": m, "n": n, "world": args.world, "exchange_overlap": args.overlap, "one_rank": {
         "sweeps": st1["sweeps"], "converged": st1["converged"], "sweep_seconds": st1["seconds"], "wall_s": t1},
         "loopback": {"per_rank_sweep_seconds": [r[0]["seconds"] for r in res if r], "wall_s": tP,
                      "sweeps": [r[0]["sweeps"] for r in res if r], "errors": errs},

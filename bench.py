@@ -305,8 +305,12 @@ def run_reference(args):
     sweeps = args.ref_sweeps if args.ref_sweeps > 0 else REF_SWEEPS.get(args.config, 36)
     m, n = F0.shape
     vals = []
+    # each step is a bounded sample; the whole --steps K --warmup W run stays within a few
+    # minutes (about 8 x ref_budget of sampling in total once K + W exceeds 8)
+    per_step = args.ref_budget if args.warmup + args.steps <= 8 else \
+        max(2.0, 8.0 * args.ref_budget / (args.warmup + args.steps))
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline_sample(F0, J0, G0, args.config, sweeps, budget_s=args.ref_budget)
+        cb = cpu_baseline_sample(F0, J0, G0, args.config, sweeps, budget_s=per_step)
         if i >= args.warmup:
             vals.append(cb["value"])
     v = float(np.mean(vals))

@@ -32,6 +32,21 @@ __device__ __forceinline__ void amax_merge(double& v, long long& i, double v2, l
     i = i2;
   }
 }
+// the Schur updates' pivot tracking of one updated entry w at (i, j): diagonal |w_ii|,
+// strictly lower |w_ij|^2 with index j r + i -- the same choices as amax_merge, written as
+// selects so that the diagonal crossing a warp's rows does not split it into branches
+__device__ __forceinline__ void track_entry(double2 w, int i, int j, int r, double& mu1, long long& id, double& mu0,
+                                            long long& oidx) {
+  const double dv = fabs(w.x);
+  const bool td = (i == j) && (dv > mu1 || (dv == mu1 && (long long)i < id));
+  mu1 = td ? dv : mu1;
+  id = td ? (long long)i : id;
+  const double ov = __dadd_rn(__dmul_rn(w.x, w.x), __dmul_rn(w.y, w.y));
+  const long long oi = (long long)(j * r + i);
+  const bool to = (i > j) && (ov > mu0 || (ov == mu0 && oi < oidx));
+  mu0 = to ? ov : mu0;
+  oidx = to ? oi : oidx;
+}
 
 // Shared-memory scratch of the routines below, passed in by the caller (the blocked
 // variant places it in dynamic shared memory it no longer needs, so its kernels carry no
@@ -250,8 +265,7 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
         for (int i = k + 1 + lane; i < r; i += 32) {
           const double2 w = sub(W[i + j * ldw], scale(mul(W[i + k * ldw], cj), inv));
           W[i + j * ldw] = w;
-          if (i == j) amax_merge(mu1, id, fabs(w.x), i);
-          else if (i > j) amax_merge(mu0, oidx, cabs2(w), (long long)j * r + i);
+          track_entry(w, i, j, r, mu1, id, mu0, oidx);
         }
       }
       if (threadIdx.x == 0) {
@@ -278,8 +292,7 @@ __device__ int hebpj_dev(double2* W, int r, long long ldw, double2* M, long long
           const double2 t = add(mul(W[i + k * ldw], c0), mul(W[i + (k + 1) * ldw], c1));
           const double2 w = sub(W[i + j * ldw], t);
           W[i + j * ldw] = w;
-          if (i == j) amax_merge(mu1, id, fabs(w.x), i);
-          else if (i > j) amax_merge(mu0, oidx, cabs2(w), (long long)j * r + i);
+          track_entry(w, i, j, r, mu1, id, mu0, oidx);
         }
       }
       if (threadIdx.x == 0) {
@@ -396,10 +409,21 @@ __device__ int pchol_dev(double2* S, int r, long long lds, double2* Gh, long lon
     const double inv = __ddiv_rn(1.0, lkk);
     // Schur complement with L(:,k) = S(:,k) / l_kk formed on the fly; column k and the
     // diagonal entry (k, k) are not written in this phase
+    // (the lane's L(i,k) for its rows i = k+1+lane+32t are formed once, not once per j)
+    constexpr int NR = (RMAX + 31) / 32;
+    double2 li[NR];
+#pragma unroll
+    for (int t = 0; t < NR; t++) {
+      const int i = k + 1 + lane + 32 * t;
+      li[t] = i < r ? scale(S[i + k * lds], inv) : mk(0.0, 0.0);
+    }
     for (int j = k + 1 + warp; j < r; j += NW) {
       const double2 cj = conj(scale(S[j + k * lds], inv));
-      for (int i = k + 1 + lane; i < r; i += 32)
-        S[i + j * lds] = sub(S[i + j * lds], mul(scale(S[i + k * lds], inv), cj));
+#pragma unroll
+      for (int t = 0; t < NR; t++) {
+        const int i = k + 1 + lane + 32 * t;
+        if (i < r) S[i + j * lds] = sub(S[i + j * lds], mul(li[t], cj));
+      }
     }
     if (threadIdx.x == 0) {
       dg[k] = lkk;

@@ -19,16 +19,23 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--widths", type=int, nargs="+", default=[16, 32, 64])
+    ap.add_argument("--cases", nargs="+", default=["illcond_16_49_1024_s31", "datasetC_1024_s5"])
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02", "blockwidth_sweeps.json"))
     args = ap.parse_args()
     import oracle
     from paper_1907_08560_b200 import inputs
     cases = {}
-    at = inputs.illcond_atoms(31, 16, 49, 1024)
-    cases["illcond_16_49_1024_s31"] = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
-    P = inputs.dataset_c(7, 1024)
-    cases["datasetC_1024"] = (P.F, P.J, P.G)
-    res = {"what": "or_hz_blocked BO sweeps by block width w (nblk = 2 ceil(n / 2w)), C_max 64", "cases": {}}
+    if "illcond_16_49_1024_s31" in args.cases:
+        at = inputs.illcond_atoms(31, 16, 49, 1024)
+        cases["illcond_16_49_1024_s31"] = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    if "datasetC_1024_s5" in args.cases:
+        # (seed 7 draws an eigenvalue of F small enough that a block pivot is numerically
+        # singular: the stop the paper prescribes)
+        P = inputs.dataset_c(5, 1024)
+        cases["datasetC_1024_s5"] = (P.F, P.J, P.G)
+    res = json.load(open(args.out)) if os.path.exists(args.out) else {}
+    res.update({"what": "or_hz_blocked BO sweeps by block width w (nblk = 2 ceil(n / 2w)), C_max 64"})
+    res.setdefault("cases", {})
     for name, (F, J, G) in cases.items():
         n = F.shape[1]
         res["cases"][name] = {}

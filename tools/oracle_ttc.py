@@ -28,6 +28,9 @@ def main():
     import oracle
     from paper_1907_08560_b200 import inputs
     cores = b._cores()
+    # untimed warm-up: the first OpenMP region of the process starts the thread pool (~0.8 s)
+    k0, p0 = inputs.make_config(0)
+    oracle.hz_pointwise(*b.oracle_factors(k0, p0, 0), cmax=1, nthreads=cores)
     res = {"cpu_model": b._cpu_model(), "threads": cores, "what": "oracle.hz_pointwise to convergence (C_max 64), "
            "timed end to end on the oracle's own starting factors", "configs": {}}
     for c in args.configs:

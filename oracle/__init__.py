@@ -92,6 +92,10 @@ def lib():
                                   ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.or_hz_blocked.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, I64, Ci, D, Ci, Ci, Ci,
                                     ctypes.POINTER(_Stats)]
+        L.or_hz_blocked_ord.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, I64, Ci, I64, Ci, D, Ci,
+                                        Ci, Ci, ctypes.POINTER(_Stats)]
+        L.or_order_steps.argtypes = [Ci, I64, I64, ctypes.POINTER(I64)]
+        L.or_order_pair.argtypes = [Ci, I64, I64, I64, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.or_extract.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, P, P, P, P, I64]
         L.or_block_partition.argtypes = [I64, I64, P, P]
         L.or_hz_pointwise_inv.argtypes = [I64, I64, P, I64, P, P, I64, P, I64, P, I64, D, Ci, Ci, Ci,
@@ -191,17 +195,39 @@ def hz_steps(F, J, G, Z, s0, ns, eps=EPS, criterion=CRIT_RELATIVE, nthreads=0):
     return F, G, Z, a.value, b.value
 
 
+ORDER_RR, ORDER_LEVEL3, ORDER_HIER = 0, 1, 2
+
+
+def order_steps(ordering, nblk, nsup=0):
+    """Block steps per sweep of a block ordering (or_order_steps; reading R2-5)."""
+    v = ctypes.c_int64()
+    _chk(lib().or_order_steps(ordering, nblk, nsup, ctypes.byref(v)), "order_steps")
+    return v.value
+
+
+def order_pair(ordering, nblk, nsup, s, k):
+    """Block pair (p < q) of slot k in block step s (or_order_pair; reading R2-5)."""
+    p, q = ctypes.c_int64(), ctypes.c_int64()
+    _chk(lib().or_order_pair(ordering, nblk, nsup, s, k, ctypes.byref(p), ctypes.byref(q)), "order_pair")
+    return p.value, q.value
+
+
 def hz_blocked(F, J, G, nblk, inner_sweeps=1, eps=EPS, criterion=CRIT_RELATIVE, cmax=30,
-               nthreads=0):
+               nthreads=0, ordering=ORDER_RR, nsup=0):
     F = _cf(F)
     G = _cf(G)
     J = np.ascontiguousarray(J, dtype=np.int8)
     m, n = F.shape
     Z = np.zeros((n, n), dtype=np.complex128, order="F")
     st = _Stats()
-    _chk(lib().or_hz_blocked(m, n, _ptr(F), m, _ptr(J), _ptr(G), m, _ptr(Z), n, nblk,
-                             inner_sweeps, eps, criterion, cmax, nthreads, ctypes.byref(st)),
-         "hz_blocked")
+    if ordering == ORDER_RR:
+        rc = lib().or_hz_blocked(m, n, _ptr(F), m, _ptr(J), _ptr(G), m, _ptr(Z), n, nblk,
+                                 inner_sweeps, eps, criterion, cmax, nthreads, ctypes.byref(st))
+    else:
+        rc = lib().or_hz_blocked_ord(m, n, _ptr(F), m, _ptr(J), _ptr(G), m, _ptr(Z), n, nblk,
+                                     ordering, nsup, inner_sweeps, eps, criterion, cmax, nthreads,
+                                     ctypes.byref(st))
+    _chk(rc, "hz_blocked")
     return F, G, Z, st.todict()
 
 

@@ -70,6 +70,72 @@ int or_rr_pair(int64_t n, int64_t s, int64_t k, int64_t *p, int64_t *q) {
   return OR_OK;
 }
 
+/* ----------------------------------------------- level-3 block orderings */
+/* PAPER.md:1815-1824 (Sec 6.4): "a multilevel blocking principle can be applied ...
+ * The same principle can be applied recursively further"; the paper builds Level 2
+ * only.  Reading R2-5: nblk block columns are grouped into nsup = 2Q super
+ * blocks of B = nblk / nsup consecutive block columns, and the block pairs of a block
+ * sweep are ordered by super block:
+ *  OR_ORDER_LEVEL3 (1): the Level-2 principle applied once more.  An outer round-robin
+ *    over the 2Q super blocks (2Q - 1 outer steps t, super pair slots u < Q); a super
+ *    pair is a Level-3 pivot of 2B block columns and receives ONE inner round-robin
+ *    block sweep over them (2B - 1 inner steps i, slots v < B; block-oriented at Level
+ *    3).  Step s = t (2B - 1) + i, slot k = u B + v.  Block pairs inside a super block
+ *    are visited in every outer step (2Q - 1 times per sweep), the others once.
+ *  OR_ORDER_HIER (2): every block pair exactly once per sweep, grouped by super pair:
+ *    B - 1 intra steps (round-robin over the B blocks of each super block of the super
+ *    pairs of outer step 0: slots v < B/2 pair inside the lower super block, the rest
+ *    inside the upper one), then for every outer step t, B bipartite steps i pairing
+ *    block v of the lower super block with block (v + i) mod B of the upper one.
+ *    B must be even or 1.
+ * LEVEL3 reduces to the Level-2 round-robin when nsup = 2 or nsup = nblk, HIER when nsup = nblk. */
+static int order_args(int ord, int64_t nblk, int64_t nsup) {
+  if (nblk < 2 || (nblk & 1)) return OR_E_ARG;
+  if (ord == OR_ORDER_RR) return OR_OK;
+  if (ord != OR_ORDER_LEVEL3 && ord != OR_ORDER_HIER) return OR_E_ARG;
+  if (nsup < 2 || (nsup & 1) || nblk % nsup) return OR_E_ARG;
+  int64_t B = nblk / nsup;
+  if (ord == OR_ORDER_HIER && B != 1 && (B & 1)) return OR_E_ARG;
+  return OR_OK;
+}
+
+int or_order_steps(int ord, int64_t nblk, int64_t nsup, int64_t *nsteps) {
+  if (order_args(ord, nblk, nsup)) return OR_E_ARG;
+  if (ord == OR_ORDER_RR) { *nsteps = nblk - 1; return OR_OK; }
+  int64_t B = nblk / nsup;
+  if (ord == OR_ORDER_LEVEL3) *nsteps = (nsup - 1) * (2 * B - 1);
+  else *nsteps = (B - 1) + (nsup - 1) * B;
+  return OR_OK;
+}
+
+int or_order_pair(int ord, int64_t nblk, int64_t nsup, int64_t s, int64_t k, int64_t *p, int64_t *q) {
+  int64_t nst;
+  if (or_order_steps(ord, nblk, nsup, &nst) || s < 0 || s >= nst || k < 0 || k >= nblk / 2)
+    return OR_E_ARG;
+  if (ord == OR_ORDER_RR) return or_rr_pair(nblk, s, k, p, q);
+  int64_t B = nblk / nsup, u = k / B, v = k % B, P, Q, a, b;
+  if (ord == OR_ORDER_LEVEL3) {
+    int64_t t = s / (2 * B - 1), i = s % (2 * B - 1);
+    or_rr_pair(nsup, t, u, &P, &Q);         /* outer: super pair u of outer step t */
+    or_rr_pair(2 * B, i, v, &a, &b);        /* inner: local block indices in [0, 2B) */
+    *p = a < B ? P * B + a : Q * B + (a - B);
+    *q = b < B ? P * B + b : Q * B + (b - B);
+  } else if (s < B - 1) {                   /* HIER, intra steps (outer step 0's super pairs) */
+    or_rr_pair(nsup, 0, u, &P, &Q);
+    int64_t half = B / 2, base = v < half ? P * B : Q * B;
+    or_rr_pair(B, s, v % half, &a, &b);
+    *p = base + a;
+    *q = base + b;
+  } else {                                  /* HIER, bipartite steps */
+    int64_t s2 = s - (B - 1), t = s2 / B, i = s2 % B;
+    or_rr_pair(nsup, t, u, &P, &Q);
+    *p = P * B + v;
+    *q = Q * B + (v + i) % B;
+  }
+  if (*p > *q) { int64_t x = *p; *p = *q; *q = x; }
+  return OR_OK;
+}
+
 /* ------------------------------------------------------- 2x2 transform */
 /* PAPER.md:1365-1573.  Exactly the sequence of Sec. 6.1.1-6.1.7:
  *   prescale by D0 (Sec 6.1.1), test (6.12), x = |s_pq|, alpha_1 = arg s_pq
@@ -672,7 +738,17 @@ int or_hz_blocked(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
                   orc *G, int64_t ldg, orc *Z, int64_t ldz, int64_t nblk,
                   int inner_sweeps, double eps, int criterion, int cmax,
                   int nthreads, or_stats *st) {
-  if (m < 1 || n < 2 || nblk < 2 || (nblk & 1) || nblk > n || cmax < 1 || inner_sweeps < 1)
+  return or_hz_blocked_ord(m, n, F, ldf, J, G, ldg, Z, ldz, nblk, OR_ORDER_RR, 0, inner_sweeps,
+                           eps, criterion, cmax, nthreads, st);
+}
+
+int or_hz_blocked_ord(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
+                      orc *G, int64_t ldg, orc *Z, int64_t ldz, int64_t nblk, int ord,
+                      int64_t nsup, int inner_sweeps, double eps, int criterion, int cmax,
+                      int nthreads, or_stats *st) {
+  int64_t nst;
+  if (m < 1 || n < 2 || nblk < 2 || (nblk & 1) || nblk > n || cmax < 1 || inner_sweeps < 1 ||
+      or_order_steps(ord, nblk, nsup, &nst))
     return OR_E_ARG;
   set_threads(nthreads);
   memset(st, 0, sizeof(*st));
@@ -684,13 +760,13 @@ int or_hz_blocked(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
   int rc = OR_OK;
   for (int sw = 0; sw < cmax && rc == 0; sw++) {
     int64_t all = 0, big = 0;
-    for (int64_t s = 0; s < nblk - 1 && rc == 0; s++) {
+    for (int64_t s = 0; s < nst && rc == 0; s++) {
       int err = 0;
       int64_t a_all = 0, a_big = 0;
 #pragma omp parallel for schedule(static) reduction(+ : a_all, a_big)
       for (int64_t kk = 0; kk < nblk / 2; kk++) {
         int64_t bp, bq;
-        or_rr_pair(nblk, s, kk, &bp, &bq);
+        or_order_pair(ord, nblk, nsup, s, kk, &bp, &bq);
         int64_t la = 0, lb = 0;
         int e = block_pivot(m, n, F, ldf, J, G, ldg, Z, ldz, bs[bp], bw[bp], bs[bq], bw[bq],
                             inner_sweeps, eps, criterion, &la, &lb);

@@ -89,6 +89,21 @@ int or_hz_blocked(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
                   int inner_sweeps, double eps, int criterion, int cmax,
                   int nthreads, or_stats *st);
 
+/* Block orderings (reading R2-5 of PAPER.md:1815-1824, Sec 6.4; see ghsvd_oracle.c):
+ * OR_ORDER_RR the Level-2 round-robin (nsup ignored), OR_ORDER_LEVEL3 the recursive
+ * (Level-3, block-oriented) ordering over nsup super blocks, OR_ORDER_HIER every block
+ * pair once per sweep grouped by super pair.  or_order_steps: block steps per sweep;
+ * or_order_pair: block pair (p < q) of slot k in step s. */
+enum { OR_ORDER_RR = 0, OR_ORDER_LEVEL3 = 1, OR_ORDER_HIER = 2 };
+int or_order_steps(int ord, int64_t nblk, int64_t nsup, int64_t *nsteps);
+int or_order_pair(int ord, int64_t nblk, int64_t nsup, int64_t s, int64_t k, int64_t *p, int64_t *q);
+
+/* or_hz_blocked with the block pairs of each sweep in the given ordering. */
+int or_hz_blocked_ord(int64_t m, int64_t n, orc *F, int64_t ldf, const int8_t *J,
+                      orc *G, int64_t ldg, orc *Z, int64_t ldz, int64_t nblk, int ord,
+                      int64_t nsup, int inner_sweeps, double eps, int criterion, int cmax,
+                      int nthreads, or_stats *st);
+
 /* The Sec 6.4.1 partition (widths w or w-1, non-increasing) and one block pivot
  * (Sec 6.4.2-6.4.3) of block columns [p0, p0+wp) and [q0, q0+wq), in place. */
 int or_block_partition(int64_t n, int64_t nblk, int64_t *start, int64_t *width);

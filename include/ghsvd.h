@@ -52,7 +52,16 @@ typedef enum {
 } ghsvd_status;
 
 enum { GHSVD_POINTWISE = 0, GHSVD_BLOCKED_BO = 1, GHSVD_BLOCKED_FB = 2 };
-enum { GHSVD_ORDER_ROUND_ROBIN = 0 };
+/* Block orderings of the blocked variants (csrc/ordering.h).  ROUND_ROBIN: the circle
+ * method over the block columns (Sec 6.3-6.4, reading C-11).  LEVEL3 and HIER (reading R2-5
+ * of PAPER.md:1815-1824, Sec 6.4: the blocking principle "applied recursively further")
+ * group the block columns into super_blocks = 2Q super blocks: LEVEL3 runs an outer circle
+ * method over the super blocks and ONE inner block sweep over every super pair (a Level-3
+ * pivot of 2 super blocks, block-oriented; block pairs inside a super block are visited in
+ * every outer step); HIER visits every block pair once per sweep, grouped by super pair.
+ * With one super pair per rank (super_blocks = 2 * world_size) block columns change rank
+ * only between outer steps: 2Q - 1 exchanges per sweep instead of nblocks - 1. */
+enum { GHSVD_ORDER_ROUND_ROBIN = 0, GHSVD_ORDER_LEVEL3 = 1, GHSVD_ORDER_HIER = 2 };
 /* Transformation criterion, eq (6.12) PAPER.md:1552-1562.  RELATIVE (default):
  * |H_pq| >= eps sqrt(n) |H_pp|^(1/2) |H_qq|^(1/2) or |S_pq| >= eps sqrt(n) on the
  * prescaled pivot; LITERAL: |H_pq| >= (max|H_ii| eps sqrt(n)) min|H_ii| as printed. */
@@ -72,7 +81,7 @@ typedef struct {
                         * events and a host barrier (600 s timeout -> GHSVD_E_NCCL).  It runs
                         * the multi-GPU schedule of the blocked sweep without several GPUs. */
   int variant;         /* GHSVD_POINTWISE | GHSVD_BLOCKED_BO | GHSVD_BLOCKED_FB */
-  int ordering;        /* GHSVD_ORDER_ROUND_ROBIN */
+  int ordering;        /* GHSVD_ORDER_* (blocked variants; the pointwise variant is round-robin only) */
   int nblocks;         /* blocked: number of block columns (even; 0 = auto); Sec 6.4.1 */
   int max_sweeps;      /* C_max, default 30 (Algorithm 2) */
   int criterion;       /* GHSVD_CRIT_RELATIVE | GHSVD_CRIT_LITERAL */
@@ -108,6 +117,9 @@ typedef struct {
   int gram_splits;     /* blocked: row splits of the block Grams (0 = planned against wave quantization) */
   const char* trace_path; /* blocked: write the first sweep's launch timeline (first-CTA start,
                           last-CTA end per launch) as CSV to this path (NULL = off) */
+  int super_blocks;    /* LEVEL3 / HIER orderings: number of super blocks, even, dividing the number of
+                          block columns (HIER: an even number of block columns per super block, or 1);
+                          0 = 2 * world_size, or 4 on one GPU */
 } ghsvd_options;
 /* ghsvd_options.schedule bits.  ghsvd_default_options seeds schedule, groups, gram_splits and
  * trace_path from the environment (GHSVD_SERIAL, GHSVD_PRIO=0, GHSVD_SPLIT_BND, GHSVD_GRAM3M=0,
@@ -298,6 +310,17 @@ int ghsvd_exchange_plan(int nblk, int world, int rank, int s, int s_next, int64_
                         int64_t* send_peer, int64_t* nsend, int64_t* recv_blk, int64_t* recv_peer,
                         int64_t* nrecv);
 int ghsvd_nccl_unique_id(void* out128);
+/* The same for any block ordering (ordering = GHSVD_ORDER_*, nsup = the resolved number of
+ * super blocks, ignored for ROUND_ROBIN; see ghsvd_options.super_blocks).
+ * ghsvd_order_steps: block steps per sweep (-1 on bad args).
+ * ghsvd_order_pair: block pair (*p < *q) of slot k in block step s; 0 or -1.
+ * ghsvd_block_owner_ord / ghsvd_exchange_plan_ord: as the round-robin forms above. */
+int64_t ghsvd_order_steps(int ordering, int nblk, int nsup);
+int ghsvd_order_pair(int ordering, int nblk, int nsup, int64_t s, int64_t k, int64_t* p, int64_t* q);
+int ghsvd_block_owner_ord(int ordering, int nblk, int nsup, int world, int64_t s, int b);
+int ghsvd_exchange_plan_ord(int ordering, int nblk, int nsup, int world, int rank, int64_t s, int64_t s_next,
+                            int64_t* send_blk, int64_t* send_peer, int64_t* nsend, int64_t* recv_blk,
+                            int64_t* recv_peer, int64_t* nrecv);
 
 const char* ghsvd_last_error(ghsvd_ctx ctx);
 void ghsvd_destroy(ghsvd_ctx ctx);

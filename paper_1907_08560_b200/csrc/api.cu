@@ -116,7 +116,9 @@ static bool opts_ok(const ghsvd_options* o) {
   if (!o) return false;
   if (o->world_size < 1 || o->rank < 0 || o->rank >= o->world_size) return false;
   if (o->variant < 0 || o->variant > 2) return false;
-  if (o->ordering != GHSVD_ORDER_ROUND_ROBIN) return false;
+  if (o->ordering < GHSVD_ORDER_ROUND_ROBIN || o->ordering > GHSVD_ORDER_HIER) return false;
+  if (o->ordering != GHSVD_ORDER_ROUND_ROBIN && o->variant == GHSVD_POINTWISE) return false;
+  if (o->super_blocks < 0 || (o->super_blocks & 1)) return false;
   if (o->max_sweeps < 1 || o->max_sweeps > 64) return false;
   if (o->criterion != 0 && o->criterion != 1) return false;
   if (o->nblocks < 0 || (o->nblocks & 1)) return false;

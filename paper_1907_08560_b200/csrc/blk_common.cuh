@@ -56,6 +56,7 @@ struct BlkArgs {
   double2* Z;
   long long ldm, ldn, m, n, npos;
   int nblk, s, slot0, npairs;
+  int ord, nsup;            // block ordering (ordering.h) and its super blocks
   int pair0;                // first local pair handled by this launch (blockIdx.x offset)
   const int* bstart;
   const int* bwidth;
@@ -97,7 +98,7 @@ __device__ __forceinline__ void trace_end(const BlkArgs& a) {
 
 __device__ __forceinline__ void pair_cols(const BlkArgs& a, int pl, int& c0p, int& wp, int& c0q, int& wq) {
   long long bp, bq;
-  rr_pair(a.nblk, a.s, a.slot0 + pl, &bp, &bq);
+  blk_order_pair(a.ord, a.nblk, a.nsup, a.s, a.slot0 + pl, &bp, &bq);
   c0p = a.bstart[bp];
   wp = a.bwidth[bp];
   c0q = a.bstart[bq];

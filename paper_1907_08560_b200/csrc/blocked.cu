@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "ordering.h"
 // the kernels (one translation unit: these files are included only here)
 #include "blk_common.cuh"
 #include "blk_gram.cuh"
@@ -60,7 +61,17 @@ int auto_nblk(int64_t n, const ghsvd_options* o) {
 struct BlkPlan {
   int nblk, K, slot0, nsplit;
   long long split_rows;
+  int nsup;   // super blocks of a LEVEL3 / HIER ordering (0 for the round-robin)
+  int nst;    // block steps per sweep
 };
+
+// super blocks of the LEVEL3 / HIER orderings: the option, else one super pair per rank
+// (4 super blocks on one GPU)
+int resolve_nsup(const ghsvd_options* o) {
+  if (o->ordering == GHSVD_ORDER_ROUND_ROBIN) return 0;
+  if (o->super_blocks > 0) return o->super_blocks;
+  return o->world_size > 1 ? 2 * o->world_size : 4;
+}
 
 BlkPlan make_plan(const Ctx* ctx) {
   BlkPlan p;
@@ -68,6 +79,8 @@ BlkPlan make_plan(const Ctx* ctx) {
   const int P = std::max(1, ctx->o.world_size);
   p.K = p.nblk / 2 / P;
   p.slot0 = ctx->o.rank * p.K;
+  p.nsup = resolve_nsup(&ctx->o);
+  p.nst = blk_order_check(ctx->o.ordering, p.nblk, p.nsup) ? -1 : (int)blk_order_steps(ctx->o.ordering, p.nblk, p.nsup);
   // Row split of the Gram launches, chosen against wave quantization: a launch covers
   // M = 2 * (pairs per launch) matrices x nsplit CTAs with R CTAs resident at once;
   // cost ~ waves x (32-row stages per CTA + fill/partial overhead).  Deterministic for a
@@ -107,7 +120,7 @@ static size_t blk_scratch_for(int64_t K, int64_t nb, bool want_x) {
   return al256((size_t)K * 2 * MAX_SPLIT * KM * KM * 16) + al256((size_t)2 * K * KM * KM * 16) +
          al256((size_t)2 * K * 4) + 2 * al256((size_t)(nb + 2) * 4) + 2 * al256((size_t)K * KM * KM * 16) +
          al256((size_t)K * KM) + al256((size_t)2 * K * 4) + (want_x ? al256((size_t)2 * K * KM * KM * 16) : 0) +
-         al256((size_t)(nb + 2) * TRACE_SLOTS * 16) + al256((size_t)2 * K * 4) + al256((size_t)(nb + 2) * 8) +
+         al256((size_t)(2 * nb + 2) * TRACE_SLOTS * 16) + al256((size_t)2 * K * 4) + al256((size_t)(2 * nb + 2) * 8) +
          4096;
 }
 
@@ -142,6 +155,11 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
     ctx->err = "blocked: nblocks must be even, <= n and a multiple of 2*world_size";
     return GHSVD_E_INVALID_ARG;
   }
+  if (pl.nst < 1) {
+    ctx->err = "blocked: invalid block ordering (super_blocks must be even and divide nblocks; HIER needs an even "
+               "number of block columns per super block, or 1)";
+    return GHSVD_E_INVALID_ARG;
+  }
   const int64_t w = (ctx->n + pl.nblk - 1) / pl.nblk;
   if (2 * w > KM) {
     ctx->err = "blocked: block width " + std::to_string(w) + " > 32 (increase nblocks)";
@@ -169,13 +187,14 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   } else {
     a.zinvT = nullptr;
   }
-  S.trace_buf = (unsigned long long*)p; p += al256((size_t)(pl.nblk + 2) * TRACE_SLOTS * 16);
-  a.upd_k2 = (unsigned long long*)p; p += al256((size_t)(pl.nblk + 2) * 8);
+  // step-indexed arrays: a sweep has at most 2 nblk block steps (LEVEL3: (2Q-1)(2B-1) < 4QB)
+  S.trace_buf = (unsigned long long*)p; p += al256((size_t)(2 * pl.nblk + 2) * TRACE_SLOTS * 16);
+  a.upd_k2 = (unsigned long long*)p; p += al256((size_t)(2 * pl.nblk + 2) * 8);
   a.trace = nullptr;
   a.trace_id = 0;
   k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
   GH_CUDA(cudaMemsetAsync(a.gcnt, 0, (size_t)2 * pl.K * 4, str));
-  GH_CUDA(cudaMemsetAsync(a.upd_k2, 0, (size_t)(pl.nblk + 2) * 8, str));
+  GH_CUDA(cudaMemsetAsync(a.upd_k2, 0, (size_t)(2 * pl.nblk + 2) * 8, str));
   GH_CUDA(cudaGetLastError());
   S.bs_h.assign(pl.nblk, 0);
   S.bw_h.assign(pl.nblk, 0);
@@ -193,6 +212,9 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   a.n = ctx->n;
   a.npos = ctx->npos;
   a.nblk = pl.nblk;
+  a.ord = ctx->o.ordering;
+  a.nsup = pl.nsup;
+  ctx->blk_nsup = pl.nsup;
   a.slot0 = pl.slot0;
   a.npairs = pl.K;
   a.bstart = bstart;
@@ -282,8 +304,8 @@ ghsvd_status blk_run_steps(Ctx* ctx, int64_t s0, int64_t ns) {
   BlkSetup S;
   ghsvd_status e = blk_setup(ctx, S);
   if (e) return e;
-  if (s0 < 0 || ns < 0 || s0 + ns > S.pl.nblk - 1) {
-    ctx->err = "run_steps: block step range outside [0, nblk-2]";
+  if (s0 < 0 || ns < 0 || s0 + ns > S.pl.nst) {
+    ctx->err = "run_steps: block step range outside the block sweep";
     return GHSVD_E_INVALID_ARG;
   }
   if (ctx->o.world_size > 1) {
@@ -324,7 +346,7 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
   const int tF = S.tF, tZ = S.tZ;
   cudaStream_t str = ctx->stream;
   const uint64_t pairs = (uint64_t)ctx->n * (ctx->n - 1) / 2;
-  const int nst = pl.nblk - 1;
+  const int nst = pl.nst;
   while ((int)ctx->grp_streams.size() < G) {
     cudaStream_t t;
     GH_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
@@ -349,7 +371,7 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
   for (int s = 0; s < nst; s++)
     for (int kk = pl.slot0; kk < pl.slot0 + pl.K; kk++) {
       long long bp, bq;
-      rr_pair(pl.nblk, s, kk, &bp, &bq);
+      blk_order_pair(a.ord, pl.nblk, pl.nsup, s, kk, &bp, &bq);
       const double kq = S.bw_h[bp] + S.bw_h[bq];
       fl_gram_sweep += 8.0 * kq * (kq + 1) * ctx->m;
     }
@@ -447,7 +469,7 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
   GH_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   st->seconds = ms * 1e-3;
   st->alg_flops = st->flops_gram + st->flops_update;
-  st->alg_bytes = (uint64_t)((double)st->sweeps * (pl.nblk - 1) * 16.0 * (double)ctx->n *
+  st->alg_bytes = (uint64_t)((double)st->sweeps * pl.nst * 16.0 * (double)ctx->n *
                              (2.0 * ctx->m + 2.0 * (2.0 * ctx->m + ctx->n)));
   return GHSVD_OK;
 }
@@ -465,7 +487,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     // (blk_sweep_groups; measured 1-2 % slower than the two-stream schedule below on
     // config 3, kept as an experiment)
     const int G = std::min(S.pl.K, ctx->o.groups);
-    if (!multi && G >= 2) return blk_sweep_groups(ctx, st, S, G);
+    if (!multi && G >= 2 && ctx->o.ordering == GHSVD_ORDER_ROUND_ROBIN) return blk_sweep_groups(ctx, st, S, G);
   }
   BlkPlan& pl = S.pl;
   BlkArgs a = S.a;
@@ -487,7 +509,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   // runs without a concurrent Z' update, so it must not be over-represented); with fewer
   // than 2 * TSTRIDE block steps every step is sampled
   int cur_sw = 0;
-  const int nst_all = pl.nblk - 1;
+  const int nst_all = pl.nst;
   auto sampled = [&](int s) {
     return timing && (tstride == 1 || nst_all < 2 * tstride || s % tstride == cur_sw % tstride);
   };
@@ -531,12 +553,19 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
     fp_st[1] = hs_st[1];
   }
   const int h_pair0[2] = {0, KA}, h_np[2] = {KA, pl.K - KA};
-  const int nst = pl.nblk - 1;
+  const int nst = pl.nst;
   std::vector<cudaEvent_t> ev_piv(2), ev_fg(2), ev_zdone(2), ev_gr(2), ev_bnd(2), tev;
   // GHSVD_SPLIT_BND=1 (experiment): split each half's F/G update into its boundary pair
   // and the rest, so half 0 of step s+1 may start while half 1 of step s still updates;
   // measured equal to the plain halves on config 3 (2.42 ms per block step either way)
-  const bool split_bnd = !multi && nh == 2 && KA >= 2 && pl.K - KA >= 2 && (ctx->o.schedule & GHSVD_SCHED_SPLIT_BND) != 0;
+  const bool split_bnd = !multi && nh == 2 && KA >= 2 && pl.K - KA >= 2 && (ctx->o.schedule & GHSVD_SCHED_SPLIT_BND) != 0 &&
+                         ctx->o.ordering == GHSVD_ORDER_ROUND_ROBIN;
+  // multi-GPU: does the exchange after step s move any block column?  (Inside an outer step
+  // of a Level-3 ordering with one super pair per rank nothing moves: no exchange, and the
+  // next step's Grams need not wait for this step's Z' update.)
+  std::vector<char> moves(nst, 0);
+  if (multi)
+    for (int s = 0; s < nst; s++) moves[s] = comm_step_moves(ctx, pl.nblk, s, (s + 1) % nst) ? 1 : 0;
   cudaEvent_t ev_x;
   GH_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
   for (int i = 0; i < 2; i++) {
@@ -569,7 +598,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   for (int s = 0; s < nst; s++)
     for (int kk = pl.slot0; kk < pl.slot0 + pl.K; kk++) {
       long long bp, bq;
-      rr_pair(pl.nblk, s, kk, &bp, &bq);
+      blk_order_pair(a.ord, pl.nblk, pl.nsup, s, kk, &bp, &bq);
       const double kq = bw_h[bp] + bw_h[bq];
       fl_gram[s] += 8.0 * kq * (kq + 1) * ctx->m;
     }
@@ -603,7 +632,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
         GH_CUDA(cudaStreamWaitEvent(hs_st[1], split_bnd ? ev_bnd[0] : ev_fg[0], 0));
       }
       // multi-GPU: the exchange after step s-1 (on str) precedes every Gram of step s
-      if (multi && s > 0)
+      if (multi && s > 0 && moves[s - 1])
         for (int h = 0; h < nh; h++)
           if (hs_st[h] != str) GH_CUDA(cudaStreamWaitEvent(hs_st[h], ev_x, 0));
       for (int h = 0; h < nh; h++) {
@@ -649,7 +678,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       launch_update(S, a, 0, pl.K, 2 * tF, 2 * tF + tZ, 0, aux);
       a.trace_id = s * TRACE_SLOTS + 9;
       if (a.W) launch_update(S, a, 0, pl.K, 0, tZ, 1, aux);
-      if (multi && xch_overlap) {
+      if (multi && xch_overlap && moves[s]) {
         // exchange_overlap = 1: the exchange after step s in two parts (NEXT-2, comm/compute
         // overlap): the Z', W block columns leave right after the Z' update, on the aux
         // stream and a second communicator, while the F, G block columns leave as soon as
@@ -666,7 +695,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
       }
       GH_CUDA(cudaEventRecord(ev_zdone[b], aux));
       GH_CUDA(cudaGetLastError());
-      if (multi) {
+      if (multi && moves[s]) {
         // default (exchange_overlap = 0): ONE communicator, one grouped exchange of the F, G,
         // Z' (and W) block columns on the context stream after every update of step s --
         // no two NCCL operations are ever in flight on different streams
@@ -779,7 +808,7 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   st->alg_flops = st->flops_gram + st->flops_update;
   // HBM bytes the blocked sweep must move per block step: Grams read F, G pairs once,
   // updates read + write F, G, Z pairs once
-  st->alg_bytes = (uint64_t)((double)st->sweeps * (pl.nblk - 1) / std::max(1, ctx->o.world_size) *
+  st->alg_bytes = (uint64_t)((double)st->sweeps * pl.nst / std::max(1, ctx->o.world_size) *
                              16.0 * (double)ctx->n * (2.0 * ctx->m + 2.0 * (2.0 * ctx->m + ctx->n)));
   return GHSVD_OK;
 }

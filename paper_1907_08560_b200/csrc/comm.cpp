@@ -23,60 +23,35 @@
 #include <vector>
 
 #include "internal.h"
+#include "ordering.h"
 
 namespace ghsvd {
 
 // ------------------------------------------------------------------ schedule
-// Round-robin pair of slot k in step s (same closed form as hz2x2.cuh rr_pair).
-static void rr(long long n, long long s, long long k, long long* p, long long* q) {
-  long long a, b;
-  if (k == 0) {
-    a = n - 1;
-    b = s;
-  } else {
-    const long long r = n - 1;
-    a = (s + k) % r;
-    b = ((s - k) % r + r) % r;
-  }
-  *p = a < b ? a : b;
-  *q = a < b ? b : a;
-}
-
-// owner[b] = rank owning block b in step s
-static void owners(int nblk, int world, int s, std::vector<int>& own) {
+// owner[b] = rank owning block b in step s of the block ordering (ordering.h)
+static void owners(int ord, int nsup, int nblk, int world, long long s, std::vector<int>& own) {
   own.assign(nblk, -1);
   const int K = nblk / 2 / world;
   for (int k = 0; k < nblk / 2; k++) {
     long long p, q;
-    rr(nblk, s, k, &p, &q);
+    blk_order_pair(ord, nblk, nsup, s, k, &p, &q);
     own[p] = own[q] = k / K;
   }
 }
 
-}  // namespace ghsvd
-
-extern "C" {
-
-// Rank owning block column b in block step s (nblk even, world | nblk/2).  -1 on bad args.
-int ghsvd_block_owner(int nblk, int world, int s, int b) {
-  if (nblk < 2 || (nblk & 1) || world < 1 || (nblk / 2) % world || s < 0 || s > nblk - 2 || b < 0 || b >= nblk)
-    return -1;
-  std::vector<int> own;
-  ghsvd::owners(nblk, world, s, own);
-  return own[b];
+static bool plan_args_ok(int ord, int nblk, int nsup, int world) {
+  return world >= 1 && blk_order_check(ord, nblk, nsup) == 0 && (nblk / 2) % world == 0;
 }
 
-// Exchange plan of `rank` between block steps s and s_next: blocks it sends
-// (send_blk[i] to send_peer[i]) and receives (recv_blk[i] from recv_peer[i]),
-// in increasing block order.  Arrays must hold nblk entries.  Returns 0 / -1.
-int ghsvd_exchange_plan(int nblk, int world, int rank, int s, int s_next, int64_t* send_blk, int64_t* send_peer,
-                        int64_t* nsend, int64_t* recv_blk, int64_t* recv_peer, int64_t* nrecv) {
-  if (nblk < 2 || (nblk & 1) || world < 1 || (nblk / 2) % world || rank < 0 || rank >= world || s < 0 ||
-      s > nblk - 2 || s_next < 0 || s_next > nblk - 2)
-    return -1;
+static int exchange_plan(int ord, int nblk, int nsup, int world, int rank, long long s, long long s_next,
+                         int64_t* send_blk, int64_t* send_peer, int64_t* nsend, int64_t* recv_blk,
+                         int64_t* recv_peer, int64_t* nrecv) {
+  if (!plan_args_ok(ord, nblk, nsup, world) || rank < 0 || rank >= world) return -1;
+  const long long nst = blk_order_steps(ord, nblk, nsup);
+  if (s < 0 || s >= nst || s_next < 0 || s_next >= nst) return -1;
   std::vector<int> o1, o2;
-  ghsvd::owners(nblk, world, s, o1);
-  ghsvd::owners(nblk, world, s_next, o2);
+  owners(ord, nsup, nblk, world, s, o1);
+  owners(ord, nsup, nblk, world, s_next, o2);
   int64_t ns = 0, nr = 0;
   for (int b = 0; b < nblk; b++) {
     if (o1[b] == rank && o2[b] != rank) {
@@ -93,6 +68,66 @@ int ghsvd_exchange_plan(int nblk, int world, int rank, int s, int s_next, int64_
   *nsend = ns;
   *nrecv = nr;
   return 0;
+}
+
+// true if some block column changes rank between steps s and s_next (the same on every rank)
+bool comm_step_moves(const Ctx* ctx, int nblk, long long s, long long s_next) {
+  const int world = ctx->o.world_size;
+  if (world <= 1) return false;
+  std::vector<int> o1, o2;
+  owners(ctx->o.ordering, ctx->blk_nsup, nblk, world, s, o1);
+  owners(ctx->o.ordering, ctx->blk_nsup, nblk, world, s_next, o2);
+  return o1 != o2;
+}
+
+}  // namespace ghsvd
+
+extern "C" {
+
+// Rank owning block column b in block step s (nblk even, world | nblk/2).  -1 on bad args.
+int ghsvd_block_owner(int nblk, int world, int s, int b) {
+  return ghsvd_block_owner_ord(GHSVD_ORDER_ROUND_ROBIN, nblk, 0, world, s, b);
+}
+
+// Exchange plan of `rank` between block steps s and s_next: blocks it sends
+// (send_blk[i] to send_peer[i]) and receives (recv_blk[i] from recv_peer[i]),
+// in increasing block order.  Arrays must hold nblk entries.  Returns 0 / -1.
+int ghsvd_exchange_plan(int nblk, int world, int rank, int s, int s_next, int64_t* send_blk, int64_t* send_peer,
+                        int64_t* nsend, int64_t* recv_blk, int64_t* recv_peer, int64_t* nrecv) {
+  return ghsvd::exchange_plan(GHSVD_ORDER_ROUND_ROBIN, nblk, 0, world, rank, s, s_next, send_blk, send_peer, nsend,
+                              recv_blk, recv_peer, nrecv);
+}
+
+int64_t ghsvd_order_steps(int ordering, int nblk, int nsup) {
+  if (ghsvd::blk_order_check(ordering, nblk, nsup)) return -1;
+  return ghsvd::blk_order_steps(ordering, nblk, nsup);
+}
+
+int ghsvd_order_pair(int ordering, int nblk, int nsup, int64_t s, int64_t k, int64_t* p, int64_t* q) {
+  if (ghsvd::blk_order_check(ordering, nblk, nsup) || s < 0 || s >= ghsvd::blk_order_steps(ordering, nblk, nsup) ||
+      k < 0 || k >= nblk / 2 || !p || !q)
+    return -1;
+  long long a, b;
+  ghsvd::blk_order_pair(ordering, nblk, nsup, s, k, &a, &b);
+  *p = a;
+  *q = b;
+  return 0;
+}
+
+int ghsvd_block_owner_ord(int ordering, int nblk, int nsup, int world, int64_t s, int b) {
+  if (!ghsvd::plan_args_ok(ordering, nblk, nsup, world) || s < 0 ||
+      s >= ghsvd::blk_order_steps(ordering, nblk, nsup) || b < 0 || b >= nblk)
+    return -1;
+  std::vector<int> own;
+  ghsvd::owners(ordering, nsup, nblk, world, s, own);
+  return own[b];
+}
+
+int ghsvd_exchange_plan_ord(int ordering, int nblk, int nsup, int world, int rank, int64_t s, int64_t s_next,
+                            int64_t* send_blk, int64_t* send_peer, int64_t* nsend, int64_t* recv_blk,
+                            int64_t* recv_peer, int64_t* nrecv) {
+  return ghsvd::exchange_plan(ordering, nblk, nsup, world, rank, s, s_next, send_blk, send_peer, nsend, recv_blk,
+                              recv_peer, nrecv);
 }
 
 }  // extern "C"
@@ -338,10 +373,12 @@ ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int*
     ctx->err = "multi-GPU: no communicator";
     return GHSVD_E_NCCL;
   }
+  // nothing moves on any rank (e.g. inside an outer step of a Level-3 ordering)
+  if (!comm_step_moves(ctx, nblk, s_now, s_next)) return GHSVD_OK;
   std::vector<int64_t> sb(nblk), sp(nblk), rb(nblk), rp(nblk);
   int64_t ns = 0, nr = 0;
-  if (ghsvd_exchange_plan(nblk, ctx->o.world_size, ctx->o.rank, s_now, s_next, sb.data(), sp.data(), &ns, rb.data(),
-                          rp.data(), &nr)) {
+  if (exchange_plan(ctx->o.ordering, nblk, ctx->blk_nsup, ctx->o.world_size, ctx->o.rank, s_now, s_next, sb.data(),
+                    sp.data(), &ns, rb.data(), rp.data(), &nr)) {
     ctx->err = "multi-GPU: bad exchange plan arguments";
     return GHSVD_E_INVALID_ARG;
   }
@@ -411,7 +448,7 @@ ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c) {
 // the final exchange of every sweep restores).
 void comm_owned_blocks(const Ctx* ctx, int nblk, std::vector<int>& blocks) {
   std::vector<int> own;
-  owners(nblk, ctx->o.world_size, 0, own);
+  owners(ctx->o.ordering, ctx->blk_nsup, nblk, ctx->o.world_size, 0, own);
   blocks.clear();
   for (int b = 0; b < nblk; b++)
     if (own[b] == ctx->o.rank) blocks.push_back(b);
@@ -427,7 +464,7 @@ ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const 
     return GHSVD_E_NCCL;
   }
   std::vector<int> own;
-  owners(nblk, ctx->o.world_size, 0, own);
+  owners(ctx->o.ordering, ctx->blk_nsup, nblk, ctx->o.world_size, 0, own);
   cudaStream_t st = ctx->stream;
   if (handle(ctx)->kind == 2) {
     // the sum of the disjointly owned outputs, as a gather from each column's owner

@@ -74,6 +74,7 @@ struct Ctx {
   cudaEvent_t ev0, ev1, ev2, ev3;
   // blocked partition of the last blocked sweep (host copies)
   std::vector<int> blk_start, blk_width;
+  int blk_nsup = 0;              // resolved super blocks of a LEVEL3 / HIER ordering (ordering.h)
   // multi-GPU
   void* comm;                    // ncclComm_t (opaque)
   void* cublas = nullptr;        // cublasHandle_t of the blocked Phase 2 (dlopen'ed cuBLAS), lazily
@@ -123,6 +124,7 @@ enum { XCH_FG = 1, XCH_ZW = 2 };   // parts of the block-column exchange
 ghsvd_status comm_exchange(Ctx* ctx, int nblk, int s_now, int s_next, const int* bstart, const int* bwidth, int part,
                            cudaStream_t st);
 ghsvd_status comm_allreduce_counters(Ctx* ctx, DevCounters* c);
+bool comm_step_moves(const Ctx* ctx, int nblk, long long s, long long s_next);
 void comm_owned_blocks(const Ctx* ctx, int nblk, std::vector<int>& blocks);
 ghsvd_status comm_finalize_outputs(Ctx* ctx, int nblk, const int* bstart, const int* bwidth, double* lam,
                                    double* sf, double* sg, double2* Zout, int64_t ldz, double2* Xout);

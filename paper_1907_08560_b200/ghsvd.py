@@ -35,7 +35,8 @@ EXPORTS = ["ghsvd_default_options", "ghsvd_workspace_bytes", "ghsvd_create", "gh
            "ghsvd_extract", "ghsvd_extract_local", "ghsvd_extract_x", "ghsvd_get_transformed", "ghsvd_get_state", "ghsvd_set_state",
            "ghsvd_hz2x2_batch", "ghsvd_last_error",
            "ghsvd_destroy", "ghsvd_version", "ghsvd_block_owner", "ghsvd_exchange_plan",
-           "ghsvd_nccl_unique_id"]
+           "ghsvd_nccl_unique_id", "ghsvd_order_steps", "ghsvd_order_pair", "ghsvd_block_owner_ord",
+           "ghsvd_exchange_plan_ord"]
 
 
 class GHSVDError(RuntimeError):
@@ -46,6 +47,8 @@ class GHSVDError(RuntimeError):
 
 SCHED_SERIAL, SCHED_NO_PRIO, SCHED_SPLIT_BND, SCHED_GRAM4M, SCHED_UPD4M, SCHED_PIVOT_CL = 1, 2, 4, 8, 16, 32
 SCHED_SPLIT_FACTOR = 64
+ORDER_ROUND_ROBIN, ORDER_LEVEL3, ORDER_HIER = 0, 1, 2
+ORDERINGS = {"rr": ORDER_ROUND_ROBIN, "level3": ORDER_LEVEL3, "hier": ORDER_HIER}
 
 
 class Options(ctypes.Structure):
@@ -56,7 +59,7 @@ class Options(ctypes.Structure):
                 ("threads", ctypes.c_int), ("use_graph", ctypes.c_int), ("kernel", ctypes.c_int),
                 ("detail_timing", ctypes.c_int), ("want_x", ctypes.c_int), ("exchange_overlap", ctypes.c_int),
                 ("schedule", ctypes.c_int), ("groups", ctypes.c_int), ("gram_splits", ctypes.c_int),
-                ("trace_path", ctypes.c_char_p)]
+                ("trace_path", ctypes.c_char_p), ("super_blocks", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -129,6 +132,11 @@ def load():
     L.ghsvd_version.restype = ctypes.c_char_p
     L.ghsvd_block_owner.argtypes = [Ci, Ci, Ci, Ci]
     L.ghsvd_exchange_plan.argtypes = [Ci, Ci, Ci, Ci, Ci, P, P, P, P, P, P]
+    L.ghsvd_order_steps.argtypes = [Ci, Ci, Ci]
+    L.ghsvd_order_steps.restype = I64
+    L.ghsvd_order_pair.argtypes = [Ci, Ci, Ci, I64, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+    L.ghsvd_block_owner_ord.argtypes = [Ci, Ci, Ci, Ci, I64, Ci]
+    L.ghsvd_exchange_plan_ord.argtypes = [Ci, Ci, Ci, Ci, Ci, I64, I64, P, P, P, P, P, P]
     L.ghsvd_nccl_unique_id.argtypes = [P]
     for f in ("ghsvd_create", "ghsvd_factor", "ghsvd_set_factors", "ghsvd_reduce", "ghsvd_get_factors",
               "ghsvd_sweep", "ghsvd_run_steps", "ghsvd_extract", "ghsvd_extract_local", "ghsvd_get_transformed",
@@ -184,7 +192,7 @@ class Context:
                  cluster: int = 0, threads: int = 0, use_graph: bool = True, kernel: int = 0,
                  detail_timing=False, want_x: bool = False, exchange_overlap: bool = False,
                  schedule: Optional[int] = None, groups: Optional[int] = None, gram_splits: Optional[int] = None,
-                 trace_path: Optional[str] = None):
+                 trace_path: Optional[str] = None, ordering="rr", super_blocks: int = 0):
         import torch
         L = load()
         self._L = L
@@ -202,6 +210,8 @@ class Context:
             o.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         o.variant = VARIANTS[variant] if isinstance(variant, str) else int(variant)
         o.nblocks = nblocks
+        o.ordering = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
+        o.super_blocks = super_blocks
         o.max_sweeps = max_sweeps
         o.criterion = CRITERIA[criterion] if isinstance(criterion, str) else int(criterion)
         o.eps = eps
@@ -432,14 +442,36 @@ def block_owner(nblk: int, world: int, s: int, b: int) -> int:
     return load().ghsvd_block_owner(nblk, world, s, b)
 
 
-def exchange_plan(nblk: int, world: int, rank: int, s: int, s_next: int):
+def order_steps(ordering, nblk: int, nsup: int = 0) -> int:
+    """Block steps per sweep of a block ordering (csrc/ordering.h); -1 on bad arguments."""
+    o = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
+    return int(load().ghsvd_order_steps(o, nblk, nsup))
+
+
+def order_pair(ordering, nblk: int, nsup: int, s: int, k: int):
+    """Block pair (p < q) of slot k in block step s (csrc/ordering.h)."""
+    o = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
+    p, q = ctypes.c_int64(), ctypes.c_int64()
+    if load().ghsvd_order_pair(o, nblk, nsup, s, k, ctypes.byref(p), ctypes.byref(q)) != 0:
+        raise GHSVDError(-1, "order_pair: bad arguments")
+    return p.value, q.value
+
+
+def block_owner_ord(ordering, nblk: int, nsup: int, world: int, s: int, b: int) -> int:
+    o = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
+    return load().ghsvd_block_owner_ord(o, nblk, nsup, world, s, b)
+
+
+def exchange_plan(nblk: int, world: int, rank: int, s: int, s_next: int, ordering="rr", nsup: int = 0):
     """-> (sends [(block, peer)], recvs [(block, peer)]) between block steps s and s_next."""
     L = load()
+    o = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
     arr = [np.zeros(nblk, np.int64) for _ in range(4)]
     ns, nr = ctypes.c_int64(), ctypes.c_int64()
-    rc = L.ghsvd_exchange_plan(nblk, world, rank, s, s_next, *[a.ctypes.data_as(ctypes.c_void_p) for a in arr[:2]],
-                               ctypes.byref(ns), *[a.ctypes.data_as(ctypes.c_void_p) for a in arr[2:]],
-                               ctypes.byref(nr))
+    rc = L.ghsvd_exchange_plan_ord(o, nblk, nsup, world, rank, s, s_next,
+                                   *[a.ctypes.data_as(ctypes.c_void_p) for a in arr[:2]],
+                                   ctypes.byref(ns), *[a.ctypes.data_as(ctypes.c_void_p) for a in arr[2:]],
+                                   ctypes.byref(nr))
     if rc != 0:
         raise GHSVDError(-1, "exchange_plan: bad arguments")
     sends = list(zip(arr[0][:ns.value].tolist(), arr[1][:ns.value].tolist()))

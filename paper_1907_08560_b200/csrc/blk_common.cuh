@@ -57,6 +57,7 @@ struct BlkArgs {
   long long ldm, ldn, m, n, npos;
   int nblk, s, slot0, npairs;
   int ord, nsup;            // block ordering (ordering.h) and its super blocks
+  const int4* ptab;         // [block step][global slot] = (start p, width p, start q, width q)
   int pair0;                // first local pair handled by this launch (blockIdx.x offset)
   const int* bstart;
   const int* bwidth;
@@ -97,12 +98,12 @@ __device__ __forceinline__ void trace_end(const BlkArgs& a) {
 }
 
 __device__ __forceinline__ void pair_cols(const BlkArgs& a, int pl, int& c0p, int& wp, int& c0q, int& wq) {
-  long long bp, bq;
-  blk_order_pair(a.ord, a.nblk, a.nsup, a.s, a.slot0 + pl, &bp, &bq);
-  c0p = a.bstart[bp];
-  wp = a.bwidth[bp];
-  c0q = a.bstart[bq];
-  wq = a.bwidth[bq];
+  // the block pair of this slot and step, tabulated on the host from the ordering (ordering.h)
+  const int4 t = __ldg(&a.ptab[(size_t)a.s * (a.nblk / 2) + a.slot0 + pl]);
+  c0p = t.x;
+  wp = t.y;
+  c0q = t.z;
+  wq = t.w;
 }
 
 // global column of pivot column c (c < wp: block p, else block q), -1 if padding

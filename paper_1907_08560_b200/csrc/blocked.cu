@@ -30,6 +30,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -47,6 +48,8 @@ namespace {
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
+int resolve_nsup(const ghsvd_options* o);
+
 // tuning knobs (experiments only; defaults are the measured best)
 int auto_nblk(int64_t n, const ghsvd_options* o) {
   if (o->nblocks > 0) return o->nblocks;
@@ -54,6 +57,11 @@ int auto_nblk(int64_t n, const ghsvd_options* o) {
   nb += nb & 1;
   const int64_t P = std::max(1, o->world_size);
   nb = round_up(nb, 2 * P);
+  // Level-3 orderings: whole super blocks (HIER: an even number of block columns in each)
+  const int64_t ns = resolve_nsup(o);
+  if (o->ordering == GHSVD_ORDER_LEVEL3) nb = round_up(nb, std::lcm<int64_t>(2 * P, std::max<int64_t>(2, ns)));
+  if (o->ordering == GHSVD_ORDER_HIER) nb = round_up(nb, std::lcm<int64_t>(2 * P, 2 * std::max<int64_t>(2, ns)));
+  if (o->ordering != GHSVD_ORDER_ROUND_ROBIN && nb > n) nb = n - (n & 1);
   return (int)std::max<int64_t>(2, nb);
 }
 
@@ -121,7 +129,7 @@ static size_t blk_scratch_for(int64_t K, int64_t nb, bool want_x) {
          al256((size_t)2 * K * 4) + 2 * al256((size_t)(nb + 2) * 4) + 2 * al256((size_t)K * KM * KM * 16) +
          al256((size_t)K * KM) + al256((size_t)2 * K * 4) + (want_x ? al256((size_t)2 * K * KM * KM * 16) : 0) +
          al256((size_t)(2 * nb + 2) * TRACE_SLOTS * 16) + al256((size_t)2 * K * 4) + al256((size_t)(2 * nb + 2) * 8) +
-         4096;
+         al256((size_t)(2 * nb + 2) * (nb / 2) * 16) + 4096;
 }
 
 // workspace bound at ghsvd_create for factors of up to n columns: the sweep may see
@@ -190,6 +198,7 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   // step-indexed arrays: a sweep has at most 2 nblk block steps (LEVEL3: (2Q-1)(2B-1) < 4QB)
   S.trace_buf = (unsigned long long*)p; p += al256((size_t)(2 * pl.nblk + 2) * TRACE_SLOTS * 16);
   a.upd_k2 = (unsigned long long*)p; p += al256((size_t)(2 * pl.nblk + 2) * 8);
+  int4* ptab = (int4*)p; p += al256((size_t)(2 * pl.nblk + 2) * (pl.nblk / 2) * 16);
   a.trace = nullptr;
   a.trace_id = 0;
   k_blk_partition<<<1, 32, 0, str>>>(bstart, bwidth, pl.nblk, ctx->n);
@@ -203,6 +212,19 @@ static ghsvd_status blk_setup(Ctx* ctx, BlkSetup& S) {
   GH_CUDA(cudaStreamSynchronize(str));
   ctx->blk_start = S.bs_h;
   ctx->blk_width = S.bw_h;
+  {
+    // pair table of the whole block sweep: the kernels read their block pair from it
+    std::vector<int4> t((size_t)pl.nst * (pl.nblk / 2));
+    for (int s = 0; s < pl.nst; s++)
+      for (int k = 0; k < pl.nblk / 2; k++) {
+        long long bp, bq;
+        blk_order_pair(ctx->o.ordering, pl.nblk, pl.nsup, s, k, &bp, &bq);
+        t[(size_t)s * (pl.nblk / 2) + k] = make_int4(S.bs_h[bp], S.bw_h[bp], S.bs_h[bq], S.bw_h[bq]);
+      }
+    GH_CUDA(cudaMemcpyAsync(ptab, t.data(), t.size() * sizeof(int4), cudaMemcpyHostToDevice, str));
+    GH_CUDA(cudaStreamSynchronize(str));
+  }
+  a.ptab = ptab;
   a.F = ctx->F;
   a.G = ctx->G;
   a.Z = ctx->Z;

@@ -32,23 +32,44 @@ def exchange_stats(ordering, nblk, nsup, world, m, n):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--runs", nargs="+", default=["rr_0", "level3_4", "hier_4", "level3_8", "hier_8"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--reduce", action="store_true", help="Phase 2 before the sweep (configs 2, 6)")
     ap.add_argument("--out", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                   "profiles", "r02", "level3_c3.json"))
     args = ap.parse_args()
     build.build()
     warnings.simplefilter("ignore")
     import numpy as np
-    kind, at = inputs.make_config(3, backend="torch")
-    NA, NL, NG = at.A.shape
-    m, n = 2 * NA * NL, NG
-    res = {"config": "c3_illcond_4096", "m": m, "n": n, "nblk": 128, "runs": {}, "exchange_plans": {}}
+    kind, at = inputs.make_config(args.config, backend="torch" if args.config == 3 else "numpy")
+    if kind == "atoms":
+        NA, NL, NG = at.A.shape
+        m, n = 2 * NA * NL, NG
+    else:
+        (m, n), NL = at.F.shape, 0
+    import math
+
+    def auto_nblk(ordering, nsup):   # the library's auto partition (blocked.cu auto_nblk), one GPU
+        nb = (n + (n & 1) + 31) // 32
+        nb += nb & 1
+        if ordering != "rr":
+            L = math.lcm(2, nsup if ordering == "level3" else 2 * nsup)
+            nb = -(-nb // L) * L
+        return nb
+    nblk = auto_nblk("rr", 0)
+    res = {"config": inputs.CONFIGS[args.config]["name"], "m": m, "n": n, "nblk": nblk, "reduce": args.reduce,
+           "runs": {}, "exchange_plans": {}}
     lam_rr = None
     for run in args.runs:
         ordering, _, ns = run.partition("_")
         nsup = int(ns)
         ctx = ghsvd.Context(m, n, NL, variant="bo", max_sweeps=64, ordering=ordering, super_blocks=nsup,
                             detail_timing=2)
-        ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+        if kind == "atoms":
+            ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+        else:
+            ctx.set_factors(at.F, at.J, at.G)
+        if args.reduce:
+            ctx.reduce()
         st = ctx.sweep()
         lam, *_ = ctx.extract(want_z=False)
         ctx.close()
@@ -56,8 +77,9 @@ def main():
         if lam_rr is None and ordering == "rr":
             lam_rr = lam
         d = float(np.max(np.abs(lam - lam_rr) / np.abs(lam_rr))) if lam_rr is not None else None
-        nst = ghsvd.order_steps(ordering, 128, nsup)
-        res["runs"][run] = {"ordering": ordering, "super_blocks": nsup, "sweeps": st["sweeps"],
+        nb = auto_nblk(ordering, nsup)
+        nst = ghsvd.order_steps(ordering, nb, nsup)
+        res["runs"][run] = {"ordering": ordering, "super_blocks": nsup, "nblk": nb, "sweeps": st["sweeps"],
                             "converged": st["converged"], "seconds": st["seconds"],
                             "steps_per_sweep": nst, "block_steps": nst * st["sweeps"],
                             "ms_per_block_step": 1e3 * st["seconds"] / (nst * st["sweeps"]),
@@ -67,7 +89,8 @@ def main():
     for world in (2, 4, 8):
         for ordering in ("rr", "level3", "hier"):
             nsup = 0 if ordering == "rr" else 2 * world
-            res["exchange_plans"][f"{ordering}_P{world}"] = exchange_stats(ordering, 128, nsup, world, m, n)
+            nb = -(-nblk // (4 * world)) * 4 * world
+            res["exchange_plans"][f"{ordering}_P{world}"] = exchange_stats(ordering, nb, nsup, world, m, n)
     print(json.dumps(res["exchange_plans"], indent=1))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(res, open(args.out, "w"), indent=1)

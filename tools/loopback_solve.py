@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--max-sweeps", type=int, default=64)
     ap.add_argument("--overlap", type=int, default=0, help="exchange_overlap of the P-rank run (0: one grouped exchange)")
+    ap.add_argument("--ordering", default="rr", help="rr | level3 | hier (block ordering, csrc/ordering.h)")
+    ap.add_argument("--super-blocks", type=int, default=0, help="super blocks of level3 / hier (0: 2 * world)")
     args = ap.parse_args()
     import torch
     from paper_1907_08560_b200 import build, ghsvd, inputs
@@ -34,10 +36,13 @@ def main():
     assert kind == "atoms"
     NA, NL, NG = at.A.shape
     m, n = 2 * NA * NL, NG
+    # the SAME ordering and super blocks on one rank and on P ranks (bitwise comparison)
+    nsup = 0 if args.ordering == "rr" else (args.super_blocks or 2 * args.world)
 
     def make(world, rank, lid, stream):
         c = ghsvd.Context(m, n, NL, variant="bo", max_sweeps=args.max_sweeps, world_size=world, rank=rank,
-                          nccl_id=lid, stream=stream, exchange_overlap=bool(args.overlap) and world > 1)
+                          nccl_id=lid, stream=stream, exchange_overlap=bool(args.overlap) and world > 1,
+                          ordering=args.ordering, super_blocks=nsup)
         c.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
         return c
 
@@ -51,7 +56,7 @@ def main():
     del c
     torch.cuda.empty_cache()
     # P ranks
-    lid = ghsvd.loopback_id(f"cfg{args.config}_w{args.world}_x{args.overlap}")
+    lid = ghsvd.loopback_id(f"cfg{args.config}_w{args.world}_x{args.overlap}_{args.ordering}")
     ctxs = [make(args.world, r, lid, torch.cuda.Stream()) for r in range(args.world)]
     res, errs = [None] * args.world, []
 
@@ -73,7 +78,8 @@ def main():
         c.close()
     ok = not errs and all(r is not None and r[0]["sweeps"] == st1["sweeps"] and np.array_equal(r[1], lam1)
                           for r in res)
-    out = {"config": args.config, "m": m, "n": n, "world": args.world, "exchange_overlap": args.overlap, "one_rank": {
+    out = {"config": args.config, "m": m, "n": n, "world": args.world, "exchange_overlap": args.overlap,
+           "ordering": args.ordering, "super_blocks": nsup, "one_rank": {
         "sweeps": st1["sweeps"], "converged": st1["converged"], "sweep_seconds": st1["seconds"], "wall_s": t1},
         "loopback": {"per_rank_sweep_seconds": [r[0]["seconds"] for r in res if r], "wall_s": tP,
                      "sweeps": [r[0]["sweeps"] for r in res if r], "errors": errs},

@@ -399,9 +399,14 @@ def run_ours(args):
             idt.copy_(torch.frombuffer(bytearray(ghsvd.nccl_unique_id()), dtype=torch.uint8))
         torch.distributed.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
+    # block ordering (blocked variants; DESIGN.md 6 "Level-3 orderings", reading R2-5): HIER by
+    # default -- each block pair once per sweep grouped by super pair, 2P - 1 exchanges per
+    # sweep on P GPUs; --ordering rr is the paper's round-robin (reading C-11)
+    ordering = args.ordering if blocked else "rr"
     ctx = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=args.max_sweeps,
                         cluster=args.cluster, threads=args.threads, nblocks=args.nblocks, world_size=ws,
-                        rank=rank, nccl_id=nccl_id, detail_timing=2 if blocked else 0, want_x=args.want_x)
+                        rank=rank, nccl_id=nccl_id, detail_timing=2 if blocked else 0, want_x=args.want_x,
+                        ordering=ordering, super_blocks=args.super_blocks)
     phase1_s = None
     phase2_s = None
     with torch.cuda.stream(stream):
@@ -506,7 +511,8 @@ def run_ours(args):
         iso = None
         if ws == 1:
             cp = ghsvd.Context(m, n, nl, variant=args.variant, device=local, stream=stream, max_sweeps=1,
-                               nblocks=args.nblocks, detail_timing=True, schedule=ghsvd.SCHED_SERIAL)
+                               nblocks=args.nblocks, detail_timing=True, schedule=ghsvd.SCHED_SERIAL,
+                               ordering=ordering, super_blocks=args.super_blocks)
             with torch.cuda.stream(stream), warnings.catch_warnings():
                 warnings.simplefilter("ignore")   # one-sweep probe: "not converged" is expected
                 cp.set_factors(Fh, Jh, Gh)
@@ -573,6 +579,9 @@ def run_ours(args):
         "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant, "max_sweeps": args.max_sweeps,
+                   "ordering": ordering if blocked else "round-robin (pointwise)",
+                   "super_blocks": (args.super_blocks or (2 * ws if ws > 1 else 4)) if blocked and ordering != "rr"
+                   else None,
                    "want_x": bool(args.want_x),
                    "l2": f"inputs ({2 * mb * nb * 16 / 1e9:.2f} GB) vs L2 126 MB",
                    "phase2": ("column-pivoted QR of G P2 (--reduce colpiv, PAPER.md:925-943)" if args.reduce == "colpiv"
@@ -616,6 +625,9 @@ def main():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--nblocks", type=int, default=0)
+    ap.add_argument("--ordering", default="hier", choices=["hier", "rr", "level3"],
+                    help="block ordering of the blocked variants (DESIGN.md 6, reading R2-5)")
+    ap.add_argument("--super-blocks", type=int, default=0, help="super blocks of hier / level3 (0: 2 N, 4 on one GPU)")
     ap.add_argument("--max-sweeps", type=int, default=64,
                     help="C_max; config 3 (S condition 1e12) needs ~36 sweeps, beyond the paper's usual 30")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -207,16 +207,26 @@ ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* 
  * BLOCKED (NEXT-4, the paper's "blocking and delaying the columns updates",
  * PAPER.md:1271-1275): left-looking panels of <= 33 reflectors in the compact form
  * I + S T S^* J, the trailing columns updated once per panel by two ZGEMMs (cuBLAS,
- * loaded at run time), pivot searches on downdated J-norms / norms (exact at every
- * panel start; a panel is cut when a formed pivot column disagrees with its estimate).
+ * loaded at run time).  The JQR's pivots are PLANNED on the J-Grammian H = F^* J F (formed
+ * once by ZGEMM, its Schur complements updated per pivot): the paper's diagonal + partial
+ * pivoting rule applied to H_k instead of to the columns (equal in exact arithmetic), each
+ * planned pivot checked on the exact J-Grammian of its formed column(s) before use; the
+ * first one off by more than a quarter (or of another inertia) hands over to the column
+ * search.  GHSVD_REDUCE_COLSEARCH: the column search throughout (pivot searches on
+ * downdated J-norms, exact at every panel start; a panel is cut when a formed pivot column
+ * disagrees with its estimate).  The QR of G P2 searches its column-pivoted form likewise.
  * The pivot sequence may differ from the unblocked one on near-ties; the Grammians and
  * the pencil are preserved alike (tests).  GHSVD_REDUCE_UNBLOCKED: one reflector
  * application per column (round 1), also the fallback when cuBLAS cannot be loaded or
  * the n x n output-Z buffer cannot hold the panel (m > ~n^2 / 35).
  * Errors: GHSVD_E_RANK_DEFICIENT on a degenerate JQR pivot or rank-deficient G;
  * GHSVD_E_NONFINITE on non-finite J-norms; INVALID_ARG on unknown flags. */
-enum { GHSVD_REDUCE_COLPIV = 1, GHSVD_REDUCE_UNBLOCKED = 2, GHSVD_REDUCE_BLOCKED = 4 };
+enum { GHSVD_REDUCE_COLPIV = 1, GHSVD_REDUCE_UNBLOCKED = 2, GHSVD_REDUCE_BLOCKED = 4, GHSVD_REDUCE_COLSEARCH = 8 };
 ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
+/* After a blocked ghsvd_reduce with planned JQR pivots: the first column whose planned pivot
+ * the exact J-Grammian rejected (the column search continued from there), or -1 (every
+ * planned pivot used, or no planned JQR ran).  No GPU work. */
+int64_t ghsvd_reduce_fallback_col(ghsvd_ctx ctx);
 
 /* Export the factors the sweep will start from (after factor/set_factors,
  * the J row sort, [reduce] and bordering): *m, *n (bordered sizes); F, G

@@ -297,6 +297,8 @@ ghsvd_status ghsvd_factor(ghsvd_ctx h, int64_t NA, int64_t NL, int64_t NG, const
   return GHSVD_OK;
 }
 
+int64_t ghsvd_reduce_fallback_col(ghsvd_ctx h) { return h ? h->c.p2_fallback_col : -1; }
+
 ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
   if (!h) return GHSVD_E_INVALID_ARG;
   Ctx* ctx = &h->c;
@@ -304,7 +306,7 @@ ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
     ctx->err = "reduce: must follow factor/set_factors (once) and precede sweep";
     return GHSVD_E_STATE;
   }
-  if ((flags & ~(GHSVD_REDUCE_COLPIV | GHSVD_REDUCE_UNBLOCKED | GHSVD_REDUCE_BLOCKED)) ||
+  if ((flags & ~(GHSVD_REDUCE_COLPIV | GHSVD_REDUCE_UNBLOCKED | GHSVD_REDUCE_BLOCKED | GHSVD_REDUCE_COLSEARCH)) ||
       ((flags & GHSVD_REDUCE_UNBLOCKED) && (flags & GHSVD_REDUCE_BLOCKED))) {
     ctx->err = "reduce: unknown flags";
     return GHSVD_E_INVALID_ARG;
@@ -315,6 +317,7 @@ ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
   // redone by the next prepare()
   ctx->m = ctx->m_user;
   ctx->n = ctx->n_user;
+  ctx->p2_fallback_col = -1;
   TRY(phase2_reduce(ctx, flags));
   ctx->have_p2 = true;
   ctx->bordered = false;

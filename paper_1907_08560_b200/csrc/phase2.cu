@@ -15,7 +15,9 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -707,11 +709,281 @@ __global__ void k_qr_rout(const double2* X, long long ld, double2* out, long lon
   }
 }
 
+// ------------------------------------------------ pivot plan from the J-Grammian (JQR)
+// The JQR's diagonal + partial (Bunch-Kaufman) pivot decisions (Sec 5.2.1) read only the
+// J-Grammian of the unreduced columns, H_k = F_k^* J_k F_k, which after each reduction step
+// is the Schur complement of the previous one (a hyperbolic reflector leaves the trailing
+// columns' J-products unchanged on the rows it keeps; the removed row carries exactly
+// h_j1 h_11^{-1} h_1l, or the 2x2 analogue).  So the whole pivot sequence can be chosen
+// first, on H = F^* J F formed once (two ZGEMMs, O(m n^2)) and reduced by symmetric rank-1
+// / rank-2 Schur updates (O(n^3)) -- the "complete" use of H that PAPER.md:984-990 rules
+// out only for its O(m^2 n^2) cost when recomputed from F each step -- after which the
+// JQR needs no per-column pass over the trailing columns.  Every planned pivot is checked
+// against the exact J-Grammian of its formed column(s) before it is used (jqr_planned).
+// H is kept in the lower triangle of the trailing block (column-major, ld).
+struct BkPlan {
+  int* type;       // [n] 1, 2 (first column of a 2x2 pivot) or 0 (its second column)
+  long long* sw1;  // [n] diagonal-pivot swap partner of position k
+  long long* sw2;  // [n] second swap partner (Bunch-Kaufman), -1 if none
+  int* sw2pos;     // [n] position (k or k + 1) the second swap moves into
+  double2* d;      // [3 n] predicted H_kk, H_{k+1,k}, H_{k+1,k+1} at the pivot
+  int* st;         // [0] next k, [2] k of the last step, [3] its type (0: none), [4] error
+};
+
+__device__ __forceinline__ double2 hget(const double2* H, long long ld, long long j, long long l) {
+  return j >= l ? H[j + l * ld] : cconj(H[l + j * ld]);
+}
+
+// symmetric interchange of indices a < b of the trailing Hermitian block [k, n) (lower storage)
+__device__ void hswap(double2* H, long long ld, long long n, long long k, long long a, long long b) {
+  if (a == b) return;
+  if (a > b) { const long long t = a; a = b; b = t; }
+  for (long long l = k + threadIdx.x; l < a; l += blockDim.x) {
+    const double2 t = H[a + l * ld]; H[a + l * ld] = H[b + l * ld]; H[b + l * ld] = t;
+  }
+  for (long long j = a + 1 + threadIdx.x; j < b; j += blockDim.x) {
+    const double2 t = H[j + a * ld]; H[j + a * ld] = cconj(H[b + j * ld]); H[b + j * ld] = cconj(t);
+  }
+  for (long long j = b + 1 + threadIdx.x; j < n; j += blockDim.x) {
+    const double2 t = H[j + a * ld]; H[j + a * ld] = H[j + b * ld]; H[j + b * ld] = t;
+  }
+  if (threadIdx.x == 0) {
+    const double2 t = H[a + a * ld]; H[a + a * ld] = H[b + b * ld]; H[b + b * ld] = t;
+    H[b + a * ld] = cconj(H[b + a * ld]);
+  }
+  __syncthreads();
+}
+
+// One pivot decision at k = st[0] (no-op once k >= n): exactly the rule of k_piv_a / k_piv_b /
+// k_piv_c on the Schur complement instead of on the columns.
+__global__ void __launch_bounds__(T2) k_bk_select(double2* H, long long ld, long long n, BkPlan pl) {
+  const long long k = pl.st[0];
+  if (k >= n) {
+    if (threadIdx.x == 0) pl.st[3] = 0;
+    return;
+  }
+  constexpr long long NONE = 0x7fffffffffffffffll;
+  double v = -1.0;
+  long long jm = NONE;
+  for (long long j = k + threadIdx.x; j < n; j += T2) {
+    const double a = fabs(H[j + j * ld].x);
+    if (a > v) { v = a; jm = j; }
+  }
+  block_argmax(v, jm);
+  if (jm == NONE) {   // NaN diagonal
+    if (threadIdx.x == 0 && pl.st[4] == 0) pl.st[4] = -8;
+    jm = k;
+  }
+  hswap(H, ld, n, k, k, jm);
+  int type = 1;
+  long long s2 = -1;
+  int s2pos = -1;
+  if (k < n - 1) {
+    double h1i = -1.0;
+    long long ii = NONE;
+    for (long long j = k + 1 + threadIdx.x; j < n; j += T2) {
+      const double a = cabs_(H[j + k * ld]);
+      if (a > h1i) { h1i = a; ii = j; }
+    }
+    block_argmax(h1i, ii);
+    if (ii == NONE) ii = k + 1;
+    const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+    const double h11 = fabs(H[k + k * ld].x);
+    if (!(h11 >= alpha * h1i)) {
+      double hij = -1.0;
+      long long li = NONE;
+      for (long long l = k + threadIdx.x; l < n; l += T2) {
+        if (l == ii) continue;
+        const double a = cabs_(hget(H, ld, ii, l));
+        if (a > hij) { hij = a; li = l; }
+      }
+      block_argmax(hij, li);
+      if (h11 * hij >= alpha * h1i * h1i) {
+        type = 1;
+      } else if (fabs(H[ii + ii * ld].x) >= alpha * hij) {
+        s2 = ii; s2pos = 0;
+        hswap(H, ld, n, k, k, ii);
+      } else {
+        type = 2;
+        s2 = ii; s2pos = 1;
+        hswap(H, ld, n, k, k + 1, ii);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    pl.type[k] = type;
+    pl.sw1[k] = jm;
+    pl.sw2[k] = s2;
+    pl.sw2pos[k] = s2pos;
+    pl.d[3 * k] = H[k + k * ld];
+    if (type == 2) {
+      pl.d[3 * k + 1] = H[k + 1 + k * ld];
+      pl.d[3 * k + 2] = H[k + 1 + (k + 1) * ld];
+      pl.type[k + 1] = 0;
+    }
+    pl.st[2] = (int)k;
+    pl.st[3] = type;
+    pl.st[0] = (int)(k + type);
+  }
+}
+
+// Schur update of the trailing block after the step recorded in st: lower triangle of
+// [k + t, n)^2 minus H_{:,p} D^{-1} H_{p,:}, p the pivot index(es).  32 x 32 tiles.
+__global__ void __launch_bounds__(256) k_bk_update(double2* H, long long ld, long long n, BkPlan pl) {
+  const int t = pl.st[3];
+  if (t == 0 || blockIdx.y > blockIdx.x) return;
+  const long long k = pl.st[2], b0 = k + t;
+  const long long j0 = b0 + 32LL * blockIdx.x, l0 = b0 + 32LL * blockIdx.y;
+  if (j0 >= n) return;
+  __shared__ double2 vj[32][2], ul[32][2];
+  const int tid = threadIdx.x;
+  if (tid < 64) {
+    const int r = tid & 31;
+    const bool rows = tid < 32;
+    const long long x = (rows ? j0 : l0) + r;
+    double2 u0 = cmk(0, 0), u1 = cmk(0, 0);
+    if (x < n) {
+      u0 = H[x + k * ld];
+      if (t == 2) u1 = H[x + (k + 1) * ld];
+    }
+    if (rows) {
+      if (t == 1) {
+        const double d = H[k + k * ld].x;
+        vj[r][0] = cmk(u0.x / d, u0.y / d);
+        vj[r][1] = cmk(0, 0);
+      } else {
+        const double a = H[k + k * ld].x, c = H[k + 1 + (k + 1) * ld].x;
+        const double2 b = H[k + 1 + k * ld];
+        const double det = a * c - (b.x * b.x + b.y * b.y);
+        // v = u D^{-1}, D = [[a, conj b], [b, c]]
+        const double2 v0 = cadd(cmk(u0.x * c, u0.y * c), cmul(u1, cmk(-b.x, -b.y)));
+        const double2 v1 = cadd(cmul(u0, cmk(-b.x, b.y)), cmk(u1.x * a, u1.y * a));
+        vj[r][0] = cmk(v0.x / det, v0.y / det);
+        vj[r][1] = cmk(v1.x / det, v1.y / det);
+      }
+    } else {
+      ul[r][0] = u0;
+      ul[r][1] = u1;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < 32 * 32; e += 256) {
+    const int r = e & 31, c = e >> 5;
+    const long long j = j0 + r, l = l0 + c;
+    if (j >= n || l >= n || l > j) continue;
+    double2 a = cmul(vj[r][0], cconj(ul[c][0]));
+    if (t == 2) a = cadd(a, cmul(vj[r][1], cconj(ul[c][1])));
+    double2& h = H[j + l * ld];
+    h = cmk(h.x - a.x, h.y - a.y);
+    if (j == l) h.y = 0.0;   // the diagonal stays real
+  }
+}
+
+// The planned column interchanges of position k: F columns (all m rows) and p2
+__global__ void k_plan_swaps(double2* F, long long ld, long long m, long long k, long long* p2, BkPlan pl) {
+  const long long a = pl.sw1[k];
+  const long long b = pl.sw2[k];
+  const long long bp = k + pl.sw2pos[k];
+  for (int pass = 0; pass < 2; pass++) {
+    const long long x = pass == 0 ? k : bp, y = pass == 0 ? a : b;
+    if (pass == 1 && b < 0) break;
+    if (x == y) continue;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+      const double2 t = F[i + x * ld]; F[i + x * ld] = F[i + y * ld]; F[i + y * ld] = t;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const long long t = p2[x]; p2[x] = p2[y]; p2[y] = t;
+    }
+    __syncthreads();   // (the passes touch different column pairs; grid-wide order comes from
+                       // each element being swapped by the same thread in both passes)
+  }
+}
+
+// Check a planned pivot against the exact J-Grammian of its formed column(s) fx (, fx2),
+// rows >= k: ctl[5] = 1 when it is off by more than a quarter (or changes sign / inertia).
+__global__ void __launch_bounds__(T2) k_plan_check(const double2* fx, const double2* fx2, const int8_t* J,
+                                                   long long k, long long m, int type, BkPlan pl, P2Scr s) {
+  __shared__ double2 sh[T2 / 32];
+  const double a = jdot(fx, fx, J, k, m, true, sh).x;
+  double c = 0.0;
+  double2 b = cmk(0, 0);
+  if (type == 2) {
+    c = jdot(fx2, fx2, J, k, m, true, sh).x;
+    b = jdot(fx2, fx, J, k, m, true, sh);   // H_{k+1,k} = f_{k+1}^* J f_k
+  }
+  if (threadIdx.x != 0) return;
+  const double ap = pl.d[3 * k].x;
+  bool bad;
+  if (type == 1) {
+    bad = !(a != 0.0) || !isfinite(a) || ((a > 0.0) != (ap > 0.0)) || fabs(a - ap) > 0.25 * fmax(fabs(a), fabs(ap));
+  } else {
+    const double cp = pl.d[3 * k + 2].x;
+    const double2 bp = pl.d[3 * k + 1];
+    const double da = a - ap, dc = c - cp, dbx = b.x - bp.x, dby = b.y - bp.y;
+    const double diff = sqrt(da * da + dc * dc + 2.0 * (dbx * dbx + dby * dby));
+    const double na = sqrt(a * a + c * c + 2.0 * (b.x * b.x + b.y * b.y));
+    const double np = sqrt(ap * ap + cp * cp + 2.0 * (bp.x * bp.x + bp.y * bp.y));
+    const double det = a * c - (b.x * b.x + b.y * b.y), detp = ap * cp - (bp.x * bp.x + bp.y * bp.y);
+    bad = !isfinite(diff) || !(det != 0.0) || ((det > 0.0) != (detp > 0.0)) || diff > 0.25 * fmax(na, np);
+  }
+  if (bad) s.ctl[5] = 1;
+}
+
+// Y[i + j PB] = sum over the nb row-chunk partials part[b][i + j nr] (Kahan-compensated, in
+// chunk order): the J-products of the planned JQR's flush summed in short pieces, about as
+// accurate as the column search's block-reduced dots (one long GEMM accumulation over the
+// m rows lost a factor 3-10 in the Grammian preservation, measured)
+__global__ void k_sum_chunks(const double2* part, int nb, long long pstride, int nr, long long ncol, double2* Y) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)nr * ncol) return;
+  const int i = (int)(e % nr);
+  const long long j = e / nr;
+  double sx = 0.0, sy = 0.0, cx = 0.0, cy = 0.0;
+  for (int b = 0; b < nb; b++) {
+    const double2 v = part[b * pstride + e];
+    const double yx = v.x - cx, yy = v.y - cy;
+    const double tx = sx + yx, ty = sy + yy;
+    cx = (tx - sx) - yx;
+    cy = (ty - sy) - yy;
+    sx = tx;
+    sy = ty;
+  }
+  Y[i + j * PB] = cmk(sx, sy);
+}
+
+// SJ = J S (rows [r0, m) of nr columns; ld lds)
+__global__ void k_scale_j(const double2* S, double2* SJ, long long lds, const int8_t* J, long long r0, long long m,
+                          int nr) {
+  const long long tot = (m - r0) * (long long)nr;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e / (m - r0), r = r0 + e % (m - r0);
+    const double2 v = S[r + c * lds];
+    SJ[r + c * lds] = J[r] > 0 ? v : cmk(-v.x, -v.y);
+  }
+}
+
 }  // namespace
 
 size_t phase2_scratch_bytes(int64_t m, int64_t n) {
-  return al256((size_t)n * 8) + 2 * al256((size_t)n * 16) + al256((size_t)m * 16) + 512 + 256;
+  // P2Scr, then the JQR pivot plan (BkPlan: 72 bytes per column + control)
+  return al256((size_t)n * 8) + 2 * al256((size_t)n * 16) + al256((size_t)m * 16) + 512 + 256 +
+         2 * al256((size_t)n * 4) + 2 * al256((size_t)n * 8) + al256((size_t)3 * n * 16) + 256;
 }
+
+namespace {
+// the BkPlan arrays, carved after P2Scr in the same scratch
+BkPlan carve_plan(char* scr, int64_t m, int64_t n) {
+  char* p = scr + al256((size_t)n * 8) + 2 * al256((size_t)n * 16) + al256((size_t)m * 16) + 512 + 256;
+  BkPlan pl;
+  pl.type = (int*)p; p += al256((size_t)n * 4);
+  pl.sw2pos = (int*)p; p += al256((size_t)n * 4);
+  pl.sw1 = (long long*)p; p += al256((size_t)n * 8);
+  pl.sw2 = (long long*)p; p += al256((size_t)n * 8);
+  pl.d = (double2*)p; p += al256((size_t)3 * n * 16);
+  pl.st = (int*)p;
+  return pl;
+}
+}  // namespace
 
 #define P2CHK()                                    \
   do {                                             \
@@ -734,6 +1006,9 @@ struct Cublas {
   cublasStatus_t (*Zgemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const cuDoubleComplex*,
                           const cuDoubleComplex*, int, const cuDoubleComplex*, int, const cuDoubleComplex*,
                           cuDoubleComplex*, int) = nullptr;
+  cublasStatus_t (*ZgemmSB)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
+                            const cuDoubleComplex*, const cuDoubleComplex*, int, long long, const cuDoubleComplex*, int,
+                            long long, const cuDoubleComplex*, cuDoubleComplex*, int, long long, int) = nullptr;
 };
 Cublas* cublas_lib() {
   static Cublas c;
@@ -748,7 +1023,8 @@ Cublas* cublas_lib() {
   c.Destroy = (decltype(c.Destroy))dlsym(h, "cublasDestroy_v2");
   c.SetStream = (decltype(c.SetStream))dlsym(h, "cublasSetStream_v2");
   c.Zgemm = (decltype(c.Zgemm))dlsym(h, "cublasZgemm_v2");
-  c.ok = c.Create && c.Destroy && c.SetStream && c.Zgemm;
+  c.ZgemmSB = (decltype(c.ZgemmSB))dlsym(h, "cublasZgemmStridedBatched");
+  c.ok = c.Create && c.Destroy && c.SetStream && c.Zgemm && c.ZgemmSB;
   return c.ok ? &c : nullptr;
 }
 }  // namespace
@@ -779,6 +1055,9 @@ namespace {
 
 struct Panel {
   double2 *S, *T, *Y, *W, *tv, *u, *fx;
+  double2 *fx2, *SJ;   // planned JQR: second formed pivot column, J-scaled panel
+  double2* part;       // planned JQR: row-chunk partials of the flush's J-products
+  long long part_cap;  // entries available at part
   long long lds;
 };
 
@@ -797,7 +1076,7 @@ ghsvd_status flush_update(Ctx* ctx, Cublas* cb, const Panel& P, double2* X, long
 
 // Blocked JQR of F (in place, like the unblocked loop of phase2_reduce), see the
 // "blocked Phase 2" comment above.  Returns GHSVD_OK with s.ctl[3] clear, or an error.
-static ghsvd_status jqr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s) {
+static ghsvd_status jqr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, int64_t k_start = 0) {
   const int64_t m = ctx->m_user, n = ctx->n_user;
   const long long ld = ctx->ldm;
   cudaStream_t st = ctx->stream;
@@ -811,7 +1090,7 @@ static ghsvd_status jqr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s) {
     return GHSVD_OK;
   };
   const unsigned gm = (unsigned)std::min<int64_t>(1024, (m + 255) / 256);
-  int64_t k = 0;
+  int64_t k = k_start;
   while (k < n) {
     const int64_t k0 = k;
     int nr = 0, pend = 0;   // reflectors in the panel; newest ones without Y rows yet
@@ -892,6 +1171,149 @@ static ghsvd_status jqr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s) {
                                                                              nr, k, 0, k, n, s.hd);
       TRY(flush_update(ctx, cb, P, F, ld, k0, m, k, n, nr));
       P2CHK();
+    }
+  }
+  return GHSVD_OK;
+}
+
+// The JQR pivot plan (see BkPlan): H = F^* J F (rows J-sorted: F_+^* F_+ - F_-^* F_-, two
+// ZGEMMs) into the n x n buffer Hb, then one k_bk_select + k_bk_update per step.  Fills the
+// host copy of the pivot types.  p2 is not touched (the JQR applies the interchanges).
+static ghsvd_status jqr_plan(Ctx* ctx, Cublas* cb, double2* Hb, long long ldh, const BkPlan& pl,
+                             std::vector<int>& type_h) {
+  const int64_t m = ctx->m_user, n = ctx->n_user;
+  const long long ld = ctx->ldm;
+  cudaStream_t st = ctx->stream;
+  const int64_t np = std::min<int64_t>(std::max<int64_t>(ctx->npos, 0), m);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), mone = make_cuDoubleComplex(-1.0, 0.0),
+                        zero = make_cuDoubleComplex(0.0, 0.0);
+  const cuDoubleComplex* Fp = (const cuDoubleComplex*)ctx->F;
+  if (np > 0)
+    P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, (int)n, (int)n, (int)np, &one, Fp, (int)ld,
+                    Fp, (int)ld, &zero, (cuDoubleComplex*)Hb, (int)ldh));
+  if (m > np)
+    P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, (int)n, (int)n, (int)(m - np), &mone,
+                    Fp + np, (int)ld, Fp + np, (int)ld, np > 0 ? &one : &zero, (cuDoubleComplex*)Hb, (int)ldh));
+  GH_CUDA(cudaMemsetAsync(pl.st, 0, 32, st));
+  GH_CUDA(cudaMemsetAsync(pl.type, 0, (size_t)n * 4, st));
+  for (int64_t i = 0; i < n; i++) {
+    // the device step index k is >= i (each step advances by 1 or 2): a grid for the
+    // trailing block [i + 1, n) covers it; steps past the end are no-ops
+    k_bk_select<<<1, T2, 0, st>>>(Hb, ldh, n, pl);
+    const unsigned nt = (unsigned)((n - i - 1 + 31) / 32);
+    if (nt) k_bk_update<<<dim3(nt, nt), 256, 0, st>>>(Hb, ldh, n, pl);
+  }
+  P2CHK();
+  type_h.assign(n, 0);
+  int stv[8];
+  GH_CUDA(cudaMemcpyAsync(type_h.data(), pl.type, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaMemcpyAsync(stv, pl.st, 32, cudaMemcpyDeviceToHost, st));
+  GH_CUDA(cudaStreamSynchronize(st));
+  if (stv[4]) {
+    ctx->err = "reduce: non-finite J-Grammian in the JQR pivot plan";
+    return GHSVD_E_NONFINITE;
+  }
+  return GHSVD_OK;
+}
+
+// Blocked JQR with the planned pivots: per step the planned column interchanges, the pivot
+// column(s) formed from the panel (y = S^* J x, w = T y, x + S w) and CHECKED against the
+// plan (k_plan_check), then the reflectors exactly as jqr_blocked; the trailing columns are
+// updated once per panel by ZGEMMs (Y = (J S)^* X, W = T Y, X += S W) -- no pass over them
+// per column.  A pivot the exact J-Grammian contradicts ends the plan: the panel is flushed
+// and jqr_blocked (pivots searched on the columns) continues from that column.
+static ghsvd_status jqr_planned(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, const BkPlan& pl,
+                                const std::vector<int>& ptype, int64_t* k_fallback) {
+  const int64_t m = ctx->m_user, n = ctx->n_user;
+  const long long ld = ctx->ldm;
+  cudaStream_t st = ctx->stream;
+  double2* F = ctx->F;
+  int8_t* J = ctx->J;
+  long long* p2 = (long long*)ctx->p2;
+  int ctl[8];
+  const unsigned gm = (unsigned)std::min<int64_t>(1024, (m + 255) / 256);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  *k_fallback = -1;
+  GH_CUDA(cudaMemsetAsync(s.ctl, 0, 32, st));
+  int64_t k = 0;
+  while (k < n) {
+    const int64_t k0 = k;
+    int nr = 0;
+    bool stop = false;
+    GH_CUDA(cudaMemsetAsync(P.T, 0, (size_t)PB * PB * 16, st));
+    while (k < n && nr + std::max(ptype[k], 1) <= PB) {
+      const int type = ptype[k] == 2 && k + 1 < n ? 2 : 1;
+      k_plan_swaps<<<gm, 256, 0, st>>>(F, ld, m, k, p2, pl);
+      // the pivot column(s) with the panel's delayed update, into fx (, fx2)
+      for (int c = 0; c < type; c++) {
+        double2* x = F + (k + c) * ld;
+        double2* out = c ? P.fx2 : P.fx;
+        if (nr) {
+          k_ycol<<<nr, T2, 0, st>>>(x, P.S, P.lds, J, k0, m, P.u);
+          k_tw<<<1, 64, 0, st>>>(P.T, P.u, P.tv, nr);
+          k_form<<<gm, 256, 0, st>>>(x, out, P.S, P.lds, P.tv, nr, k0, m);
+        } else {
+          GH_CUDA(cudaMemcpyAsync(out + k0, x + k0, (size_t)(m - k0) * 16, cudaMemcpyDeviceToDevice, st));
+        }
+      }
+      k_plan_check<<<1, T2, 0, st>>>(P.fx, P.fx2, J, k, m, type, pl, s);
+      GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
+      GH_CUDA(cudaStreamSynchronize(st));
+      if (ctl[3]) return GHSVD_OK;   // error flag: the caller reports it
+      if (ctl[5]) {
+        stop = true;
+        break;
+      }
+      for (int c = 0; c < type; c++)
+        GH_CUDA(cudaMemcpyAsync(F + (k + c) * ld + k0, (c ? P.fx2 : P.fx) + k0, (size_t)(m - k0) * 16,
+                                cudaMemcpyDeviceToDevice, st));
+      // the reflector(s), as in jqr_blocked
+      if (type == 2) k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, +1, s);
+      for (int t = 0; t < type; t++) {
+        const long long kk = k + t;
+        k_refl_prep<<<1, T2, 0, st>>>(F, ld, J, m, n, kk, s, P.S, P.lds, nr);
+        if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, J, kk, m, P.tv);
+        k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, kk, m, nr, P.T, P.tv, s);
+        nr++;
+        if (t == 0 && type == 2) k_refl_apply<<<1, T2, 0, st>>>(F, ld, J, m, kk, kk + 1, nullptr, 1, s);
+        k_refl_fin<<<1, T2, 0, st>>>(F, ld, m, kk, s);
+      }
+      if (type == 2) k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, -1, s);
+      P2CHK();
+      k += type;
+    }
+    // flush: the delayed update of the stale columns [k, n)
+    if (k < n && nr) {
+      // Y = (J S)^* X over rows [k0, m) as partials over row chunks of 32 (strided-batched
+      // ZGEMMs, column slabs sized to the free panel buffer), summed with compensation
+      // (k_sum_chunks): short accumulations, as in the column search's block-reduced dots
+      k_scale_j<<<gm, 256, 0, st>>>(P.S, P.SJ, P.lds, J, k0, m, nr);
+      const long long rows = m - k0, kc = 32, nb = (rows + kc - 1) / kc, full = rows / kc;
+      const long long ns = std::max<long long>(1, std::min<long long>(n - k, P.part_cap / (nb * nr)));
+      for (long long j0 = k; j0 < n; j0 += ns) {
+        const long long ncol = std::min<long long>(ns, n - j0), pstride = (long long)nr * ncol;
+        if (full > 0)
+          P2CUB(cb->ZgemmSB((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, nr, (int)ncol, (int)kc, &one,
+                            (const cuDoubleComplex*)(P.SJ + k0), (int)P.lds, kc,
+                            (const cuDoubleComplex*)(F + k0 + j0 * ld), (int)ld, kc, &zero,
+                            (cuDoubleComplex*)P.part, nr, pstride, (int)full));
+        if (full < nb)   // the ragged last chunk
+          P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, nr, (int)ncol, (int)(rows - full * kc),
+                          &one, (const cuDoubleComplex*)(P.SJ + k0 + full * kc), (int)P.lds,
+                          (const cuDoubleComplex*)(F + k0 + full * kc + j0 * ld), (int)ld, &zero,
+                          (cuDoubleComplex*)(P.part + full * pstride), nr));
+        k_sum_chunks<<<(unsigned)((pstride + 255) / 256), 256, 0, st>>>(P.part, (int)nb, pstride, nr, ncol,
+                                                                         P.Y + j0 * PB);
+      }
+      P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, nr, (int)(n - k), nr, &one,
+                      (const cuDoubleComplex*)P.T, PB, (const cuDoubleComplex*)(P.Y + k * PB), PB, &zero,
+                      (cuDoubleComplex*)(P.W + k * PB), PB));
+      TRY(flush_update(ctx, cb, P, F, ld, k0, m, k, n, nr));
+      P2CHK();
+    }
+    if (stop) {
+      *k_fallback = k;
+      return GHSVD_OK;
     }
   }
   return GHSVD_OK;
@@ -993,11 +1415,28 @@ static ghsvd_status phase2_reduce_blocked(Ctx* ctx, int flags, Cublas* cb) {
   P.tv = P.W + (size_t)PB * n;
   P.u = P.tv + PB;
   P.fx = P.u + PB;
+  P.fx2 = P.fx + P.lds;
+  P.SJ = P.fx2 + P.lds;
+  P.part = P.SJ + (size_t)P.lds * PB;
+  P.part_cap = (long long)ctx->ldn * (ctx->n_cap + 1) - (long long)(P.part - ctx->Z2);
   GH_CUDA(cudaMemsetAsync(s.ctl, 0, 256, st));
   GH_CUDA(cudaMemsetAsync(P.S, 0, (size_t)P.lds * PB * 16, st));
   k_iota<<<8, 256, 0, st>>>(p2, n);
   P2CHK();
-  TRY(jqr_blocked(ctx, cb, P, s));
+  if (flags & GHSVD_REDUCE_COLSEARCH) {
+    TRY(jqr_blocked(ctx, cb, P, s));
+  } else {
+    // pivots planned on the J-Grammian (in the n x n Z buffer, free until R_F is copied
+    // into it below), each checked on its formed column; the column search takes over
+    // from the first pivot the check rejects
+    const BkPlan pl = carve_plan(ctx->scr, m, n);
+    std::vector<int> ptype;
+    TRY(jqr_plan(ctx, cb, ctx->Z, ctx->ldn, pl, ptype));
+    int64_t kf = -1;
+    TRY(jqr_planned(ctx, cb, P, s, pl, ptype, &kf));
+    ctx->p2_fallback_col = kf;
+    if (kf >= 0) TRY(jqr_blocked(ctx, cb, P, s, kf));
+  }
   int ctl[8];
   GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
   GH_CUDA(cudaStreamSynchronize(st));
@@ -1063,7 +1502,7 @@ ghsvd_status phase2_reduce(Ctx* ctx, int flags) {
   // logic outweighs the traffic it saves (config 2, 1568 x 1024: 0.26 s blocked vs 0.09 s)
   const bool big = (double)m * (double)n * (double)n >= 2e10;
   if (!(flags & GHSVD_REDUCE_UNBLOCKED) && (big || (flags & GHSVD_REDUCE_BLOCKED))) {
-    const size_t need = ((size_t)round_up(m, 16) * PB + PB * PB + 2 * (size_t)PB * n + 2 * PB + m) * 16;
+    const size_t need = ((size_t)round_up(m, 16) * (2 * PB + 2) + PB * PB + 2 * (size_t)PB * n + 2 * PB + m) * 16;
     const size_t have = (size_t)ctx->ldn * (ctx->n_cap + 1) * 16;
     Cublas* cb = cublas_lib();
     if (cb && need <= have) {

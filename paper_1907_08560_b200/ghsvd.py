@@ -36,7 +36,7 @@ EXPORTS = ["ghsvd_default_options", "ghsvd_workspace_bytes", "ghsvd_create", "gh
            "ghsvd_hz2x2_batch", "ghsvd_last_error",
            "ghsvd_destroy", "ghsvd_version", "ghsvd_block_owner", "ghsvd_exchange_plan",
            "ghsvd_nccl_unique_id", "ghsvd_order_steps", "ghsvd_order_pair", "ghsvd_block_owner_ord",
-           "ghsvd_exchange_plan_ord"]
+           "ghsvd_exchange_plan_ord", "ghsvd_reduce_fallback_col"]
 
 
 class GHSVDError(RuntimeError):
@@ -132,6 +132,8 @@ def load():
     L.ghsvd_version.restype = ctypes.c_char_p
     L.ghsvd_block_owner.argtypes = [Ci, Ci, Ci, Ci]
     L.ghsvd_exchange_plan.argtypes = [Ci, Ci, Ci, Ci, Ci, P, P, P, P, P, P]
+    L.ghsvd_reduce_fallback_col.argtypes = [P]
+    L.ghsvd_reduce_fallback_col.restype = I64
     L.ghsvd_order_steps.argtypes = [Ci, Ci, Ci]
     L.ghsvd_order_steps.restype = I64
     L.ghsvd_order_pair.argtypes = [Ci, Ci, Ci, I64, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -299,12 +301,15 @@ class Context:
         self._check(self._L.ghsvd_factor(self._h, NA, NL, NG, pa, pb, pu, ptaa, ptab, ptbb), "factor")
         self.m, self.n = 2 * NA * NL, NG
 
-    def reduce(self, colpiv: bool = False, unblocked: Optional[bool] = None):
+    def reduce(self, colpiv: bool = False, unblocked: Optional[bool] = None, colsearch: bool = False):
         """Phase 2; colpiv: column-pivoted QR of G P2 (GHSVD_REDUCE_COLPIV); unblocked: True forces
         the one-reflector-per-column form (GHSVD_REDUCE_UNBLOCKED), False the blocked one
-        (GHSVD_REDUCE_BLOCKED), None lets the library choose by size (see ghsvd.h)."""
-        fl = (1 if colpiv else 0) | (0 if unblocked is None else (2 if unblocked else 4))
+        (GHSVD_REDUCE_BLOCKED), None lets the library choose by size (see ghsvd.h); colsearch:
+        the blocked JQR searches its pivots on the columns instead of planning them on the
+        J-Grammian (GHSVD_REDUCE_COLSEARCH)."""
+        fl = (1 if colpiv else 0) | (0 if unblocked is None else (2 if unblocked else 4)) | (8 if colsearch else 0)
         self._check(self._L.ghsvd_reduce(self._h, fl), "reduce")
+        self.reduce_fallback_col = int(self._L.ghsvd_reduce_fallback_col(self._h))
         self.m = self.n
 
     def get_factors(self):

@@ -22,16 +22,23 @@ def gh():
     return ghsvd
 
 
-@pytest.mark.parametrize("unblocked", [False, True])
+MODES = {"planned": dict(unblocked=False), "colsearch": dict(unblocked=False, colsearch=True),
+         "unblocked": dict(unblocked=True)}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("m,n,neg", [(60, 12, 0.5), (200, 40, 0.4), (150, 150, 0.5), (300, 64, 0.1), (97, 31, 0.5),
                                      (500, 300, 0.5), (400, 133, 0.3)])
-def test_reduce_grammians(gh, m, n, neg, unblocked):
-    """Both Phase-2 forms (blocked default: panels of <= 33 delayed reflectors, several
-    panels and ragged last panels here; unblocked: one reflector application per column)."""
+def test_reduce_grammians(gh, m, n, neg, mode):
+    """Every Phase-2 form (blocked with planned JQR pivots -- the default --, blocked with the
+    pivots searched on the columns, unblocked: one reflector application per column; panels
+    of <= 33 delayed reflectors, several panels and ragged last panels here)."""
     P = inputs.random_pencil(50 + m, m, n, neg)
     ctx = gh.Context(m, n)
     ctx.set_factors(P.F, P.J, P.G)
-    ctx.reduce(unblocked=unblocked)
+    ctx.reduce(**MODES[mode])
+    if mode == "planned":
+        assert ctx.reduce_fallback_col == -1   # every planned pivot confirmed on its column
     F, J, G, p2 = ctx.get_factors()
     if n % 2:
         F, G, J = F[:-1, :-1], G[:-1, :-1], J[:-1]
@@ -139,10 +146,10 @@ def test_blocked_and_unblocked_reduce_same_pencil(gh, colpiv):
     at = inputs.lapw_atoms(12, 4, 49, 300, 39 / 98)
     m, n = 2 * 4 * 49, 300
     lams = []
-    for unb in (False, True):
+    for kw in MODES.values():
         ctx = gh.Context(m, n, 49, variant="bo")
         ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
-        ctx.reduce(colpiv=colpiv, unblocked=unb)
+        ctx.reduce(colpiv=colpiv, **kw)
         st = ctx.sweep()
         lams.append(np.sort(ctx.extract(want_z=False)[0]))
         ctx.close()
@@ -152,3 +159,43 @@ def test_blocked_and_unblocked_reduce_same_pencil(gh, colpiv):
     lo = np.sort(oracle.extract(Fr, Jo, Gr, Zp)[0])
     for lam in lams:
         assert np.max(np.abs(lam - lo) / np.abs(lo)) <= 1e-9
+
+
+@pytest.mark.parametrize("m,n,neg,seed", [(300, 64, 0.4, 1), (500, 200, 0.5, 2), (97, 31, 0.5, 3)])
+def test_planned_jqr_pivots_equal_column_search(gh, m, n, neg, seed):
+    """The planned pivots are the paper's rule applied to the Schur complements of
+    H = F^* J F, which equal the J-Grammians the column search reads: away from near-ties
+    both choose the same interchanges and 1x1 / 2x2 pivots (same P2 and inertia)."""
+    P = inputs.random_pencil(90 + seed, m, n, neg)
+    out = {}
+    for mode in ("planned", "colsearch"):
+        ctx = gh.Context(m, n)
+        ctx.set_factors(P.F, P.J, P.G)
+        ctx.reduce(**MODES[mode])
+        F, J, G, p2 = ctx.get_factors()
+        out[mode] = (p2, int((J > 0).sum()), ctx.reduce_fallback_col)
+        ctx.close()
+    assert out["planned"][2] == -1
+    assert np.array_equal(out["planned"][0], out["colsearch"][0])
+    assert out["planned"][1] == out["colsearch"][1]
+
+
+def test_planned_jqr_on_illconditioned_config3_recipe(gh):
+    """Config-3 recipe (S condition 1e12) at reduced size: the planned JQR keeps the
+    Grammians and reduces the same pencil as the column search (converged lambda 1e-6)."""
+    at = inputs.illcond_atoms(3, 8, 40, 256)
+    m, n = 2 * 8 * 40, 256
+    lams = []
+    for mode in ("planned", "colsearch"):
+        ctx = gh.Context(m, n, 40, variant="bo")
+        ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+        F0, J0, G0, _ = ctx.get_factors()
+        ctx.reduce(**MODES[mode])
+        F, J, G, p2 = ctx.get_factors()
+        H0 = F0.conj().T @ (J0[:, None] * F0)
+        assert np.linalg.norm(F.conj().T @ (J[:, None] * F) - H0[np.ix_(p2, p2)]) / np.linalg.norm(H0) < 1e-11
+        st = ctx.sweep()
+        lams.append(np.sort(ctx.extract(want_z=False)[0]))
+        ctx.close()
+        assert st["converged"]
+    assert np.max(np.abs(lams[0] - lams[1]) / np.abs(lams[1])) <= 1e-6

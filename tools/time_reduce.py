@@ -35,7 +35,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        ctx.reduce(colpiv=mode.endswith("colpiv"), unblocked=mode.startswith("unblocked"))
+        ctx.reduce(colpiv="colpiv" in mode, unblocked=mode.startswith("unblocked"), colsearch="colsearch" in mode)
         e1.record()
         torch.cuda.synchronize()
         secs = e0.elapsed_time(e1) * 1e-3
@@ -57,7 +57,8 @@ def main():
         Sr = Gr.conj().T @ Gr
         eh = float(torch.linalg.norm(Hr - H[pt][:, pt]) / torch.linalg.norm(H))
         es = float(torch.linalg.norm(Sr - S[pt][:, pt]) / torch.linalg.norm(S))
-        print(json.dumps({"config": args.config, "mode": mode, "seconds": secs, "grammian_err_H": eh,
+        print(json.dumps({"config": args.config, "mode": mode, "seconds": secs,
+                          "fallback_col": getattr(ctx, "reduce_fallback_col", None), "grammian_err_H": eh,
                           "grammian_err_S": es, "m": m, "n": n}), flush=True)
         ctx.close()
         del Ft, Gt, Fr, Gr, H, S, Hr, Sr

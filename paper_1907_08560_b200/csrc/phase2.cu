@@ -756,7 +756,9 @@ __device__ void hswap(double2* H, long long ld, long long n, long long k, long l
 
 // One pivot decision at k = st[0] (no-op once k >= n): exactly the rule of k_piv_a / k_piv_b /
 // k_piv_c on the Schur complement instead of on the columns.
-__global__ void __launch_bounds__(T2) k_bk_select(double2* H, long long ld, long long n, BkPlan pl) {
+// diag_only: only the diagonal pivoting (the column-pivoted QR's largest remaining norm on
+// the Schur complements of S = X^* X, i.e. diagonally pivoted Cholesky)
+__global__ void __launch_bounds__(T2) k_bk_select(double2* H, long long ld, long long n, BkPlan pl, int diag_only) {
   const long long k = pl.st[0];
   if (k >= n) {
     if (threadIdx.x == 0) pl.st[3] = 0;
@@ -778,7 +780,7 @@ __global__ void __launch_bounds__(T2) k_bk_select(double2* H, long long ld, long
   int type = 1;
   long long s2 = -1;
   int s2pos = -1;
-  if (k < n - 1) {
+  if (k < n - 1 && !diag_only) {
     double h1i = -1.0;
     long long ii = NONE;
     for (long long j = k + 1 + threadIdx.x; j < n; j += T2) {
@@ -949,6 +951,33 @@ __global__ void k_sum_chunks(const double2* part, int nb, long long pstride, int
     sy = ty;
   }
   Y[i + j * PB] = cmk(sx, sy);
+}
+
+// Planned column interchange of the column-pivoted QR at position k: X and Rf columns, p2
+__global__ void k_plan_swap_qr(double2* X, long long ldx, long long mx, double2* Rf, long long ldr, long long mr,
+                               long long k, long long* p2, BkPlan pl) {
+  const long long a = pl.sw1[k];
+  if (a == k) return;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mx; i += (long long)gridDim.x * blockDim.x) {
+    const double2 t = X[i + k * ldx]; X[i + k * ldx] = X[i + a * ldx]; X[i + a * ldx] = t;
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mr; i += (long long)gridDim.x * blockDim.x) {
+    const double2 t = Rf[i + k * ldr]; Rf[i + k * ldr] = Rf[i + a * ldr]; Rf[i + a * ldr] = t;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t = p2[k]; p2[k] = p2[a]; p2[a] = t;
+  }
+}
+
+// The formed QR pivot column's squared norm (rows >= k) against the planned Schur diagonal:
+// ctl[5] = 1 when off by more than a quarter
+__global__ void __launch_bounds__(T2) k_plan_check_qr(const double2* x, long long k, long long m, BkPlan pl, P2Scr s) {
+  __shared__ double2 sh[T2 / 32];
+  const double a = jdot(x, x, nullptr, k, m, false, sh).x;
+  if (threadIdx.x == 0) {
+    const double ap = pl.d[3 * k].x;
+    if (!(a > 0.0) || !isfinite(a) || fabs(a - ap) > 0.25 * fmax(a, fabs(ap))) s.ctl[5] = 1;
+  }
 }
 
 // SJ = J S (rows [r0, m) of nr columns; ld lds)
@@ -1179,15 +1208,16 @@ static ghsvd_status jqr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, i
 // The JQR pivot plan (see BkPlan): H = F^* J F (rows J-sorted: F_+^* F_+ - F_-^* F_-, two
 // ZGEMMs) into the n x n buffer Hb, then one k_bk_select + k_bk_update per step.  Fills the
 // host copy of the pivot types.  p2 is not touched (the JQR applies the interchanges).
-static ghsvd_status jqr_plan(Ctx* ctx, Cublas* cb, double2* Hb, long long ldh, const BkPlan& pl,
-                             std::vector<int>& type_h) {
+// X (m x n, ld): the first np rows carry J = +1, the rest J = -1 (np = m: the QR's S = X^* X,
+// diag_only).
+static ghsvd_status gram_plan(Ctx* ctx, Cublas* cb, const double2* X, long long ld, int64_t np, int diag_only,
+                              double2* Hb, long long ldh, const BkPlan& pl, std::vector<int>& type_h) {
   const int64_t m = ctx->m_user, n = ctx->n_user;
-  const long long ld = ctx->ldm;
   cudaStream_t st = ctx->stream;
-  const int64_t np = std::min<int64_t>(std::max<int64_t>(ctx->npos, 0), m);
+  np = std::min<int64_t>(std::max<int64_t>(np, 0), m);
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), mone = make_cuDoubleComplex(-1.0, 0.0),
                         zero = make_cuDoubleComplex(0.0, 0.0);
-  const cuDoubleComplex* Fp = (const cuDoubleComplex*)ctx->F;
+  const cuDoubleComplex* Fp = (const cuDoubleComplex*)X;
   if (np > 0)
     P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, (int)n, (int)n, (int)np, &one, Fp, (int)ld,
                     Fp, (int)ld, &zero, (cuDoubleComplex*)Hb, (int)ldh));
@@ -1199,7 +1229,7 @@ static ghsvd_status jqr_plan(Ctx* ctx, Cublas* cb, double2* Hb, long long ldh, c
   for (int64_t i = 0; i < n; i++) {
     // the device step index k is >= i (each step advances by 1 or 2): a grid for the
     // trailing block [i + 1, n) covers it; steps past the end are no-ops
-    k_bk_select<<<1, T2, 0, st>>>(Hb, ldh, n, pl);
+    k_bk_select<<<1, T2, 0, st>>>(Hb, ldh, n, pl, diag_only);
     const unsigned nt = (unsigned)((n - i - 1 + 31) / 32);
     if (nt) k_bk_update<<<dim3(nt, nt), 256, 0, st>>>(Hb, ldh, n, pl);
   }
@@ -1210,7 +1240,7 @@ static ghsvd_status jqr_plan(Ctx* ctx, Cublas* cb, double2* Hb, long long ldh, c
   GH_CUDA(cudaMemcpyAsync(stv, pl.st, 32, cudaMemcpyDeviceToHost, st));
   GH_CUDA(cudaStreamSynchronize(st));
   if (stv[4]) {
-    ctx->err = "reduce: non-finite J-Grammian in the JQR pivot plan";
+    ctx->err = "reduce: non-finite Grammian in the Phase-2 pivot plan";
     return GHSVD_E_NONFINITE;
   }
   return GHSVD_OK;
@@ -1323,23 +1353,30 @@ static ghsvd_status jqr_planned(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, c
 // buffer X (G P2 gathered), left-looking panels as above with J = I; the column swaps of
 // the pivoted form are applied to p2 and to the n x n R_F copy Rf (F' = F P5).
 static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, double2* X, long long ld,
-                               bool colpiv, double2* Rf, long long ldr) {
+                               bool colpiv, double2* Rf, long long ldr, int64_t k_start = 0,
+                               const BkPlan* plan = nullptr) {
   const int64_t m = ctx->m_user, n = ctx->n_user;
   cudaStream_t st = ctx->stream;
   long long* p2 = (long long*)ctx->p2;
   int ctl[8];
   const unsigned gm = (unsigned)std::min<int64_t>(1024, (m + 255) / 256);
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-  int64_t k = 0;
+  // plan (column-pivoted form only): the planned interchanges instead of the norm search,
+  // each formed pivot checked against its planned norm; after a panel with a rejected pivot
+  // the search takes over (colpiv_plan off)
+  bool use_plan = colpiv && plan != nullptr;
+  if (use_plan) GH_CUDA(cudaMemsetAsync(s.ctl + 5, 0, 4, st));
+  int64_t k = k_start;
   while (k < n) {
     const int64_t k0 = k;
     int nr = 0, pend = 0;
     GH_CUDA(cudaMemsetAsync(P.T, 0, (size_t)PB * PB * 16, st));
     GH_CUDA(cudaMemsetAsync(P.Y + k * PB, 0, (size_t)PB * (n - k) * 16, st));
     GH_CUDA(cudaMemsetAsync(P.W + k * PB, 0, (size_t)PB * (n - k) * 16, st));
-    if (colpiv) k_norms<<<(unsigned)(n - k), T2, 0, st>>>(X, ld, k, m, s);
+    const bool dyn = colpiv && !use_plan;   // pivots searched on the (downdated) norms
+    if (dyn) k_norms<<<(unsigned)(n - k), T2, 0, st>>>(X, ld, k, m, s);
     while (k < n && nr + 1 <= PB) {
-      if (colpiv) {
+      if (dyn) {
         if (pend) {
           k_vdot<<<(unsigned)(n - k), T2, 0, st>>>(P.S + (size_t)(nr - 1) * P.lds, X, ld, nullptr, k0, m, k,
                                                   P.Y + (nr - 1) + k * PB, PB);
@@ -1357,10 +1394,14 @@ static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, do
           GH_CUDA(cudaStreamSynchronize(st));
           if (ctl[5]) break;   // downdated norm was off: flush, then exact norms again
         }
-      } else if (nr) {
-        k_ycol<<<nr, T2, 0, st>>>(X + k * ld, P.S, P.lds, nullptr, k0, m, P.u);
-        k_tw<<<1, 64, 0, st>>>(P.T, P.u, P.tv, nr);
-        k_form<<<gm, 256, 0, st>>>(X + k * ld, X + k * ld, P.S, P.lds, P.tv, nr, k0, m);
+      } else {
+        if (use_plan) k_plan_swap_qr<<<gm, 256, 0, st>>>(X, ld, m, Rf, ldr, n, k, p2, *plan);
+        if (nr) {
+          k_ycol<<<nr, T2, 0, st>>>(X + k * ld, P.S, P.lds, nullptr, k0, m, P.u);
+          k_tw<<<1, 64, 0, st>>>(P.T, P.u, P.tv, nr);
+          k_form<<<gm, 256, 0, st>>>(X + k * ld, X + k * ld, P.S, P.lds, P.tv, nr, k0, m);
+        }
+        if (use_plan) k_plan_check_qr<<<1, T2, 0, st>>>(X + k * ld, k, m, *plan, s);
       }
       k_qr_prep_c<<<1, T2, 0, st>>>(X, ld, m, k, s);
       if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, nullptr, k, m, P.tv);
@@ -1371,7 +1412,7 @@ static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, do
       P2CHK();
     }
     if (k < n && nr) {
-      if (colpiv) {
+      if (dyn) {
         if (pend) {
           k_vdot<<<(unsigned)(n - k), T2, 0, st>>>(P.S + (size_t)(nr - 1) * P.lds, X, ld, nullptr, k0, m, k,
                                                   P.Y + (nr - 1) + k * PB, PB);
@@ -1389,6 +1430,16 @@ static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, do
       }
       TRY(flush_update(ctx, cb, P, X, ld, k0, m, k, n, nr));
       P2CHK();
+    }
+    if (use_plan) {
+      // one read-back per panel: a pivot the formed column contradicted ends the plan
+      GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
+      GH_CUDA(cudaStreamSynchronize(st));
+      if (ctl[3]) break;
+      if (ctl[5]) {
+        use_plan = false;
+        if (ctx->p2_fallback_qr < 0) ctx->p2_fallback_qr = k;
+      }
     }
   }
   GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
@@ -1431,7 +1482,7 @@ static ghsvd_status phase2_reduce_blocked(Ctx* ctx, int flags, Cublas* cb) {
     // from the first pivot the check rejects
     const BkPlan pl = carve_plan(ctx->scr, m, n);
     std::vector<int> ptype;
-    TRY(jqr_plan(ctx, cb, ctx->Z, ctx->ldn, pl, ptype));
+    TRY(gram_plan(ctx, cb, ctx->F, ctx->ldm, ctx->npos, 0, ctx->Z, ctx->ldn, pl, ptype));
     int64_t kf = -1;
     TRY(jqr_planned(ctx, cb, P, s, pl, ptype, &kf));
     ctx->p2_fallback_col = kf;
@@ -1458,7 +1509,17 @@ static ghsvd_status phase2_reduce_blocked(Ctx* ctx, int flags, Cublas* cb) {
   P2CHK();
   GH_CUDA(cudaMemsetAsync(s.ctl, 0, 256, st));
   GH_CUDA(cudaMemsetAsync(P.S, 0, (size_t)P.lds * PB * 16, st));
-  TRY(qr_blocked(ctx, cb, P, s, ctx->F, ld, (flags & GHSVD_REDUCE_COLPIV) != 0, ctx->Z, ldz));
+  if ((flags & GHSVD_REDUCE_COLPIV) && !(flags & GHSVD_REDUCE_COLSEARCH)) {
+    // column pivots planned on S = (G P2)^* (G P2) (diagonally pivoted Cholesky of its Schur
+    // complements = the largest remaining column norms), S in the G buffer (G P2 now lives in
+    // the F buffer)
+    const BkPlan pl = carve_plan(ctx->scr, m, n);
+    std::vector<int> ptype;
+    TRY(gram_plan(ctx, cb, ctx->F, ld, m, 1, ctx->G, ld, pl, ptype));
+    TRY(qr_blocked(ctx, cb, P, s, ctx->F, ld, true, ctx->Z, ldz, 0, &pl));
+  } else {
+    TRY(qr_blocked(ctx, cb, P, s, ctx->F, ld, (flags & GHSVD_REDUCE_COLPIV) != 0, ctx->Z, ldz));
+  }
   GH_CUDA(cudaMemsetAsync(ctx->G, 0, (size_t)ld * (ctx->n_cap + 1) * 16, st));
   k_qr_rout<<<(unsigned)n, T2, 0, st>>>(ctx->F, ld, ctx->G, ld, n);
   P2CHK();

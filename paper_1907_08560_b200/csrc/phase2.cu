@@ -243,13 +243,11 @@ __global__ void __launch_bounds__(T2) k_piv_c(double2* F, long long ld, long lon
   }
 }
 
-// Reflector for column k (Thm 5.1): sign-compatibility row swap, s, tau, c1.
-__global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8_t* J, long long m, long long n,
-                                                  long long k, P2Scr s, double2* Sb = nullptr, long long lds = 0,
-                                                  int nrs = 0) {
-  __shared__ double2 sh[T2 / 32];
+// Reflector for column k (Thm 5.1): sign-compatibility row swap, s, tau, c1; hn = the
+// column's J-norm over rows >= k (uniform over the block).
+__device__ void refl_prep_body(double2* F, long long ld, int8_t* J, long long m, long long n, long long k, P2Scr s,
+                               double2* Sb, long long lds, int nrs, const double hn) {
   double2* f = F + k * ld;
-  const double hn = jdot(f, f, J, k, m, true, sh).x;
   if (hn == 0.0 || !isfinite(hn)) {
     if (threadIdx.x == 0 && s.ctl[3] == 0) s.ctl[3] = -7;
     return;
@@ -297,6 +295,15 @@ __global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8
   }
 }
 
+__global__ void __launch_bounds__(T2) k_refl_prep(double2* F, long long ld, int8_t* J, long long m, long long n,
+                                                  long long k, P2Scr s, double2* Sb = nullptr, long long lds = 0,
+                                                  int nrs = 0) {
+  __shared__ double2 sh[T2 / 32];
+  double2* f = F + k * ld;
+  const double hn = jdot(f, f, J, k, m, true, sh).x;
+  refl_prep_body(F, ld, J, m, n, k, s, Sb, lds, nrs, hn);
+}
+
 // columns j > k: x += tau s (s^* J x)   (or, for QR with useJ = 0: x += (-2/vv) v (v^* x))
 __global__ void __launch_bounds__(T2) k_refl_apply(double2* F, long long ld, const int8_t* J, long long m,
                                                    long long k, long long j0, const long long* colmap, int useJ,
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(T2) k_refl_apply(double2* F, long long ld, con
 }
 
 __global__ void k_refl_fin(double2* F, long long ld, long long m, long long k, P2Scr s) {
-  if (s.ctl[3]) return;
+  if (s.ctl[3] || s.ctl[8]) return;
   double2* f = F + k * ld;
   for (long long i = k + 1 + threadIdx.x; i < m; i += blockDim.x) f[i] = cmk(0, 0);
   if (threadIdx.x == 0) f[k] = cmk(-s.dctl[1], -s.dctl[2]);
@@ -523,10 +530,35 @@ __global__ void __launch_bounds__(T2) k_sdots(const double2* snew, const double2
   if (threadIdx.x == 0) tv[blockIdx.x] = d;
 }
 
+// k_panel_add + k_refl_fin of the JQR in one launch (F column k: rows > k zeroed, row k = -c1)
+__global__ void __launch_bounds__(T2) k_panel_add_fin(double2* S, long long lds, const double2* sv, long long r0,
+                                                      long long m, int nr, double2* T, const double2* tv, P2Scr s,
+                                                      double2* F, long long ld) {
+  if (s.ctl[3] || s.ctl[8]) return;
+  const double tau = s.dctl[0];
+  double2* col = S + (size_t)nr * lds;
+  double2* f = F + r0 * ld;
+  for (long long i = blockIdx.x * (long long)T2 + threadIdx.x; i < m; i += (long long)gridDim.x * T2) {
+    col[i] = i >= r0 ? sv[i] : cmk(0, 0);
+    if (i > r0) f[i] = cmk(0, 0);
+  }
+  if (blockIdx.x == 0) {
+    for (int c = threadIdx.x; c < nr; c += T2) {
+      double2 a = cmk(0, 0);
+      for (int i = c; i < nr; i++) a = cadd(a, cmul(tv[i], T[i + c * PB]));   // T lower triangular
+      T[nr + c * PB] = cmk(tau * a.x, tau * a.y);
+    }
+    if (threadIdx.x == 0) {
+      T[nr + nr * PB] = cmk(tau, 0.0);
+      f[r0] = cmk(-s.dctl[1], -s.dctl[2]);
+    }
+  }
+}
+
 // S[:, nr] = s (rows >= r0; zero above); T row nr = tau (tv^T T), T[nr][nr] = tau
 __global__ void __launch_bounds__(T2) k_panel_add(double2* S, long long lds, const double2* sv, long long r0,
                                                   long long m, int nr, double2* T, const double2* tv, P2Scr s) {
-  if (s.ctl[3]) return;
+  if (s.ctl[3] || s.ctl[8]) return;
   const double tau = s.dctl[0];
   double2* col = S + (size_t)nr * lds;
   for (long long i = blockIdx.x * (long long)T2 + threadIdx.x; i < m; i += (long long)gridDim.x * T2)
@@ -562,6 +594,25 @@ __global__ void k_panel_rows(const double2* X, long long ld, const int8_t* J, co
     for (int i = 0; i < nr; i++) r = cadd(r, cmul(S[kr + (size_t)i * lds], w[i]));
     const double a2 = r.x * r.x + r.y * r.y;
     hd[j] -= J ? (double)J[kr] * a2 : a2;
+  }
+}
+
+// k_tw + k_form in one launch: every CTA forms w = T y (nr x nr, in shared memory), then
+// out[r] = x[r] + (S w)[r] for r >= r0
+__global__ void k_form_tw(const double2* x, double2* out, const double2* S, long long lds, const double2* T,
+                          const double2* y, int nr, long long r0, long long m) {
+  __shared__ double2 w[PB];
+  if (threadIdx.x < nr) {
+    const int i = threadIdx.x;
+    double2 a = cmk(0, 0);
+    for (int c = 0; c <= i; c++) a = cadd(a, cmul(T[i + c * PB], y[c]));
+    w[i] = a;
+  }
+  __syncthreads();
+  for (long long r = r0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < m; r += (long long)gridDim.x * blockDim.x) {
+    double2 a = x[r];
+    for (int i = 0; i < nr; i++) a = cadd(a, cmul(S[r + (size_t)i * lds], w[i]));
+    out[r] = a;
   }
 }
 
@@ -666,10 +717,17 @@ __global__ void __launch_bounds__(T2) k_qr_colpiv_blk(double2* G, long long ldg,
 
 // Householder vector of the (explicit) contiguous column k of the QR: v = x - alph e_k,
 // tau = -2 / v^* v, x[k] = alph (R(k,k)); writes v to s.s
-__global__ void __launch_bounds__(T2) k_qr_prep_c(double2* X, long long ld, long long m, long long k, P2Scr s) {
+// pd (planned column-pivoted QR): the planned Schur diagonal, checked as in k_plan_check_qr
+__global__ void __launch_bounds__(T2) k_qr_prep_c(double2* X, long long ld, long long m, long long k, P2Scr s,
+                                                  const double2* pd = nullptr) {
   __shared__ double2 sh[T2 / 32];
   double2* x = X + k * ld;
-  const double nrm = sqrt(jdot(x, x, nullptr, k, m, false, sh).x);
+  const double nn = jdot(x, x, nullptr, k, m, false, sh).x;
+  if (pd && threadIdx.x == 0) {
+    const double ap = pd[3 * k].x;
+    if (!(nn > 0.0) || !isfinite(nn) || fabs(nn - ap) > 0.25 * fmax(nn, fabs(ap))) s.ctl[5] = 1;
+  }
+  const double nrm = sqrt(nn);
   if (nrm == 0.0) {
     if (threadIdx.x == 0 && s.ctl[3] == 0) s.ctl[3] = -7;
     return;
@@ -727,15 +785,41 @@ struct BkPlan {
   long long* sw2;  // [n] second swap partner (Bunch-Kaufman), -1 if none
   int* sw2pos;     // [n] position (k or k + 1) the second swap moves into
   double2* d;      // [3 n] predicted H_kk, H_{k+1,k}, H_{k+1,k+1} at the pivot
+  double* dg;      // [n] the current diagonal, contiguous (the diagonal-pivot search reads it)
   int* st;         // [0] next k, [2] k of the last step, [3] its type (0: none), [4] error
 };
+
+constexpr int TS = 1024;   // threads of the pivot-selection CTA (memory-latency bound)
+
+// block argmax for TS threads (same tie rule as block_argmax)
+__device__ void block_argmax_ts(double& v, long long& i) {
+  __shared__ double bv[TS / 32];
+  __shared__ long long bi[TS / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+  }
+  if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = v; bi[threadIdx.x >> 5] = i; }
+  __syncthreads();
+  v = bv[0];
+  i = bi[0];
+  for (int w = 1; w < TS / 32; w++)
+    if (bv[w] > v || (bv[w] == v && bi[w] < i)) { v = bv[w]; i = bi[w]; }
+  __syncthreads();
+}
+
+__global__ void k_bk_diag(const double2* H, long long ld, long long n, double* dg) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    dg[j] = H[j + j * ld].x;
+}
 
 __device__ __forceinline__ double2 hget(const double2* H, long long ld, long long j, long long l) {
   return j >= l ? H[j + l * ld] : cconj(H[l + j * ld]);
 }
 
 // symmetric interchange of indices a < b of the trailing Hermitian block [k, n) (lower storage)
-__device__ void hswap(double2* H, long long ld, long long n, long long k, long long a, long long b) {
+__device__ void hswap(double2* H, long long ld, long long n, long long k, long long a, long long b, double* dg) {
   if (a == b) return;
   if (a > b) { const long long t = a; a = b; b = t; }
   for (long long l = k + threadIdx.x; l < a; l += blockDim.x) {
@@ -750,6 +834,7 @@ __device__ void hswap(double2* H, long long ld, long long n, long long k, long l
   if (threadIdx.x == 0) {
     const double2 t = H[a + a * ld]; H[a + a * ld] = H[b + b * ld]; H[b + b * ld] = t;
     H[b + a * ld] = cconj(H[b + a * ld]);
+    const double u = dg[a]; dg[a] = dg[b]; dg[b] = u;
   }
   __syncthreads();
 }
@@ -758,7 +843,7 @@ __device__ void hswap(double2* H, long long ld, long long n, long long k, long l
 // k_piv_c on the Schur complement instead of on the columns.
 // diag_only: only the diagonal pivoting (the column-pivoted QR's largest remaining norm on
 // the Schur complements of S = X^* X, i.e. diagonally pivoted Cholesky)
-__global__ void __launch_bounds__(T2) k_bk_select(double2* H, long long ld, long long n, BkPlan pl, int diag_only) {
+__global__ void __launch_bounds__(TS) k_bk_select(double2* H, long long ld, long long n, BkPlan pl, int diag_only) {
   const long long k = pl.st[0];
   if (k >= n) {
     if (threadIdx.x == 0) pl.st[3] = 0;
@@ -767,48 +852,48 @@ __global__ void __launch_bounds__(T2) k_bk_select(double2* H, long long ld, long
   constexpr long long NONE = 0x7fffffffffffffffll;
   double v = -1.0;
   long long jm = NONE;
-  for (long long j = k + threadIdx.x; j < n; j += T2) {
-    const double a = fabs(H[j + j * ld].x);
+  for (long long j = k + threadIdx.x; j < n; j += TS) {
+    const double a = fabs(pl.dg[j]);
     if (a > v) { v = a; jm = j; }
   }
-  block_argmax(v, jm);
+  block_argmax_ts(v, jm);
   if (jm == NONE) {   // NaN diagonal
     if (threadIdx.x == 0 && pl.st[4] == 0) pl.st[4] = -8;
     jm = k;
   }
-  hswap(H, ld, n, k, k, jm);
+  hswap(H, ld, n, k, k, jm, pl.dg);
   int type = 1;
   long long s2 = -1;
   int s2pos = -1;
   if (k < n - 1 && !diag_only) {
     double h1i = -1.0;
     long long ii = NONE;
-    for (long long j = k + 1 + threadIdx.x; j < n; j += T2) {
+    for (long long j = k + 1 + threadIdx.x; j < n; j += TS) {
       const double a = cabs_(H[j + k * ld]);
       if (a > h1i) { h1i = a; ii = j; }
     }
-    block_argmax(h1i, ii);
+    block_argmax_ts(h1i, ii);
     if (ii == NONE) ii = k + 1;
     const double alpha = (1.0 + sqrt(17.0)) / 8.0;
     const double h11 = fabs(H[k + k * ld].x);
     if (!(h11 >= alpha * h1i)) {
       double hij = -1.0;
       long long li = NONE;
-      for (long long l = k + threadIdx.x; l < n; l += T2) {
+      for (long long l = k + threadIdx.x; l < n; l += TS) {
         if (l == ii) continue;
         const double a = cabs_(hget(H, ld, ii, l));
         if (a > hij) { hij = a; li = l; }
       }
-      block_argmax(hij, li);
+      block_argmax_ts(hij, li);
       if (h11 * hij >= alpha * h1i * h1i) {
         type = 1;
       } else if (fabs(H[ii + ii * ld].x) >= alpha * hij) {
         s2 = ii; s2pos = 0;
-        hswap(H, ld, n, k, k, ii);
+        hswap(H, ld, n, k, k, ii, pl.dg);
       } else {
         type = 2;
         s2 = ii; s2pos = 1;
-        hswap(H, ld, n, k, k + 1, ii);
+        hswap(H, ld, n, k, k + 1, ii, pl.dg);
       }
     }
   }
@@ -877,12 +962,16 @@ __global__ void __launch_bounds__(256) k_bk_update(double2* H, long long ld, lon
     if (t == 2) a = cadd(a, cmul(vj[r][1], cconj(ul[c][1])));
     double2& h = H[j + l * ld];
     h = cmk(h.x - a.x, h.y - a.y);
-    if (j == l) h.y = 0.0;   // the diagonal stays real
+    if (j == l) {   // the diagonal stays real (and its contiguous copy current)
+      h.y = 0.0;
+      pl.dg[j] = h.x;
+    }
   }
 }
 
 // The planned column interchanges of position k: F columns (all m rows) and p2
-__global__ void k_plan_swaps(double2* F, long long ld, long long m, long long k, long long* p2, BkPlan pl) {
+__global__ void k_plan_swaps(double2* F, long long ld, long long m, long long k, long long* p2, BkPlan pl, P2Scr s) {
+  if (s.ctl[8]) return;   // the plan was stopped at an earlier column of this panel
   const long long a = pl.sw1[k];
   const long long b = pl.sw2[k];
   const long long bp = k + pl.sw2pos[k];
@@ -902,10 +991,21 @@ __global__ void k_plan_swaps(double2* F, long long ld, long long m, long long k,
 }
 
 // Check a planned pivot against the exact J-Grammian of its formed column(s) fx (, fx2),
-// rows >= k: ctl[5] = 1 when it is off by more than a quarter (or changes sign / inertia).
+// rows >= k: off by more than a quarter (or another sign / inertia) stops the plan --
+// ctl[8] = 1, ctl[9] = k, ctl[10] = reflectors in the panel before it (nr).
+__device__ __forceinline__ bool plan_bad1(double a, double ap) {
+  return !(a != 0.0) || !isfinite(a) || ((a > 0.0) != (ap > 0.0)) || fabs(a - ap) > 0.25 * fmax(fabs(a), fabs(ap));
+}
+__device__ __forceinline__ void plan_stop(P2Scr s, long long k, int nr) {
+  s.ctl[8] = 1;
+  s.ctl[9] = (int)k;
+  s.ctl[10] = nr;
+}
+
 __global__ void __launch_bounds__(T2) k_plan_check(const double2* fx, const double2* fx2, const int8_t* J,
-                                                   long long k, long long m, int type, BkPlan pl, P2Scr s) {
+                                                   long long k, long long m, int type, BkPlan pl, P2Scr s, int nr) {
   __shared__ double2 sh[T2 / 32];
+  if (s.ctl[8]) return;
   const double a = jdot(fx, fx, J, k, m, true, sh).x;
   double c = 0.0;
   double2 b = cmk(0, 0);
@@ -917,7 +1017,7 @@ __global__ void __launch_bounds__(T2) k_plan_check(const double2* fx, const doub
   const double ap = pl.d[3 * k].x;
   bool bad;
   if (type == 1) {
-    bad = !(a != 0.0) || !isfinite(a) || ((a > 0.0) != (ap > 0.0)) || fabs(a - ap) > 0.25 * fmax(fabs(a), fabs(ap));
+    bad = plan_bad1(a, ap);
   } else {
     const double cp = pl.d[3 * k + 2].x;
     const double2 bp = pl.d[3 * k + 1];
@@ -928,7 +1028,26 @@ __global__ void __launch_bounds__(T2) k_plan_check(const double2* fx, const doub
     const double det = a * c - (b.x * b.x + b.y * b.y), detp = ap * cp - (bp.x * bp.x + bp.y * bp.y);
     bad = !isfinite(diff) || !(det != 0.0) || ((det > 0.0) != (detp > 0.0)) || diff > 0.25 * fmax(na, np);
   }
-  if (bad) s.ctl[5] = 1;
+  if (bad) plan_stop(s, k, nr);
+}
+
+// Planned 1x1 pivot in one launch: the formed column fx is checked against the plan (a
+// rejected pivot stops the plan, nothing written), copied into column k (rows >= k0) and
+// turned into its reflector (refl_prep_body, the same arithmetic as k_refl_prep).
+__global__ void __launch_bounds__(T2) k_refl_prep_plan(double2* F, long long ld, int8_t* J, long long m, long long n,
+                                                       long long k, long long k0, const double2* fx, P2Scr s,
+                                                       double2* Sb, long long lds, int nr, BkPlan pl) {
+  __shared__ double2 sh[T2 / 32];
+  if (s.ctl[8] || s.ctl[3]) return;
+  const double hn = jdot(fx, fx, J, k, m, true, sh).x;   // uniform over the block
+  if (plan_bad1(hn, pl.d[3 * k].x)) {
+    if (threadIdx.x == 0) plan_stop(s, k, nr);
+    return;
+  }
+  double2* f = F + k * ld;
+  for (long long i = k0 + threadIdx.x; i < m; i += T2) f[i] = fx[i];
+  __syncthreads();
+  refl_prep_body(F, ld, J, m, n, k, s, Sb, lds, nr, hn);
 }
 
 // Y[i + j PB] = sum over the nb row-chunk partials part[b][i + j nr] (Kahan-compensated, in
@@ -996,7 +1115,7 @@ __global__ void k_scale_j(const double2* S, double2* SJ, long long lds, const in
 size_t phase2_scratch_bytes(int64_t m, int64_t n) {
   // P2Scr, then the JQR pivot plan (BkPlan: 72 bytes per column + control)
   return al256((size_t)n * 8) + 2 * al256((size_t)n * 16) + al256((size_t)m * 16) + 512 + 256 +
-         2 * al256((size_t)n * 4) + 2 * al256((size_t)n * 8) + al256((size_t)3 * n * 16) + 256;
+         2 * al256((size_t)n * 4) + 3 * al256((size_t)n * 8) + al256((size_t)3 * n * 16) + 256;
 }
 
 namespace {
@@ -1009,6 +1128,7 @@ BkPlan carve_plan(char* scr, int64_t m, int64_t n) {
   pl.sw1 = (long long*)p; p += al256((size_t)n * 8);
   pl.sw2 = (long long*)p; p += al256((size_t)n * 8);
   pl.d = (double2*)p; p += al256((size_t)3 * n * 16);
+  pl.dg = (double*)p; p += al256((size_t)n * 8);
   pl.st = (int*)p;
   return pl;
 }
@@ -1226,10 +1346,11 @@ static ghsvd_status gram_plan(Ctx* ctx, Cublas* cb, const double2* X, long long 
                     Fp + np, (int)ld, Fp + np, (int)ld, np > 0 ? &one : &zero, (cuDoubleComplex*)Hb, (int)ldh));
   GH_CUDA(cudaMemsetAsync(pl.st, 0, 32, st));
   GH_CUDA(cudaMemsetAsync(pl.type, 0, (size_t)n * 4, st));
+  k_bk_diag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Hb, ldh, n, pl.dg);
   for (int64_t i = 0; i < n; i++) {
     // the device step index k is >= i (each step advances by 1 or 2): a grid for the
     // trailing block [i + 1, n) covers it; steps past the end are no-ops
-    k_bk_select<<<1, T2, 0, st>>>(Hb, ldh, n, pl, diag_only);
+    k_bk_select<<<1, TS, 0, st>>>(Hb, ldh, n, pl, diag_only);
     const unsigned nt = (unsigned)((n - i - 1 + 31) / 32);
     if (nt) k_bk_update<<<dim3(nt, nt), 256, 0, st>>>(Hb, ldh, n, pl);
   }
@@ -1260,89 +1381,112 @@ static ghsvd_status jqr_planned(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, c
   double2* F = ctx->F;
   int8_t* J = ctx->J;
   long long* p2 = (long long*)ctx->p2;
-  int ctl[8];
+  int ctl[12];
   const unsigned gm = (unsigned)std::min<int64_t>(1024, (m + 255) / 256);
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   *k_fallback = -1;
-  GH_CUDA(cudaMemsetAsync(s.ctl, 0, 32, st));
+  GH_CUDA(cudaMemsetAsync(s.ctl, 0, 48, st));
+  auto rd = [&]() -> ghsvd_status {
+    GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 48, cudaMemcpyDeviceToHost, st));
+    GH_CUDA(cudaStreamSynchronize(st));
+    return GHSVD_OK;
+  };
   int64_t k = 0;
   while (k < n) {
     const int64_t k0 = k;
     int nr = 0;
     bool stop = false;
     GH_CUDA(cudaMemsetAsync(P.T, 0, (size_t)PB * PB * 16, st));
+    // The 1x1 pivots of a panel are enqueued without read-backs: a pivot the check rejects
+    // stops the plan on the device (ctl[8]; the later kernels of the panel return at once)
+    // and the panel's end learns where.  A 2x2 pivot reads the check back first.
     while (k < n && nr + std::max(ptype[k], 1) <= PB) {
       const int type = ptype[k] == 2 && k + 1 < n ? 2 : 1;
-      k_plan_swaps<<<gm, 256, 0, st>>>(F, ld, m, k, p2, pl);
+      k_plan_swaps<<<gm, 256, 0, st>>>(F, ld, m, k, p2, pl, s);
       // the pivot column(s) with the panel's delayed update, into fx (, fx2)
       for (int c = 0; c < type; c++) {
         double2* x = F + (k + c) * ld;
         double2* out = c ? P.fx2 : P.fx;
         if (nr) {
           k_ycol<<<nr, T2, 0, st>>>(x, P.S, P.lds, J, k0, m, P.u);
-          k_tw<<<1, 64, 0, st>>>(P.T, P.u, P.tv, nr);
-          k_form<<<gm, 256, 0, st>>>(x, out, P.S, P.lds, P.tv, nr, k0, m);
+          k_form_tw<<<gm, 256, 0, st>>>(x, out, P.S, P.lds, P.T, P.u, nr, k0, m);
         } else {
           GH_CUDA(cudaMemcpyAsync(out + k0, x + k0, (size_t)(m - k0) * 16, cudaMemcpyDeviceToDevice, st));
         }
       }
-      k_plan_check<<<1, T2, 0, st>>>(P.fx, P.fx2, J, k, m, type, pl, s);
-      GH_CUDA(cudaMemcpyAsync(ctl, s.ctl, 32, cudaMemcpyDeviceToHost, st));
-      GH_CUDA(cudaStreamSynchronize(st));
-      if (ctl[3]) return GHSVD_OK;   // error flag: the caller reports it
-      if (ctl[5]) {
-        stop = true;
-        break;
-      }
-      for (int c = 0; c < type; c++)
-        GH_CUDA(cudaMemcpyAsync(F + (k + c) * ld + k0, (c ? P.fx2 : P.fx) + k0, (size_t)(m - k0) * 16,
-                                cudaMemcpyDeviceToDevice, st));
-      // the reflector(s), as in jqr_blocked
-      if (type == 2) k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, +1, s);
-      for (int t = 0; t < type; t++) {
-        const long long kk = k + t;
-        k_refl_prep<<<1, T2, 0, st>>>(F, ld, J, m, n, kk, s, P.S, P.lds, nr);
-        if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, J, kk, m, P.tv);
-        k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, kk, m, nr, P.T, P.tv, s);
+      if (type == 1) {
+        k_refl_prep_plan<<<1, T2, 0, st>>>(F, ld, J, m, n, k, k0, P.fx, s, P.S, P.lds, nr, pl);
+        if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, J, k, m, P.tv);
+        k_panel_add_fin<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s, F, ld);
         nr++;
-        if (t == 0 && type == 2) k_refl_apply<<<1, T2, 0, st>>>(F, ld, J, m, kk, kk + 1, nullptr, 1, s);
-        k_refl_fin<<<1, T2, 0, st>>>(F, ld, m, kk, s);
+      } else {
+        k_plan_check<<<1, T2, 0, st>>>(P.fx, P.fx2, J, k, m, 2, pl, s, nr);
+        TRY(rd());
+        if (ctl[3]) return GHSVD_OK;   // error flag: the caller reports it
+        if (ctl[8]) {
+          stop = true;
+          break;
+        }
+        for (int c = 0; c < 2; c++)
+          GH_CUDA(cudaMemcpyAsync(F + (k + c) * ld + k0, (c ? P.fx2 : P.fx) + k0, (size_t)(m - k0) * 16,
+                                  cudaMemcpyDeviceToDevice, st));
+        // the 2x2 pivot as in jqr_blocked: rotation, two reflectors, rotation undone
+        k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, +1, s);
+        for (int t = 0; t < 2; t++) {
+          const long long kk = k + t;
+          k_refl_prep<<<1, T2, 0, st>>>(F, ld, J, m, n, kk, s, P.S, P.lds, nr);
+          if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, J, kk, m, P.tv);
+          k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, kk, m, nr, P.T, P.tv, s);
+          nr++;
+          if (t == 0) k_refl_apply<<<1, T2, 0, st>>>(F, ld, J, m, kk, kk + 1, nullptr, 1, s);
+          k_refl_fin<<<1, T2, 0, st>>>(F, ld, m, kk, s);
+        }
+        k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, -1, s);
       }
-      if (type == 2) k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, -1, s);
       P2CHK();
       k += type;
     }
-    // flush: the delayed update of the stale columns [k, n)
-    if (k < n && nr) {
+    TRY(rd());
+    if (ctl[3]) return GHSVD_OK;
+    int64_t kf = k;
+    int nrf = nr;
+    if (ctl[8]) {   // stopped at column ctl[9] with ctl[10] reflectors in the panel
+      stop = true;
+      kf = ctl[9];
+      nrf = ctl[10];
+    }
+    // flush: the delayed update of the stale columns [kf, n)
+    if (kf < n && nrf) {
       // Y = (J S)^* X over rows [k0, m) as partials over row chunks of 32 (strided-batched
       // ZGEMMs, column slabs sized to the free panel buffer), summed with compensation
       // (k_sum_chunks): short accumulations, as in the column search's block-reduced dots
-      k_scale_j<<<gm, 256, 0, st>>>(P.S, P.SJ, P.lds, J, k0, m, nr);
+      k_scale_j<<<gm, 256, 0, st>>>(P.S, P.SJ, P.lds, J, k0, m, nrf);
       const long long rows = m - k0, kc = 32, nb = (rows + kc - 1) / kc, full = rows / kc;
-      const long long ns = std::max<long long>(1, std::min<long long>(n - k, P.part_cap / (nb * nr)));
-      for (long long j0 = k; j0 < n; j0 += ns) {
-        const long long ncol = std::min<long long>(ns, n - j0), pstride = (long long)nr * ncol;
+      const long long ns = std::max<long long>(1, std::min<long long>(n - kf, P.part_cap / (nb * nrf)));
+      for (long long j0 = kf; j0 < n; j0 += ns) {
+        const long long ncol = std::min<long long>(ns, n - j0), pstride = (long long)nrf * ncol;
         if (full > 0)
-          P2CUB(cb->ZgemmSB((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, nr, (int)ncol, (int)kc, &one,
+          P2CUB(cb->ZgemmSB((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, nrf, (int)ncol, (int)kc, &one,
                             (const cuDoubleComplex*)(P.SJ + k0), (int)P.lds, kc,
                             (const cuDoubleComplex*)(F + k0 + j0 * ld), (int)ld, kc, &zero,
-                            (cuDoubleComplex*)P.part, nr, pstride, (int)full));
+                            (cuDoubleComplex*)P.part, nrf, pstride, (int)full));
         if (full < nb)   // the ragged last chunk
-          P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, nr, (int)ncol, (int)(rows - full * kc),
-                          &one, (const cuDoubleComplex*)(P.SJ + k0 + full * kc), (int)P.lds,
-                          (const cuDoubleComplex*)(F + k0 + full * kc + j0 * ld), (int)ld, &zero,
-                          (cuDoubleComplex*)(P.part + full * pstride), nr));
-        k_sum_chunks<<<(unsigned)((pstride + 255) / 256), 256, 0, st>>>(P.part, (int)nb, pstride, nr, ncol,
+          P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, nrf, (int)ncol,
+                          (int)(rows - full * kc), &one, (const cuDoubleComplex*)(P.SJ + k0 + full * kc),
+                          (int)P.lds, (const cuDoubleComplex*)(F + k0 + full * kc + j0 * ld), (int)ld, &zero,
+                          (cuDoubleComplex*)(P.part + full * pstride), nrf));
+        k_sum_chunks<<<(unsigned)((pstride + 255) / 256), 256, 0, st>>>(P.part, (int)nb, pstride, nrf, ncol,
                                                                          P.Y + j0 * PB);
       }
-      P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, nr, (int)(n - k), nr, &one,
-                      (const cuDoubleComplex*)P.T, PB, (const cuDoubleComplex*)(P.Y + k * PB), PB, &zero,
-                      (cuDoubleComplex*)(P.W + k * PB), PB));
-      TRY(flush_update(ctx, cb, P, F, ld, k0, m, k, n, nr));
+      P2CUB(cb->Zgemm((cublasHandle_t)ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, nrf, (int)(n - kf), nrf, &one,
+                      (const cuDoubleComplex*)P.T, PB, (const cuDoubleComplex*)(P.Y + kf * PB), PB, &zero,
+                      (cuDoubleComplex*)(P.W + kf * PB), PB));
+      TRY(flush_update(ctx, cb, P, F, ld, k0, m, kf, n, nrf));
       P2CHK();
     }
     if (stop) {
-      *k_fallback = k;
+      *k_fallback = kf;
+      GH_CUDA(cudaMemsetAsync(s.ctl, 0, 48, st));   // the column search starts clean
       return GHSVD_OK;
     }
   }
@@ -1398,12 +1542,10 @@ static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, do
         if (use_plan) k_plan_swap_qr<<<gm, 256, 0, st>>>(X, ld, m, Rf, ldr, n, k, p2, *plan);
         if (nr) {
           k_ycol<<<nr, T2, 0, st>>>(X + k * ld, P.S, P.lds, nullptr, k0, m, P.u);
-          k_tw<<<1, 64, 0, st>>>(P.T, P.u, P.tv, nr);
-          k_form<<<gm, 256, 0, st>>>(X + k * ld, X + k * ld, P.S, P.lds, P.tv, nr, k0, m);
+          k_form_tw<<<gm, 256, 0, st>>>(X + k * ld, X + k * ld, P.S, P.lds, P.T, P.u, nr, k0, m);
         }
-        if (use_plan) k_plan_check_qr<<<1, T2, 0, st>>>(X + k * ld, k, m, *plan, s);
       }
-      k_qr_prep_c<<<1, T2, 0, st>>>(X, ld, m, k, s);
+      k_qr_prep_c<<<1, T2, 0, st>>>(X, ld, m, k, s, use_plan ? plan->d : nullptr);
       if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, nullptr, k, m, P.tv);
       k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s);
       nr++;

@@ -28,9 +28,10 @@ def main():
     for mode in args.modes:
         ctx = ghsvd.Context(m, n, NL, variant="bo")
         ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
-        Ft = torch.empty((n, m), dtype=torch.complex128, device=dev).t()
-        Gt = torch.empty((n, m), dtype=torch.complex128, device=dev).t()
-        Jt = torch.empty(m, dtype=torch.int8, device=dev)
+        o = n & 1   # odd n: the factors are exported bordered (one more row and column)
+        Ft = torch.empty((n + o, m + o), dtype=torch.complex128, device=dev).t()
+        Gt = torch.empty((n + o, m + o), dtype=torch.complex128, device=dev).t()
+        Jt = torch.empty(m + o, dtype=torch.int8, device=dev)
         ctx.export_factors(Ft, Jt, Gt)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -39,9 +40,9 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         secs = e0.elapsed_time(e1) * 1e-3
-        Fr = torch.empty((n, n), dtype=torch.complex128, device=dev).t()
-        Gr = torch.empty((n, n), dtype=torch.complex128, device=dev).t()
-        Jr = torch.empty(n, dtype=torch.int8, device=dev)
+        Fr = torch.empty((n + o, n + o), dtype=torch.complex128, device=dev).t()
+        Gr = torch.empty((n + o, n + o), dtype=torch.complex128, device=dev).t()
+        Jr = torch.empty(n + o, dtype=torch.int8, device=dev)
         ctx.export_factors(Fr, Jr, Gr)
         _, _, _, p2 = ctx.get_factors() if n <= 2048 else (None, None, None, None)
         if p2 is None:   # p2 only (avoid copying the factors to the host)
@@ -51,10 +52,10 @@ def main():
             ctx._L.ghsvd_get_factors(ctx._h, ctypes.byref(mm), ctypes.byref(nn), None, 0, None, None, 0,
                                      p2.ctypes.data_as(ctypes.c_void_p))
         pt = torch.from_numpy(p2).to(dev)
-        H = Ft.conj().T @ (Jt.double()[:, None] * Ft)
-        S = Gt.conj().T @ Gt
-        Hr = Fr.conj().T @ (Jr.double()[:, None] * Fr)
-        Sr = Gr.conj().T @ Gr
+        H = (Ft.conj().T @ (Jt.double()[:, None] * Ft))[:n, :n]
+        S = (Gt.conj().T @ Gt)[:n, :n]
+        Hr = (Fr.conj().T @ (Jr.double()[:, None] * Fr))[:n, :n]
+        Sr = (Gr.conj().T @ Gr)[:n, :n]
         eh = float(torch.linalg.norm(Hr - H[pt][:, pt]) / torch.linalg.norm(H))
         es = float(torch.linalg.norm(Sr - S[pt][:, pt]) / torch.linalg.norm(S))
         print(json.dumps({"config": args.config, "mode": mode, "seconds": secs,

@@ -214,7 +214,9 @@ ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* 
  * first one off by more than a quarter (or of another inertia) hands over to the column
  * search.  GHSVD_REDUCE_COLSEARCH: the column search throughout (pivot searches on
  * downdated J-norms, exact at every panel start; a panel is cut when a formed pivot column
- * disagrees with its estimate).  The QR of G P2 searches its column-pivoted form likewise.
+ * disagrees with its estimate).  The column-pivoted QR of G P2 plans its pivots likewise on
+ * S = (G P2)^* (G P2) (diagonally pivoted Cholesky of its Schur complements, checked per
+ * panel; GHSVD_REDUCE_COLSEARCH: the downdated-norm search).
  * The pivot sequence may differ from the unblocked one on near-ties; the Grammians and
  * the pencil are preserved alike (tests).  GHSVD_REDUCE_UNBLOCKED: one reflector
  * application per column (round 1), also the fallback when cuBLAS cannot be loaded or

@@ -199,3 +199,34 @@ def test_planned_jqr_on_illconditioned_config3_recipe(gh):
         ctx.close()
         assert st["converged"]
     assert np.max(np.abs(lams[0] - lams[1]) / np.abs(lams[1])) <= 1e-6
+
+
+def test_planned_pivots_fall_back_to_the_column_search(gh):
+    """Columns of F and G graded over 12 decades: the Schur complements of the explicitly
+    formed H = F^* J F and S = G^* G lose the small columns in rounding (kappa(H) ~ 1e24),
+    so the planned pivots there disagree with the formed columns.  The check must reject
+    them and the column search must finish the factorization (R2-6): fallback_col >= 0, the
+    Grammians preserved as by the column search throughout, the same inertia."""
+    m, n = 400, 160
+    P = inputs.random_pencil(77, m, n, 0.5)
+    sc = np.logspace(0, -12, n)
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(n)          # graded columns in random order
+    F = P.F * sc[perm][None, :]
+    G = P.G * sc[perm[::-1]][None, :]
+    H = F.conj().T @ (P.J[:, None] * F)
+    S = G.conj().T @ G
+    res = {}
+    for mode in ("planned", "colsearch"):
+        ctx = gh.Context(m, n)
+        ctx.set_factors(F, P.J, G)
+        ctx.reduce(colpiv=True, **MODES[mode])
+        Fr, Jr, Gr, p = ctx.get_factors()
+        res[mode] = (ctx.reduce_fallback_col, int((Jr > 0).sum()))
+        eh = np.linalg.norm(Fr.conj().T @ (Jr[:, None] * Fr) - H[np.ix_(p, p)]) / np.linalg.norm(H)
+        es = np.linalg.norm(Gr.conj().T @ Gr - S[np.ix_(p, p)]) / np.linalg.norm(S)
+        assert eh < 1e-11 and es < 1e-12, (mode, eh, es)
+        assert np.abs(np.tril(Gr, -1)).max() == 0
+        ctx.close()
+    assert res["planned"][0] >= 0          # the plan was stopped and the search took over
+    assert res["planned"][1] == res["colsearch"][1]

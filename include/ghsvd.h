@@ -225,9 +225,10 @@ ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* 
  * GHSVD_E_NONFINITE on non-finite J-norms; INVALID_ARG on unknown flags. */
 enum { GHSVD_REDUCE_COLPIV = 1, GHSVD_REDUCE_UNBLOCKED = 2, GHSVD_REDUCE_BLOCKED = 4, GHSVD_REDUCE_COLSEARCH = 8 };
 ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
-/* After a blocked ghsvd_reduce with planned JQR pivots: the first column whose planned pivot
- * the exact J-Grammian rejected (the column search continued from there), or -1 (every
- * planned pivot used, or no planned JQR ran).  No GPU work. */
+/* After ghsvd_reduce: the first column whose planned JQR pivot the exact J-Grammian of its
+ * formed column rejected (the column search continued from there); -1 if every planned
+ * pivot was used; -2 if no planned JQR ran (unblocked form -- small problems, or when the
+ * output-Z buffer cannot hold the panel --, or GHSVD_REDUCE_COLSEARCH).  No GPU work. */
 int64_t ghsvd_reduce_fallback_col(ghsvd_ctx ctx);
 
 /* Export the factors the sweep will start from (after factor/set_factors,

@@ -317,7 +317,7 @@ ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
   // redone by the next prepare()
   ctx->m = ctx->m_user;
   ctx->n = ctx->n_user;
-  ctx->p2_fallback_col = -1;
+  ctx->p2_fallback_col = -2;   // no planned JQR (yet)
   ctx->p2_fallback_qr = -1;
   TRY(phase2_reduce(ctx, flags));
   ctx->have_p2 = true;

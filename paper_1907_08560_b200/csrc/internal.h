@@ -75,7 +75,7 @@ struct Ctx {
   // blocked partition of the last blocked sweep (host copies)
   std::vector<int> blk_start, blk_width;
   int blk_nsup = 0;              // resolved super blocks of a LEVEL3 / HIER ordering (ordering.h)
-  int64_t p2_fallback_col = -1;  // planned JQR: first column whose planned pivot was rejected (-1: none)
+  int64_t p2_fallback_col = -2;  // planned JQR: first column whose planned pivot was rejected (-1: none, -2: no plan)
   int64_t p2_fallback_qr = -1;   // planned column-pivoted QR: end of the panel with the first rejected pivot
   // multi-GPU
   void* comm;                    // ncclComm_t (opaque)

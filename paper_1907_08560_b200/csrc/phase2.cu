@@ -1627,7 +1627,7 @@ static ghsvd_status phase2_reduce_blocked(Ctx* ctx, int flags, Cublas* cb) {
     TRY(gram_plan(ctx, cb, ctx->F, ctx->ldm, ctx->npos, 0, ctx->Z, ctx->ldn, pl, ptype));
     int64_t kf = -1;
     TRY(jqr_planned(ctx, cb, P, s, pl, ptype, &kf));
-    ctx->p2_fallback_col = kf;
+    ctx->p2_fallback_col = kf;   // -1: every planned pivot used
     if (kf >= 0) TRY(jqr_blocked(ctx, cb, P, s, kf));
   }
   int ctl[8];
@@ -1705,7 +1705,10 @@ ghsvd_status phase2_reduce(Ctx* ctx, int flags) {
   // logic outweighs the traffic it saves (config 2, 1568 x 1024: 0.26 s blocked vs 0.09 s)
   const bool big = (double)m * (double)n * (double)n >= 2e10;
   if (!(flags & GHSVD_REDUCE_UNBLOCKED) && (big || (flags & GHSVD_REDUCE_BLOCKED))) {
-    const size_t need = ((size_t)round_up(m, 16) * (2 * PB + 2) + PB * PB + 2 * (size_t)PB * n + 2 * PB + m) * 16;
+    // panel, its J-scaled copy, two formed columns, T, Y, W, and at least one column slab of
+    // the flush's 32-row chunk partials (PB per chunk)
+    const size_t need = ((size_t)round_up(m, 16) * (2 * PB + 2) + PB * PB + 2 * (size_t)PB * n + 2 * PB +
+                         (size_t)((m + 31) / 32 + 1) * PB) * 16;
     const size_t have = (size_t)ctx->ldn * (ctx->n_cap + 1) * 16;
     Cublas* cb = cublas_lib();
     if (cb && need <= have) {

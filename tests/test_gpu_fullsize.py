@@ -300,6 +300,21 @@ def test_c3_converged_lambda_vs_stored_oracle(gh, c3):
         assert abs(_C3_LAM["bo"][1] - mb["stats"]["sweeps"]) <= 1
 
 
+def test_c3_hier_ordering_converged_lambda_vs_stored_oracle(gh, c3):
+    """The bench's configuration of the headline config: BO in the HIER block ordering
+    (4 super blocks, reading R2-5) -- converged eigenvalues <= 1e-6 of the oracle's stored
+    pointwise solve, residuals on sampled pairs as for the round-robin solve."""
+    meta, lo = _stored_c3("pointwise")
+    assert inputs.fingerprint_close(inputs.fingerprint(c3), meta["fingerprint"])
+    ctx = _ctx_c3(gh, c3, variant="bo", max_sweeps=64, ordering="hier", super_blocks=4)
+    st = ctx.sweep()
+    lam = ctx.extract(want_z=False)[0].copy()
+    ctx.close()
+    err = _relerr(lam, lo)
+    print(f"c3 HIER: {st['sweeps']} sweeps, {st['seconds']:.2f} s, lambda vs stored oracle {err:.2e}")
+    assert st["converged"] and err <= 1e-6
+
+
 @pytest.fixture(scope="module")
 def c4():
     kind, at = inputs.make_config(4)

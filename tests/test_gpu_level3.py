@@ -87,6 +87,23 @@ def test_level3_block_steps_elementwise(gh, ordering, nsup):
         assert (np.linalg.norm(X - Y, axis=0) / np.linalg.norm(Y, axis=0)).max() < 1e-10
 
 
+@pytest.mark.parametrize("ordering,variant,want_x", [("hier", "bo", False), ("hier", "fb", False),
+                                                    ("hier", "bo", True), ("level3", "bo", True)])
+def test_level3_orderings_odd_n_fb_and_x(gh, ordering, variant, want_x):
+    """Odd n (bordered to even order, Sec 6.3.2), FB inner sweeps, and X = Z^{-1} (NEXT-1)
+    in the Level-3 orderings against the oracle's blocked sweep in the same ordering."""
+    P = inputs.known_hyperbolic(35, 150, 63, 0.4)
+    st, (lam, sf, sg, Z), X = solve(gh, P, 8, ordering, 4, variant, want_x=want_x)
+    F0, J0, G0 = device_layout(P.F, P.J, P.G)
+    Fo, Go, Zp, sto = oracle.hz_blocked(F0, J0, G0, 8, inner_sweeps=1 if variant == "bo" else 30, cmax=64,
+                                        ordering=ORD[ordering], nsup=4)
+    assert st["converged"] and sto["converged"] and abs(st["sweeps"] - sto["sweeps"]) <= 1
+    assert relerr(lam, P.lam_true) <= 1e-9
+    assert residual(P.F, P.J, P.G, lam, Z) <= 1e-12 * 63
+    if want_x:
+        assert np.abs(X @ Z - np.eye(63)).max() < 1e-10
+
+
 def test_level3_round_robin_limits_bitwise(gh):
     """LEVEL3 with 2 super blocks (or one block column per super block), HIER with one block
     column per super block: the round-robin, bitwise."""

@@ -580,8 +580,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant, "max_sweeps": args.max_sweeps,
                    "ordering": ordering if blocked else "round-robin (pointwise)",
-                   "super_blocks": (args.super_blocks or (2 * ws if ws > 1 else 4)) if blocked and ordering != "rr"
-                   else None,
+                   "nblocks": stats[-1].get("nblocks") if blocked else None,
+                   "super_blocks": stats[-1].get("super_blocks") if blocked and ordering != "rr" else None,
                    "want_x": bool(args.want_x),
                    "l2": f"inputs ({2 * mb * nb * 16 / 1e9:.2f} GB) vs L2 126 MB",
                    "phase2": ("column-pivoted QR of G P2 (--reduce colpiv, PAPER.md:925-943)" if args.reduce == "colpiv"

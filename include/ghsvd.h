@@ -119,7 +119,8 @@ typedef struct {
                           last-CTA end per launch) as CSV to this path (NULL = off) */
   int super_blocks;    /* LEVEL3 / HIER orderings: number of super blocks, even, dividing the number of
                           block columns (HIER: an even number of block columns per super block, or 1);
-                          0 = 2 * world_size, or 4 on one GPU */
+                          0 = 2 * world_size; on one GPU 4, or one super block per block column (the
+                          round-robin) when the automatic partition has fewer than 32 block columns */
 } ghsvd_options;
 /* ghsvd_options.schedule bits.  ghsvd_default_options seeds schedule, groups, gram_splits and
  * trace_path from the environment (GHSVD_SERIAL, GHSVD_PRIO=0, GHSVD_SPLIT_BND, GHSVD_GRAM3M=0,
@@ -162,6 +163,9 @@ typedef struct {
      low-priority stream that fills idle SMs and are excluded here. */
   uint64_t launches_update_fg;
   double flops_update_fg, t_update_fg;
+  /* blocked: the partition and ordering the sweep ran (block columns, super blocks of a
+     LEVEL3 / HIER ordering (0: round-robin), block steps per sweep) */
+  int nblocks, super_blocks, steps_per_sweep;
 } ghsvd_stats;
 
 /* Fill *opts with the defaults described above (device 0, world_size 1). */

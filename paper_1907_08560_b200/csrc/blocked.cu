@@ -48,19 +48,28 @@ namespace {
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
-int resolve_nsup(const ghsvd_options* o);
+int resolve_nsup(const ghsvd_options* o, int64_t nb_rr);
+
+// the round-robin partition: width w <= 32 -> block pivots of order <= 64
+int64_t auto_nblk_rr(int64_t n, const ghsvd_options* o) {
+  if (o->nblocks > 0) return o->nblocks;
+  int64_t nb = (n + 31) / 32;
+  nb += nb & 1;
+  const int64_t P = std::max(1, o->world_size);
+  return std::max<int64_t>(2, round_up(nb, 2 * P));
+}
 
 // tuning knobs (experiments only; defaults are the measured best)
 int auto_nblk(int64_t n, const ghsvd_options* o) {
   if (o->nblocks > 0) return o->nblocks;
-  int64_t nb = (n + 31) / 32;      // width w <= 32 -> block pivots of order <= 64
-  nb += nb & 1;
+  int64_t nb = auto_nblk_rr(n, o);
   const int64_t P = std::max(1, o->world_size);
-  nb = round_up(nb, 2 * P);
   // Level-3 orderings: whole super blocks (HIER: an even number of block columns in each)
-  const int64_t ns = resolve_nsup(o);
-  if (o->ordering == GHSVD_ORDER_LEVEL3) nb = round_up(nb, std::lcm<int64_t>(2 * P, std::max<int64_t>(2, ns)));
-  if (o->ordering == GHSVD_ORDER_HIER) nb = round_up(nb, std::lcm<int64_t>(2 * P, 2 * std::max<int64_t>(2, ns)));
+  const int64_t ns = resolve_nsup(o, nb);
+  if (ns != nb) {   // (ns == nb: one block column per super block, nothing to round)
+    if (o->ordering == GHSVD_ORDER_LEVEL3) nb = round_up(nb, std::lcm<int64_t>(2 * P, std::max<int64_t>(2, ns)));
+    if (o->ordering == GHSVD_ORDER_HIER) nb = round_up(nb, std::lcm<int64_t>(2 * P, 2 * std::max<int64_t>(2, ns)));
+  }
   if (o->ordering != GHSVD_ORDER_ROUND_ROBIN && nb > n) nb = n - (n & 1);
   return (int)std::max<int64_t>(2, nb);
 }
@@ -73,12 +82,15 @@ struct BlkPlan {
   int nst;    // block steps per sweep
 };
 
-// super blocks of the LEVEL3 / HIER orderings: the option, else one super pair per rank
-// (4 super blocks on one GPU)
-int resolve_nsup(const ghsvd_options* o) {
+// super blocks of the LEVEL3 / HIER orderings: the option, else one super pair per rank; on
+// one GPU 4, or (small problems, < 32 block columns in the round-robin partition) one super
+// block per block column, which IS the round-robin (rounding the partition up to whole even
+// super blocks would only shrink the blocks)
+int resolve_nsup(const ghsvd_options* o, int64_t nb_rr) {
   if (o->ordering == GHSVD_ORDER_ROUND_ROBIN) return 0;
   if (o->super_blocks > 0) return o->super_blocks;
-  return o->world_size > 1 ? 2 * o->world_size : 4;
+  if (o->world_size > 1) return 2 * o->world_size;
+  return nb_rr >= 32 ? 4 : (int)nb_rr;
 }
 
 BlkPlan make_plan(const Ctx* ctx) {
@@ -87,7 +99,7 @@ BlkPlan make_plan(const Ctx* ctx) {
   const int P = std::max(1, ctx->o.world_size);
   p.K = p.nblk / 2 / P;
   p.slot0 = ctx->o.rank * p.K;
-  p.nsup = resolve_nsup(&ctx->o);
+  p.nsup = resolve_nsup(&ctx->o, auto_nblk_rr(ctx->n, &ctx->o));
   p.nst = blk_order_check(ctx->o.ordering, p.nblk, p.nsup) ? -1 : (int)blk_order_steps(ctx->o.ordering, p.nblk, p.nsup);
   // Row split of the Gram launches, chosen against wave quantization: a launch covers
   // M = 2 * (pairs per launch) matrices x nsplit CTAs with R CTAs resident at once;
@@ -491,6 +503,9 @@ static ghsvd_status blk_sweep_groups(Ctx* ctx, ghsvd_stats* st, BlkSetup& S, int
   GH_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   st->seconds = ms * 1e-3;
   st->alg_flops = st->flops_gram + st->flops_update;
+  st->nblocks = pl.nblk;
+  st->super_blocks = pl.nsup;
+  st->steps_per_sweep = pl.nst;
   st->alg_bytes = (uint64_t)((double)st->sweeps * pl.nst * 16.0 * (double)ctx->n *
                              (2.0 * ctx->m + 2.0 * (2.0 * ctx->m + ctx->n)));
   return GHSVD_OK;
@@ -828,6 +843,9 @@ ghsvd_status blk_sweep(Ctx* ctx, ghsvd_stats* st) {
   st->seconds = ms * 1e-3;
   // algorithmic flops of this rank: per block pair 8 [k(k+1) m + k^2 (2m + n)]
   st->alg_flops = st->flops_gram + st->flops_update;
+  st->nblocks = pl.nblk;
+  st->super_blocks = pl.nsup;
+  st->steps_per_sweep = pl.nst;
   // HBM bytes the blocked sweep must move per block step: Grams read F, G pairs once,
   // updates read + write F, G, Z pairs once
   st->alg_bytes = (uint64_t)((double)st->sweeps * pl.nst / std::max(1, ctx->o.world_size) *

@@ -73,7 +73,8 @@ class Stats(ctypes.Structure):
                 ("max_offdiag_last", ctypes.c_double),
                 ("all_per_sweep", ctypes.c_uint64 * 64), ("big_per_sweep", ctypes.c_uint64 * 64),
                 ("launches_update_fg", ctypes.c_uint64), ("flops_update_fg", ctypes.c_double),
-                ("t_update_fg", ctypes.c_double)]
+                ("t_update_fg", ctypes.c_double), ("nblocks", ctypes.c_int), ("super_blocks", ctypes.c_int),
+                ("steps_per_sweep", ctypes.c_int)]
 
     def todict(self):
         k = min(self.sweeps, 64)
@@ -87,7 +88,8 @@ class Stats(ctypes.Structure):
                 "flops_update": self.flops_update,
                 "launches_update_fg": int(self.launches_update_fg),
                 "flops_update_fg": self.flops_update_fg, "t_update_fg": self.t_update_fg,
-                "max_offdiag_last": self.max_offdiag_last,
+                "max_offdiag_last": self.max_offdiag_last, "nblocks": self.nblocks,
+                "super_blocks": self.super_blocks, "steps_per_sweep": self.steps_per_sweep,
                 "all_per_sweep": [int(v) for v in self.all_per_sweep[:k]],
                 "big_per_sweep": [int(v) for v in self.big_per_sweep[:k]]}
 

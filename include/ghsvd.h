@@ -220,14 +220,17 @@ ghsvd_status ghsvd_set_factors(ghsvd_ctx ctx, int64_t m, int64_t n, const void* 
  * downdated J-norms, exact at every panel start; a panel is cut when a formed pivot column
  * disagrees with its estimate).  The column-pivoted QR of G P2 plans its pivots likewise on
  * S = (G P2)^* (G P2) (diagonally pivoted Cholesky of its Schur complements, checked per
- * panel; GHSVD_REDUCE_COLSEARCH: the downdated-norm search).
+ * panel; GHSVD_REDUCE_COLSEARCH: the downdated-norm search).  The plain QR of G P2 of the
+ * blocked form is cuSOLVER's ZGEQRF (loaded at run time; the paper's code calls LAPACK's
+ * ZGEQR there), GHSVD_REDUCE_OWN_QR: this library's blocked Householder QR instead.
  * The pivot sequence may differ from the unblocked one on near-ties; the Grammians and
  * the pencil are preserved alike (tests).  GHSVD_REDUCE_UNBLOCKED: one reflector
  * application per column (round 1), also the fallback when cuBLAS cannot be loaded or
  * the n x n output-Z buffer cannot hold the panel (m > ~n^2 / 35).
  * Errors: GHSVD_E_RANK_DEFICIENT on a degenerate JQR pivot or rank-deficient G;
  * GHSVD_E_NONFINITE on non-finite J-norms; INVALID_ARG on unknown flags. */
-enum { GHSVD_REDUCE_COLPIV = 1, GHSVD_REDUCE_UNBLOCKED = 2, GHSVD_REDUCE_BLOCKED = 4, GHSVD_REDUCE_COLSEARCH = 8 };
+enum { GHSVD_REDUCE_COLPIV = 1, GHSVD_REDUCE_UNBLOCKED = 2, GHSVD_REDUCE_BLOCKED = 4, GHSVD_REDUCE_COLSEARCH = 8,
+       GHSVD_REDUCE_OWN_QR = 16 };
 ghsvd_status ghsvd_reduce(ghsvd_ctx ctx, int flags);
 /* After ghsvd_reduce: the first column whose planned JQR pivot the exact J-Grammian of its
  * formed column rejected (the column search continued from there); -1 if every planned

@@ -306,7 +306,8 @@ ghsvd_status ghsvd_reduce(ghsvd_ctx h, int flags) {
     ctx->err = "reduce: must follow factor/set_factors (once) and precede sweep";
     return GHSVD_E_STATE;
   }
-  if ((flags & ~(GHSVD_REDUCE_COLPIV | GHSVD_REDUCE_UNBLOCKED | GHSVD_REDUCE_BLOCKED | GHSVD_REDUCE_COLSEARCH)) ||
+  if ((flags & ~(GHSVD_REDUCE_COLPIV | GHSVD_REDUCE_UNBLOCKED | GHSVD_REDUCE_BLOCKED | GHSVD_REDUCE_COLSEARCH |
+                 GHSVD_REDUCE_OWN_QR)) ||
       ((flags & GHSVD_REDUCE_UNBLOCKED) && (flags & GHSVD_REDUCE_BLOCKED))) {
     ctx->err = "reduce: unknown flags";
     return GHSVD_E_INVALID_ARG;

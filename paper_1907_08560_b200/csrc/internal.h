@@ -80,6 +80,7 @@ struct Ctx {
   // multi-GPU
   void* comm;                    // ncclComm_t (opaque)
   void* cublas = nullptr;        // cublasHandle_t of the blocked Phase 2 (dlopen'ed cuBLAS), lazily
+  void* cusolver = nullptr;      // cusolverDnHandle_t (blocked Phase 2's plain QR of G P2), lazily
   std::string err;
 };
 

@@ -12,6 +12,7 @@
 // dots and reflector applications across CTAs; pivot logic in one CTA); the
 // 1x1 / 2x2 decision is read back once per step.  Runs once per problem.
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -1178,10 +1179,56 @@ Cublas* cublas_lib() {
 }
 }  // namespace
 
+// ---------------------------------------------------------------- cuSOLVER (dlopen)
+// The plain (not column-pivoted) QR of G P2 is LAPACK's ZGEQRF in the paper's own code
+// ("the tall-and-skinny QR (ZGEQR from LAPACK)", Sec 5.4); here cuSOLVER's ZGEQRF,
+// loaded at run time like cuBLAS.  Only R is kept.
+namespace {
+struct Cusolver {
+  bool tried = false, ok = false;
+  cusolverStatus_t (*Create)(cusolverDnHandle_t*) = nullptr;
+  cusolverStatus_t (*Destroy)(cusolverDnHandle_t) = nullptr;
+  cusolverStatus_t (*SetStream)(cusolverDnHandle_t, cudaStream_t) = nullptr;
+  cusolverStatus_t (*GeqrfBuf)(cusolverDnHandle_t, int, int, cuDoubleComplex*, int, int*) = nullptr;
+  cusolverStatus_t (*Geqrf)(cusolverDnHandle_t, int, int, cuDoubleComplex*, int, cuDoubleComplex*, cuDoubleComplex*,
+                            int, int*) = nullptr;
+};
+Cusolver* cusolver_lib() {
+  static Cusolver c;
+  if (c.tried) return c.ok ? &c : nullptr;
+  c.tried = true;
+  const char* names[] = {"libcusolver.so.11", "libcusolver.so", "/usr/local/cuda/lib64/libcusolver.so.11"};
+  void* h = nullptr;
+  for (const char* nm : names)
+    if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return nullptr;
+  c.Create = (decltype(c.Create))dlsym(h, "cusolverDnCreate");
+  c.Destroy = (decltype(c.Destroy))dlsym(h, "cusolverDnDestroy");
+  c.SetStream = (decltype(c.SetStream))dlsym(h, "cusolverDnSetStream");
+  c.GeqrfBuf = (decltype(c.GeqrfBuf))dlsym(h, "cusolverDnZgeqrf_bufferSize");
+  c.Geqrf = (decltype(c.Geqrf))dlsym(h, "cusolverDnZgeqrf");
+  c.ok = c.Create && c.Destroy && c.SetStream && c.GeqrfBuf && c.Geqrf;
+  return c.ok ? &c : nullptr;
+}
+
+// a zero R diagonal entry (G P2 numerically rank deficient) -> ctl[3] = -7
+__global__ void k_qr_diag_check(const double2* X, long long ld, long long n, const int* info, P2Scr s) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const double2 d = X[k + k * ld];
+    if (!(d.x != 0.0 || d.y != 0.0) || !isfinite(d.x) || !isfinite(d.y)) atomicCAS(&s.ctl[3], 0, -7);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && *info != 0) atomicCAS(&s.ctl[3], 0, -7);
+}
+}  // namespace
+
 void phase2_release(Ctx* ctx) {
   if (ctx->cublas) {
     if (Cublas* c = cublas_lib()) c->Destroy((cublasHandle_t)ctx->cublas);
     ctx->cublas = nullptr;
+  }
+  if (ctx->cusolver) {
+    if (Cusolver* c = cusolver_lib()) c->Destroy((cusolverDnHandle_t)ctx->cusolver);
+    ctx->cusolver = nullptr;
   }
 }
 
@@ -1660,7 +1707,45 @@ static ghsvd_status phase2_reduce_blocked(Ctx* ctx, int flags, Cublas* cb) {
     TRY(gram_plan(ctx, cb, ctx->F, ld, m, 1, ctx->G, ld, pl, ptype));
     TRY(qr_blocked(ctx, cb, P, s, ctx->F, ld, true, ctx->Z, ldz, 0, &pl));
   } else {
-    TRY(qr_blocked(ctx, cb, P, s, ctx->F, ld, (flags & GHSVD_REDUCE_COLPIV) != 0, ctx->Z, ldz));
+    bool done = false;
+    Cusolver* cs = (flags & (GHSVD_REDUCE_COLPIV | GHSVD_REDUCE_OWN_QR)) ? nullptr : cusolver_lib();
+    if (cs) {
+      // the plain QR by cuSOLVER's ZGEQRF (workspace in the free n x n output-Z buffer)
+      if (!ctx->cusolver) {
+        cusolverDnHandle_t hs;
+        if (cs->Create(&hs) != CUSOLVER_STATUS_SUCCESS) {
+          ctx->err = "reduce: cusolverDnCreate failed";
+          return GHSVD_E_CUDA;
+        }
+        ctx->cusolver = hs;
+      }
+      cusolverDnHandle_t hs = (cusolverDnHandle_t)ctx->cusolver;
+      int lwork = 0;
+      const long long cap = (long long)ctx->ldn * (ctx->n_cap + 1) - n - 16;
+      if (cs->SetStream(hs, st) == CUSOLVER_STATUS_SUCCESS &&
+          cs->GeqrfBuf(hs, (int)m, (int)n, (cuDoubleComplex*)ctx->F, (int)ld, &lwork) == CUSOLVER_STATUS_SUCCESS &&
+          lwork <= cap) {
+        cuDoubleComplex* tau = (cuDoubleComplex*)ctx->Z2;
+        cuDoubleComplex* work = tau + n;
+        int* info = (int*)(work + lwork);
+        if (cs->Geqrf(hs, (int)m, (int)n, (cuDoubleComplex*)ctx->F, (int)ld, tau, work, lwork, info) !=
+            CUSOLVER_STATUS_SUCCESS) {
+          ctx->err = "reduce: cusolverDnZgeqrf failed";
+          return GHSVD_E_CUDA;
+        }
+        k_qr_diag_check<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ctx->F, ld, n, info, s);
+        P2CHK();
+        int ctl4[4];
+        GH_CUDA(cudaMemcpyAsync(ctl4, s.ctl, 16, cudaMemcpyDeviceToHost, st));
+        GH_CUDA(cudaStreamSynchronize(st));
+        if (ctl4[3]) {
+          ctx->err = "reduce: G P2 numerically rank deficient";
+          return GHSVD_E_RANK_DEFICIENT;
+        }
+        done = true;
+      }
+    }
+    if (!done) TRY(qr_blocked(ctx, cb, P, s, ctx->F, ld, (flags & GHSVD_REDUCE_COLPIV) != 0, ctx->Z, ldz));
   }
   GH_CUDA(cudaMemsetAsync(ctx->G, 0, (size_t)ld * (ctx->n_cap + 1) * 16, st));
   k_qr_rout<<<(unsigned)n, T2, 0, st>>>(ctx->F, ld, ctx->G, ld, n);

@@ -303,13 +303,16 @@ class Context:
         self._check(self._L.ghsvd_factor(self._h, NA, NL, NG, pa, pb, pu, ptaa, ptab, ptbb), "factor")
         self.m, self.n = 2 * NA * NL, NG
 
-    def reduce(self, colpiv: bool = False, unblocked: Optional[bool] = None, colsearch: bool = False):
+    def reduce(self, colpiv: bool = False, unblocked: Optional[bool] = None, colsearch: bool = False,
+               own_qr: bool = False):
         """Phase 2; colpiv: column-pivoted QR of G P2 (GHSVD_REDUCE_COLPIV); unblocked: True forces
         the one-reflector-per-column form (GHSVD_REDUCE_UNBLOCKED), False the blocked one
         (GHSVD_REDUCE_BLOCKED), None lets the library choose by size (see ghsvd.h); colsearch:
         the blocked JQR searches its pivots on the columns instead of planning them on the
-        J-Grammian (GHSVD_REDUCE_COLSEARCH)."""
-        fl = (1 if colpiv else 0) | (0 if unblocked is None else (2 if unblocked else 4)) | (8 if colsearch else 0)
+        J-Grammian (GHSVD_REDUCE_COLSEARCH); own_qr: the blocked form's plain QR of G P2 by this
+        library's kernels instead of cuSOLVER's ZGEQRF (GHSVD_REDUCE_OWN_QR)."""
+        fl = (1 if colpiv else 0) | (0 if unblocked is None else (2 if unblocked else 4)) | (8 if colsearch else 0) | \
+            (16 if own_qr else 0)
         self._check(self._L.ghsvd_reduce(self._h, fl), "reduce")
         self.reduce_fallback_col = int(self._L.ghsvd_reduce_fallback_col(self._h))
         self.m = self.n

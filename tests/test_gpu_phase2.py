@@ -23,7 +23,7 @@ def gh():
 
 
 MODES = {"planned": dict(unblocked=False), "colsearch": dict(unblocked=False, colsearch=True),
-         "unblocked": dict(unblocked=True)}
+         "unblocked": dict(unblocked=True), "own_qr": dict(unblocked=False, own_qr=True)}
 
 
 @pytest.mark.parametrize("mode", list(MODES))

@@ -532,10 +532,9 @@ __global__ void __launch_bounds__(T2) k_sdots(const double2* snew, const double2
 }
 
 // k_panel_add + k_refl_fin of the JQR in one launch (F column k: rows > k zeroed, row k = -c1)
-__global__ void __launch_bounds__(T2) k_panel_add_fin(double2* S, long long lds, const double2* sv, long long r0,
-                                                      long long m, int nr, double2* T, const double2* tv, P2Scr s,
-                                                      double2* F, long long ld) {
-  if (s.ctl[3] || s.ctl[8]) return;
+__device__ __forceinline__ void panel_add_fin_body(double2* S, long long lds, const double2* sv, long long r0,
+                                                   long long m, int nr, double2* T, const double2* tv, P2Scr s,
+                                                   double2* F, long long ld) {
   const double tau = s.dctl[0];
   double2* col = S + (size_t)nr * lds;
   double2* f = F + r0 * ld;
@@ -556,10 +555,16 @@ __global__ void __launch_bounds__(T2) k_panel_add_fin(double2* S, long long lds,
   }
 }
 
-// S[:, nr] = s (rows >= r0; zero above); T row nr = tau (tv^T T), T[nr][nr] = tau
-__global__ void __launch_bounds__(T2) k_panel_add(double2* S, long long lds, const double2* sv, long long r0,
-                                                  long long m, int nr, double2* T, const double2* tv, P2Scr s) {
+__global__ void __launch_bounds__(T2) k_panel_add_fin(double2* S, long long lds, const double2* sv, long long r0,
+                                                      long long m, int nr, double2* T, const double2* tv, P2Scr s,
+                                                      double2* F, long long ld) {
   if (s.ctl[3] || s.ctl[8]) return;
+  panel_add_fin_body(S, lds, sv, r0, m, nr, T, tv, s, F, ld);
+}
+
+// S[:, nr] = s (rows >= r0; zero above); T row nr = tau (tv^T T), T[nr][nr] = tau
+__device__ __forceinline__ void panel_add_body(double2* S, long long lds, const double2* sv, long long r0, long long m,
+                                               int nr, double2* T, const double2* tv, P2Scr s) {
   const double tau = s.dctl[0];
   double2* col = S + (size_t)nr * lds;
   for (long long i = blockIdx.x * (long long)T2 + threadIdx.x; i < m; i += (long long)gridDim.x * T2)
@@ -572,6 +577,12 @@ __global__ void __launch_bounds__(T2) k_panel_add(double2* S, long long lds, con
     }
     if (threadIdx.x == 0) T[nr + nr * PB] = cmk(tau, 0.0);
   }
+}
+
+__global__ void __launch_bounds__(T2) k_panel_add(double2* S, long long lds, const double2* sv, long long r0,
+                                                  long long m, int nr, double2* T, const double2* tv, P2Scr s) {
+  if (s.ctl[3] || s.ctl[8]) return;
+  panel_add_body(S, lds, sv, r0, m, nr, T, tv, s);
 }
 
 // Per trailing column j in [j0, n): w = T y (nr x nr lower triangular), then for each of the
@@ -971,8 +982,8 @@ __global__ void __launch_bounds__(256) k_bk_update(double2* H, long long ld, lon
 }
 
 // The planned column interchanges of position k: F columns (all m rows) and p2
-__global__ void k_plan_swaps(double2* F, long long ld, long long m, long long k, long long* p2, BkPlan pl, P2Scr s) {
-  if (s.ctl[8]) return;   // the plan was stopped at an earlier column of this panel
+__device__ __forceinline__ void plan_swaps_body(double2* F, long long ld, long long m, long long k, long long* p2,
+                                                const BkPlan& pl) {
   const long long a = pl.sw1[k];
   const long long b = pl.sw2[k];
   const long long bp = k + pl.sw2pos[k];
@@ -989,6 +1000,22 @@ __global__ void k_plan_swaps(double2* F, long long ld, long long m, long long k,
     __syncthreads();   // (the passes touch different column pairs; grid-wide order comes from
                        // each element being swapped by the same thread in both passes)
   }
+}
+
+__global__ void k_plan_swaps(double2* F, long long ld, long long m, long long k, long long* p2, BkPlan pl, P2Scr s) {
+  if (s.ctl[8]) return;   // the plan was stopped at an earlier column of this panel
+  plan_swaps_body(F, ld, m, k, p2, pl);
+}
+
+// k_panel_add_fin of pivot k plus the planned interchanges of the next step's position kn
+// (trailing columns >= kn > k: disjoint from what the panel update touches)
+__global__ void __launch_bounds__(T2) k_panel_add_fin_swap(double2* S, long long lds, const double2* sv, long long r0,
+                                                           long long m, int nr, double2* T, const double2* tv,
+                                                           P2Scr s, double2* F, long long ld, long long kn,
+                                                           long long n, long long* p2, BkPlan pl) {
+  if (s.ctl[3] || s.ctl[8]) return;
+  panel_add_fin_body(S, lds, sv, r0, m, nr, T, tv, s, F, ld);
+  if (kn < n) plan_swaps_body(F, ld, m, kn, p2, pl);
 }
 
 // Check a planned pivot against the exact J-Grammian of its formed column(s) fx (, fx2),
@@ -1074,8 +1101,8 @@ __global__ void k_sum_chunks(const double2* part, int nb, long long pstride, int
 }
 
 // Planned column interchange of the column-pivoted QR at position k: X and Rf columns, p2
-__global__ void k_plan_swap_qr(double2* X, long long ldx, long long mx, double2* Rf, long long ldr, long long mr,
-                               long long k, long long* p2, BkPlan pl) {
+__device__ __forceinline__ void plan_swap_qr_body(double2* X, long long ldx, long long mx, double2* Rf, long long ldr,
+                                                  long long mr, long long k, long long* p2, const BkPlan& pl) {
   const long long a = pl.sw1[k];
   if (a == k) return;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mx; i += (long long)gridDim.x * blockDim.x) {
@@ -1087,6 +1114,22 @@ __global__ void k_plan_swap_qr(double2* X, long long ldx, long long mx, double2*
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t = p2[k]; p2[k] = p2[a]; p2[a] = t;
   }
+}
+
+__global__ void k_plan_swap_qr(double2* X, long long ldx, long long mx, double2* Rf, long long ldr, long long mr,
+                               long long k, long long* p2, BkPlan pl) {
+  plan_swap_qr_body(X, ldx, mx, Rf, ldr, mr, k, p2, pl);
+}
+
+// k_panel_add of QR pivot k plus the planned interchange of position kn > k (trailing)
+__global__ void __launch_bounds__(T2) k_panel_add_swapqr(double2* S, long long lds, const double2* sv, long long r0,
+                                                         long long m, int nr, double2* T, const double2* tv, P2Scr s,
+                                                         double2* X, long long ldx, double2* Rf, long long ldr,
+                                                         long long mr, long long kn, long long n, long long* p2,
+                                                         BkPlan pl) {
+  if (s.ctl[3]) return;
+  panel_add_body(S, lds, sv, r0, m, nr, T, tv, s);
+  if (kn < n) plan_swap_qr_body(X, ldx, m, Rf, ldr, mr, kn, p2, pl);
 }
 
 // The formed QR pivot column's squared norm (rows >= k) against the planned Schur diagonal:
@@ -1439,6 +1482,7 @@ static ghsvd_status jqr_planned(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, c
     return GHSVD_OK;
   };
   int64_t k = 0;
+  k_plan_swaps<<<gm, 256, 0, st>>>(F, ld, m, 0, p2, pl, s);
   while (k < n) {
     const int64_t k0 = k;
     int nr = 0;
@@ -1449,7 +1493,7 @@ static ghsvd_status jqr_planned(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, c
     // and the panel's end learns where.  A 2x2 pivot reads the check back first.
     while (k < n && nr + std::max(ptype[k], 1) <= PB) {
       const int type = ptype[k] == 2 && k + 1 < n ? 2 : 1;
-      k_plan_swaps<<<gm, 256, 0, st>>>(F, ld, m, k, p2, pl, s);
+      // (the planned interchanges of position k ran with the previous step's last launch)
       // the pivot column(s) with the panel's delayed update, into fx (, fx2)
       for (int c = 0; c < type; c++) {
         double2* x = F + (k + c) * ld;
@@ -1464,7 +1508,7 @@ static ghsvd_status jqr_planned(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, c
       if (type == 1) {
         k_refl_prep_plan<<<1, T2, 0, st>>>(F, ld, J, m, n, k, k0, P.fx, s, P.S, P.lds, nr, pl);
         if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, J, k, m, P.tv);
-        k_panel_add_fin<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s, F, ld);
+        k_panel_add_fin_swap<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s, F, ld, k + 1, n, p2, pl);
         nr++;
       } else {
         k_plan_check<<<1, T2, 0, st>>>(P.fx, P.fx2, J, k, m, 2, pl, s, nr);
@@ -1489,6 +1533,7 @@ static ghsvd_status jqr_planned(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, c
           k_refl_fin<<<1, T2, 0, st>>>(F, ld, m, kk, s);
         }
         k_rot<<<1, T2, 0, st>>>(F, ld, J, m, k, -1, s);
+        if (k + 2 < n) k_plan_swaps<<<gm, 256, 0, st>>>(F, ld, m, k + 2, p2, pl, s);
       }
       P2CHK();
       k += type;
@@ -1556,7 +1601,10 @@ static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, do
   // each formed pivot checked against its planned norm; after a panel with a rejected pivot
   // the search takes over (colpiv_plan off)
   bool use_plan = colpiv && plan != nullptr;
-  if (use_plan) GH_CUDA(cudaMemsetAsync(s.ctl + 5, 0, 4, st));
+  if (use_plan) {
+    GH_CUDA(cudaMemsetAsync(s.ctl + 5, 0, 4, st));
+    if (k_start < n) k_plan_swap_qr<<<gm, 256, 0, st>>>(X, ld, m, Rf, ldr, n, k_start, p2, *plan);
+  }
   int64_t k = k_start;
   while (k < n) {
     const int64_t k0 = k;
@@ -1586,7 +1634,7 @@ static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, do
           if (ctl[5]) break;   // downdated norm was off: flush, then exact norms again
         }
       } else {
-        if (use_plan) k_plan_swap_qr<<<gm, 256, 0, st>>>(X, ld, m, Rf, ldr, n, k, p2, *plan);
+        // (a planned interchange of position k ran with the previous column's k_panel_add)
         if (nr) {
           k_ycol<<<nr, T2, 0, st>>>(X + k * ld, P.S, P.lds, nullptr, k0, m, P.u);
           k_form_tw<<<gm, 256, 0, st>>>(X + k * ld, X + k * ld, P.S, P.lds, P.T, P.u, nr, k0, m);
@@ -1594,7 +1642,11 @@ static ghsvd_status qr_blocked(Ctx* ctx, Cublas* cb, const Panel& P, P2Scr s, do
       }
       k_qr_prep_c<<<1, T2, 0, st>>>(X, ld, m, k, s, use_plan ? plan->d : nullptr);
       if (nr) k_sdots<<<nr, T2, 0, st>>>(s.s, P.S, P.lds, nullptr, k, m, P.tv);
-      k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s);
+      if (use_plan)
+        k_panel_add_swapqr<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s, X, ld, Rf, ldr, n, k + 1, n, p2,
+                                              *plan);
+      else
+        k_panel_add<<<gm, T2, 0, st>>>(P.S, P.lds, s.s, k, m, nr, P.T, P.tv, s);
       nr++;
       k++;
       pend = 1;

@@ -318,3 +318,24 @@ def reduce(F, J, G):
     _chk(lib().or_reduce(m, n, _ptr(F), m, _ptr(J), _ptr(G), m, _ptr(Fs), _ptr(Js), _ptr(Gs),
                          _ptr(p2), ctypes.byref(n2)), "reduce")
     return Fs, Js, Gs, p2, n2.value
+
+
+def pencil_eigvals(F, J, G):
+    """Eigenvalues of the pencil (H, S) = (F^* J F, G^* G) by the paper's "alternative way
+    forward" (Sec 4.5): H and S formed explicitly (S = G^* G, H = F^* (J F)
+    with F's rows scaled by J), then a generalized Hermitian-definite solver (LAPACK ZHEGVD
+    through scipy.linalg.eigh) -- the definition of the eigenvalues written out, a library
+    routine as its step.  Its absolute error is ~ eps * kappa(S) * ||H||, so it is a
+    reference only for WELL-CONDITIONED S (config 4, kappa(S) ~ 10), never for the
+    ill-conditioned config 3, where avoiding exactly this is the paper's point
+    (PAPER.md:404-407).  Returns the eigenvalues in ascending order."""
+    import scipy.linalg
+
+    F = np.asarray(F, dtype=np.complex128)
+    G = np.asarray(G, dtype=np.complex128)
+    Js = np.asarray(J, dtype=np.float64)
+    S = G.conj().T @ G
+    H = F.conj().T @ (Js[:, None] * F)
+    H = 0.5 * (H + H.conj().T)
+    S = 0.5 * (S + S.conj().T)
+    return scipy.linalg.eigh(H, S, eigvals_only=True, driver="gvd")

@@ -392,3 +392,22 @@ def test_stored_reference_script_and_fingerprint(tmp_path):
     F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
     Fo, Go, Zp, st = oracle.hz_pointwise(F, J, G, cmax=64)
     assert np.array_equal(oracle.extract(Fo, J, Go, Zp)[0], lam)
+
+
+def test_stored_dense_reference_script(tmp_path):
+    """--variant dense (the config-4 reference: oracle.factor -> oracle.pencil_eigvals) writes
+    the dense eigenvalues, kappa(S) and the input fingerprint, from the oracle alone."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "make_oracle_reference.py"), "--illcond",
+                        "2,6,16,5", "--variant", "dense", "--threads", "2", "--out", str(tmp_path)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    meta = json.load(open(tmp_path / "illcond_2_6_16_s5_oracle_dense.json"))
+    lam = np.load(tmp_path / "illcond_2_6_16_s5_oracle_dense.npz")["lam"]
+    at = inputs.illcond_atoms(5, 2, 6, 16)
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    assert np.array_equal(oracle.pencil_eigvals(F, J, G), lam)
+    assert meta["stats"]["kappa_S"] >= 1.0 and meta["stats"]["negative"] == int((lam < 0).sum())

@@ -47,7 +47,9 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--illcond", type=str, default="",
                     help="NA,NL,NG,seed: a scaled-down config-3 analog (inputs.illcond_atoms) instead of --config")
-    ap.add_argument("--variant", choices=["pointwise", "bo"], default="pointwise")
+    ap.add_argument("--variant", choices=["pointwise", "bo", "dense"], default="pointwise",
+                    help="dense: oracle.pencil_eigvals (form H, S; ZHEGVD; PAPER.md:818-836), "
+                         "for well-conditioned S only (config 4)")
     ap.add_argument("--nblk", type=int, default=0, help="BO block columns (0: 2*ceil(n/64), the GPU auto partition)")
     ap.add_argument("--cmax", type=int, default=64)
     ap.add_argument("--threads", type=int, default=0)
@@ -83,6 +85,32 @@ def main():
           f"(gen {t_gen:.1f} s, factor {t_factor:.1f} s)", flush=True)
 
     t0 = time.time()
+    if args.variant == "dense":
+        lam = oracle.pencil_eigvals(F, J, G)
+        t_sweep = time.time() - t0
+        # kappa(S) of this pencil, the justification for the dense route (its error ~ eps kappa(S) ||H||)
+        sev = np.linalg.eigvalsh(G.conj().T @ G)
+        st = {"converged": True, "sweeps": None, "kappa_S": float(sev[-1] / sev[0]),
+              "lam_abs_min": float(np.abs(lam).min()), "lam_abs_max": float(np.abs(lam).max()),
+              "negative": int((lam < 0).sum())}
+        print(f"dense: {t_sweep:.1f} s, kappa(S) = {st['kappa_S']:.3g}", flush=True)
+        stem = os.path.join(args.out, f"{name}_oracle_dense")
+        np.savez_compressed(stem + ".npz", lam=lam)
+        meta = {
+            "about": "Oracle-only reference (tools/make_oracle_reference.py --variant dense): "
+                     "inputs.make_config(numpy) -> oracle.factor -> oracle.pencil_eigvals (H = F^*JF, "
+                     "S = G^*G formed, ZHEGVD). No value comes from the CUDA path.",
+            "cite": "PAPER.md:818-836 (Sec 4.5, the alternative way forward; valid for well-conditioned S); "
+                    "SURVEY.md Sec 8(c) pins table (config 4: oracle run once, cached by an input hash)",
+            "config": name, "m": m, "n": n, "variant": "dense", "stats": st,
+            "seconds_solve": t_sweep, "seconds_factor": t_factor, "seconds_generate": t_gen,
+            "threads": threads, "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+            "inputs_sha256": raw.hexdigest(), "fingerprint": fp, "lam_file": os.path.basename(stem + ".npz"),
+        }
+        with open(stem + ".json", "w") as f:
+            json.dump(meta, f, indent=1)
+        print("wrote", stem + ".npz", stem + ".json")
+        return
     if args.variant == "pointwise":
         Fc, Gc, Zp, st = oracle.hz_pointwise(F, J, G, cmax=args.cmax, nthreads=threads)
     else:

@@ -63,3 +63,18 @@ def test_inertia_of_square_factor():
     J = np.where(rng.random(n) < 0.3, -1, 1).astype(np.int8)
     lam = oracle.pencil_eigvals(F, J, G)
     assert int((lam < 0).sum()) == int((J < 0).sum())
+
+
+def test_matches_stored_hz_oracle_on_config2():
+    """At a real LAPW shape: the dense route on the oracle's Phase-1 factors of config 2
+    (1568 x 1024, well-conditioned S) against the stored HZ oracle solve of the same atoms
+    (tests/golden/c2_oracle_bo.*, BO to convergence), per eigenvalue."""
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    meta = json.load(open(os.path.join(gold, "c2_oracle_bo.json")))
+    lam_hz = np.load(os.path.join(gold, "c2_oracle_bo.npz"))["lam"]
+    kind, at = inputs.make_config(2, backend="numpy")
+    assert inputs.fingerprint_close(inputs.fingerprint(at), meta["fingerprint"])
+    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    assert relerr(oracle.pencil_eigvals(F, J, G), lam_hz) <= 1e-10

@@ -159,23 +159,33 @@ def shared_inputs(cfg: int, ws: int, rank: int, dev):
     return kind, inputs.Pencil(out["F"], out["J"], out["G"], lam_true=lam_true)
 
 
-def stored_oracle_parity(cfg: int, at, lam):
+def stored_oracle_parity(cfg: int, at, lam, phase2=None):
     """Max relative eigenvalue error of this run against the stored oracle reference for
-    the config (tests/golden/c<cfg>_oracle_pointwise, written by the oracle-only script
-    tools/make_oracle_reference.py from the same seeded atoms), or None."""
+    the config, written by the oracle-only script tools/make_oracle_reference.py from the
+    same seeded atoms: tests/golden/c<cfg>_oracle_pointwise (HZ, Alg. 2; config 3, north-star
+    tolerance 1e-6) or c<cfg>_oracle_dense (H and S formed, ZHEGVD; config 4,
+    well-conditioned S, tolerance 1e-9); None if there is none."""
     from paper_1907_08560_b200 import inputs
-    stem = os.path.join(ROOT, "tests", "golden", f"c{cfg}_oracle_pointwise")
+    gold = os.path.join(ROOT, "tests", "golden")
+    stem, tol = os.path.join(gold, f"c{cfg}_oracle_pointwise"), 1e-6
     if not os.path.exists(stem + ".json"):
-        return None
+        stem, tol = os.path.join(gold, f"c{cfg}_oracle_dense"), 1e-9
+        if not os.path.exists(stem + ".json"):
+            return None
     meta = json.load(open(stem + ".json"))
     ok = inputs.fingerprint_close(inputs.fingerprint(at), meta["fingerprint"])
     lo = np.sort(np.load(stem + ".npz")["lam"])
     la = np.sort(np.asarray(lam))
     err = float(np.max(np.abs(la - lo) / np.abs(lo))) if ok and la.shape == lo.shape else None
-    return {"reference": os.path.relpath(stem, ROOT) + ".{json,npz}", "inputs_match": bool(ok),
-            "max_rel_lambda_err": err, "tol": 1e-6, "oracle_sweeps": meta["stats"]["sweeps"],
-            "oracle_seconds_measured": meta["seconds_sweep"], "oracle_threads": meta["threads"],
-            "oracle_cpu": meta["cpu_model"]}
+    out = {"reference": os.path.relpath(stem, ROOT) + ".{json,npz}", "inputs_match": bool(ok),
+           "max_rel_lambda_err": err, "tol": tol, "within_tol": err is not None and err <= tol,
+           "oracle_sweeps": meta["stats"]["sweeps"],
+           "oracle_seconds_measured": meta.get("seconds_sweep", meta.get("seconds_solve")),
+           "oracle_threads": meta["threads"], "oracle_cpu": meta["cpu_model"]}
+    if phase2:
+        out["note"] = ("Phase 2 (QR of the badly conditioned G) costs accuracy on this pencil, as "
+                       "PAPER.md:925-927 warns; the metric's recipe skips it (DESIGN.md Sec 8)")
+    return out
 
 
 def _cpu_model() -> str:
@@ -601,7 +611,7 @@ def run_ours(args):
     if identical is not None:
         line["inputs_identical_across_ranks"] = identical
     if kind == "atoms":
-        par = stored_oracle_parity(args.config, at, lam_h.numpy())
+        par = stored_oracle_parity(args.config, at, lam_h.numpy(), phase2=args.reduce == "colpiv")
         if par is not None:
             line["parity_vs_stored_oracle"] = par
     if not args.no_cpu_baseline and ws == 1:

@@ -42,7 +42,8 @@ def needs_build() -> bool:
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+    # GHSVD_NVCC_EXTRA: extra nvcc flags for A/B builds of the tools (e.g. -DGHSVD_GRAM_RT=48)
+    cmd = [NVCC] + ARCH + FLAGS + os.environ.get("GHSVD_NVCC_EXTRA", "").split() + ["-c", src, "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -18,12 +18,22 @@ constexpr int RT = 32;          // rows per staged tile
 // distinct 16-byte bank groups (stride 34 = 2 mod 8 overlapped two of them: ncu counted
 // 43 % of the Gram's shared wavefronts as bank conflicts).  Two CTAs of 110.6 KB fit an
 // SM because the fused factorization keeps its scratch in the same dynamic buffer.
-constexpr int GS = RT + 4;
+// Gram pipeline geometry: RTG rows per stage, GSTAGES stages (compile-time; the
+// -DGHSVD_GRAM_RT / -DGHSVD_GRAM_STAGES overrides exist for A/B builds only)
+#ifndef GHSVD_GRAM_RT
+#define GHSVD_GRAM_RT 32
+#endif
+#ifndef GHSVD_GRAM_STAGES
+#define GHSVD_GRAM_STAGES 3
+#endif
+constexpr int RTG = GHSVD_GRAM_RT;
+static_assert(RTG % 8 == 0 && (RTG + 4) % 8 == 4, "Gram stage rows: two k-steps per iteration, stride 4 mod 8");
+constexpr int GS = RTG + 4;
 constexpr int GS_FUSED = GS;
 constexpr int ZS = KM + 4;      // Z_blk column stride in smem
 constexpr int NT_G = 256, NT_P = 512, NT_U = 256;
 constexpr int US = RT + 2;      // update tile column stride
-constexpr int GSTAGES = 3;      // cp.async pipeline depth of the Gram kernel
+constexpr int GSTAGES = GHSVD_GRAM_STAGES;   // cp.async pipeline depth of the Gram kernel
 constexpr int MAX_SPLIT = 16;   // max row splits of a Gram (partials summed in order)
 constexpr int TRACE_SLOTS = 48; // trace launch slots per block step
 

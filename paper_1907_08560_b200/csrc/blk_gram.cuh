@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
   auto load_stage = [&](int st, long long r0) {
     if (r0 < r_end) {
       double2* T = gsm + (size_t)st * KM * TS;
-      for (int e = tid; e < KM * RT; e += NT_G) {
-        const int c = e / RT, r = e % RT;
+      for (int e = tid; e < KM * RTG; e += NT_G) {
+        const int c = e / RTG, r = e % RTG;
         const long long gc = gcol(c, c0p, wp, c0q, wq);
         const long long gr = r0 + r;
         const bool ok = gc >= 0 && gr < r_end;
@@ -225,12 +225,12 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
   // buffer is then refilled with the stage GSTAGES-1 ahead.
   auto pipeline = [&](auto&& consume) {
 #pragma unroll
-    for (int p = 0; p < GSTAGES - 1; p++) load_stage(p, r_begin + (long long)p * RT);
+    for (int p = 0; p < GSTAGES - 1; p++) load_stage(p, r_begin + (long long)p * RTG);
     int st = 0;
-    for (long long r0 = r_begin; r0 < r_end; r0 += RT) {
+    for (long long r0 = r_begin; r0 < r_end; r0 += RTG) {
       cp_wait<GSTAGES - 2>();
       __syncthreads();
-      load_stage((st + GSTAGES - 1) % GSTAGES, r0 + (long long)(GSTAGES - 1) * RT);
+      load_stage((st + GSTAGES - 1) % GSTAGES, r0 + (long long)(GSTAGES - 1) * RTG);
       consume(gsm + (size_t)st * KM * TS, r0);
       st = (st + 1) % GSTAGES;
     }
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
       // not unrolled: the warp-specialized tile sets are already 16 code paths, and
       // unrolling them overflowed the instruction cache (ncu: 22 % no_inst stalls)
 #pragma unroll 1
-      for (int ks = 0; ks < RT / 4; ks += 2) {
+      for (int ks = 0; ks < RTG / 4; ks += 2) {
         const int row0 = 4 * ks + (lane & 3), row1 = row0 + 4;
         const unsigned sg0 = (hs == 0 && r0 + row0 >= a.npos) ? 0x80000000u : 0u;
         const unsigned sg1 = (hs == 0 && r0 + row1 >= a.npos) ? 0x80000000u : 0u;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(NT_G, 2) k_blk_gram(BlkArgs a) {
     for (int t = 0; t < 9; t++) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
     pipeline([&](const double2* T, long long r0) {
 #pragma unroll 1
-      for (int ks = 0; ks < RT / 4; ks += 2) {
+      for (int ks = 0; ks < RTG / 4; ks += 2) {
         const int row = 4 * (ks + kh) + (lane & 3);
         const unsigned sg = (hs == 0 && r0 + row >= a.npos) ? 0x80000000u : 0u;
         switch (gi) {   // warp-uniform

@@ -115,11 +115,11 @@ BlkPlan make_plan(const Ctx* ctx) {
   long long best = -1;
   double best_cost = 0.0;
   for (int ns = 1; ns <= MAX_SPLIT; ns++) {
-    const long long rows = round_up((ctx->m + ns - 1) / ns, RT);
+    const long long rows = round_up((ctx->m + ns - 1) / ns, RTG);
     const int nseff = (int)((ctx->m + rows - 1) / rows);
     if (nseff != ns) continue;
     const double waves = (double)((M * ns + R - 1) / R);
-    const double cost = waves * (double)(rows / RT + 3);
+    const double cost = waves * (double)(rows / RTG + 3);
     if (best < 0 || cost < best_cost - 1e-9) {
       best = ns;
       best_cost = cost;
@@ -128,7 +128,7 @@ BlkPlan make_plan(const Ctx* ctx) {
   p.nsplit = (int)std::max<long long>(1, best);
   if (ctx->o.gram_splits > 0) p.nsplit = std::min(MAX_SPLIT, ctx->o.gram_splits);
   const long long rows_per = (ctx->m + p.nsplit - 1) / p.nsplit;
-  p.split_rows = round_up(std::max<long long>(rows_per, 1), RT);
+  p.split_rows = round_up(std::max<long long>(rows_per, 1), RTG);
   p.nsplit = (int)((ctx->m + p.split_rows - 1) / p.split_rows);
   return p;
 }

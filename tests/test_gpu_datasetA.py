@@ -56,3 +56,30 @@ def test_alike_lambda_vs_oracle(gh, alike, variant, reduce):
     assert err <= 1e-9
     assert int((J > 0).sum()) == 3 * NA
     assert int((lam > 0).sum()) == int((lo > 0).sum()) <= 3 * NA
+
+
+@pytest.mark.parametrize("reduce", [True, False])
+def test_config6_full_size_vs_stored_dense_oracle(gh, reduce):
+    """Config 6 at full size (26136 x 3275, 108 atoms of 3+ / 239- signs): the bench's
+    pipeline (Phase 1 -> Phase 2 -> BO in the HIER ordering) and the tall factors, against
+    the stored dense oracle reference of the same atoms (tests/golden/c6_oracle_dense.*:
+    oracle.factor -> oracle.pencil_eigvals, PAPER.md:818-836; kappa(S) = 5.6, every
+    eigenvalue negative) at the well-conditioned tolerance 1e-9."""
+    import json
+    import os
+    stem = os.path.join(os.path.dirname(__file__), "golden", "c6_oracle_dense")
+    meta = json.load(open(stem + ".json"))
+    kind, at = inputs.make_config(6)
+    assert inputs.fingerprint_close(inputs.fingerprint(at), meta["fingerprint"])
+    na, nl, ng = at.A.shape
+    ctx = gh.Context(2 * na * nl, ng, nl, variant="bo", max_sweeps=64, ordering="hier")
+    ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    if reduce:
+        ctx.reduce()
+    st = ctx.sweep()
+    lam = ctx.extract(want_z=False)[0].copy()
+    ctx.close()
+    err = relerr(lam, np.load(stem + ".npz")["lam"])
+    print(f"config 6 reduce={reduce}: {st['sweeps']} sweeps, lambda vs stored dense oracle {err:.2e}")
+    assert st["converged"] and err <= 1e-9
+    assert int((lam < 0).sum()) == meta["stats"]["negative"]

@@ -50,5 +50,38 @@ for i in range(N):
         bad += 1
         print(f"NONDETERMINISTIC: phase1 run {i}")
 print("phase1:", N, "runs")
+# the bench's configuration: HIER block ordering over super blocks (reading R2-5), and the
+# blocked Phase 2 with planned pivots (cuSOLVER ZGEQRF / own QR, column-pivoted), then BO
+for kw in ({"ordering": "hier", "super_blocks": 4}, {"ordering": "level3", "super_blocks": 4}):
+    ref = None
+    for i in range(N):
+        ctx = ghsvd.Context(600, 256, variant="bo", **kw)
+        ctx.set_factors(P.F, P.J, P.G)
+        st = ctx.sweep()
+        cur = ctx.extract()
+        ctx.close()
+        if ref is None:
+            ref = (cur, st["sweeps"])
+        elif not (all(np.array_equal(a, b) for a, b in zip(cur, ref[0])) and st["sweeps"] == ref[1]):
+            bad += 1
+            print(f"NONDETERMINISTIC: bo {kw} run {i}")
+    print(f"bo {kw}: {N} runs, sweeps {ref[1]}")
+for rkw in ({"unblocked": False}, {"unblocked": False, "own_qr": True}, {"unblocked": False, "colpiv": True}):
+    ref = None
+    for i in range(N):
+        ctx = ghsvd.Context(2 * 16 * 49, 256, 49, variant="bo")
+        ctx.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+        ctx.reduce(**rkw)
+        F, J, G, p2 = ctx.get_factors()
+        st = ctx.sweep()
+        lam = ctx.extract(want_z=False)[0].copy()
+        ctx.close()
+        cur = (F, J, G, p2, lam)
+        if ref is None:
+            ref = cur
+        elif not all(np.array_equal(a, b) for a, b in zip(cur, ref)):
+            bad += 1
+            print(f"NONDETERMINISTIC: phase2 {rkw} run {i}")
+    print(f"phase2 {rkw} + bo: {N} runs")
 print("determinism stress:", "FAIL" if bad else "OK")
 sys.exit(1 if bad else 0)

@@ -66,16 +66,22 @@ def main():
         name = f"illcond_{NA}_{NL}_{NG}_s{seed}"
     else:
         kind, at = inputs.make_config(args.config, backend="numpy")
-        assert kind == "atoms", "stored references are for the Phase-1 (atoms) configs"
         name = f"c{args.config}"
     t_gen = time.time() - t0
     fp = inputs.fingerprint(at)
     raw = hashlib.sha256()
-    for arr in ("A", "B", "U", "TAA", "TAB", "TBB"):
+    atoms = hasattr(at, "TAA")
+    for arr in (("A", "B", "U", "TAA", "TAB", "TBB") if atoms else ("F", "J", "G")):
         raw.update(np.ascontiguousarray(getattr(at, arr)).tobytes())
 
     t0 = time.time()
-    F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    if atoms:
+        F, J, G = oracle.factor(at.A, at.B, at.U, at.TAA, at.TAB, at.TBB)
+    else:
+        # a pencil given directly (config 5, dataset C: J = I, n even): the sweep's factors
+        # as given (no row sort needed with J = I, no border with n even)
+        assert np.all(at.J == 1) and at.F.shape[1] % 2 == 0, "pencil references: J = I, even n"
+        F, J, G = np.asfortranarray(at.F), np.asarray(at.J, np.int8), np.asfortranarray(at.G)
     t_factor = time.time() - t0
     del at
     m, n = F.shape

@@ -28,6 +28,8 @@ from paper_1907_08560_b200 import inputs
 
 pytestmark = pytest.mark.gpu
 EPS = oracle.EPS
+# dataset C: the north star's well-conditioned tolerance
+C5_TOL = 1e-9
 
 
 @pytest.fixture(scope="module")
@@ -401,3 +403,27 @@ def test_c4_blocked_converges_with_residuals(gh, c4):
     Sx = G0.conj().T @ (G0 @ x)
     res = np.linalg.norm(Hx - Sx * lam[idx][None, :], axis=0) / (nf2 * np.linalg.norm(x, axis=0))
     assert res.max() <= 1e-12 * NG
+
+
+@pytest.mark.parametrize("ordering", ["hier", "rr"])
+def test_c5_converged_lambda_vs_stored_oracle(gh, ordering):
+    """Dataset C at n = 4000 (config 5, the paper's GSVD workload; J = I):
+    BO in the bench's HIER ordering and in the round-robin against the stored oracle solve
+    of the same seeded pencil (tests/golden/c5_oracle_pointwise.*, oracle.hz_pointwise to
+    convergence on the pencil as generated), per eigenvalue."""
+    stem = os.path.join(GOLD, "c5_oracle_pointwise")
+    if not os.path.exists(stem + ".json"):
+        pytest.fail(f"missing stored oracle reference {stem}.json (tools/make_oracle_reference.py)")
+    meta = json.load(open(stem + ".json"))
+    kind, P = inputs.make_config(5)
+    assert inputs.fingerprint_close(inputs.fingerprint(P), meta["fingerprint"])
+    n = P.F.shape[1]
+    kw = dict(ordering="hier", super_blocks=4) if ordering == "hier" else {}
+    ctx = gh.Context(n, n, variant="bo", max_sweeps=64, **kw)
+    ctx.set_factors(P.F, P.J, P.G)
+    st = ctx.sweep()
+    lam = ctx.extract(want_z=False)[0].copy()
+    ctx.close()
+    err = _relerr(lam, np.load(stem + ".npz")["lam"])
+    print(f"c5 {ordering}: {st['sweeps']} sweeps (oracle {meta['stats']['sweeps']}), lambda vs stored oracle {err:.2e}")
+    assert st["converged"] and err <= C5_TOL

@@ -644,6 +644,12 @@ def run_ours(args):
     par = stored_oracle_parity(args.config, payload, lam_h.numpy(), phase2=args.reduce == "colpiv")
     if par is not None:
         line["parity_vs_stored_oracle"] = par
+    lam_true = getattr(payload, "lam_true", None)
+    if lam_true is not None:   # config 1: the closed-form spectrum lambda = alpha^2 / beta^2
+        lt, la = np.sort(np.asarray(lam_true)), np.sort(lam_h.numpy())
+        err = float(np.max(np.abs(la - lt) / np.abs(lt))) if la.shape == lt.shape else None
+        line["parity_vs_known_spectrum"] = {"max_rel_lambda_err": err, "tol": 1e-9,
+                                            "within_tol": err is not None and err <= 1e-9}
     if not args.no_cpu_baseline and ws == 1:
         cb = cpu_baseline_fresh_process(args.config, sweeps, args.ref_budget)
         if isinstance(cb, tuple):

@@ -357,7 +357,7 @@ def run_reference(args):
     cb["value"] = v
     line = {"impl": "reference", "metric": metric_name(args.config, n), "value": v, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": {"workload": inputs.CONFIGS[args.config]["name"], "m": m, "n": n,
                        "variant": "oracle-pointwise", "sweeps_extrapolated": None if cb["measured"] else cb["sweeps"],
                        "phase2": "oracle.reduce" if "reduce" in inputs.CONFIGS[args.config].get("entry", "")
@@ -616,7 +616,7 @@ def run_ours(args):
     metric = metric_name(args.config, n)
     line = {
         "metric": metric, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong" if ws > 1 else "weak",
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg["name"], "m": mb, "n": nb, "variant": args.variant, "max_sweeps": args.max_sweeps,
                    "ordering": ordering if blocked else "round-robin (pointwise)",

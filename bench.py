@@ -314,8 +314,9 @@ def cpu_baseline_fresh_process(cfg: int, sweeps: int, budget_s: float):
     """cpu_baseline_sample in a FRESH process (this script's --impl reference leg, one
     step): in the bench process, beside its CUDA context and torch's threads, the oracle's
     OpenMP update passes measured ~1.6x slower per pair than in the reference arm's own
-    process on the same host, so the two lines disagreed by tens of percent.  Falls back
-    to sampling in-process (and says so) if the child fails."""
+    process on the same host, so the two lines disagreed by tens of percent.  Returns
+    (cpu_baseline, None), or (None, error) if the child fails (the caller then samples
+    in-process and says so)."""
     drop = ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "GROUP_RANK", "ROLE_RANK", "MASTER_ADDR",
             "MASTER_PORT", "TORCHELASTIC_RUN_ID")
     env = {k: v for k, v in os.environ.items() if k not in drop}
@@ -327,7 +328,7 @@ def cpu_baseline_fresh_process(cfg: int, sweeps: int, budget_s: float):
         if r.returncode == 0 and js:
             cb = json.loads(js[-1])["cpu_baseline"]
             cb["process"] = "fresh process (bench.py --impl reference --steps 1 --warmup 0)"
-            return cb
+            return cb, None
         err = (r.stderr or "")[-300:]
     except (subprocess.SubprocessError, OSError, ValueError, KeyError) as e:
         err = repr(e)
@@ -651,12 +652,11 @@ def run_ours(args):
         line["parity_vs_known_spectrum"] = {"max_rel_lambda_err": err, "tol": 1e-9,
                                             "within_tol": err is not None and err <= 1e-9}
     if not args.no_cpu_baseline and ws == 1:
-        cb = cpu_baseline_fresh_process(args.config, sweeps, args.ref_budget)
-        if isinstance(cb, tuple):
+        cb, err = cpu_baseline_fresh_process(args.config, sweeps, args.ref_budget)
+        if cb is None:
             F0, J0, G0 = oracle_factors(kind, payload, args.config)
-            cb_in = cpu_baseline_sample(F0, J0, G0, args.config, sweeps, budget_s=args.ref_budget)
-            cb_in["process"] = f"bench process (fresh-process sample failed: {cb[1]})"
-            cb = cb_in
+            cb = cpu_baseline_sample(F0, J0, G0, args.config, sweeps, budget_s=args.ref_budget)
+            cb["process"] = f"bench process (fresh-process sample failed: {err})"
         line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
     ctx.close()

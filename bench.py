@@ -265,22 +265,25 @@ def cpu_baseline_sample(F0, J0, G0, cfg: int, fallback_sweeps: int, budget_s: fl
     JE = np.ones(m, dtype=np.int8)
 
     def per_step(F, J, G, budget):
-        # each call copies F, G, Z first: per-step cost = (t(1 + K) - t(1)) / K, after one
-        # untimed call (first-touch page faults of the copies inflate the first call)
+        # each call copies F, G, Z first: per-step cost = (t(1 + ns) - t(1)) / ns, after one
+        # untimed call (first-touch page faults of the copies inflate the first call).  ns
+        # doubles until the steps alone take half the budget or the calls the whole budget:
+        # the time stays bounded even when the copy overhead swamps a short probe (a probe
+        # of 4 Gram-only steps once extrapolated to a 33 s sample)
         oracle.hz_steps(F, J, G, Z, 0, 1)
         t = time.perf_counter()
         oracle.hz_steps(F, J, G, Z, 0, 1)
         ta = time.perf_counter() - t
-        K = 4
-        t = time.perf_counter()
-        oracle.hz_steps(F, J, G, Z, 0, 1 + K)
-        tb = time.perf_counter() - t
-        est = max((tb - ta) / K, 1e-6)
-        ns = int(max(K, min(n - 2, budget / est)))
-        t = time.perf_counter()
-        oracle.hz_steps(F, J, G, Z, 0, 1 + ns)
-        tc = time.perf_counter() - t
-        return max(tc - ta, 1e-9) / ns, ns, ta + tb + tc
+        ns, total = 4, ta
+        while True:
+            t = time.perf_counter()
+            oracle.hz_steps(F, J, G, Z, 0, 1 + ns)
+            tc = time.perf_counter() - t
+            total += tc
+            if tc - ta >= 0.5 * budget or total >= budget or ns >= n - 2:
+                break
+            ns = min(n - 2, 2 * ns)
+        return max(tc - ta, 1e-9) / ns, ns, total
 
     c_full, ns_f, s1 = per_step(F0, J0, G0, 0.7 * budget_s)
     c_gram, ns_g, s2 = per_step(E, JE, E, 0.3 * budget_s)
